@@ -1,0 +1,165 @@
+"""Parity ORACLE (test infrastructure only).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  It wraps ``liboracle.so``
+(oracle/oracle.cpp), a plain fp64 CPU implementation of GS(p), SpMV, the
+canonical dot product, SELL-C-sigma layout, Bi-CGSTAB and GMRES(m) written from
+the paper (see the header of oracle.cpp for the passages and DESIGN.md §4 for the
+arithmetic contract).  It shares no code with ``paper_0812_2769_b200``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("restarts", ctypes.c_int32), ("history_len", ctypes.c_int32),
+                ("breakdown_at", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("relres", ctypes.c_double), ("true_relres", ctypes.c_double),
+                ("true_relres_w", ctypes.c_double), ("best_relres", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run make (or __graft_entry__.build())")
+        lib = ctypes.CDLL(path)
+        vp, i64, d, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        lib.orc_num_threads.restype = i32
+        lib.orc_dot.argtypes = [i64, vp, vp]
+        lib.orc_dot.restype = d
+        lib.orc_wnorm2.argtypes = [i64, vp, vp]
+        lib.orc_wnorm2.restype = d
+        lib.orc_spmv.argtypes = [i64, vp, vp, vp, vp, vp]
+        lib.orc_spmv.restype = None
+        lib.orc_gs_scale.argtypes = [i64, vp, vp, vp, i32, vp, vp, vp, vp]
+        lib.orc_gs_scale.restype = i32
+        lib.orc_sell_size.argtypes = [i64, vp, i32, i32]
+        lib.orc_sell_size.restype = i64
+        lib.orc_sell_build.argtypes = [i64, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        lib.orc_sell_build.restype = i32
+        lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, vp, d, i32, vp, vp,
+                                     ctypes.POINTER(Report)]
+        lib.orc_bicgstab.restype = i32
+        lib.orc_gmres.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, d, i32, vp, vp,
+                                  ctypes.POINTER(Report)]
+        lib.orc_gmres.restype = i32
+        _LIB = lib
+    return _LIB
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def num_threads() -> int:
+    return _lib().orc_num_threads()
+
+
+def dot(a, b) -> float:
+    a, b = _f64(a), _f64(b)
+    return _lib().orc_dot(a.size, _p(a), _p(b))
+
+
+def wnorm2(a, w=None) -> float:
+    a, w = _f64(a), _f64(w)
+    return _lib().orc_wnorm2(a.size, _p(a), _p(w))
+
+
+def spmv(row_ptr, col, val, x):
+    row_ptr, col, val, x = _i32(row_ptr), _i32(col), _f64(val), _f64(x)
+    n = row_ptr.size - 1
+    y = np.empty(n, np.float64)
+    _lib().orc_spmv(n, _p(row_ptr), _p(col), _p(val), _p(x), _p(y))
+    return y
+
+
+class ZeroRowError(ValueError):
+    def __init__(self, row):
+        super().__init__(f"row {row} has zero L_p norm")
+        self.row = row
+
+
+def gs_scale(row_ptr, val, b, p):
+    """Return (val', b', d) = (D A, D b, diag D) with D = diag(1/||a_i||_p)."""
+    row_ptr, val = _i32(row_ptr), _f64(val)
+    b = _f64(b)
+    n = row_ptr.size - 1
+    vo = np.empty_like(val)
+    bo = None if b is None else np.empty_like(b)
+    d = np.empty(n, np.float64)
+    bad = ctypes.c_int32(-1)
+    rc = _lib().orc_gs_scale(n, _p(row_ptr), _p(val), _p(b), int(p), _p(vo), _p(bo), _p(d),
+                             ctypes.addressof(bad))
+    if rc == -1:
+        raise ValueError("p must be >= 1")
+    if rc == -2:
+        raise ZeroRowError(bad.value)
+    return vo, bo, d
+
+
+def sell_build(row_ptr, col, val, C=32, sigma=256):
+    row_ptr, col, val = _i32(row_ptr), _i32(col), _f64(val)
+    n = row_ptr.size - 1
+    nch = (n + C - 1) // C
+    tot = _lib().orc_sell_size(n, _p(row_ptr), C, sigma)
+    out = {"chunk_ptr": np.zeros(nch + 1, np.int32), "chunk_len": np.zeros(nch, np.int32),
+           "scol": np.zeros(tot, np.int32), "sval": np.zeros(tot, np.float64),
+           "roff": np.zeros(nch * C, np.uint8)}
+    rc = _lib().orc_sell_build(n, _p(row_ptr), _p(col), _p(val), C, sigma,
+                               *(_p(out[k]) for k in ("chunk_ptr", "chunk_len", "scol", "sval", "roff")))
+    if rc != 0:
+        raise ValueError("bad SELL parameters")
+    return out
+
+
+def bicgstab(row_ptr, col, val, b, tol, maxit, x0=None, weights=None):
+    """Returns (x, hist, report-dict)."""
+    row_ptr, col, val, b = _i32(row_ptr), _i32(col), _f64(val), _f64(b)
+    x0, w = _f64(x0), _f64(weights)
+    n = row_ptr.size - 1
+    x = np.empty(n, np.float64)
+    hist = np.empty(maxit + 1, np.float64)
+    rep = Report()
+    rc = _lib().orc_bicgstab(n, _p(row_ptr), _p(col), _p(val), _p(b), _p(x0), _p(w),
+                             float(tol), int(maxit), _p(x), _p(hist), ctypes.byref(rep))
+    if rc != 0:
+        raise ValueError("bad arguments")
+    return x, hist[:rep.history_len].copy(), rep.as_dict()
+
+
+def gmres(row_ptr, col, val, b, m, tol, maxit, x0=None, weights=None):
+    """Returns (x, hist, report-dict)."""
+    row_ptr, col, val, b = _i32(row_ptr), _i32(col), _f64(val), _f64(b)
+    x0, w = _f64(x0), _f64(weights)
+    n = row_ptr.size - 1
+    x = np.empty(n, np.float64)
+    hist = np.empty(maxit + 1, np.float64)
+    rep = Report()
+    rc = _lib().orc_gmres(n, _p(row_ptr), _p(col), _p(val), _p(b), _p(x0), _p(w), int(m),
+                          float(tol), int(maxit), _p(x), _p(hist), ctypes.byref(rep))
+    if rc != 0:
+        raise ValueError("bad arguments")
+    return x, hist[:rep.history_len].copy(), rep.as_dict()

@@ -1,0 +1,368 @@
+// oracle/oracle.cpp — the parity ORACLE.  TEST INFRASTRUCTURE ONLY.
+//
+// Plain, slow, obviously-correct fp64 CPU implementation of what the hot path
+// computes.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+// --impl reference legs may load it.  It shares no code, header or constant with
+// the CUDA path (paper_0812_2769_b200/csrc); the two meet only in the seeded
+// inputs from workloads/.
+//
+// Paper: Gordon & Gordon, "Geometric scaling: a simple preconditioner for certain
+// linear systems with discontinuous coefficients" (arXiv 0812.2769).
+//   GS(p)      PAPER.md:92-97 and Eq. (2)
+//   L_p norm   PAPER.md:193-196 (|.| applied, reading G1)
+//   solvers    PAPER.md:100-102, 232-235 (restarted GMRES, Bi-CGSTAB)
+//   stopping   PAPER.md:299-321 (relative residual < eps, breakdown)
+//   u0 = 0
+// The paper is silent on summation order, FMA use and the Givens / back-solve
+// details; the arithmetic contract AC-1..AC-7 of DESIGN.md §4 fixes them and is
+// followed here literally:
+//   AC-2 no contraction: built with -ffp-contract=off; every fma is std::fma.
+//   AC-3 SpMV row: acc = +0; for k ascending: acc = fma(val[k], x[col[k]], acc).
+//   AC-5 dot: q_i = RN(a_i*b_i), zero-padded to L = 2^ceil(log2 n), pairwise
+//        tree T(2k) = T(first k) + T(last k), result T + 0.0.
+//
+// Build: g++ -O2 -mfma -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC.
+// OpenMP only splits loops whose iterations are independent (rows, elements, the
+// pairs of one tree level), so results do not depend on the thread count.
+//
+// Parity status per function (pins live in tests/test_oracle*.py):
+//   orc_dot, orc_spmv, orc_gs_scale, orc_bicgstab, orc_gmres, orc_sell_build: pinned.
+#include <cstdint>
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+#include <numeric>
+#include <omp.h>
+
+extern "C" {
+
+// Report (mirrors the fields of the C-ABI report by name; independent definition).
+struct orc_report {
+  int32_t status;        // 0 converged, 1 maxit, 2 breakdown, 3 diverged
+  int32_t iterations;
+  int32_t restarts;
+  int32_t history_len;
+  int32_t breakdown_at;
+  int32_t pad_;
+  double relres;         // last history value
+  double true_relres;    // ||b-Ax|| / ||b-Ax0|| (unweighted, solved frame)
+  double true_relres_w;  // same with stopping-frame weights (== true_relres if none)
+  double best_relres;    // min over the history
+};
+
+int orc_num_threads() { return omp_get_max_threads(); }
+
+// ---- AC-5: canonical pairwise tree --------------------------------------------------
+static double tree_sum(std::vector<double>& q, int64_t n) {
+  int64_t L = 1;
+  while (L < n) L <<= 1;
+  q.resize(L, 0.0);
+  for (int64_t i = n; i < L; ++i) q[i] = 0.0;
+  // one tree level at a time: out[i] = in[2i] + in[2i+1] (separate buffers, so
+  // splitting a level across threads cannot change any value)
+  std::vector<double> nxt(L / 2 > 0 ? L / 2 : 1);
+  for (int64_t len = L; len > 1; len >>= 1) {
+    #pragma omp parallel for schedule(static) if (len > 65536)
+    for (int64_t i = 0; i < len / 2; ++i) nxt[i] = q[2 * i] + q[2 * i + 1];
+    std::copy(nxt.begin(), nxt.begin() + len / 2, q.begin());
+  }
+  return q[0] + 0.0;
+}
+
+// <a, b> under AC-5.
+double orc_dot(int64_t n, const double* a, const double* b) {
+  std::vector<double> q(n > 0 ? n : 1);
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) q[i] = a[i] * b[i];
+  return tree_sum(q, n);
+}
+
+// sum_i (w_i a_i)^2 under AC-5 (w null: plain <a,a>).
+double orc_wnorm2(int64_t n, const double* a, const double* w) {
+  std::vector<double> q(n > 0 ? n : 1);
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double u = w ? w[i] * a[i] : a[i];
+    q[i] = u * u;
+  }
+  return tree_sum(q, n);
+}
+
+// ---- SpMV, AC-3 (SPEC sparse-core spmv; y = A x) -----------------------------------
+void orc_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+              const double* x, double* y) {
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) acc = std::fma(v[k], x[ci[k]], acc);
+    y[i] = acc;
+  }
+}
+
+// ---- GS(p): Eq. (2), PAPER.md:207-214 ------------------------------------------------
+// d_i = 1/||a_i||_p ; (DA)_ij = a_ij * d_i ; (Db)_i = b_i * d_i   (reading G2: multiply
+// by D as written).  AC-4 norm: p=2 acc = fma(a,a,acc), sqrt; p=1 acc += |a|;
+// p>=3 |a|^p by repeated multiplication, root pow(acc, 1/p).
+// Returns 0, -1 (p<1), or -2 (zero row; *bad_row = smallest such row).  Outputs may
+// alias inputs.  b / b_out / d_out may be null.
+int orc_gs_scale(int64_t n, const int32_t* rp, const double* val, const double* b, int p,
+                 double* val_out, double* b_out, double* d_out, int32_t* bad_row) {
+  if (p < 1) return -1;
+  std::vector<double> d(n);
+  int64_t bad = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
+      double a = std::fabs(val[k]);
+      if (p == 1) acc = acc + a;
+      else if (p == 2) acc = std::fma(val[k], val[k], acc);
+      else {
+        double t = a;
+        for (int e = 1; e < p; ++e) t = t * a;
+        acc = acc + t;
+      }
+    }
+    double nrm = (p == 1) ? acc : (p == 2 ? std::sqrt(acc) : std::pow(acc, 1.0 / p));
+    if (nrm == 0.0) { if (bad < 0) bad = i; d[i] = 0.0; continue; }
+    d[i] = 1.0 / nrm;
+  }
+  if (bad >= 0) { if (bad_row) *bad_row = (int32_t)bad; return -2; }
+  for (int64_t i = 0; i < n; ++i) {
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) val_out[k] = val[k] * d[i];
+    if (b && b_out) b_out[i] = b[i] * d[i];
+    if (d_out) d_out[i] = d[i];
+  }
+  return 0;
+}
+
+// ---- SELL-C-sigma layout (BASELINE.json configs[3]) -------------------------------
+// Windows of sigma consecutive rows; inside a window rows are stably sorted by
+// descending length (ties keep row order); chunks of C sorted rows; chunk_len =
+// longest row of the chunk; slot (k, lane) of chunk c at chunk_ptr[c] + k*C + lane,
+// holding the row's k-th CSR entry (CSR order kept) or col -1 / val 0 as padding;
+// roff[c*C + lane] = in-window offset of the row (uint8, sigma <= 256).
+int64_t orc_sell_size(int64_t n, const int32_t* rp, int C, int sigma) {
+  int64_t nch = (n + C - 1) / C, tot = 0;
+  for (int64_t w = 0; w * sigma < n; ++w) {
+    int64_t r0 = w * sigma, r1 = std::min<int64_t>(n, r0 + sigma);
+    std::vector<int32_t> len;
+    for (int64_t r = r0; r < r1; ++r) len.push_back(rp[r + 1] - rp[r]);
+    std::stable_sort(len.begin(), len.end(), [](int32_t a, int32_t b) { return a > b; });
+    for (size_t s = 0; s < len.size(); s += C) tot += (int64_t)len[s] * C;
+  }
+  (void)nch;
+  return tot;
+}
+
+int orc_sell_build(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, int C,
+                   int sigma, int32_t* chunk_ptr, int32_t* chunk_len, int32_t* scol,
+                   double* sval, uint8_t* roff) {
+  if (C <= 0 || sigma <= 0 || sigma % C != 0 || sigma > 256) return -1;
+  int64_t nch = (n + C - 1) / C;
+  chunk_ptr[0] = 0;
+  for (int64_t w = 0; w * sigma < n; ++w) {
+    int64_t r0 = w * sigma, r1 = std::min<int64_t>(n, r0 + sigma), cnt = r1 - r0;
+    std::vector<int32_t> order(cnt);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return (rp[r0 + a + 1] - rp[r0 + a]) > (rp[r0 + b + 1] - rp[r0 + b]);
+    });
+    int64_t c0 = r0 / C, c1 = (r1 + C - 1) / C;
+    for (int64_t c = c0; c < c1; ++c) {
+      int64_t s0 = c * C - r0;  // first sorted position of the chunk in this window
+      int32_t L = rp[r0 + order[s0] + 1] - rp[r0 + order[s0]];
+      chunk_len[c] = L;
+      chunk_ptr[c + 1] = chunk_ptr[c] + L * C;
+      for (int lane = 0; lane < C; ++lane) {
+        int64_t s = s0 + lane;
+        bool real = s < cnt;
+        int64_t row = real ? r0 + order[s] : -1;
+        roff[c * C + lane] = (uint8_t)(real ? order[s] : s);
+        int32_t len = real ? rp[row + 1] - rp[row] : 0;
+        for (int32_t k = 0; k < L; ++k) {
+          int64_t slot = (int64_t)chunk_ptr[c] + (int64_t)k * C + lane;
+          if (k < len) { scol[slot] = ci[rp[row] + k]; sval[slot] = v[rp[row] + k]; }
+          else { scol[slot] = -1; sval[slot] = 0.0; }
+        }
+      }
+    }
+  }
+  (void)nch;
+  return 0;
+}
+
+// ---- Bi-CGSTAB (van der Vorst 1992, cited PAPER.md:102) ----------------------------
+// DESIGN.md §4 algorithm B, arithmetic AC-6; stopping PAPER.md:302-307 (reading B1/B2:
+// strict <, frame weights w optional); breakdown exact-zero tests (PAPER.md:315-321,
+// reading B5); ||s|| half-step exit (B4); iterations = completed iterations (B6).
+// hist[maxit+1] (nullable).  x0 nullable (= 0).  Returns 0 or -1 (bad args).
+int orc_bicgstab(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+                 const double* b, const double* x0, const double* w, double tol, int maxit,
+                 double* x, double* hist, orc_report* rep) {
+  if (n < 1 || maxit < 1 || !(tol > 0)) return -1;
+  std::vector<double> r(n), rh(n), p(n, 0.0), vv(n, 0.0), s(n), t(n), ax(n);
+  for (int64_t i = 0; i < n; ++i) x[i] = x0 ? x0[i] : 0.0;
+  orc_spmv(n, rp, ci, v, x, ax.data());
+  for (int64_t i = 0; i < n; ++i) { r[i] = b[i] - ax[i]; rh[i] = r[i]; }
+  const double n0 = std::sqrt(orc_wnorm2(n, r.data(), w));
+  const double n0u = std::sqrt(orc_wnorm2(n, r.data(), nullptr));
+  std::memset(rep, 0, sizeof(*rep));
+  std::vector<double> H;  // history
+  H.push_back(n0 == 0.0 ? 0.0 : 1.0);
+  int status = 1, iters = 0, bd = 0;
+  if (n0 == 0.0) {
+    status = 0;
+  } else {
+    double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+    double rho = orc_dot(n, rh.data(), r.data());
+    for (int i = 1; i <= maxit; ++i) {
+      if (rho == 0.0) { status = 2; bd = i; break; }
+      double beta = (rho / rho_prev) * (alpha / omega);
+      for (int64_t k = 0; k < n; ++k) p[k] = std::fma(beta, std::fma(-omega, vv[k], p[k]), r[k]);
+      orc_spmv(n, rp, ci, v, p.data(), vv.data());
+      double sigma = orc_dot(n, rh.data(), vv.data());
+      if (sigma == 0.0) { status = 2; bd = i; break; }
+      alpha = rho / sigma;
+      for (int64_t k = 0; k < n; ++k) s[k] = std::fma(-alpha, vv[k], r[k]);
+      double sn = std::sqrt(orc_wnorm2(n, s.data(), w)) / n0;
+      if (sn < tol) {
+        for (int64_t k = 0; k < n; ++k) x[k] = std::fma(alpha, p[k], x[k]);
+        H.push_back(sn); iters = i; status = 0;
+        break;
+      }
+      orc_spmv(n, rp, ci, v, s.data(), t.data());
+      double tt = orc_dot(n, t.data(), t.data());
+      if (tt == 0.0) { status = 2; bd = i; break; }
+      double ts = orc_dot(n, t.data(), s.data());
+      omega = ts / tt;
+      for (int64_t k = 0; k < n; ++k) {
+        x[k] = std::fma(omega, s[k], std::fma(alpha, p[k], x[k]));
+        r[k] = std::fma(-omega, t[k], s[k]);
+      }
+      rho_prev = rho;
+      double rn = std::sqrt(orc_wnorm2(n, r.data(), w)) / n0;
+      H.push_back(rn); iters = i;
+      if (!std::isfinite(rn)) { status = 3; break; }
+      if (rn < tol) { status = 0; break; }
+      if (omega == 0.0) { status = 2; bd = i; break; }
+      if (i == maxit) { status = 1; break; }
+      rho = orc_dot(n, rh.data(), r.data());
+    }
+  }
+  // final true residual (one extra SpMV), PAPER.md:672-677 / SPEC true_relres
+  orc_spmv(n, rp, ci, v, x, ax.data());
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - ax[i];
+  double tn = std::sqrt(orc_wnorm2(n, r.data(), nullptr));
+  double tw = std::sqrt(orc_wnorm2(n, r.data(), w));
+  rep->status = status;
+  rep->iterations = iters;
+  rep->restarts = 0;
+  rep->history_len = (int32_t)H.size();
+  rep->breakdown_at = bd;
+  rep->relres = H.back();
+  rep->true_relres = n0u == 0.0 ? 0.0 : tn / n0u;
+  rep->true_relres_w = n0 == 0.0 ? 0.0 : tw / n0;
+  rep->best_relres = *std::min_element(H.begin(), H.end());
+  if (hist) std::memcpy(hist, H.data(), sizeof(double) * H.size());
+  return 0;
+}
+
+// ---- restarted GMRES(m) (Saad & Schultz 1986, cited PAPER.md:101) ------------------
+// DESIGN.md §4 algorithm G, arithmetic AC-7: modified Gram-Schmidt (reading B9),
+// Givens rotations, column-oriented back substitution, x += sum_k y_k v_k (k
+// ascending).  Iterations count inner Arnoldi steps (B6).  hist[it] is the
+// least-squares residual estimate |g_{j+1}|/||r0||.  w (nullable) only enters the
+// reported true_relres_w.
+int orc_gmres(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+              const double* b, const double* x0, const double* w, int m, double tol, int maxit,
+              double* x, double* hist, orc_report* rep) {
+  if (n < 1 || maxit < 1 || m < 1 || !(tol > 0)) return -1;
+  std::vector<double> r(n), ax(n), wv(n);
+  std::vector<std::vector<double>> V(m + 1, std::vector<double>(n));
+  std::vector<double> Hm((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m);
+  auto h = [&](int i, int j) -> double& { return Hm[(size_t)i * m + j]; };  // 0-based
+  for (int64_t i = 0; i < n; ++i) x[i] = x0 ? x0[i] : 0.0;
+  orc_spmv(n, rp, ci, v, x, ax.data());
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - ax[i];
+  const double beta0 = std::sqrt(orc_dot(n, r.data(), r.data()));
+  const double n0w = std::sqrt(orc_wnorm2(n, r.data(), w));
+  std::memset(rep, 0, sizeof(*rep));
+  std::vector<double> H;
+  H.push_back(beta0 == 0.0 ? 0.0 : 1.0);
+  int status = 1, it = 0, restarts = 0;
+  if (beta0 == 0.0) status = 0;
+  bool done = (beta0 == 0.0);
+  while (!done) {
+    double beta = std::sqrt(orc_dot(n, r.data(), r.data()));
+    double inv = 1.0 / beta;
+    for (int64_t i = 0; i < n; ++i) V[0][i] = r[i] * inv;
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    bool stop_conv = false, stop_div = false;
+    for (int j = 0; j < m; ++j) {  // Arnoldi step j+1
+      ++it;
+      orc_spmv(n, rp, ci, v, V[j].data(), wv.data());
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        h(i, j) = orc_dot(n, wv.data(), V[i].data());
+        for (int64_t q = 0; q < n; ++q) wv[q] = std::fma(-h(i, j), V[i][q], wv[q]);
+      }
+      double hn = std::sqrt(orc_dot(n, wv.data(), wv.data()));
+      h(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {  // previous rotations on column j
+        double a = h(i, j), bb = h(i + 1, j);
+        h(i, j) = std::fma(cs[i], a, sn[i] * bb);
+        h(i + 1, j) = std::fma(-sn[i], a, cs[i] * bb);
+      }
+      double a = h(j, j), bb = h(j + 1, j);
+      double delta = std::sqrt(std::fma(a, a, bb * bb));
+      cs[j] = a / delta;
+      sn[j] = bb / delta;
+      h(j, j) = delta;
+      h(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      double rel = std::fabs(g[j + 1]) / beta0;
+      H.push_back(rel);
+      k = j + 1;
+      if (!std::isfinite(rel)) { stop_div = true; break; }
+      if (rel < tol) { stop_conv = true; break; }
+      if (hn == 0.0 || it == maxit) break;
+      double invh = 1.0 / hn;
+      for (int64_t q = 0; q < n; ++q) V[j + 1][q] = wv[q] * invh;
+    }
+    if (stop_div) { status = 3; break; }
+    // column-oriented back substitution R y = g (R = upper k x k of H)
+    std::vector<double> acc(g.begin(), g.begin() + k);
+    for (int kk = k - 1; kk >= 0; --kk) {
+      y[kk] = acc[kk] / h(kk, kk);
+      for (int l = 0; l < kk; ++l) acc[l] = std::fma(-h(l, kk), y[kk], acc[l]);
+    }
+    for (int kk = 0; kk < k; ++kk)
+      for (int64_t q = 0; q < n; ++q) x[q] = std::fma(y[kk], V[kk][q], x[q]);
+    orc_spmv(n, rp, ci, v, x, ax.data());
+    for (int64_t i = 0; i < n; ++i) r[i] = b[i] - ax[i];
+    bool fin = true;
+    for (int kk = 0; kk < k; ++kk) fin = fin && std::isfinite(y[kk]);
+    if (!fin) { status = 3; break; }
+    if (stop_conv) { status = 0; break; }
+    if (it >= maxit) { status = 1; break; }
+    ++restarts;
+  }
+  double tn = std::sqrt(orc_dot(n, r.data(), r.data()));
+  double tw = std::sqrt(orc_wnorm2(n, r.data(), w));
+  rep->status = status;
+  rep->iterations = it;
+  rep->restarts = restarts;
+  rep->history_len = (int32_t)H.size();
+  rep->breakdown_at = 0;
+  rep->relres = H.back();
+  rep->true_relres = beta0 == 0.0 ? 0.0 : tn / beta0;
+  rep->true_relres_w = n0w == 0.0 ? 0.0 : tw / n0w;
+  rep->best_relres = *std::min_element(H.begin(), H.end());
+  if (hist) std::memcpy(hist, H.data(), sizeof(double) * H.size());
+  return 0;
+}
+
+}  // extern "C"

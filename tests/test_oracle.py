@@ -1,0 +1,363 @@
+"""Oracle pins (oracle/): each function checked against what the paper and the
+mathematics fix, never against a retyped copy of itself.
+
+  dot / wnorm2   exactness on integer data, the pairwise-tree shape on a hand-derived
+                 case, the ceil(log2 n) u sum|q| error bound, thread-count invariance
+  spmv           dense matvec; exact integer products
+  gs_scale       Eq. (2) worked examples, unit L_p rows, solution invariance,
+                 idempotence, errors
+  sell_build     lossless round trip to CSR, window sort order, padding
+  bicgstab/gmres dense LU on small systems, finite termination, Krylov least-squares
+                 optimality, within-cycle monotonicity, A = I
+"""
+import json
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def csr_from_dense(A):
+    n = A.shape[0]
+    rp, col, val = [0], [], []
+    for i in range(n):
+        nz = np.nonzero(A[i])[0]
+        col += list(nz)
+        val += list(A[i, nz])
+        rp.append(len(col))
+    return np.array(rp, np.int32), np.array(col, np.int32), np.array(val, np.float64)
+
+
+def dense(rp, col, val, n):
+    A = np.zeros((n, n))
+    for i in range(n):
+        for k in range(rp[i], rp[i + 1]):
+            A[i, col[k]] += val[k]
+    return A
+
+
+# ---------------------------------------------------------------- dot (AC-5)
+def test_dot_exact_on_integers():
+    rng = np.random.default_rng(1)
+    for n in [1, 2, 3, 7, 1000, 4097, 100003]:
+        a = rng.integers(-2 ** 20, 2 ** 20, n).astype(np.float64)
+        b = rng.integers(-2 ** 12, 2 ** 12, n).astype(np.float64)
+        exact = sum(int(x) * int(y) for x, y in zip(a, b))  # |sum| < 2^53
+        assert oracle.dot(a, b) == float(exact)
+
+
+def test_dot_tree_shape_hand_case():
+    # (1e16 + 1) + (-1e16 + 1) rounds each pair to +-1e16 (ties-to-even), so the
+    # pairwise tree gives 0 whereas left-to-right summation gives 1.
+    a = np.array([1e16, 1.0, -1e16, 1.0])
+    assert oracle.dot(a, np.ones(4)) == 0.0
+    # 8 elements: ((x0+x1)+(x2+x3)) + ((x4+x5)+(x6+x7)); the right half cancels to 0,
+    # the left half is 2^53 + 2 computed as (2^53 + 0) + (1 + 1) = 2^53 + 2.
+    x = np.array([2.0 ** 53, 0.0, 1.0, 1.0, 1e300, -1e300, 5.0, -5.0])
+    assert oracle.dot(x, np.ones(8)) == 2.0 ** 53 + 2
+    # zero padding: n = 3 behaves as (x0 + x1) + (x2 + 0)
+    y = np.array([2.0 ** 53, 1.0, 1.0])
+    assert oracle.dot(y, np.ones(3)) == 2.0 ** 53  # (2^53+1 -> 2^53) + 1 -> 2^53
+
+
+def test_dot_error_bound_and_signed_zero():
+    rng = np.random.default_rng(2)
+    n = 1 << 18
+    a = rng.standard_normal(n) * np.exp(rng.uniform(-12, 12, n))
+    b = rng.standard_normal(n)
+    q = a * b
+    ref = math.fsum(q)
+    err = abs(oracle.dot(a, b) - ref)
+    assert err <= math.ceil(math.log2(n)) * 2 ** -53 * np.abs(q).sum()
+    assert math.copysign(1.0, oracle.dot(np.array([-0.0]), np.array([1.0]))) == 1.0  # T + 0.0
+
+
+def test_wnorm2():
+    r = np.array([3.0, 4.0, 12.0])
+    assert oracle.wnorm2(r) == 169.0
+    assert oracle.wnorm2(r, np.array([2.0, 0.5, 0.25])) == 36.0 + 4.0 + 9.0
+
+
+def test_dot_thread_count_invariance():
+    code = ("import sys; sys.path.insert(0, %r); import numpy as np, oracle, workloads;"
+            "a = workloads.uniform(300001, 3, 9); b = workloads.uniform(300001, 4, 9);"
+            "print(repr(oracle.dot(a, b)), oracle.num_threads())" % ROOT)
+    outs = set()
+    for t in ("1", "3", "8"):
+        env = dict(os.environ, OMP_NUM_THREADS=t)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                             text=True, check=True).stdout.split()
+        assert out[1] == t
+        outs.add(out[0])
+    assert len(outs) == 1
+
+
+# ---------------------------------------------------------------- spmv
+def test_spmv_vs_dense():
+    rng = np.random.default_rng(3)
+    for n in [1, 5, 60, 200]:
+        A = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.1)
+        np.fill_diagonal(A, 1.0 + rng.random(n))
+        rp, col, val = csr_from_dense(A)
+        x = rng.standard_normal(n)
+        y = oracle.spmv(rp, col, val, x)
+        assert np.allclose(y, A @ x, rtol=1e-13, atol=1e-13 * np.abs(A).sum(1).max() * np.abs(x).max())
+
+
+def test_spmv_exact_integers():
+    s = workloads.generate("C3", N=10)
+    rng = np.random.default_rng(4)
+    val = rng.integers(-1000, 1000, s["nnz"]).astype(np.float64)
+    x = rng.integers(-1000, 1000, s["n"]).astype(np.float64)
+    y = oracle.spmv(s["row_ptr"], s["col"], val, x)
+    A = dense(s["row_ptr"], s["col"], val, s["n"]).astype(np.int64)
+    assert np.array_equal(y, (A @ x.astype(np.int64)).astype(np.float64))
+
+
+# ---------------------------------------------------------------- GS(p), Eq. (2)
+def ulps(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.abs(a.view(np.int64) - b.view(np.int64)).max() if a.size else 0
+
+
+def test_gs_worked_examples():
+    ex = json.load(open(os.path.join(GOLD, "gs_examples.json")))["examples"]
+    for e in ex:
+        n = len(e["rows"])
+        A = np.zeros((n, max(max(c) for c in e["cols"]) + 1))
+        for i in range(n):
+            A[i, e["cols"][i]] = e["vals"][i]
+        rp = np.array([0] + list(np.cumsum([len(c) for c in e["cols"]])), np.int32)
+        val = np.concatenate([np.array(v, np.float64) for v in e["vals"]])
+        vo, bo, d = oracle.gs_scale(rp, val, np.array(e["b"]), e["p"])
+        if "scaled_vals" in e:
+            assert ulps(vo, np.concatenate(e["scaled_vals"])) <= 1
+            assert ulps(bo, e["scaled_b"]) <= 1
+            assert ulps(d, e["d"]) <= 1
+        if "norm" in e:
+            assert ulps(1.0 / d, e["norm"]) <= 2
+
+
+@pytest.mark.parametrize("name,N", [("C1", 32), ("C2", 64), ("C3", 16), ("C4", 16), ("C5", 64),
+                                    ("P1", 40), ("P4", 12)])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_gs_unit_row_norms(name, N, p):
+    """After GS(p) every row has unit L_p norm: BASELINE north star
+    asks 1e-14 relative."""
+    s = workloads.generate(name, N=N)
+    vo, bo, d = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], p)
+    rp = s["row_ptr"]
+    a = np.abs(vo)
+    sums = np.add.reduceat(a ** p, rp[:-1])
+    norms = sums ** (1.0 / p)
+    assert np.max(np.abs(norms - 1.0)) <= 1e-14
+    # pattern preserved, b scaled by the same d
+    assert np.all((vo == 0) == (s["val"] == 0))
+    assert np.allclose(bo, s["b"] * d, rtol=0, atol=0)
+
+
+def test_gs_solution_invariance_dense_lu():
+    """GS leaves the solution of Ax=b unchanged (DAx = Db)."""
+    for name, N in [("C1", 12), ("P1", 14), ("C4", 5), ("C2", 13)]:
+        s = workloads.generate(name, N=N)
+        A = dense(s["row_ptr"], s["col"], s["val"], s["n"])
+        for p in (1, 2):
+            vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], p)
+            DA = dense(s["row_ptr"], s["col"], vo, s["n"])
+            x1 = np.linalg.solve(A, s["b"])
+            x2 = np.linalg.solve(DA, bo)
+            assert np.linalg.norm(x1 - x2) <= 1e-10 * np.linalg.norm(x1)
+
+
+def test_gs_identity_idempotence_errors():
+    n = 9
+    rp = np.arange(n + 1, dtype=np.int32)
+    vo, _, d = oracle.gs_scale(rp, np.ones(n), np.ones(n), 2)
+    assert np.array_equal(vo, np.ones(n)) and np.array_equal(d, np.ones(n))
+    s = workloads.generate("C2", N=32)
+    v1, b1, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    v2, b2, d2 = oracle.gs_scale(s["row_ptr"], v1, b1, 2)
+    assert np.max(np.abs(v2 - v1) / np.abs(v1).clip(1e-300)) <= 4e-16 * 4
+    assert np.max(np.abs(d2 - 1)) <= 4e-16 * 2
+    with pytest.raises(ValueError):
+        oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 0)
+    val = s["val"].copy()
+    for r in (40, 17):
+        val[s["row_ptr"][r]:s["row_ptr"][r + 1]] = 0.0
+    with pytest.raises(oracle.ZeroRowError) as ei:
+        oracle.gs_scale(s["row_ptr"], val, s["b"], 2)
+    assert ei.value.row == 17  # smallest zero row
+
+
+def test_gs1_bounds_spectrum():
+    """GS(1): ||DA||_inf = 1, hence every eigenvalue has |lambda| <= 1."""
+    s = workloads.generate("P1", N=20)
+    vo, _, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 1)
+    DA = dense(s["row_ptr"], s["col"], vo, s["n"])
+    assert np.abs(np.abs(DA).sum(1) - 1).max() < 1e-15
+    assert np.abs(np.linalg.eigvals(DA)).max() <= 1 + 1e-12
+
+
+# ---------------------------------------------------------------- SELL-C-sigma
+@pytest.mark.parametrize("C,sigma", [(32, 256), (4, 8), (32, 32)])
+def test_sell_round_trip(C, sigma):
+    rng = np.random.default_rng(5)
+    n = 1000
+    lens = rng.integers(0, 9, n)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.standard_normal(rp[-1])
+    S = oracle.sell_build(rp, col, val, C, sigma)
+    S["roff"] = S["roff"].astype(np.int64)
+    nch = (n + C - 1) // C
+    assert S["chunk_ptr"][-1] == S["scol"].size
+    seen = np.zeros(n, bool)
+    for c in range(nch):
+        L = S["chunk_len"][c]
+        assert S["chunk_ptr"][c + 1] - S["chunk_ptr"][c] == L * C
+        w0 = (c * C) // sigma * sigma
+        prev = None
+        for lane in range(C):
+            row = w0 + S["roff"][c * C + lane]
+            if row >= n:
+                continue
+            assert not seen[row]
+            seen[row] = True
+            ln = rp[row + 1] - rp[row]
+            assert ln <= L
+            if lane == 0:
+                assert ln == L
+            slots = S["chunk_ptr"][c] + np.arange(L) * C + lane
+            assert np.array_equal(S["scol"][slots[:ln]], col[rp[row]:rp[row + 1]])
+            assert np.array_equal(S["sval"][slots[:ln]], val[rp[row]:rp[row + 1]])
+            assert np.all(S["scol"][slots[ln:]] == -1) and np.all(S["sval"][slots[ln:]] == 0)
+    assert seen.all()
+    # within a window the sorted order is by descending length, ties by row id
+    for w0 in range(0, n, sigma):
+        rows = [w0 + S["roff"][s] for s in range(w0, min(w0 + sigma, nch * C))
+                if w0 + S["roff"][s] < n]
+        key = [(-(rp[r + 1] - rp[r]), r) for r in rows]
+        assert key == sorted(key)
+
+
+# ---------------------------------------------------------------- solvers
+def small_system(n, seed, kappa=1e3):
+    """Nonsymmetric D + S with diag D in [1, kappa] and ||S||_2 ~ 0.6, so the field of
+    values lies in the right half plane and cond(A) <= ~kappa."""
+    rng = np.random.default_rng(seed)
+    d = np.geomspace(1.0, kappa, n)
+    S = rng.standard_normal((n, n)) * (0.3 / np.sqrt(n))
+    return np.diag(d) + S, rng.standard_normal(n)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_solvers_match_dense_lu(seed):
+    """n <= 200 with kappa <= 1e3: both solvers vs dense LU to 1e-10 (north star)."""
+    n = [20, 50, 80, 120, 160, 200][seed]
+    A, b = small_system(n, seed, kappa=30.0)
+    rp, col, val = csr_from_dense(A)
+    xs = np.linalg.solve(A, b)
+    x, h, rep = oracle.gmres(rp, col, val, b, n, 1e-14, 5 * n)
+    assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs)
+    x, h, rep = oracle.bicgstab(rp, col, val, b, 1e-14, 20 * n)
+    assert rep["status"] == 0
+    assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs) * 10
+
+
+def test_identity_one_iteration():
+    n = 50
+    rp = np.arange(n + 1, dtype=np.int32)
+    col = np.arange(n, dtype=np.int32)
+    b = np.linspace(-1, 2, n)
+    x, h, rep = oracle.bicgstab(rp, col, np.ones(n), b, 1e-12, 10)
+    assert rep["status"] == 0 and rep["iterations"] == 1 and np.array_equal(x, b)
+    x, h, rep = oracle.gmres(rp, col, np.ones(n), b, 5, 1e-12, 10)
+    assert rep["status"] == 0 and rep["iterations"] == 1 and np.allclose(x, b, rtol=1e-15)
+
+
+def test_finite_termination_diagonal():
+    """Diagonal A with k distinct eigenvalues: Krylov dimension k, so GMRES(m>=k)
+    converges in <= k steps and Bi-CGSTAB in <= k iterations (exact arithmetic)."""
+    n = 300
+    eigs = np.array([1.0, 2.5, 4.0, 7.0, 9.0])
+    d = eigs[np.arange(n) % 5]
+    rp = np.arange(n + 1, dtype=np.int32)
+    col = np.arange(n, dtype=np.int32)
+    b = workloads.uniform(n, 1, 1)
+    x, h, rep = oracle.gmres(rp, col, d, b, 10, 1e-12, 100)
+    assert rep["status"] == 0 and rep["iterations"] <= 5
+    x, h, rep = oracle.bicgstab(rp, col, d, b, 1e-12, 100)
+    assert rep["status"] == 0 and rep["iterations"] <= 5
+    assert np.allclose(x, b / d, rtol=1e-10)
+
+
+def test_gmres_is_krylov_least_squares():
+    """hist[j] * ||r0|| = min over x in x0 + K_j(A, r0) of ||b - A x|| (GMRES's
+    defining property, Saad & Schultz 1986); checked by brute-force least squares
+    on an orthonormalised explicit Krylov basis."""
+    n = 60
+    A, b = small_system(n, 11, kappa=10.0)
+    rp, col, val = csr_from_dense(A)
+    x, h, rep = oracle.gmres(rp, col, val, b, n, 1e-15, n)
+    beta0 = np.linalg.norm(b)
+    K = [b / beta0]
+    for j in range(1, 30):  # K_j = span{r0, A r0, ..., A^{j-1} r0}
+        Q, _ = np.linalg.qr(np.array(K).T)
+        K.append(A @ Q[:, -1])
+        y, *_ = np.linalg.lstsq(A @ Q, b, rcond=None)
+        best = np.linalg.norm(b - A @ Q @ y)
+        assert abs(h[j] * beta0 - best) <= 1e-8 * beta0 + 1e-6 * best, j
+
+
+def test_gmres_nonincreasing_within_cycle():
+    s = workloads.generate("C1")
+    vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    m = 20
+    x, h, rep = oracle.gmres(s["row_ptr"], s["col"], vo, bo, m, 1e-8, 400)
+    assert rep["restarts"] >= 10
+    for c0 in range(0, len(h) - 1, m):
+        seg = h[c0 + 1:c0 + m + 1] if c0 else h[0:m + 1]
+        assert np.all(np.diff(seg) <= np.spacing(seg[:-1]))  # 1-ulp slack (reading B13)
+
+
+def test_true_relres_recomputed():
+    """Frame consistency: the reported true residual is ||b - A x|| / ||b - A x0||."""
+    s = workloads.generate("C2", N=48)
+    vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    for solve in ("bicgstab", "gmres"):
+        if solve == "bicgstab":
+            x, h, rep = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-9, 3000)
+        else:
+            x, h, rep = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 30, 1e-9, 3000)
+        DA = dense(s["row_ptr"], s["col"], vo, s["n"])
+        tr = np.linalg.norm(bo - DA @ x) / np.linalg.norm(bo)
+        assert abs(tr - rep["true_relres"]) <= 1e-6 * tr + 1e-15
+        assert rep["history_len"] == len(h) == rep["iterations"] + 1
+
+
+def test_breakdown_on_exact_zero_rho():
+    """Bi-CGSTAB breakdown (exact-zero reading B5): a skew
+    system with r0 orthogonal to A r0 gives sigma = <r0, A r0> = 0 at iteration 1."""
+    A = np.array([[0.0, 1.0], [-1.0, 0.0]])
+    rp, col, val = csr_from_dense(A)
+    x, h, rep = oracle.bicgstab(rp, col, val, np.array([1.0, 0.0]), 1e-10, 10)
+    assert rep["status"] == 2 and rep["breakdown_at"] == 1 and rep["iterations"] == 0
+
+
+def test_zero_rhs_converges_immediately():
+    s = workloads.generate("C1", N=8)
+    b = np.zeros(s["n"])
+    for f in (oracle.bicgstab, ):
+        x, h, rep = f(s["row_ptr"], s["col"], s["val"], b, 1e-8, 10)
+        assert rep["status"] == 0 and rep["iterations"] == 0 and np.all(x == 0)
+    x, h, rep = oracle.gmres(s["row_ptr"], s["col"], s["val"], b, 5, 1e-8, 10)
+    assert rep["status"] == 0 and rep["iterations"] == 0
