@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py — driver benchmark contract for the GS(p) + Krylov hot path on B200.
+
+A *step* is one pass of the whole hot path over one synthetic
+system: GS(2) of A and b (a2), the SELL value refresh of the plan (a3), the
+Bi-CGSTAB solve (a4-a7) and the GMRES(m) solve (a4-a6, a8-a9) to the config's
+tolerance, each ending in its true-residual check (a10); all control runs on the
+device (a11).  At N=1 the workload is BASELINE.json configs[3] (C4: 256^3, 7-point
+upwind, 5 slabs, SELL-C-32-256; the headline roofline config), generated with the
+seeded recipe of DESIGN.md §3 and resident in HBM before timing.
+
+value  = solver iterations per second (Bi-CGSTAB + GMRES iterations of the step,
+         summed over ranks, / max-over-ranks device time); unit "iters/s".
+e2e    = the same through the public API with the system copied from pinned host
+         memory every step (plan rebuilt) and x read back.
+roofline: the dominant kernel (Bi-CGSTAB fused pass v = A p) — algorithmic bytes
+         12 nnz + 4(n+1) + 6*8n per launch / its CUDA-event time.
+--impl reference: the CPU oracle (oracle/) on a bounded sample of the same work.
+Multi-GPU: the north star is one GPU; --gpus N runs N independent replicas
+(weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gsk", choices=["gsk", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--N", type=int, default=None, help="override grid size (debug only)")
+    ap.add_argument("--gmres-maxit", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time-to-tol without GS / with GS(1)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(idx), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def byte_model(n, nnz):
+    BA = 12 * nnz + 4 * (n + 1)
+    return {"spmv": BA + 16 * n, "bicg_p1": BA + 48 * n, "bicg_p2": BA + 24 * n,
+            "bicg_iter": 2 * BA + 17 * 8 * n, "gs": 16 * nnz + 4 * (n + 1) + 24 * n}
+
+
+def oracle_sample(sys_, cfg, m, kb=3, kg=3):
+    """Bounded oracle sample of the step: GS(2), kb Bi-CGSTAB iterations, kg GMRES steps."""
+    import oracle
+    t = time.perf_counter()
+    vo, bo, _ = oracle.gs_scale(sys_["row_ptr"], sys_["val"], sys_["b"], 2)
+    _, _, rb = oracle.bicgstab(sys_["row_ptr"], sys_["col"], vo, bo, cfg.tol, kb)
+    _, _, rg = oracle.gmres(sys_["row_ptr"], sys_["col"], vo, bo, m, cfg.tol, kg)
+    dt = time.perf_counter() - t
+    its = rb["iterations"] + rg["iterations"]
+    return its / dt, its, dt, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = workloads.CONFIGS[args.config]
+    s = workloads.generate(args.config, N=args.N)
+    m = 30
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, its, dt, cores = oracle_sample(s, cfg, m)
+        if i >= args.warmup:
+            vals.append((v, its, dt))
+    value = float(np.mean([v for v, _, _ in vals]))
+    ms = float(np.mean([dt for _, _, dt in vals]) * 1e3)
+    sample = "GS(2) + 3 Bi-CGSTAB iterations + 3 GMRES(30) steps of the full system"
+    line = {
+        "impl": "reference", "metric": "solver iters/s (GS(2)+Bi-CGSTAB+GMRES(30) step)", "value": value,
+        "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": config_desc(args, cfg, s),
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_desc(args, cfg, s):
+    return {"workload": f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", "n": int(s["n"]),
+            "nnz": int(s["nnz"]), "grid": f"{cfg.N if args.N is None else args.N}^{3 if cfg.cfg in (3, 4) else 2}",
+            "format": "SELL-C-32-256" if cfg.sell else "CSR", "scaling": "GS(2)",
+            "solvers": ["Bi-CGSTAB", "GMRES(30)"], "tol": cfg.tol, "seed": cfg.seed,
+            "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % ((12 * s["nnz"] + 4 * s["n"]) / 1e9)}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_0812_2769_b200 as gsk
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workloads.CONFIGS[args.config]
+    m = 30
+    gmaxit = args.gmres_maxit or cfg.maxit
+    s = workloads.generate(args.config, N=args.N)
+    n, nnz = s["n"], s["nnz"]
+    A0 = gsk.CSR.from_system(s)
+    b0 = torch.tensor(s["b"], device="cuda")
+    vbuf = torch.empty_like(A0.val)
+    bbuf = torch.empty_like(b0)
+    dbuf = torch.empty_like(b0)
+    As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
+    fmt = "sell" if cfg.sell else "csr"
+    plan = gsk.Plan(As, fmt=fmt)
+    x1 = torch.empty(n, dtype=torch.float64, device="cuda")
+    x2 = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def step():
+        gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
+        plan.refresh()
+        _, _, r1 = plan.bicgstab(bbuf, tol=cfg.tol, maxit=cfg.maxit, x=x1, hist=False)
+        _, _, r2 = plan.gmres(bbuf, m=m, tol=cfg.tol, maxit=gmaxit, x=x2, hist=False)
+        return r1, r2
+
+    for _ in range(args.warmup):
+        step()
+    for k in range(4):
+        plan_probe_reset = plan.probe(k)  # noqa: F841 (probes accumulate; deltas below)
+    probes0 = [plan.probe(k) for k in range(4)]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks(local)
+    launches0 = gsk.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    reps = []
+    for _ in range(args.steps):
+        reps.append(step())
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = gsk.launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    its = sum(r1["iterations"] + r2["iterations"] for r1, r2 in reps)
+    if dist:
+        t = torch.tensor([ms, float(its)], device="cuda", dtype=torch.float64)
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms, its = float(tmax[0]), float(t[1])
+    value = its / (ms / 1e3)
+
+    # dominant kernel: per-launch time from the CUDA-event probes inside the timed steps
+    probes = []
+    for k in range(4):
+        tot, cnt = plan.probe(k)
+        t0, c0 = probes0[k]
+        dc = cnt - c0
+        probes.append(((tot * cnt - t0 * c0) / dc) if dc > 0 else None)
+    bm = byte_model(n, nnz)
+    hbm, src = peaks()
+    p1_ms = probes[0]
+    roof = None
+    if p1_ms:
+        ach = bm["bicg_p1"] / (p1_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "kernel": "fused_pass<SELL, OpP1> (v = A p, <r^,v>)",
+                "bytes_per_launch": bm["bicg_p1"], "ms_per_launch": p1_ms, "peak_source": src}
+
+    # SpMV standalone roofline (same plan, 50 back-to-back launches)
+    x = torch.tensor(workloads.uniform(n, 9, 9), device="cuda")
+    y = torch.empty_like(x)
+    for _ in range(3):
+        plan.spmv(x, y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50):
+        plan.spmv(x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    spmv_ms = e0.elapsed_time(e1) / 50
+    spmv_gbps = bm["spmv"] / (spmv_ms / 1e3) / 1e9
+
+    r1, r2 = reps[-1]
+    extra = {
+        "bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
+                     "relres": r1["relres"], "true_relres": r1["true_relres"], "solve_ms": r1["solve_ms"],
+                     "iters_per_s": r1["iterations"] / (r1["solve_ms"] / 1e3) if r1["solve_ms"] else None,
+                     "gbps_model": bm["bicg_iter"] * r1["iterations"] / (r1["solve_ms"] / 1e3) / 1e9
+                     if r1["solve_ms"] else None},
+        "gmres": {"m": m, "iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
+                  "relres": r2["relres"], "true_relres": r2["true_relres"], "solve_ms": r2["solve_ms"],
+                  "iters_per_s": r2["iterations"] / (r2["solve_ms"] / 1e3) if r2["solve_ms"] else None},
+        "spmv": {"ms": spmv_ms, "gbps": spmv_gbps, "frac_of_hbm": spmv_gbps / hbm,
+                 "frac_of_8TBps": spmv_gbps / 8000.0},
+        "probe_ms": {"bicg_p1": probes[0], "bicg_p2": probes[1], "gmres_mgs": probes[2],
+                     "gmres_arnoldi_spmv": probes[3]},
+    }
+    if roof:
+        extra["bicg_p1_frac_of_8TBps"] = roof["achieved"] / 8000.0
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, its_c, dt, cores = oracle_sample(s, cfg, m)
+        cpu = {"value": v, "unit": "iters/s", "cores": cores, "kind": "oracle",
+               "sample": f"GS(2) + 3 Bi-CGSTAB its + 3 GMRES(30) steps of {cfg.name} ({dt:.1f} s)"}
+    if args.extras and rank == 0:
+        extra["time_to_tol"] = time_to_tol(gsk, torch, s, cfg, fmt)
+
+    if rank == 0:
+        line = {
+            "metric": "solver iters/s (GS(2)+Bi-CGSTAB+GMRES(30) step, C4 256^3)", "value": value,
+            "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_desc(args, cfg, s),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args):
+    """Every step: pinned host -> device copy of the system, GS(2), plan build (SELL),
+    both solves, x read back; timed with CUDA events on the current stream."""
+    pin = {k: torch.from_numpy(np.ascontiguousarray(s[k])).pin_memory() for k in ("row_ptr", "col", "val", "b")}
+    h2d = sum(t.numel() * t.element_size() for t in pin.values())
+    n = s["n"]
+    xo1 = torch.empty(n, dtype=torch.float64).pin_memory()
+    xo2 = torch.empty(n, dtype=torch.float64).pin_memory()
+    d2h = 2 * n * 8
+
+    def step():
+        dev = {k: v.to("cuda", non_blocking=True) for k, v in pin.items()}
+        A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
+        As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
+        P = gsk.Plan(As, fmt=fmt)
+        x1, _, r1 = P.bicgstab(bs, tol=cfg.tol, maxit=cfg.maxit, hist=False)
+        x2, _, r2 = P.gmres(bs, m=m, tol=cfg.tol, maxit=gmaxit, hist=False)
+        xo1.copy_(x1, non_blocking=True)
+        xo2.copy_(x2, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        P.close()
+        return r1["iterations"] + r2["iterations"]
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its = 0
+    k = max(1, min(args.steps, 2))
+    for _ in range(k):
+        its += step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"value": its / (ms / 1e3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
+
+
+def time_to_tol(gsk, torch, s, cfg, fmt):
+    """Time to cfg.tol with and without GS (north-star metric), Bi-CGSTAB, stopping
+    measured in the GS(2) frame."""
+    out = {}
+    A0 = gsk.CSR.from_system(s)
+    _, _, d2 = gsk.gs_scale(A0, s["b"], 2)
+    for name, p in (("none", None), ("GS1", 1), ("GS2", 2)):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        A = gsk.CSR.from_system(s)
+        b = torch.tensor(s["b"], device="cuda")
+        w = d2
+        if p is not None:
+            A, b, dp = gsk.gs_scale(A, b, p, inplace=True)
+            w = None if p == 2 else d2 / dp
+        P = gsk.Plan(A, fmt=fmt, weights=w)
+        _, h, r = P.bicgstab(b, tol=cfg.tol, maxit=cfg.maxit)
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = {"ms": e0.elapsed_time(e1), "iterations": r["iterations"],
+                     "status": gsk.STATUS[r["status"]], "best_relres": r["best_relres"]}
+        P.close()
+    return out
+
+
+if __name__ == "__main__":
+    main()

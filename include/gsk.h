@@ -1,0 +1,145 @@
+/* gsk.h — C-ABI of libgsk.so: geometric scaling GS(p) + Krylov solvers on one B200.
+ *
+ * Paper: Gordon & Gordon, "Geometric scaling: a simple preconditioner for certain
+ * linear systems with discontinuous coefficients", arXiv 0812.2769.
+ *
+ * Conventions (all entry points)
+ *  - Array arguments are DEVICE pointers unless marked [host].  The caller owns
+ *    every buffer it passes; the library owns only its internal workspace (held
+ *    by a gsk_plan, or allocated and freed inside a plan-less call).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Work is ordered after prior work on `stream`; every call returns only after
+ *    its results are complete and visible on `stream` (status, iteration counts and
+ *    the report are needed on the host).
+ *  - Indices are 0-based int32: 1 <= n, nnz < 2^31.  CSR rows must have strictly
+ *    increasing column indices in [0, n) (the order in which a row is summed).
+ *  - Negative return = API error (gsk_last_error() has a message); 0 = GSK_OK.
+ *    Non-convergence of a solver is NOT an error: it is reported in
+ *    gsk_report.status.
+ *  - Arithmetic: IEEE binary64 under the arithmetic contract of DESIGN.md §4
+ *    (explicit FMAs, canonical pairwise-tree reductions); results are
+ *    deterministic and bit-identical run to run.
+ */
+#ifndef GSK_H
+#define GSK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* A square sparse matrix in CSR form (the paper's A in Eq. (1)). */
+typedef struct gsk_csr {
+  int32_t n;                /* rows = columns                                      */
+  int32_t nnz;              /* stored entries = row_ptr[n]                          */
+  const int32_t *row_ptr;   /* [n+1] device; row_ptr[0] = 0, nondecreasing          */
+  const int32_t *col_idx;   /* [nnz] device; strictly increasing within each row    */
+  double *values;           /* [nnz] device; a_ij                                   */
+} gsk_csr;
+
+enum { GSK_OK = 0, GSK_E_INVALID = -1, GSK_E_ZERO_ROW = -2, GSK_E_CUDA = -3, GSK_E_NOMEM = -4 };
+enum { GSK_CONVERGED = 0, GSK_MAXIT = 1, GSK_BREAKDOWN = 2, GSK_DIVERGED = 3 };
+enum { GSK_FMT_CSR = 0, GSK_FMT_SELL = 1 };
+
+/* [host] Outcome of a solve.
+ *  history_len = iterations + 1; hist[0] = 1 (0 if the initial residual is 0).
+ *  relres      = hist[history_len-1]: the solver's own residual estimate
+ *                (Bi-CGSTAB: recursive ||r_i||/||r_0||, or ||s||/||r_0|| on the
+ *                half-step exit; GMRES: least-squares estimate |g_{j+1}|/||r_0||).
+ *  true_relres = ||b - A x|| / ||b - A x0|| recomputed after the solve (one extra
+ *                SpMV) in the solved frame; true_relres_w the same with the
+ *                stopping-frame weights of the plan (== true_relres if none).
+ *  breakdown_at = iteration whose breakdown test fired (0 if none).
+ *  solve_ms    = device time of the solve (CUDA events on the library stream). */
+typedef struct gsk_report {
+  int32_t status, iterations, restarts, history_len, breakdown_at, pad_;
+  double relres, true_relres, true_relres_w, best_relres;
+  double solve_ms;
+} gsk_report;
+
+/* Plan options.  format: GSK_FMT_CSR or GSK_FMT_SELL (SELL-C-sigma, C = 32,
+ * sigma = 256, built on the device from the CSR at plan creation).
+ * weights: NULL, or DEVICE [n] w_i > 0.  When set, Bi-CGSTAB's stopping test and
+ * history use ||w o r|| / ||w o r0|| — the paper measures the relative residual on
+ * the GS(2)-scaled system, i.e. w = d_GS(2) / d_applied.
+ * poll: iterations per device-resident batch between host checks (0 = auto). */
+typedef struct gsk_opts {
+  int32_t format;
+  int32_t poll;
+  const double *weights;
+} gsk_opts;
+
+typedef struct gsk_plan gsk_plan;
+
+/* GS(p), PAPER.md:92-97 and Eq. (2) PAPER.md:207-214:
+ *   d_i = 1 / ||a_i||_p,  values_out = D A (same pattern),  b_out = D b.
+ * ||a_i||_p = (sum_j |a_ij|^p)^(1/p) (PAPER.md:193-196 with |.|).  p >= 1.
+ * values_out may equal A->values (in place); b_out may equal b; b/b_out and d_out
+ * may be NULL.  One pass over the nnz (one warp-cooperative row-segment pass).
+ * Errors: GSK_E_INVALID (p < 1, bad sizes/pointers); GSK_E_ZERO_ROW if some row has
+ * zero norm (the paper assumes none): *bad_row [host, nullable]
+ * receives the smallest such row, its d_i is 0 and its values stay 0; every other
+ * row is scaled. */
+int gsk_gs_scale(const gsk_csr *A, const double *b, int p, double *values_out,
+                 double *b_out, double *d_out, int32_t *bad_row, void *stream);
+
+/* y = A x (SPEC sparse-core spmv): y_i = sum_k val_k x_col_k, k ascending, one
+ * fused multiply-add per entry from +0.  x and y must not overlap. */
+int gsk_spmv(const gsk_csr *A, const double *x, double *y, void *stream);
+
+/* [host] *result = <a, b> under the canonical pairwise tree. */
+int gsk_dot(int64_t n, const double *a, const double *b, double *result, void *stream);
+
+/* Plans: keep the SELL build, workspace and captured CUDA graphs out of repeated
+ * solves.  The plan keeps A's pointers (not a copy) for CSR; for SELL it copies the
+ * values, so rescaling A after gsk_plan_create needs gsk_plan_refresh. */
+int gsk_plan_create(const gsk_csr *A, const gsk_opts *opts, gsk_plan **plan, void *stream);
+int gsk_plan_refresh(gsk_plan *plan, void *stream);
+int gsk_plan_spmv(gsk_plan *plan, const double *x, double *y, void *stream);
+/* SELL layout sizes / copy-out (integer parity tests).  chunk arrays have
+ * nchunks = ceil(n/32) (+1 for chunk_ptr), slot arrays nslots, roff nchunks*32. */
+int gsk_plan_sell_info(gsk_plan *plan, int64_t *nchunks, int64_t *nslots);
+int gsk_plan_sell_copy(gsk_plan *plan, int32_t *chunk_ptr, int32_t *chunk_len,
+                       int32_t *scol, double *sval, uint8_t *roff, void *stream);
+void gsk_plan_destroy(gsk_plan *plan);
+
+/* Bi-CGSTAB (van der Vorst 1992) on A x = b.
+ *   x0: DEVICE [n] or NULL (= 0).  x: DEVICE [n] output (may
+ *   alias x0).  tol > 0: stop when hist[i] < tol.  maxit >= 1
+ *   (PAPER.md:308-309 uses 10,000).  hist: [host] [maxit+1] or NULL.
+ *   Breakdown = exact zero of rho, <r0^,v>, <t,t> or omega.
+ *   The plan-less form runs on CSR with no frame weights. */
+int gsk_bicgstab_solve(const gsk_csr *A, const double *b, const double *x0, double tol,
+                       int maxit, double *x, double *hist, gsk_report *rep, void *stream);
+int gsk_bicgstab_solve_plan(gsk_plan *plan, const double *b, const double *x0, double tol,
+                            int maxit, double *x, double *hist, gsk_report *rep, void *stream);
+
+/* Restarted GMRES(m) (Saad & Schultz 1986) with modified
+ * Gram-Schmidt Arnoldi and Givens least squares.  1 <= m <= 128.  Iterations count
+ * Arnoldi steps; hist[it] = |g_{j+1}| / ||r0||.  Other arguments as Bi-CGSTAB. */
+int gsk_gmres_solve(const gsk_csr *A, const double *b, const double *x0, int m, double tol,
+                    int maxit, double *x, double *hist, gsk_report *rep, void *stream);
+int gsk_gmres_solve_plan(gsk_plan *plan, const double *b, const double *x0, int m, double tol,
+                         int maxit, double *x, double *hist, gsk_report *rep, void *stream);
+
+/* ||w o (b - A x)||_2 under the canonical tree (w DEVICE [n] or NULL). [host] *result. */
+int gsk_plan_residual_norm(gsk_plan *plan, const double *b, const double *x, const double *w,
+                           double *result, void *stream);
+
+/* Kernel timing probe for the roofline report: average device time (ms) of the
+ * dominant kernel family of the last solve on this plan, sampled with CUDA events
+ * around one launch per captured batch.  kind: 0 = Bi-CGSTAB fused SpMV pass
+ * (v = A p), 1 = Bi-CGSTAB fused SpMV pass (t = A s), 2 = GMRES MGS projection
+ * pass.  Returns samples in *count. */
+int gsk_plan_probe(gsk_plan *plan, int kind, double *avg_ms, int64_t *count);
+
+/* Diagnostics. */
+const char *gsk_last_error(void);
+int64_t gsk_launch_count(void);   /* kernels launched by this library so far */
+int gsk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSK_H */

@@ -61,30 +61,42 @@ static double tree_sum(std::vector<double>& q, int64_t n) {
   for (int64_t i = n; i < L; ++i) q[i] = 0.0;
   // one tree level at a time: out[i] = in[2i] + in[2i+1] (separate buffers, so
   // splitting a level across threads cannot change any value)
-  std::vector<double> nxt(L / 2 > 0 ? L / 2 : 1);
+  static thread_local std::vector<double> nxt;
+  nxt.resize(L / 2 > 0 ? L / 2 : 1);
+  double* in = q.data();
+  double* out = nxt.data();
   for (int64_t len = L; len > 1; len >>= 1) {
     #pragma omp parallel for schedule(static) if (len > 65536)
-    for (int64_t i = 0; i < len / 2; ++i) nxt[i] = q[2 * i] + q[2 * i + 1];
-    std::copy(nxt.begin(), nxt.begin() + len / 2, q.begin());
+    for (int64_t i = 0; i < len / 2; ++i) out[i] = in[2 * i] + in[2 * i + 1];
+    std::copy(out, out + len / 2, in);
   }
   return q[0] + 0.0;
 }
 
+// products buffer reused across calls (allocation only; no arithmetic involved)
+static std::vector<double>& leaves(int64_t n) {
+  static thread_local std::vector<double> q;
+  q.assign(n > 0 ? n : 1, 0.0);
+  return q;
+}
+
 // <a, b> under AC-5.
 double orc_dot(int64_t n, const double* a, const double* b) {
-  std::vector<double> q(n > 0 ? n : 1);
+  std::vector<double>& q = leaves(n);
+  double* qp = q.data();
   #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < n; ++i) q[i] = a[i] * b[i];
+  for (int64_t i = 0; i < n; ++i) qp[i] = a[i] * b[i];
   return tree_sum(q, n);
 }
 
 // sum_i (w_i a_i)^2 under AC-5 (w null: plain <a,a>).
 double orc_wnorm2(int64_t n, const double* a, const double* w) {
-  std::vector<double> q(n > 0 ? n : 1);
+  std::vector<double>& q = leaves(n);
+  double* qp = q.data();
   #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
     double u = w ? w[i] * a[i] : a[i];
-    q[i] = u * u;
+    qp[i] = u * u;
   }
   return tree_sum(q, n);
 }

@@ -1,0 +1,12 @@
+"""paper_0812_2769_b200 — geometric scaling GS(p) + Bi-CGSTAB / GMRES(m) on one B200.
+
+Gordon & Gordon, "Geometric scaling: a simple preconditioner for certain linear
+systems with discontinuous coefficients" (arXiv 0812.2769).  The hot path runs in
+hand-written sm_100a kernels behind the C-ABI of ``libgsk.so`` (include/gsk.h);
+this package is the thin ctypes binding (argument marshalling only).
+"""
+from ._gsk import (CSR, Plan, GskError, STATUS, SYMBOLS, LIB_PATH, bicgstab_solve, dot,  # noqa: F401
+                   gmres_solve, gs_scale, launch_count, load, spmv)
+
+__all__ = ["CSR", "Plan", "GskError", "STATUS", "SYMBOLS", "LIB_PATH", "bicgstab_solve", "dot",
+           "gmres_solve", "gs_scale", "launch_count", "load", "spmv"]

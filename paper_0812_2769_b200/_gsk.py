@@ -1,0 +1,299 @@
+"""ctypes binding of libgsk.so (include/gsk.h): argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels; PyTorch provides
+device memory and the current stream.  There is no CPU fallback: if the in-tree
+``libgsk.so`` is missing or CUDA is unavailable, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsk.so")
+
+GSK_OK, GSK_E_INVALID, GSK_E_ZERO_ROW, GSK_E_CUDA, GSK_E_NOMEM = 0, -1, -2, -3, -4
+STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}
+FMT = {"csr": 0, "sell": 1}
+
+# exported symbols (include/gsk.h); tests check the library exports all of them
+SYMBOLS = ("gsk_gs_scale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
+           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_destroy",
+           "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
+           "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
+           "gsk_last_error", "gsk_launch_count", "gsk_version")
+
+
+class CsrStruct(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("nnz", ctypes.c_int32), ("row_ptr", ctypes.c_void_p),
+                ("col_idx", ctypes.c_void_p), ("values", ctypes.c_void_p)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("restarts", ctypes.c_int32), ("history_len", ctypes.c_int32),
+                ("breakdown_at", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("relres", ctypes.c_double), ("true_relres", ctypes.c_double),
+                ("true_relres_w", ctypes.c_double), ("best_relres", ctypes.c_double),
+                ("solve_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("poll", ctypes.c_int32), ("weights", ctypes.c_void_p)]
+
+
+class GskError(RuntimeError):
+    def __init__(self, code, msg, bad_row=None):
+        super().__init__(f"gsk error {code}: {msg}")
+        self.code = code
+        self.bad_row = bad_row
+
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libgsk.so (raises if it is missing: no fallback path exists)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `make` or __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    P = ctypes.POINTER
+    lib.gsk_gs_scale.argtypes = [P(CsrStruct), vp, i32, vp, vp, vp, P(ctypes.c_int32), vp]
+    lib.gsk_spmv.argtypes = [P(CsrStruct), vp, vp, vp]
+    lib.gsk_dot.argtypes = [i64, vp, vp, P(d), vp]
+    lib.gsk_plan_create.argtypes = [P(CsrStruct), P(Opts), P(vp), vp]
+    lib.gsk_plan_refresh.argtypes = [vp, vp]
+    lib.gsk_plan_spmv.argtypes = [vp, vp, vp, vp]
+    lib.gsk_plan_sell_info.argtypes = [vp, P(i64), P(i64)]
+    lib.gsk_plan_sell_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    lib.gsk_plan_destroy.argtypes = [vp]
+    lib.gsk_plan_destroy.restype = None
+    lib.gsk_bicgstab_solve.argtypes = [P(CsrStruct), vp, vp, d, i32, vp, vp, P(Report), vp]
+    lib.gsk_bicgstab_solve_plan.argtypes = [vp, vp, vp, d, i32, vp, vp, P(Report), vp]
+    lib.gsk_gmres_solve.argtypes = [P(CsrStruct), vp, vp, i32, d, i32, vp, vp, P(Report), vp]
+    lib.gsk_gmres_solve_plan.argtypes = [vp, vp, vp, i32, d, i32, vp, vp, P(Report), vp]
+    lib.gsk_plan_residual_norm.argtypes = [vp, vp, vp, vp, P(d), vp]
+    lib.gsk_plan_probe.argtypes = [vp, i32, P(d), P(i64)]
+    lib.gsk_last_error.restype = ctypes.c_char_p
+    lib.gsk_launch_count.restype = i64
+    for name in SYMBOLS:
+        if name not in ("gsk_last_error", "gsk_launch_count", "gsk_plan_destroy"):
+            getattr(lib, name).restype = ctypes.c_int
+    _LIB = lib
+    return lib
+
+
+def _check(rc, bad_row=None):
+    if rc != GSK_OK:
+        msg = load().gsk_last_error().decode(errors="replace")
+        raise GskError(rc, msg, bad_row)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dev_f64(t, n=None):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(np.ascontiguousarray(t, dtype=np.float64))
+    t = t.to(device="cuda", dtype=torch.float64).contiguous()
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} entries, got {t.numel()}")
+    return t
+
+
+def _dev_i32(t):
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(np.ascontiguousarray(t, dtype=np.int32))
+    return t.to(device="cuda", dtype=torch.int32).contiguous()
+
+
+class CSR:
+    """A CSR matrix resident on the GPU (int32 indices, fp64 values)."""
+
+    def __init__(self, row_ptr, col, val):
+        if not torch.cuda.is_available():
+            raise RuntimeError("CUDA device required (no CPU fallback)")
+        self.row_ptr = _dev_i32(row_ptr)
+        self.col = _dev_i32(col)
+        self.val = _dev_f64(val)
+        self.n = self.row_ptr.numel() - 1
+        self.nnz = self.col.numel()
+        if self.val.numel() != self.nnz:
+            raise ValueError("col / val size mismatch")
+
+    @classmethod
+    def from_system(cls, s: dict):
+        return cls(s["row_ptr"], s["col"], s["val"])
+
+    def struct(self, values=None) -> CsrStruct:
+        v = self.val if values is None else values
+        return CsrStruct(self.n, self.nnz, self.row_ptr.data_ptr(), self.col.data_ptr(), v.data_ptr())
+
+
+def gs_scale(A: CSR, b=None, p: int = 2, inplace: bool = False, out=None):
+    """GS(p) (Eq. (2)): returns (A', b', d) with A' = D A, b' = D b.
+    ``out=(values, b, d)`` writes into preallocated device tensors."""
+    lib = load()
+    b = _dev_f64(b, A.n)
+    if out is not None:
+        vout, bout, d = out
+    else:
+        vout = A.val if inplace else torch.empty_like(A.val)
+        bout = None if b is None else (b if inplace else torch.empty_like(b))
+        d = torch.empty(A.n, dtype=torch.float64, device="cuda")
+    bad = ctypes.c_int32(-1)
+    rc = lib.gsk_gs_scale(ctypes.byref(A.struct()), _ptr(b), int(p), _ptr(vout), _ptr(bout), _ptr(d),
+                          ctypes.byref(bad), _stream())
+    _check(rc, bad.value if rc == GSK_E_ZERO_ROW else None)
+    As = A if (inplace and out is None) else CSR.__new__(CSR)
+    if As is not A:
+        As.row_ptr, As.col, As.val, As.n, As.nnz = A.row_ptr, A.col, vout, A.n, A.nnz
+    return As, bout, d
+
+
+def spmv(A: CSR, x):
+    x = _dev_f64(x, A.n)
+    y = torch.empty_like(x)
+    _check(load().gsk_spmv(ctypes.byref(A.struct()), _ptr(x), _ptr(y), _stream()))
+    return y
+
+
+def dot(a, b) -> float:
+    a, b = _dev_f64(a), _dev_f64(b)
+    out = ctypes.c_double()
+    _check(load().gsk_dot(a.numel(), _ptr(a), _ptr(b), ctypes.byref(out), _stream()))
+    return out.value
+
+
+def launch_count() -> int:
+    return int(load().gsk_launch_count())
+
+
+class Plan:
+    """gsk_plan: SELL build, workspace and captured graphs reused across solves."""
+
+    def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0):
+        lib = load()
+        self.A = A
+        self.weights = _dev_f64(weights, A.n)
+        opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr())
+        self._csr = A.struct()
+        h = ctypes.c_void_p()
+        _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))
+        self.h = h
+        self.fmt = fmt
+
+    def close(self):
+        if getattr(self, "h", None):
+            load().gsk_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def refresh(self):
+        _check(load().gsk_plan_refresh(self.h, _stream()))
+
+    def spmv(self, x, y=None):
+        x = _dev_f64(x, self.A.n)
+        y = torch.empty_like(x) if y is None else y
+        _check(load().gsk_plan_spmv(self.h, _ptr(x), _ptr(y), _stream()))
+        return y
+
+    def residual_norm(self, b, x, w=None) -> float:
+        out = ctypes.c_double()
+        b, x, w = _dev_f64(b, self.A.n), _dev_f64(x, self.A.n), _dev_f64(w, self.A.n)
+        _check(load().gsk_plan_residual_norm(self.h, _ptr(b), _ptr(x), _ptr(w), ctypes.byref(out), _stream()))
+        return out.value
+
+    def sell_arrays(self):
+        lib = load()
+        nch, nsl = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.gsk_plan_sell_info(self.h, ctypes.byref(nch), ctypes.byref(nsl)))
+        dev = "cuda"
+        out = {"chunk_ptr": torch.empty(nch.value + 1, dtype=torch.int32, device=dev),
+               "chunk_len": torch.empty(nch.value, dtype=torch.int32, device=dev),
+               "scol": torch.empty(max(nsl.value, 1), dtype=torch.int32, device=dev),
+               "sval": torch.empty(max(nsl.value, 1), dtype=torch.float64, device=dev),
+               "roff": torch.empty(nch.value * 32, dtype=torch.uint8, device=dev)}
+        _check(lib.gsk_plan_sell_copy(self.h, *(_ptr(out[k]) for k in
+                                                ("chunk_ptr", "chunk_len", "scol", "sval", "roff")), _stream()))
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res["scol"] = res["scol"][:nsl.value]
+        res["sval"] = res["sval"][:nsl.value]
+        return res
+
+    def probe(self, kind: int):
+        ms, cnt = ctypes.c_double(), ctypes.c_int64()
+        _check(load().gsk_plan_probe(self.h, kind, ctypes.byref(ms), ctypes.byref(cnt)))
+        return ms.value, cnt.value
+
+    def _solve(self, which, b, x0, tol, maxit, m=None, x=None, hist=True):
+        lib = load()
+        b = _dev_f64(b, self.A.n)
+        x0 = _dev_f64(x0, self.A.n)
+        x = torch.empty(self.A.n, dtype=torch.float64, device="cuda") if x is None else x
+        H = np.empty(maxit + 1, np.float64) if hist else None
+        rep = Report()
+        hp = None if H is None else H.ctypes.data_as(ctypes.c_void_p)
+        if which == "bicgstab":
+            rc = lib.gsk_bicgstab_solve_plan(self.h, _ptr(b), _ptr(x0), float(tol), int(maxit), _ptr(x),
+                                             hp, ctypes.byref(rep), _stream())
+        else:
+            rc = lib.gsk_gmres_solve_plan(self.h, _ptr(b), _ptr(x0), int(m), float(tol), int(maxit), _ptr(x),
+                                          hp, ctypes.byref(rep), _stream())
+        _check(rc)
+        r = rep.as_dict()
+        return x, (None if H is None else H[:rep.history_len].copy()), r
+
+    def bicgstab(self, b, x0=None, tol=1e-8, maxit=10000, x=None, hist=True):
+        """Bi-CGSTAB on the plan's system; returns (x, hist, report)."""
+        return self._solve("bicgstab", b, x0, tol, maxit, x=x, hist=hist)
+
+    def gmres(self, b, x0=None, m=30, tol=1e-8, maxit=10000, x=None, hist=True):
+        """Restarted GMRES(m) on the plan's system; returns (x, hist, report)."""
+        return self._solve("gmres", b, x0, tol, maxit, m=m, x=x, hist=hist)
+
+
+def bicgstab_solve(A: CSR, b, x0=None, tol=1e-8, maxit=10000):
+    """bicgstab_solve(csr, b, x0, tol, maxit) of the north star (plan-less, CSR)."""
+    lib = load()
+    b, x0 = _dev_f64(b, A.n), _dev_f64(x0, A.n)
+    x = torch.empty(A.n, dtype=torch.float64, device="cuda")
+    H = np.empty(maxit + 1, np.float64)
+    rep = Report()
+    _check(lib.gsk_bicgstab_solve(ctypes.byref(A.struct()), _ptr(b), _ptr(x0), float(tol), int(maxit),
+                                  _ptr(x), H.ctypes.data_as(ctypes.c_void_p), ctypes.byref(rep), _stream()))
+    return x, H[:rep.history_len].copy(), rep.as_dict()
+
+
+def gmres_solve(A: CSR, b, x0=None, m=30, tol=1e-8, maxit=10000):
+    """gmres_solve(csr, b, x0, m, tol, maxit) of the north star (plan-less, CSR)."""
+    lib = load()
+    b, x0 = _dev_f64(b, A.n), _dev_f64(x0, A.n)
+    x = torch.empty(A.n, dtype=torch.float64, device="cuda")
+    H = np.empty(maxit + 1, np.float64)
+    rep = Report()
+    _check(lib.gsk_gmres_solve(ctypes.byref(A.struct()), _ptr(b), _ptr(x0), int(m), float(tol), int(maxit),
+                               _ptr(x), H.ctypes.data_as(ctypes.c_void_p), ctypes.byref(rep), _stream()))
+    return x, H[:rep.history_len].copy(), rep.as_dict()

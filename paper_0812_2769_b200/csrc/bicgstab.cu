@@ -1,0 +1,422 @@
+// bicgstab.cu — Bi-CGSTAB (van der Vorst 1992) as three
+// fused device passes per iteration with device-resident scalars:
+//
+//   P1  p = r + beta (p_old - omega v_old)  recomputed at every gathered column,
+//       v = A p,   sigma = <r^, v>          -> alpha = rho / sigma
+//   P2  s = r - alpha v  recomputed at every gathered column,
+//       t = A s,   <t,s>, <t,t>, ||s||_w^2  -> half-step exit or omega = <t,s>/<t,t>
+//   P3  x += alpha p + omega s,  r = s - omega t,  <r^, r>, ||r||_w^2
+//       -> history, stopping test, breakdown tests
+//          (PAPER.md:315-321), rho, beta
+//
+// p and v are double-buffered (the pass that writes p_new/v_new still gathers
+// p_old/v_old at neighbouring columns).  Recomputing p and s at the gather is the
+// same operation on the same operands as the stored value, so results are
+// bit-identical to the unfused algorithm (AC-6) while moving 2 B_A + 17 vectors
+// per iteration instead of 2 B_A + 19+.  Each pass ends in the canonical grid
+// reduction; the last CTA runs the scalar epilogue, so iterations run back to back
+// from a captured CUDA graph (poll iterations per replay) with one host check of
+// the `done` flag per replay.
+#include <cmath>
+#include <vector>
+#include "internal.cuh"
+
+namespace gsk {
+
+struct OpInit {  // r = b - A x; r^ = r; p_old = v_old = 0
+  static constexpr int D = 2;
+  static constexpr bool kSpmv = true;
+  const double* x;
+  const double* b;
+  const double* w;
+  double *r, *rh, *pa, *va, *hist;
+  BicgState* st;
+  __device__ bool begin() { return true; }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int i, double y, double (&c)[2]) const {
+    const double ri = b[i] - y;
+    r[i] = ri;
+    rh[i] = ri;
+    pa[i] = 0.0;
+    va[i] = 0.0;
+    const double u = w ? w[i] * ri : ri;
+    c[0] = u * u;
+    c[1] = ri * ri;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const {
+    if (lane) return;
+    const double n0 = sqrt(s[0]);
+    st->n0 = n0;
+    st->n0u = sqrt(s[1]);
+    hist[0] = n0 == 0.0 ? 0.0 : 1.0;
+    st->hist_len = 1;
+    st->iter = 1;
+    st->rho_prev = 1.0;
+    st->alpha = 1.0;
+    st->omega = 1.0;
+    st->status = GSK_MAXIT;
+    st->bd = 0;
+    st->halfstep = 0;
+    st->done = 0;
+    if (n0 == 0.0) {
+      st->status = GSK_CONVERGED;
+      st->done = 1;
+      return;
+    }
+    const double rho = s[1];  // <r^, r> = <r, r>: the same leaves in the same tree
+    st->rho = rho;
+    if (rho == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = 1;
+      st->done = 1;
+      return;
+    }
+    st->beta = (rho / st->rho_prev) * (st->alpha / st->omega);
+  }
+};
+
+struct OpP1 {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = true;
+  const double *r, *po, *vo, *rh;
+  double *pn, *vn;
+  BicgState* st;
+  double beta, momega;
+  __device__ bool begin() {
+    if (st->done) return false;
+    beta = st->beta;
+    momega = -st->omega;
+    return true;
+  }
+  __device__ __forceinline__ double pval(int c) const {
+    return __fma_rn(beta, __fma_rn(momega, __ldg(vo + c), __ldg(po + c)), __ldg(r + c));
+  }
+  __device__ double gather(int c) const { return pval(c); }
+  __device__ void row(int i, double y, double (&c)[1]) const {
+    pn[i] = pval(i);
+    vn[i] = y;
+    c[0] = rh[i] * y;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane) return;
+    const double sigma = s[0];
+    if (sigma == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = st->iter;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / sigma;
+  }
+};
+
+struct OpP2 {
+  static constexpr int D = 3;
+  static constexpr bool kSpmv = true;
+  const double *r, *vn, *w;
+  double *t, *hist;
+  BicgState* st;
+  double malpha;
+  __device__ bool begin() {
+    if (st->done) return false;
+    malpha = -st->alpha;
+    return true;
+  }
+  __device__ __forceinline__ double sval(int c) const { return __fma_rn(malpha, __ldg(vn + c), __ldg(r + c)); }
+  __device__ double gather(int c) const { return sval(c); }
+  __device__ void row(int i, double y, double (&c)[3]) const {
+    const double s = sval(i);
+    t[i] = y;
+    c[0] = y * s;
+    c[1] = y * y;
+    const double u = w ? w[i] * s : s;
+    c[2] = u * u;
+  }
+  __device__ void finish(const double (&s)[3], int lane) const {
+    if (lane) return;
+    const int i = st->iter;
+    const double sn = sqrt(s[2]) / st->n0;
+    if (sn < st->tol) {  // half-step exit (reading B4): x += alpha p in P3
+      hist[i] = sn;
+      st->hist_len = i + 1;
+      st->status = GSK_CONVERGED;
+      st->halfstep = 1;
+      st->done = 1;
+      return;
+    }
+    if (s[1] == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = i;
+      st->done = 1;
+      return;
+    }
+    st->omega = s[0] / s[1];
+  }
+};
+
+struct OpP3 {
+  static constexpr int D = 2;
+  static constexpr bool kSpmv = false;
+  const double *vn, *pn, *t, *rh, *w;
+  double *x, *r, *hist;
+  BicgState* st;
+  double alpha, malpha, omega, momega;
+  int half;
+  __device__ bool begin() {
+    half = st->halfstep;
+    if (st->done && !half) return false;
+    alpha = st->alpha;
+    malpha = -alpha;
+    omega = st->omega;
+    momega = -omega;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int i, double, double (&c)[2]) const {
+    if (half) {
+      x[i] = __fma_rn(alpha, pn[i], x[i]);
+      c[0] = 0.0;
+      c[1] = 0.0;
+      return;
+    }
+    const double s = __fma_rn(malpha, vn[i], r[i]);
+    x[i] = __fma_rn(omega, s, __fma_rn(alpha, pn[i], x[i]));
+    const double rr = __fma_rn(momega, t[i], s);
+    r[i] = rr;
+    c[0] = rh[i] * rr;
+    const double u = w ? w[i] * rr : rr;
+    c[1] = u * u;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const {
+    if (lane) return;
+    if (half) {
+      st->halfstep = 0;
+      return;
+    }
+    const int i = st->iter;
+    const double rho_prev = st->rho;
+    st->rho_prev = rho_prev;
+    const double rn = sqrt(s[1]) / st->n0;
+    hist[i] = rn;
+    st->hist_len = i + 1;
+    if (!isfinite(rn)) {
+      st->status = GSK_DIVERGED;
+      st->done = 1;
+    } else if (rn < st->tol) {
+      st->status = GSK_CONVERGED;
+      st->done = 1;
+    } else if (omega == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = i;
+      st->done = 1;
+    } else if (i == st->maxit) {
+      st->status = GSK_MAXIT;
+      st->done = 1;
+    } else {
+      const double rho = s[0];
+      st->rho = rho;
+      if (rho == 0.0) {
+        st->status = GSK_BREAKDOWN;
+        st->bd = i + 1;
+        st->done = 1;
+      } else {
+        st->beta = (rho / rho_prev) * (alpha / omega);
+        st->iter = i + 1;
+      }
+    }
+  }
+};
+
+struct OpFinal {  // true residual ||b - A x|| (unweighted and weighted)
+  static constexpr int D = 2;
+  static constexpr bool kSpmv = true;
+  const double *x, *b, *w;
+  BicgState* st;
+  __device__ bool begin() { return true; }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int i, double y, double (&c)[2]) const {
+    const double ri = b[i] - y;
+    c[0] = ri * ri;
+    const double u = w ? w[i] * ri : ri;
+    c[1] = u * u;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const {
+    if (lane) return;
+    st->true_rel = st->n0u == 0.0 ? 0.0 : sqrt(s[0]) / st->n0u;
+    st->true_rel_w = st->n0 == 0.0 ? 0.0 : sqrt(s[1]) / st->n0;
+  }
+};
+
+static int batch_size(const gsk_plan* P) {
+  int K = P->poll;
+  if (K <= 0) {
+    const long long n = P->A.n;
+    K = (int)std::min<long long>(64, std::max<long long>(2, (1LL << 23) / n));
+  }
+  return (K + 1) & ~1;  // even: p/v buffer parity repeats per replay
+}
+
+static int capture_bicg(gsk_plan* P, const double* b, double* x, int K, int copy, cudaGraphExec_t* out) {
+  const int n = P->A.n;
+  double* V = P->bvec;
+  double *r = V, *rh = V + (size_t)n, *pa = V + 2 * (size_t)n, *pb = V + 3 * (size_t)n,
+         *va = V + 4 * (size_t)n, *vb = V + 5 * (size_t)n, *t = V + 6 * (size_t)n;
+  const double* w = P->weights;
+  cudaStream_t s = P->st;
+  GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = GSK_OK;
+  for (int k = 0; k < K && rc == GSK_OK; ++k) {
+    double *po = (k & 1) ? pb : pa, *vo = (k & 1) ? vb : va;
+    double *pn = (k & 1) ? pa : pb, *vn = (k & 1) ? va : vb;
+    OpP1 p1{r, po, vo, rh, pn, vn, P->bstate, 0, 0};
+    OpP2 p2{r, vn, w, t, P->hist_d, P->bstate, 0};
+    OpP3 p3{vn, pn, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0, 0, 0};
+    if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[0][copy][0], s, cudaEventRecordExternal));
+    rc = run_pass(P, p1, 1, s);
+    if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[0][copy][1], s, cudaEventRecordExternal));
+    if (rc == GSK_OK) {
+      if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[1][copy][0], s, cudaEventRecordExternal));
+      rc = run_pass(P, p2, 2, s);
+      if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[1][copy][1], s, cudaEventRecordExternal));
+    }
+    if (rc == GSK_OK) rc = run_pass(P, p3, 3, s);
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (rc != GSK_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) {
+    set_error("bicgstab graph capture: %s", cudaGetErrorString(e));
+    return GSK_E_CUDA;
+  }
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    set_error("bicgstab graph instantiate: %s", cudaGetErrorString(e));
+    return GSK_E_CUDA;
+  }
+  // the launches recorded during capture are counted per replay instead
+  g_launches.fetch_sub(3LL * K);
+  return GSK_OK;
+}
+
+static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double tol, int maxit,
+                        double* x, double* hist, gsk_report* rep, cudaStream_t caller) {
+  if (!b || !x || !rep || !(tol > 0) || maxit < 1) {
+    set_error("bicgstab: invalid arguments (b, x, rep non-null; tol > 0; maxit >= 1)");
+    return GSK_E_INVALID;
+  }
+  const int n = P->A.n;
+  if (!P->bvec) GSK_CUDA(cudaMalloc(&P->bvec, sizeof(double) * 7 * (size_t)n));
+  if (!P->bstate) GSK_CUDA(cudaMalloc(&P->bstate, sizeof(BicgState)));
+  GSK_TRY(ensure_hist(P, maxit));
+  const int K = batch_size(P);
+  if (!P->bgraph[0] || P->bkey_b != b || P->bkey_x != x || P->bK != K || P->bkey_h != P->hist_d) {
+    for (auto& g : P->bgraph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+    GSK_TRY(capture_bicg(P, b, x, K, 0, &P->bgraph[0]));
+    GSK_TRY(capture_bicg(P, b, x, K, 1, &P->bgraph[1]));
+    P->bkey_b = b;
+    P->bkey_x = x;
+    P->bK = K;
+    P->bkey_h = P->hist_d;
+  }
+  cudaStream_t s = P->st;
+  GSK_TRY(join_in(P, caller));
+  GSK_CUDA(cudaEventRecord(P->t0, s));
+  if (x0) {
+    if (x0 != x) GSK_CUDA(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    GSK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  }
+  BicgState h{};
+  h.tol = tol;
+  h.maxit = maxit;
+  GSK_CUDA(cudaMemcpyAsync(P->bstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  double* V = P->bvec;
+  OpInit init{x, b, P->weights, V, V + (size_t)n, V + 2 * (size_t)n, V + 4 * (size_t)n, P->hist_d, P->bstate};
+  GSK_TRY(run_pass(P, init, 0, s));
+  // batches of K iterations; the next batch is queued before the flag of the
+  // previous one is read, so the GPU never idles on the host check
+  const long long maxb = (maxit + K - 1) / K + 1;
+  long long nb = 0;
+  GSK_CUDA(cudaGraphLaunch(P->bgraph[0], s));
+  g_launches.fetch_add(3LL * K);
+  ++nb;
+  cudaEvent_t ev;
+  GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  for (;;) {
+    const int copy = (int)((nb - 1) & 1);
+    GSK_CUDA(cudaMemcpyAsync(P->h_flag, &P->bstate->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaEventRecord(ev, s));
+    const bool more = nb < maxb;
+    if (more) {
+      GSK_CUDA(cudaGraphLaunch(P->bgraph[nb & 1], s));
+      g_launches.fetch_add(3LL * K);
+      ++nb;
+    }
+    GSK_CUDA(cudaEventSynchronize(ev));
+    for (int kind = 0; kind < 2; ++kind) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, P->pev[kind][copy][0], P->pev[kind][copy][1]) == cudaSuccess) {
+        P->probe_ms[kind] += ms;
+        P->probe_n[kind] += 1;
+      }
+    }
+    if (P->h_flag[0] || !more) break;
+  }
+  cudaEventDestroy(ev);
+  OpFinal fin{x, b, P->weights, P->bstate};
+  GSK_TRY(run_pass(P, fin, 4, s));
+  GSK_CUDA(cudaEventRecord(P->t1, s));
+  BicgState hs{};
+  GSK_CUDA(cudaMemcpyAsync(&hs, P->bstate, sizeof hs, cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  std::vector<double> H(hs.hist_len);
+  GSK_CUDA(cudaMemcpy(H.data(), P->hist_d, sizeof(double) * hs.hist_len, cudaMemcpyDeviceToHost));
+  if (hist) std::copy(H.begin(), H.end(), hist);
+  float ms = 0;
+  GSK_CUDA(cudaEventElapsedTime(&ms, P->t0, P->t1));
+  rep->status = hs.status;
+  rep->iterations = hs.hist_len - 1;
+  rep->restarts = 0;
+  rep->history_len = hs.hist_len;
+  rep->breakdown_at = hs.bd;
+  rep->pad_ = 0;
+  rep->relres = H.back();
+  rep->true_relres = hs.true_rel;
+  rep->true_relres_w = hs.true_rel_w;
+  double best = H[0];
+  for (double v : H) best = std::min(best, v);
+  rep->best_relres = best;
+  rep->solve_ms = ms;
+  GSK_TRY(join_out(P, caller));
+  return GSK_OK;
+}
+
+}  // namespace gsk
+
+using namespace gsk;
+
+extern "C" int gsk_bicgstab_solve_plan(gsk_plan* plan, const double* b, const double* x0, double tol,
+                                       int maxit, double* x, double* hist, gsk_report* rep, void* stream) {
+  if (!plan) {
+    set_error("gsk_bicgstab_solve_plan: plan is NULL");
+    return GSK_E_INVALID;
+  }
+  return bicgstab_run(plan, b, x0, tol, maxit, x, hist, rep, as_stream(stream));
+}
+
+extern "C" int gsk_bicgstab_solve(const gsk_csr* A, const double* b, const double* x0, double tol,
+                                  int maxit, double* x, double* hist, gsk_report* rep, void* stream) {
+  gsk_plan* P = nullptr;
+  GSK_TRY(gsk_plan_create(A, nullptr, &P, stream));
+  int rc = bicgstab_run(P, b, x0, tol, maxit, x, hist, rep, as_stream(stream));
+  gsk_plan_destroy(P);
+  return rc;
+}

@@ -1,0 +1,453 @@
+// gmres.cu — restarted GMRES(m) (Saad & Schultz 1986) with
+// modified Gram-Schmidt Arnoldi (BASELINE north star; reading B9) and the Givens
+// least-squares update in one warp (arithmetic AC-7).
+//
+// Arnoldi step j (1-based) is j+1 fused passes over the rows:
+//   S_j      w = A v_j                       h_1j = <w, v_1>
+//   M_{i,j}  w = w - h_ij v_i   (i < j)      h_{i+1,j} = <w, v_{i+1}>
+//   L_j      w = w - h_jj v_j                ||w||^2 -> h_{j+1,j}; rotations, g,
+//                                            history; back substitution at cycle end
+// The basis is stored unnormalised (w_j) with inv_j = 1/h_{j,j-1}; every use
+// recomputes v_j = RN(w_j * inv_j), the same operation as explicit normalisation, so
+// it is bit-identical while saving a read and a write per step.
+// A cycle is one captured CUDA graph: the steps, then X (x += sum_k y_k v_k) and R
+// (r = b - A x -> next v_1, restart, or the final true residual).  Passes after a
+// cycle-ending step return at once (device flag), so the host checks once per cycle.
+#include <cmath>
+#include <vector>
+#include "internal.cuh"
+
+namespace gsk {
+
+constexpr int MAX_M = 128;
+
+// r = b - A x stored as basis slot 1; ||r||^2 and ||w o r||^2.
+struct OpGResid {
+  static constexpr int D = 2;
+  static constexpr bool kSpmv = true;
+  const double *x, *b, *w;
+  double* W1;
+  double* hist;
+  GmresState* st;
+  int init;
+  __device__ bool begin() { return !st->done; }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int i, double y, double (&c)[2]) const {
+    const double ri = b[i] - y;
+    W1[i] = ri;
+    c[0] = ri * ri;
+    const double u = w ? w[i] * ri : ri;
+    c[1] = u * u;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const {
+    if (lane) return;
+    const double beta = sqrt(s[0]);
+    if (init) {
+      st->beta0 = beta;
+      st->n0w = sqrt(s[1]);
+      hist[0] = beta == 0.0 ? 0.0 : 1.0;
+      st->hist_len = 1;
+      st->it = 0;
+      st->restarts = 0;
+      if (beta == 0.0) {
+        st->status = GSK_CONVERGED;
+        st->true_rel = 0.0;
+        st->true_rel_w = 0.0;
+        st->done = 1;
+        return;
+      }
+    } else if (st->final_) {
+      st->status = st->diverged ? GSK_DIVERGED : (st->conv ? GSK_CONVERGED : GSK_MAXIT);
+      st->true_rel = beta / st->beta0;
+      st->true_rel_w = st->n0w == 0.0 ? 0.0 : sqrt(s[1]) / st->n0w;
+      st->done = 1;
+      return;
+    } else {
+      st->restarts += 1;
+    }
+    st->inv[1] = 1.0 / beta;
+    st->g[0] = beta;
+    for (int q = 1; q <= st->m; ++q) st->g[q] = 0.0;
+    st->k = 0;
+    st->cycle_stop = 0;
+  }
+};
+
+// S_j: w = A v_j into slot j+1; h_1j = <w, v_1>
+struct OpArnoldi {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = true;
+  const double *Wj, *W1;
+  double* Wn;
+  GmresState* st;
+  int j;
+  double invj, inv1;
+  __device__ bool begin() {
+    if (st->done || st->cycle_stop) return false;
+    invj = st->inv[j];
+    inv1 = st->inv[1];
+    return true;
+  }
+  __device__ double gather(int c) const { return __ldg(Wj + c) * invj; }
+  __device__ void row(int i, double y, double (&c)[1]) const {
+    Wn[i] = y;
+    c[0] = y * (W1[i] * inv1);
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane == 0) st->H[0 * st->m + (j - 1)] = s[0];
+  }
+};
+
+// M_{i,j}: w -= h_ij v_i; h_{i+1,j} = <w, v_{i+1}>
+struct OpMgs {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = false;
+  const double *Wi, *Wi1;
+  double* Wn;
+  GmresState* st;
+  int i, j;
+  double mh, invi, invi1;
+  __device__ bool begin() {
+    if (st->done || st->cycle_stop) return false;
+    mh = -st->H[(i - 1) * st->m + (j - 1)];
+    invi = st->inv[i];
+    invi1 = st->inv[i + 1];
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int q, double, double (&c)[1]) const {
+    const double w = __fma_rn(mh, Wi[q] * invi, Wn[q]);
+    Wn[q] = w;
+    c[0] = w * (Wi1[q] * invi1);
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane == 0) st->H[i * st->m + (j - 1)] = s[0];
+  }
+};
+
+// L_j: w -= h_jj v_j; ||w||^2 -> Givens update, history, stopping, back-solve.
+struct OpLast {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = false;
+  const double* Wj;
+  double* Wn;
+  double* hist;
+  GmresState* st;
+  int j;
+  double mh, invj;
+  __device__ bool begin() {
+    if (st->done || st->cycle_stop) return false;
+    mh = -st->H[(j - 1) * st->m + (j - 1)];
+    invj = st->inv[j];
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int q, double, double (&c)[1]) const {
+    const double w = __fma_rn(mh, Wj[q] * invj, Wn[q]);
+    Wn[q] = w;
+    c[0] = w * w;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    GmresState* S = st;
+    const int m = S->m, col = j - 1;
+    double* H = S->H;
+    __shared__ int need_bs;
+    if (lane == 0) {
+      const double hn = sqrt(s[0]);
+      H[j * m + col] = hn;
+      for (int i = 0; i < col; ++i) {  // previous rotations on column j
+        const double a = H[i * m + col], b = H[(i + 1) * m + col];
+        H[i * m + col] = __fma_rn(S->cs[i], a, S->sn[i] * b);
+        H[(i + 1) * m + col] = __fma_rn(-S->sn[i], a, S->cs[i] * b);
+      }
+      const double a = H[col * m + col], b = H[j * m + col];
+      const double delta = sqrt(__fma_rn(a, a, b * b));
+      const double cj = a / delta, sj = b / delta;
+      S->cs[col] = cj;
+      S->sn[col] = sj;
+      H[col * m + col] = delta;
+      H[j * m + col] = 0.0;
+      const double gj = S->g[col];
+      S->g[col + 1] = -sj * gj;
+      S->g[col] = cj * gj;
+      const double rel = fabs(S->g[col + 1]) / S->beta0;
+      const int it = S->it + 1;
+      S->it = it;
+      hist[it] = rel;
+      S->hist_len = it + 1;
+      S->k = j;
+      int stop = 0;
+      if (!isfinite(rel)) {
+        S->diverged = 1;
+        S->skip_x = 1;
+        S->final_ = 1;
+        stop = 1;
+      } else if (rel < S->tol) {
+        S->conv = 1;
+        S->final_ = 1;
+        stop = 1;
+      } else if (hn == 0.0 || it == S->maxit) {
+        if (it == S->maxit) S->final_ = 1;
+        stop = 1;
+      } else {
+        S->inv[j + 1] = 1.0 / hn;
+      }
+      S->cycle_stop = stop;
+      need_bs = (stop && !S->skip_x) || (j == m);
+    }
+    __syncwarp();
+    if (need_bs) {
+      // column-oriented back substitution R y = g (AC-7), lanes own rows
+      const int k = j;
+      double acc[MAX_M / 32];
+#pragma unroll
+      for (int q = 0; q < MAX_M / 32; ++q) {
+        const int l = lane + 32 * q;
+        acc[q] = l < k ? S->g[l] : 0.0;
+      }
+      bool fin = true;
+      for (int kk = k - 1; kk >= 0; --kk) {
+        const int owner = kk & 31, qo = kk >> 5;
+        double mine = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAX_M / 32; ++q)
+          if (q == qo) mine = acc[q];
+        const double ykk = __shfl_sync(0xffffffffu, mine, owner) / H[kk * m + kk];
+        fin = fin && isfinite(ykk);
+        if (lane == 0) S->y[kk] = ykk;
+#pragma unroll
+        for (int q = 0; q < MAX_M / 32; ++q) {
+          const int l = lane + 32 * q;
+          if (l < kk) acc[q] = __fma_rn(-H[l * m + kk], ykk, acc[q]);
+        }
+      }
+      if (lane == 0 && !fin) {
+        S->diverged = 1;
+        S->final_ = 1;
+      }
+    }
+  }
+};
+
+// X: x += sum_{k=1..K} y_k v_k (k ascending)
+struct OpXupd {
+  static constexpr int D = 0;
+  static constexpr bool kSpmv = false;
+  const double* W;
+  double* x;
+  GmresState* st;
+  size_t n;
+  int K;
+  const double *y, *inv;
+  __device__ bool begin() {
+    if (st->done || st->skip_x) return false;
+    K = st->k;
+    y = st->y;
+    inv = st->inv;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int q, double, double (&)[1]) const {
+    double xv = x[q];
+    for (int k = 0; k < K; ++k) xv = __fma_rn(__ldg(y + k), W[(size_t)k * n + q] * __ldg(inv + k + 1), xv);
+    x[q] = xv;
+  }
+};
+
+static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int copy, cudaGraphExec_t* out) {
+  const size_t n = (size_t)P->A.n;
+  cudaStream_t s = P->st;
+  GmresState* st = P->gstate;
+  auto slot = [&](int j) { return P->W + (size_t)(j - 1) * n; };
+  GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = GSK_OK;
+  int nk = 0;
+  for (int j = 1; j <= m && rc == GSK_OK; ++j) {
+    OpArnoldi a{slot(j), slot(1), slot(j + 1), st, j, 0, 0};
+    if (j == 1) GSK_CUDA(cudaEventRecordWithFlags(P->pev[3][copy][0], s, cudaEventRecordExternal));
+    rc = run_pass(P, a, 0, s);
+    if (j == 1) GSK_CUDA(cudaEventRecordWithFlags(P->pev[3][copy][1], s, cudaEventRecordExternal));
+    ++nk;
+    for (int i = 1; i < j && rc == GSK_OK; ++i) {
+      OpMgs mg{slot(i), slot(i + 1), slot(j + 1), st, i, j, 0, 0, 0};
+      const bool probe = (j == 2 && i == 1);
+      if (probe) GSK_CUDA(cudaEventRecordWithFlags(P->pev[2][copy][0], s, cudaEventRecordExternal));
+      rc = run_pass(P, mg, 1, s);
+      if (probe) GSK_CUDA(cudaEventRecordWithFlags(P->pev[2][copy][1], s, cudaEventRecordExternal));
+      ++nk;
+    }
+    if (rc == GSK_OK) {
+      OpLast l{slot(j), slot(j + 1), P->hist_d, st, j, 0, 0};
+      rc = run_pass(P, l, 2, s);
+      ++nk;
+    }
+  }
+  if (rc == GSK_OK) {
+    OpXupd xu{P->W, x, st, n, 0, nullptr, nullptr};
+    rc = run_pass(P, xu, 3, s);
+    ++nk;
+  }
+  if (rc == GSK_OK) {
+    OpGResid r{x, b, P->weights, slot(1), P->hist_d, st, 0};
+    rc = run_pass(P, r, 4, s);
+    ++nk;
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (rc != GSK_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) {
+    set_error("gmres graph capture: %s", cudaGetErrorString(e));
+    return GSK_E_CUDA;
+  }
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    set_error("gmres graph instantiate: %s", cudaGetErrorString(e));
+    return GSK_E_CUDA;
+  }
+  g_launches.fetch_sub(nk);
+  return GSK_OK;
+}
+
+static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, double tol, int maxit,
+                     double* x, double* hist, gsk_report* rep, cudaStream_t caller) {
+  if (!b || !x || !rep || !(tol > 0) || maxit < 1 || m < 1 || m > MAX_M) {
+    set_error("gmres: invalid arguments (b, x, rep non-null; tol > 0; maxit >= 1; 1 <= m <= %d)", MAX_M);
+    return GSK_E_INVALID;
+  }
+  const size_t n = (size_t)P->A.n;
+  if (P->Wm < m) {
+    if (P->W) GSK_CUDA(cudaFree(P->W));
+    P->W = nullptr;
+    cudaError_t e = cudaMalloc(&P->W, sizeof(double) * (size_t)(m + 1) * n);
+    if (e != cudaSuccess) {
+      set_error("gmres: cannot allocate the (m+1) x n basis: %s", cudaGetErrorString(e));
+      P->Wm = 0;
+      return GSK_E_NOMEM;
+    }
+    P->Wm = m;
+    for (auto& g : P->ggraph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+  }
+  if (!P->gstate) GSK_CUDA(cudaMalloc(&P->gstate, sizeof(GmresState)));
+  if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 5 * MAX_M + 8)));
+  GSK_TRY(ensure_hist(P, maxit));
+  if (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d) {
+    for (auto& g : P->ggraph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+    GSK_TRY(capture_cycle(P, b, x, m, 0, &P->ggraph[0]));
+    GSK_TRY(capture_cycle(P, b, x, m, 1, &P->ggraph[1]));
+    P->gkey_b = b;
+    P->gkey_x = x;
+    P->gkey_m = m;
+    P->gkey_h = P->hist_d;
+  }
+  const long long kernels_per_cycle = (long long)m * (m + 3) / 2 + 2;
+  cudaStream_t s = P->st;
+  GSK_TRY(join_in(P, caller));
+  GSK_CUDA(cudaEventRecord(P->t0, s));
+  if (x0) {
+    if (x0 != x) GSK_CUDA(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    GSK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  }
+  GmresState h{};
+  double* A = P->garr;
+  h.H = A;
+  h.cs = A + (MAX_M + 1) * MAX_M;
+  h.sn = h.cs + MAX_M;
+  h.g = h.sn + MAX_M;
+  h.y = h.g + MAX_M + 1;
+  h.inv = h.y + MAX_M;
+  h.tol = tol;
+  h.maxit = maxit;
+  h.m = m;
+  GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 5 * MAX_M + 8), s));
+  GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  OpGResid init{x, b, P->weights, P->W, P->hist_d, P->gstate, 1};
+  GSK_TRY(run_pass(P, init, 4, s));
+  const long long maxc = (long long)maxit + 2;
+  long long nc = 0;
+  GSK_CUDA(cudaGraphLaunch(P->ggraph[0], s));
+  g_launches.fetch_add(kernels_per_cycle);
+  ++nc;
+  cudaEvent_t ev;
+  GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  for (;;) {
+    const int copy = (int)((nc - 1) & 1);
+    GSK_CUDA(cudaMemcpyAsync(P->h_flag, &P->gstate->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaEventRecord(ev, s));
+    const bool more = nc < maxc;
+    if (more) {
+      GSK_CUDA(cudaGraphLaunch(P->ggraph[nc & 1], s));
+      g_launches.fetch_add(kernels_per_cycle);
+      ++nc;
+    }
+    GSK_CUDA(cudaEventSynchronize(ev));
+    for (int kind = 2; kind < 4; ++kind) {
+      if (kind == 2 && m < 2) continue;
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, P->pev[kind][copy][0], P->pev[kind][copy][1]) == cudaSuccess) {
+        P->probe_ms[kind] += ms;
+        P->probe_n[kind] += 1;
+      }
+    }
+    if (P->h_flag[0] || !more) break;
+  }
+  cudaEventDestroy(ev);
+  GSK_CUDA(cudaEventRecord(P->t1, s));
+  GmresState hs{};
+  GSK_CUDA(cudaMemcpyAsync(&hs, P->gstate, sizeof hs, cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  std::vector<double> H(hs.hist_len);
+  GSK_CUDA(cudaMemcpy(H.data(), P->hist_d, sizeof(double) * hs.hist_len, cudaMemcpyDeviceToHost));
+  if (hist) std::copy(H.begin(), H.end(), hist);
+  float ms = 0;
+  GSK_CUDA(cudaEventElapsedTime(&ms, P->t0, P->t1));
+  rep->status = hs.status;
+  rep->iterations = hs.it;
+  rep->restarts = hs.restarts;
+  rep->history_len = hs.hist_len;
+  rep->breakdown_at = 0;
+  rep->pad_ = 0;
+  rep->relres = H.back();
+  rep->true_relres = hs.true_rel;
+  rep->true_relres_w = hs.true_rel_w;
+  double best = H[0];
+  for (double v : H) best = std::min(best, v);
+  rep->best_relres = best;
+  rep->solve_ms = ms;
+  GSK_TRY(join_out(P, caller));
+  return GSK_OK;
+}
+
+}  // namespace gsk
+
+using namespace gsk;
+
+extern "C" int gsk_gmres_solve_plan(gsk_plan* plan, const double* b, const double* x0, int m, double tol,
+                                    int maxit, double* x, double* hist, gsk_report* rep, void* stream) {
+  if (!plan) {
+    set_error("gsk_gmres_solve_plan: plan is NULL");
+    return GSK_E_INVALID;
+  }
+  return gmres_run(plan, b, x0, m, tol, maxit, x, hist, rep, as_stream(stream));
+}
+
+extern "C" int gsk_gmres_solve(const gsk_csr* A, const double* b, const double* x0, int m, double tol,
+                               int maxit, double* x, double* hist, gsk_report* rep, void* stream) {
+  gsk_plan* P = nullptr;
+  GSK_TRY(gsk_plan_create(A, nullptr, &P, stream));
+  int rc = gmres_run(P, b, x0, m, tol, maxit, x, hist, rep, as_stream(stream));
+  gsk_plan_destroy(P);
+  return rc;
+}

@@ -1,0 +1,143 @@
+// internal.cuh — host-side plumbing of libgsk: errors, launch accounting, geometry,
+// the plan object and the device-resident solver states.
+#pragma once
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include "common.cuh"
+#include "gsk.h"
+
+namespace gsk {
+
+void set_error(const char* fmt, ...);
+extern std::atomic<int64_t> g_launches;
+
+#define GSK_CUDA(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      ::gsk::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                       __LINE__);                                                           \
+      return GSK_E_CUDA;                                                                    \
+    }                                                                                       \
+  } while (0)
+
+#define GSK_LAUNCHED(k)                         \
+  do {                                          \
+    ::gsk::g_launches.fetch_add(k);             \
+    cudaError_t e_ = cudaGetLastError();        \
+    if (e_ != cudaSuccess) {                    \
+      ::gsk::set_error("kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return GSK_E_CUDA;                        \
+    }                                           \
+  } while (0)
+
+// Tile geometry: sub-tiles of 256 rows, `sub` of them per CTA (pow2), chosen so that
+// the per-tile partials stay <= 8192 (one last-CTA pass reads them).
+struct Geometry {
+  int n = 0, sub = 1, ntiles = 0, np2 = 1;
+};
+Geometry make_geometry(int n);
+
+// Device-resident Bi-CGSTAB state (scalars + control flags), DESIGN.md §5.
+struct BicgState {
+  double rho, rho_prev, alpha, omega, beta, n0, n0u, tol;
+  double true_rel, true_rel_w;
+  int iter, maxit, done, status, halfstep, bd, hist_len, pad;
+};
+
+// Device-resident GMRES(m) state; arrays H[(m+1)*m] (row-major), cs[m], sn[m],
+// g[m+1], y[m], inv[m+2] (inv[j] = 1/||w_j||, basis slot j is stored unnormalised).
+struct GmresState {
+  double beta0, n0w, tol, true_rel, true_rel_w;
+  double *H, *cs, *sn, *g, *y, *inv;
+  int it, maxit, m, k, cycle_stop, final_, conv, diverged, skip_x, done, status, restarts,
+      hist_len, pad;
+};
+
+cudaStream_t as_stream(void* s);
+
+}  // namespace gsk
+
+struct gsk_plan {
+  gsk_csr A{};
+  int fmt = GSK_FMT_CSR;
+  int poll = 0;
+  const double* weights = nullptr;
+  gsk::Geometry geo;
+  gsk::CsrView csr{};
+  gsk::SellView sell{};
+  // SELL storage (owned)
+  int* cptr = nullptr;
+  int* clen = nullptr;
+  int* scol = nullptr;
+  double* sval = nullptr;
+  uint8_t* roff = nullptr;
+  int64_t nchunks = 0, nslots = 0;
+  // reduction scratch
+  double* part = nullptr;      // [MAXD][ntiles]
+  unsigned* tickets = nullptr; // [16]
+  double* scratch = nullptr;   // [n] (residual norms)
+  cudaStream_t st = nullptr;
+  int* h_flag = nullptr;       // pinned
+  // Bi-CGSTAB workspace
+  double* bvec = nullptr;      // 7 vectors: r, rhat, pa, pb, va, vb, t
+  gsk::BicgState* bstate = nullptr;
+  cudaGraphExec_t bgraph[2] = {nullptr, nullptr};
+  const double* bkey_b = nullptr;
+  const double* bkey_x = nullptr;
+  int bK = 0;
+  const double* bkey_h = nullptr;
+  // GMRES workspace
+  double* W = nullptr;         // (m+1) n
+  int Wm = 0;
+  gsk::GmresState* gstate = nullptr;
+  double* garr = nullptr;      // H, cs, sn, g, y, inv
+  cudaGraphExec_t ggraph[2] = {nullptr, nullptr};
+  const double* gkey_b = nullptr;
+  const double* gkey_x = nullptr;
+  int gkey_m = 0;
+  const double* gkey_h = nullptr;
+  // history (device)
+  double* hist_d = nullptr;
+  int hist_cap = 0;
+  // kernel probes: per kind, events recorded around one launch per batch
+  // kinds: 0 Bi-CGSTAB v = A p pass, 1 Bi-CGSTAB t = A s pass, 2 GMRES MGS pass,
+  // 3 GMRES Arnoldi SpMV pass; [graph copy][start/stop]
+  static constexpr int NPROBE = 4;
+  cudaEvent_t pev[NPROBE][2][2] = {};
+  double probe_ms[NPROBE] = {};
+  int64_t probe_n[NPROBE] = {};
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+namespace gsk {
+// Launch one fused pass over the plan's rows: Op::kSpmv selects an SpMV pass in the
+// plan's format (CSR or SELL) or a pure vector pass.
+template <class Op>
+int run_pass(gsk_plan* P, const Op& op, int ticket, cudaStream_t s) {
+  Red red{P->part, P->tickets + ticket, P->geo.ntiles, P->geo.np2};
+  Tiles tl{P->geo.n, P->geo.sub};
+  if constexpr (!Op::kSpmv) {
+    fused_pass<0, Op><<<P->geo.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+  } else {
+    if (P->fmt == GSK_FMT_SELL)
+      fused_pass<2, Op><<<P->geo.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+    else
+      fused_pass<1, Op><<<P->geo.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+  }
+  GSK_LAUNCHED(1);
+  return GSK_OK;
+}
+#define GSK_TRY(x)              \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_ != GSK_OK) return rc_; \
+  } while (0)
+
+int sell_build(gsk_plan* P, cudaStream_t s);
+int sell_fill_values(gsk_plan* P, cudaStream_t s);
+int ensure_hist(gsk_plan* P, int maxit);
+int join_in(gsk_plan* P, cudaStream_t caller);
+int join_out(gsk_plan* P, cudaStream_t caller);
+}  // namespace gsk

@@ -1,0 +1,311 @@
+// plan.cu — plan lifecycle and the non-solver entry points of the C-ABI:
+// gsk_spmv / gsk_plan_spmv (SPEC sparse-core spmv; AC-3), gsk_dot (AC-5),
+// gsk_plan_residual_norm, SELL copy-out, probes, diagnostics.
+#include <cstring>
+#include <string>
+#include "internal.cuh"
+
+namespace gsk {
+
+static thread_local std::string t_err;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+Geometry make_geometry(int n) {
+  Geometry g;
+  g.n = n;
+  const int nsub = (n + TB - 1) / TB;
+  g.sub = 1;
+  while ((nsub + g.sub - 1) / g.sub > 8192 && g.sub < MAX_SUB) g.sub <<= 1;
+  g.ntiles = (nsub + g.sub - 1) / g.sub;
+  g.np2 = 1;
+  while (g.np2 < g.ntiles) g.np2 <<= 1;
+  return g;
+}
+
+// ---- ops --------------------------------------------------------------------------
+struct OpSpmv {
+  static constexpr int D = 0;
+  static constexpr bool kSpmv = true;
+  const double* x;
+  double* y;
+  __device__ bool begin() { return true; }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int i, double v, double (&)[1]) const { y[i] = v; }
+};
+
+struct OpDot {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = false;
+  const double* a;
+  const double* b;
+  double* out;
+  __device__ bool begin() { return true; }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int i, double, double (&c)[1]) const { c[0] = a[i] * b[i]; }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane == 0) *out = s[0];
+  }
+};
+
+// ||w o (b - A x)||^2
+struct OpResNorm {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = true;
+  const double* x;
+  const double* b;
+  const double* w;
+  double* out;
+  __device__ bool begin() { return true; }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int i, double y, double (&c)[1]) const {
+    const double r = b[i] - y;
+    const double u = w ? w[i] * r : r;
+    c[0] = u * u;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane == 0) *out = s[0];
+  }
+};
+
+static int plan_alloc_common(gsk_plan* P) {
+  P->geo = make_geometry(P->A.n);
+  GSK_CUDA(cudaMalloc(&P->part, sizeof(double) * MAXD * (size_t)P->geo.ntiles));
+  GSK_CUDA(cudaMalloc(&P->tickets, sizeof(unsigned) * 16));
+  GSK_CUDA(cudaMemset(P->tickets, 0, sizeof(unsigned) * 16));
+  GSK_CUDA(cudaMalloc(&P->scratch, sizeof(double) * 8));
+  GSK_CUDA(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+  GSK_CUDA(cudaMallocHost(&P->h_flag, sizeof(int) * 16));
+  GSK_CUDA(cudaEventCreate(&P->t0));
+  GSK_CUDA(cudaEventCreate(&P->t1));
+  for (auto& k : P->pev)
+    for (auto& e : k) {
+      GSK_CUDA(cudaEventCreate(&e[0]));
+      GSK_CUDA(cudaEventCreate(&e[1]));
+    }
+  P->csr = CsrView{P->A.n, P->A.row_ptr, P->A.col_idx, P->A.values};
+  return GSK_OK;
+}
+
+static int check_csr(const gsk_csr* A, const char* who) {
+  if (!A || A->n < 1 || A->nnz < 0 || !A->row_ptr || (A->nnz > 0 && (!A->col_idx || !A->values))) {
+    set_error("%s: invalid gsk_csr (n >= 1, nnz >= 0, non-null arrays required)", who);
+    return GSK_E_INVALID;
+  }
+  return GSK_OK;
+}
+
+// Order work on the plan stream after the caller's stream (and vice versa at the end).
+int join_in(gsk_plan* P, cudaStream_t caller) {
+  cudaEvent_t e;
+  GSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  GSK_CUDA(cudaEventRecord(e, caller));
+  GSK_CUDA(cudaStreamWaitEvent(P->st, e, 0));
+  GSK_CUDA(cudaEventDestroy(e));
+  return GSK_OK;
+}
+int join_out(gsk_plan* P, cudaStream_t caller) {
+  cudaEvent_t e;
+  GSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  GSK_CUDA(cudaEventRecord(e, P->st));
+  GSK_CUDA(cudaStreamWaitEvent(caller, e, 0));
+  GSK_CUDA(cudaEventDestroy(e));
+  return GSK_OK;
+}
+
+int ensure_hist(gsk_plan* P, int maxit) {
+  if (P->hist_cap >= maxit + 1) return GSK_OK;
+  if (P->hist_d) GSK_CUDA(cudaFree(P->hist_d));
+  P->hist_d = nullptr;
+  GSK_CUDA(cudaMalloc(&P->hist_d, sizeof(double) * (size_t)(maxit + 1)));
+  P->hist_cap = maxit + 1;
+  return GSK_OK;
+}
+
+}  // namespace gsk
+
+using namespace gsk;
+
+extern "C" {
+
+const char* gsk_last_error(void) { return t_err.c_str(); }
+int64_t gsk_launch_count(void) { return g_launches.load(); }
+int gsk_version(void) { return 1; }
+
+int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, void* stream) {
+  GSK_TRY(check_csr(A, "gsk_plan_create"));
+  if (!plan) {
+    set_error("gsk_plan_create: plan is NULL");
+    return GSK_E_INVALID;
+  }
+  int fmt = opts ? opts->format : GSK_FMT_CSR;
+  if (fmt != GSK_FMT_CSR && fmt != GSK_FMT_SELL) {
+    set_error("gsk_plan_create: unknown format %d", fmt);
+    return GSK_E_INVALID;
+  }
+  gsk_plan* P = new gsk_plan();
+  P->A = *A;
+  P->fmt = fmt;
+  P->poll = opts ? opts->poll : 0;
+  P->weights = opts ? opts->weights : nullptr;
+  int rc = plan_alloc_common(P);
+  if (rc == GSK_OK && fmt == GSK_FMT_SELL) {
+    cudaStream_t s = as_stream(stream);
+    rc = join_in(P, s);
+    if (rc == GSK_OK) rc = sell_build(P, P->st);
+    if (rc == GSK_OK) rc = join_out(P, s);
+    if (rc == GSK_OK && cudaStreamSynchronize(P->st) != cudaSuccess) rc = GSK_E_CUDA;
+  }
+  if (rc != GSK_OK) {
+    gsk_plan_destroy(P);
+    return rc;
+  }
+  *plan = P;
+  return GSK_OK;
+}
+
+int gsk_plan_refresh(gsk_plan* P, void* stream) {
+  if (!P) return GSK_E_INVALID;
+  if (P->fmt != GSK_FMT_SELL) return GSK_OK;
+  cudaStream_t s = as_stream(stream);
+  GSK_TRY(join_in(P, s));
+  GSK_TRY(sell_fill_values(P, P->st));
+  GSK_TRY(join_out(P, s));
+  GSK_CUDA(cudaStreamSynchronize(P->st));
+  return GSK_OK;
+}
+
+void gsk_plan_destroy(gsk_plan* P) {
+  if (!P) return;
+  if (P->st) cudaStreamSynchronize(P->st);
+  for (auto g : P->bgraph)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto g : P->ggraph)
+    if (g) cudaGraphExecDestroy(g);
+  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->tickets, P->scratch,
+                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (P->h_flag) cudaFreeHost(P->h_flag);
+  for (auto& k : P->pev)
+    for (auto& e : k) {
+      if (e[0]) cudaEventDestroy(e[0]);
+      if (e[1]) cudaEventDestroy(e[1]);
+    }
+  if (P->t0) cudaEventDestroy(P->t0);
+  if (P->t1) cudaEventDestroy(P->t1);
+  if (P->st) cudaStreamDestroy(P->st);
+  delete P;
+}
+
+int gsk_plan_spmv(gsk_plan* P, const double* x, double* y, void* stream) {
+  if (!P || !x || !y) {
+    set_error("gsk_plan_spmv: NULL argument");
+    return GSK_E_INVALID;
+  }
+  cudaStream_t s = as_stream(stream);
+  OpSpmv op{x, y};
+  GSK_TRY(run_pass(P, op, 0, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
+
+int gsk_spmv(const gsk_csr* A, const double* x, double* y, void* stream) {
+  gsk_plan* P = nullptr;
+  GSK_TRY(gsk_plan_create(A, nullptr, &P, stream));
+  int rc = gsk_plan_spmv(P, x, y, stream);
+  gsk_plan_destroy(P);
+  return rc;
+}
+
+int gsk_plan_residual_norm(gsk_plan* P, const double* b, const double* x, const double* w,
+                           double* result, void* stream) {
+  if (!P || !b || !x || !result) {
+    set_error("gsk_plan_residual_norm: NULL argument");
+    return GSK_E_INVALID;
+  }
+  cudaStream_t s = as_stream(stream);
+  OpResNorm op{x, b, w, P->scratch};
+  GSK_TRY(run_pass(P, op, 1, s));
+  double v = 0;
+  GSK_CUDA(cudaMemcpyAsync(&v, P->scratch, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  *result = sqrt(v);
+  return GSK_OK;
+}
+
+int gsk_dot(int64_t n, const double* a, const double* b, double* result, void* stream) {
+  if (n < 1 || n > 0x7fffffff || !a || !b || !result) {
+    set_error("gsk_dot: invalid arguments");
+    return GSK_E_INVALID;
+  }
+  gsk_plan tmp;
+  tmp.A.n = (int)n;
+  tmp.geo = make_geometry((int)n);
+  cudaStream_t s = as_stream(stream);
+  GSK_CUDA(cudaMallocAsync(&tmp.part, sizeof(double) * MAXD * (size_t)tmp.geo.ntiles, s));
+  GSK_CUDA(cudaMallocAsync(&tmp.tickets, sizeof(unsigned) * 16 + sizeof(double) * 2, s));
+  GSK_CUDA(cudaMemsetAsync(tmp.tickets, 0, sizeof(unsigned) * 16, s));
+  double* out = reinterpret_cast<double*>(tmp.tickets + 16);
+  OpDot op{a, b, out};
+  int rc = run_pass(&tmp, op, 0, s);
+  double v = 0;
+  if (rc == GSK_OK && cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    rc = GSK_E_CUDA;
+  cudaFreeAsync(tmp.part, s);
+  cudaFreeAsync(tmp.tickets, s);
+  tmp.part = nullptr;
+  tmp.tickets = nullptr;
+  if (cudaStreamSynchronize(s) != cudaSuccess) rc = GSK_E_CUDA;
+  *result = v;
+  return rc;
+}
+
+int gsk_plan_sell_info(gsk_plan* P, int64_t* nchunks, int64_t* nslots) {
+  if (!P || P->fmt != GSK_FMT_SELL) {
+    set_error("gsk_plan_sell_info: plan is not SELL");
+    return GSK_E_INVALID;
+  }
+  if (nchunks) *nchunks = P->nchunks;
+  if (nslots) *nslots = P->nslots;
+  return GSK_OK;
+}
+
+int gsk_plan_sell_copy(gsk_plan* P, int32_t* chunk_ptr, int32_t* chunk_len, int32_t* scol,
+                       double* sval, uint8_t* roff, void* stream) {
+  if (!P || P->fmt != GSK_FMT_SELL) {
+    set_error("gsk_plan_sell_copy: plan is not SELL");
+    return GSK_E_INVALID;
+  }
+  cudaStream_t s = as_stream(stream);
+  GSK_CUDA(cudaStreamSynchronize(P->st));
+  if (chunk_ptr) GSK_CUDA(cudaMemcpyAsync(chunk_ptr, P->cptr, sizeof(int) * (P->nchunks + 1), cudaMemcpyDeviceToDevice, s));
+  if (chunk_len) GSK_CUDA(cudaMemcpyAsync(chunk_len, P->clen, sizeof(int) * P->nchunks, cudaMemcpyDeviceToDevice, s));
+  if (scol) GSK_CUDA(cudaMemcpyAsync(scol, P->scol, sizeof(int) * P->nslots, cudaMemcpyDeviceToDevice, s));
+  if (sval) GSK_CUDA(cudaMemcpyAsync(sval, P->sval, sizeof(double) * P->nslots, cudaMemcpyDeviceToDevice, s));
+  if (roff) GSK_CUDA(cudaMemcpyAsync(roff, P->roff, P->nchunks * SELL_C, cudaMemcpyDeviceToDevice, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
+
+int gsk_plan_probe(gsk_plan* P, int kind, double* avg_ms, int64_t* count) {
+  if (!P || kind < 0 || kind >= gsk_plan::NPROBE) {
+    set_error("gsk_plan_probe: bad arguments");
+    return GSK_E_INVALID;
+  }
+  if (avg_ms) *avg_ms = P->probe_n[kind] ? P->probe_ms[kind] / P->probe_n[kind] : 0.0;
+  if (count) *count = P->probe_n[kind];
+  return GSK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// sell.cu — CSR -> SELL-C-sigma (C = 32, sigma = 256) on the device (BASELINE.json
+// configs[3]).  Integer work, bit-exact with the oracle's layout:
+//   1. per sigma-window: stable rank of rows by descending length (ties by row id);
+//      roff[sorted slot] = in-window row offset; chunk_len = longest row of a chunk;
+//   2. chunk_ptr = exclusive scan of 32 * chunk_len (one CTA);
+//   3. fill: slot (k, lane) of chunk c at chunk_ptr[c] + 32 k + lane, CSR order kept,
+//      padding col = -1, val = 0 (predicated off in the SpMV, AC-3).
+#include "internal.cuh"
+
+namespace gsk {
+
+__global__ void __launch_bounds__(TB) sell_rank_kernel(int n, int nchunks, const int* __restrict__ rp,
+                                                       uint8_t* roff, int* clen) {
+  __shared__ int len[TB];
+  __shared__ int slen[TB];
+  const int w = blockIdx.x, t = threadIdx.x, r = w * TB + t;
+  len[t] = r < n ? rp[r + 1] - rp[r] : 0;
+  __syncthreads();
+  const int li = len[t];
+  int rank = 0;
+  for (int j = 0; j < TB; ++j) {
+    const int lj = len[j];
+    rank += (lj > li) || (lj == li && j < t);
+  }
+  slen[rank] = li;
+  const int c = w * (TB / SELL_C) + (rank >> 5);
+  if (c < nchunks) roff[(size_t)w * TB + rank] = (uint8_t)t;
+  __syncthreads();
+  if ((t & 31) == 0) {
+    const int cc = w * (TB / SELL_C) + (t >> 5);
+    if (cc < nchunks) clen[cc] = slen[t];
+  }
+}
+
+// exclusive scan of 32*clen into cptr[0..nchunks] (single CTA, one-off)
+__global__ void __launch_bounds__(1024) sell_scan_kernel(int nchunks, const int* __restrict__ clen, int* cptr) {
+  __shared__ long long part[1024];
+  const int t = threadIdx.x;
+  const int per = (nchunks + 1023) / 1024;
+  const int a = t * per, b = min(nchunks, a + per);
+  long long s = 0;
+  for (int i = a; i < b; ++i) s += (long long)clen[i] * SELL_C;
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    long long v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  long long run = t ? part[t - 1] : 0;
+  for (int i = a; i < b; ++i) {
+    cptr[i] = (int)run;
+    run += (long long)clen[i] * SELL_C;
+  }
+  if (t == 1023) cptr[nchunks] = (int)part[1023];
+}
+
+__global__ void __launch_bounds__(TB) sell_fill_kernel(int n, int nchunks, const int* __restrict__ rp,
+                                                       const int* __restrict__ ci, const double* __restrict__ v,
+                                                       const int* __restrict__ cptr, const uint8_t* __restrict__ roff,
+                                                       int* scol, double* sval, bool values_only) {
+  const int w = blockIdx.x, t = threadIdx.x, lane = t & 31;
+  const int c = w * (TB / SELL_C) + (t >> 5);
+  if (c >= nchunks) return;
+  const int row = w * TB + roff[(size_t)c * SELL_C + lane];
+  const int p0 = cptr[c], L = (cptr[c + 1] - p0) / SELL_C;
+  const int a = row < n ? rp[row] : 0;
+  const int len = row < n ? rp[row + 1] - a : 0;
+  for (int k = 0; k < L; ++k) {
+    const size_t slot = (size_t)p0 + (size_t)k * SELL_C + lane;
+    if (k < len) {
+      if (!values_only) scol[slot] = ci[a + k];
+      sval[slot] = v[a + k];
+    } else {
+      if (!values_only) scol[slot] = -1;
+      sval[slot] = 0.0;
+    }
+  }
+}
+
+int sell_build(gsk_plan* P, cudaStream_t s) {
+  const int n = P->A.n;
+  const int nwin = (n + TB - 1) / TB;
+  P->nchunks = (n + SELL_C - 1) / SELL_C;
+  GSK_CUDA(cudaMalloc(&P->clen, sizeof(int) * P->nchunks));
+  GSK_CUDA(cudaMalloc(&P->cptr, sizeof(int) * (P->nchunks + 1)));
+  GSK_CUDA(cudaMalloc(&P->roff, (size_t)P->nchunks * SELL_C));
+  sell_rank_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->roff, P->clen);
+  GSK_LAUNCHED(1);
+  sell_scan_kernel<<<1, 1024, 0, s>>>((int)P->nchunks, P->clen, P->cptr);
+  GSK_LAUNCHED(1);
+  int tot = 0;
+  GSK_CUDA(cudaMemcpyAsync(&tot, P->cptr + P->nchunks, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  P->nslots = tot;
+  GSK_CUDA(cudaMalloc(&P->scol, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_CUDA(cudaMalloc(&P->sval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
+  sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
+                                       P->cptr, P->roff, P->scol, P->sval, false);
+  GSK_LAUNCHED(1);
+  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff};
+  return GSK_OK;
+}
+
+int sell_fill_values(gsk_plan* P, cudaStream_t s) {
+  const int n = P->A.n;
+  const int nwin = (n + TB - 1) / TB;
+  sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
+                                       P->cptr, P->roff, P->scol, P->sval, true);
+  GSK_LAUNCHED(1);
+  return GSK_OK;
+}
+
+}  // namespace gsk

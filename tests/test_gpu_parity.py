@@ -1,0 +1,270 @@
+"""GPU <-> oracle parity through the C-ABI (north-star contract).
+
+Under the arithmetic contract the CUDA path and the oracle are bit-identical, so
+every comparison is exact (==): integer work, GS values, SpMV, histories, x,
+iteration counts and verdicts.  `tolerance_report` additionally evaluates the
+north-star tolerances (GS <= 2 ulp, per-iteration relres <= 1e-9 relative over the
+first 50 iterations, iterations +-2, x <= 1e-7 relative) so that a contract slip
+is distinguishable from a tolerance failure.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+gsk = pytest.importorskip("paper_0812_2769_b200")
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # collected on CPU boxes but never run there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def ulps(a, b):
+    a = np.ascontiguousarray(a, np.float64).view(np.int64)
+    b = np.ascontiguousarray(b, np.float64).view(np.int64)
+    return int(np.abs(a - b).max()) if a.size else 0
+
+
+def cpu(t):
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+
+
+def tolerance_report(h_gpu, h_orc, x_gpu, x_orc, it_gpu, it_orc):
+    k = min(len(h_gpu), len(h_orc), 51)
+    rel = np.abs(h_gpu[:k] - h_orc[:k]) / np.maximum(np.abs(h_orc[:k]), 1e-300)
+    assert rel.max() <= 1e-9
+    assert abs(it_gpu - it_orc) <= 2
+    xs = np.linalg.norm(x_orc)
+    assert np.linalg.norm(x_gpu - x_orc) <= 1e-7 * (xs if xs > 0 else 1.0)
+
+
+def assert_same_solve(g, o):
+    xg, hg, rg = g
+    xo, ho, ro = o
+    xg = cpu(xg)
+    for k in ("status", "iterations", "history_len", "breakdown_at", "restarts"):
+        assert rg[k] == ro[k], (k, rg, ro)
+    assert np.array_equal(hg, ho), np.flatnonzero(hg != ho)[:5]
+    assert np.array_equal(xg, xo)
+    for k in ("relres", "best_relres", "true_relres", "true_relres_w"):
+        assert rg[k] == ro[k], (k, rg[k], ro[k])
+    tolerance_report(hg, ho, xg, xo, rg["iterations"], ro["iterations"])
+
+
+CASES = [("C1", None), ("C2", 100), ("C2", 128), ("C3", 20), ("C4", 24), ("C5", 96), ("P1", 64)]
+
+
+# ---------------------------------------------------------------- GS(p)
+@pytest.mark.parametrize("name,N", CASES + [("C4", None), ("C5", None)])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_gs_scale_parity(name, N, p):
+    s = workloads.generate(name, N=N)
+    A = gsk.CSR.from_system(s)
+    As, bs, d = gsk.gs_scale(A, s["b"], p)
+    vo, bo, do = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], p)
+    if p in (1, 2):  # AC-4: bit-exact
+        assert np.array_equal(cpu(As.val), vo)
+        assert np.array_equal(cpu(bs), bo)
+        assert np.array_equal(cpu(d), do)
+    else:  # pow() is libm-dependent: north-star 2 ulp on the norm, a few on the products
+        assert ulps(1.0 / cpu(d), 1.0 / do) <= 2
+        assert ulps(cpu(As.val), vo) <= 4
+    # in place gives the same bits
+    A2 = gsk.CSR.from_system(s)
+    b2 = torch.tensor(s["b"], device="cuda")
+    gsk.gs_scale(A2, b2, p, inplace=True)
+    assert np.array_equal(cpu(A2.val), cpu(As.val)) and np.array_equal(cpu(b2), cpu(bs))
+
+
+def test_gs_errors():
+    s = workloads.generate("C2", N=40)
+    val = s["val"].copy()
+    for r in (700, 33, 1599):
+        val[s["row_ptr"][r]:s["row_ptr"][r + 1]] = 0.0
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    with pytest.raises(gsk.GskError) as ei:
+        gsk.gs_scale(A, s["b"], 2)
+    assert ei.value.code == -2 and ei.value.bad_row == 33
+    with pytest.raises(gsk.GskError) as ei:
+        gsk.gs_scale(gsk.CSR.from_system(s), s["b"], 0)
+    assert ei.value.code == -1
+
+
+# ---------------------------------------------------------------- SpMV, dot, SELL
+@pytest.mark.parametrize("name,N", CASES + [("C4", None), ("C5", None)])
+@pytest.mark.parametrize("fmt", ["csr", "sell"])
+def test_spmv_parity(name, N, fmt):
+    s = workloads.generate(name, N=N)
+    A = gsk.CSR.from_system(s)
+    P = gsk.Plan(A, fmt=fmt)
+    x = workloads.uniform(s["n"], 77, 3)
+    y = cpu(P.spmv(x))
+    assert np.array_equal(y, oracle.spmv(s["row_ptr"], s["col"], s["val"], x))
+    if fmt == "csr":
+        assert np.array_equal(cpu(gsk.spmv(A, x)), y)
+
+
+def test_spmv_long_rows_fallback():
+    # rows longer than the shared-memory stage (2048 entries per 256 rows) take the
+    # direct path; results must not change
+    rng = np.random.default_rng(8)
+    n = 700
+    lens = rng.integers(0, 40, n)
+    lens[:256] = 30
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.standard_normal(rp[-1])
+    x = rng.standard_normal(n)
+    for fmt in ("csr", "sell"):
+        y = cpu(gsk.Plan(gsk.CSR(rp, col, val), fmt=fmt).spmv(x))
+        assert np.array_equal(y, oracle.spmv(rp, col, val, x))
+
+
+@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 100), ("C3", 20), ("C4", None), ("C5", 300)])
+def test_sell_layout_parity(name, N):
+    s = workloads.generate(name, N=N)
+    P = gsk.Plan(gsk.CSR.from_system(s), fmt="sell")
+    g = P.sell_arrays()
+    o = oracle.sell_build(s["row_ptr"], s["col"], s["val"], 32, 256)
+    for k in ("chunk_ptr", "chunk_len", "scol", "sval", "roff"):
+        assert np.array_equal(g[k], o[k]), k
+
+
+@pytest.mark.parametrize("n", [1, 3, 255, 256, 257, 4097, 65536, 65537, 1000003, 3000001])
+def test_dot_parity(n):
+    a = workloads.uniform(n, 5, 11) * np.exp(workloads.uniform(n, 6, 11, -20, 20))
+    b = workloads.uniform(n, 7, 11)
+    assert gsk.dot(a, b) == oracle.dot(a, b)
+
+
+# ---------------------------------------------------------------- solvers
+def system(name, N, scaling):
+    s = workloads.generate(name, N=N)
+    if scaling == "none":
+        return s, s["val"], s["b"], None
+    vo, bo, d = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], scaling)
+    return s, vo, bo, d
+
+
+@pytest.mark.parametrize("name,N", CASES)
+@pytest.mark.parametrize("scaling", ["none", 1, 2])
+@pytest.mark.parametrize("fmt", ["csr", "sell"])
+def test_bicgstab_parity(name, N, scaling, fmt):
+    s, val, b, _ = system(name, N, scaling)
+    maxit = 600
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt)
+    g = P.bicgstab(b, tol=1e-8, maxit=maxit)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-8, maxit)
+    assert_same_solve(g, o)
+
+
+def test_bicgstab_frame_weights():
+    """Stopping in the GS(2) frame for an unscaled / GS(1) solve."""
+    s = workloads.generate("P1", N=64)
+    _, _, d2 = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    for p in ("none", 1):
+        if p == "none":
+            val, b, w = s["val"], s["b"], d2
+        else:
+            val, b, d1 = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 1)
+            w = d2 / d1
+        P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), weights=w)
+        g = P.bicgstab(b, tol=1e-10, maxit=3000)
+        o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-10, 3000, weights=w)
+        assert_same_solve(g, o)
+
+
+@pytest.mark.parametrize("name,N", CASES)
+@pytest.mark.parametrize("scaling", ["none", 2])
+@pytest.mark.parametrize("m", [1, 20, 30, 50])
+def test_gmres_parity(name, N, scaling, m):
+    s, val, b, _ = system(name, N, scaling)
+    maxit = 400
+    fmt = "sell" if name == "C4" else "csr"
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt)
+    g = P.gmres(b, m=m, tol=1e-8, maxit=maxit)
+    o = oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-8, maxit)
+    assert_same_solve(g, o)
+
+
+def test_solver_edge_cases():
+    n = 300
+    rp = np.arange(n + 1, dtype=np.int32)
+    col = np.arange(n, dtype=np.int32)
+    ones = np.ones(n)
+    b = workloads.uniform(n, 1, 2)
+    A = gsk.CSR(rp, col, ones)
+    P = gsk.Plan(A)
+    # A = I: Bi-CGSTAB half-step exit at iteration 1; GMRES 1 step (lucky)
+    assert_same_solve(P.bicgstab(b, tol=1e-12, maxit=10), oracle.bicgstab(rp, col, ones, b, 1e-12, 10))
+    assert_same_solve(P.gmres(b, m=5, tol=1e-12, maxit=10), oracle.gmres(rp, col, ones, b, 5, 1e-12, 10))
+    # b = 0: converged at 0
+    z = np.zeros(n)
+    assert_same_solve(P.bicgstab(z, tol=1e-8, maxit=10), oracle.bicgstab(rp, col, ones, z, 1e-8, 10))
+    assert_same_solve(P.gmres(z, m=5, tol=1e-8, maxit=10), oracle.gmres(rp, col, ones, z, 5, 1e-8, 10))
+    # nonzero x0
+    s = workloads.generate("C2", N=50)
+    x0 = workloads.uniform(s["n"], 3, 4)
+    P2 = gsk.Plan(gsk.CSR.from_system(s))
+    assert_same_solve(P2.bicgstab(s["b"], x0=x0, tol=1e-9, maxit=300),
+                      oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-9, 300, x0=x0))
+    assert_same_solve(P2.gmres(s["b"], x0=x0, m=7, tol=1e-9, maxit=300),
+                      oracle.gmres(s["row_ptr"], s["col"], s["val"], s["b"], 7, 1e-9, 300, x0=x0))
+    # breakdown: skew 2x2 gives <r0^, A r0> = 0 at iteration 1
+    rp2 = np.array([0, 1, 2], np.int32)
+    c2 = np.array([1, 0], np.int32)
+    v2 = np.array([1.0, -1.0])
+    bb = np.array([1.0, 0.0])
+    g = gsk.Plan(gsk.CSR(rp2, c2, v2)).bicgstab(bb, tol=1e-10, maxit=10)
+    assert_same_solve(g, oracle.bicgstab(rp2, c2, v2, bb, 1e-10, 10))
+    assert g[2]["status"] == 2 and g[2]["breakdown_at"] == 1
+    # maxit = 1 and m >= n
+    s3 = workloads.generate("C1", N=6)
+    P3 = gsk.Plan(gsk.CSR.from_system(s3))
+    assert_same_solve(P3.bicgstab(s3["b"], tol=1e-14, maxit=1),
+                      oracle.bicgstab(s3["row_ptr"], s3["col"], s3["val"], s3["b"], 1e-14, 1))
+    assert_same_solve(P3.gmres(s3["b"], m=40, tol=1e-14, maxit=100),
+                      oracle.gmres(s3["row_ptr"], s3["col"], s3["val"], s3["b"], 40, 1e-14, 100))
+
+
+def test_plan_less_entry_points():
+    s = workloads.generate("C1")
+    A = gsk.CSR.from_system(s)
+    assert_same_solve(gsk.bicgstab_solve(A, s["b"], tol=1e-8, maxit=300),
+                      oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-8, 300))
+    assert_same_solve(gsk.gmres_solve(A, s["b"], m=20, tol=1e-8, maxit=300),
+                      oracle.gmres(s["row_ptr"], s["col"], s["val"], s["b"], 20, 1e-8, 300))
+
+
+def test_repeat_solves_are_deterministic():
+    s = workloads.generate("C3", N=16)
+    P = gsk.Plan(gsk.CSR.from_system(s), fmt="sell")
+    a = P.bicgstab(s["b"], tol=1e-9, maxit=500)
+    b = P.bicgstab(s["b"], tol=1e-9, maxit=500)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(cpu(a[0]), cpu(b[0]))
+    c = P.gmres(s["b"], m=30, tol=1e-9, maxit=300)
+    d = P.gmres(s["b"], m=30, tol=1e-9, maxit=300)
+    assert np.array_equal(c[1], d[1]) and np.array_equal(cpu(c[0]), cpu(d[0]))
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_full_size_parity(name):
+    """Each BASELINE config at full size, in the launch configuration bench.py uses
+    (GS(2) then SELL for C4, CSR otherwise): GS bit-exact, the first 50 Bi-CGSTAB
+    iterations and one GMRES(30) cycle + 2 steps bit-exact against the oracle."""
+    c = workloads.CONFIGS[name]
+    s = workloads.generate(name)
+    A = gsk.CSR.from_system(s)
+    As, bs, d = gsk.gs_scale(A, s["b"], 2)
+    vo, bo, do = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    assert np.array_equal(cpu(As.val), vo) and np.array_equal(cpu(bs), bo)
+    P = gsk.Plan(As, fmt="sell" if c.sell else "csr")
+    g = P.bicgstab(bs, tol=c.tol, maxit=50)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, c.tol, 50)
+    assert_same_solve(g, o)
+    g = P.gmres(bs, m=30, tol=c.tol, maxit=32)
+    o = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 30, c.tol, 32)
+    assert_same_solve(g, o)
