@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time-to-tol without GS / with GS(1)")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
     return ap.parse_args()
 
 
@@ -184,7 +185,7 @@ def main():
     dbuf = torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
     fmt = "sell" if cfg.sell else "csr"
-    plan = gsk.Plan(As, fmt=fmt)
+    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule)
     x1 = torch.empty(n, dtype=torch.float64, device="cuda")
     x2 = torch.empty(n, dtype=torch.float64, device="cuda")
 

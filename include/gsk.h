@@ -60,6 +60,9 @@ typedef struct gsk_report {
 
 /* Plan options.  format: GSK_FMT_CSR or GSK_FMT_SELL (SELL-C-sigma, C = 32,
  * sigma = 256, built on the device from the CSR at plan creation).
+ * bicg_schedule: 0 = auto, 1 = fused 3-pass iteration (p and s recomputed at the
+ * SpMV gather), 2 = split 5-pass iteration (plain SpMV gathers); both give
+ * bit-identical results.
  * weights: NULL, or DEVICE [n] w_i > 0.  When set, Bi-CGSTAB's stopping test and
  * history use ||w o r|| / ||w o r0|| — the paper measures the relative residual on
  * the GS(2)-scaled system, i.e. w = d_GS(2) / d_applied.
@@ -68,7 +71,11 @@ typedef struct gsk_opts {
   int32_t format;
   int32_t poll;
   const double *weights;
+  int32_t bicg_schedule;
+  int32_t reserved_;
 } gsk_opts;
+
+enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2 };
 
 typedef struct gsk_plan gsk_plan;
 

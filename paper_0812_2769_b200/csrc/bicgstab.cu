@@ -174,17 +174,17 @@ struct OpP3 {
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int i, double, double (&c)[2]) const {
     if (half) {
-      x[i] = __fma_rn(alpha, pn[i], x[i]);
+      x[i] = __fma_rn(alpha, __ldg(pn + i), x[i]);
       c[0] = 0.0;
       c[1] = 0.0;
       return;
     }
-    const double s = __fma_rn(malpha, vn[i], r[i]);
-    x[i] = __fma_rn(omega, s, __fma_rn(alpha, pn[i], x[i]));
-    const double rr = __fma_rn(momega, t[i], s);
+    const double s = __fma_rn(malpha, __ldg(vn + i), r[i]);
+    x[i] = __fma_rn(omega, s, __fma_rn(alpha, __ldg(pn + i), x[i]));
+    const double rr = __fma_rn(momega, __ldg(t + i), s);
     r[i] = rr;
-    c[0] = rh[i] * rr;
-    const double u = w ? w[i] * rr : rr;
+    c[0] = __ldg(rh + i) * rr;
+    const double u = w ? __ldg(w + i) * rr : rr;
     c[1] = u * u;
   }
   __device__ void finish(const double (&s)[2], int lane) const {
@@ -227,6 +227,154 @@ struct OpP3 {
   }
 };
 
+// ---- split schedule (5 passes, plain SpMV gathers) -------------------
+// S0  p = r + beta (p - omega v)                       (vector pass)
+// S1  v = A p, sigma = <r^, v>                          -> alpha
+// S2  s = r - alpha v, ||s||_w^2                        -> half-step exit
+// S3  t = A s, <t,s>, <t,t>                             -> omega
+// S4  x += alpha p + omega s, r = s - omega t, <r^,r>, ||r||_w^2 (as P3)
+struct OpS0 {
+  static constexpr int D = 0;
+  static constexpr bool kSpmv = false;
+  const double *r, *v;
+  double* p;
+  BicgState* st;
+  double beta, momega;
+  __device__ bool begin() {
+    if (st->done) return false;
+    beta = st->beta;
+    momega = -st->omega;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int i, double, double (&)[1]) const {
+    p[i] = __fma_rn(beta, __fma_rn(momega, __ldg(v + i), p[i]), __ldg(r + i));
+  }
+};
+
+struct OpS1 {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = true;
+  const double *p, *rh;
+  double* v;
+  BicgState* st;
+  __device__ bool begin() { return !st->done; }
+  __device__ double gather(int c) const { return __ldg(p + c); }
+  __device__ void row(int i, double y, double (&c)[1]) const {
+    v[i] = y;
+    c[0] = __ldg(rh + i) * y;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane) return;
+    const double sigma = s[0];
+    if (sigma == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = st->iter;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / sigma;
+  }
+};
+
+struct OpS2 {
+  static constexpr int D = 1;
+  static constexpr bool kSpmv = false;
+  const double *r, *v, *w;
+  double *s_, *hist;
+  BicgState* st;
+  double malpha;
+  __device__ bool begin() {
+    if (st->done) return false;
+    malpha = -st->alpha;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int i, double, double (&c)[1]) const {
+    const double s = __fma_rn(malpha, __ldg(v + i), __ldg(r + i));
+    s_[i] = s;
+    const double u = w ? __ldg(w + i) * s : s;
+    c[0] = u * u;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane) return;
+    const int i = st->iter;
+    const double sn = sqrt(s[0]) / st->n0;
+    if (sn < st->tol) {  // half-step exit (reading B4): x += alpha p in S4
+      hist[i] = sn;
+      st->hist_len = i + 1;
+      st->status = GSK_CONVERGED;
+      st->halfstep = 1;
+      st->done = 1;
+    }
+  }
+};
+
+struct OpS3 {
+  static constexpr int D = 2;
+  static constexpr bool kSpmv = true;
+  const double* s_;
+  double* t;
+  BicgState* st;
+  __device__ bool begin() { return !st->done; }
+  __device__ double gather(int c) const { return __ldg(s_ + c); }
+  __device__ void row(int i, double y, double (&c)[2]) const {
+    t[i] = y;
+    c[0] = y * __ldg(s_ + i);
+    c[1] = y * y;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const {
+    if (lane) return;
+    if (s[1] == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = st->iter;
+      st->done = 1;
+      return;
+    }
+    st->omega = s[0] / s[1];
+  }
+};
+
+// S4 = OpP3 with s read instead of recomputed
+struct OpS4 {
+  static constexpr int D = 2;
+  static constexpr bool kSpmv = false;
+  const double *s_, *p, *t, *rh, *w;
+  double *x, *r, *hist;
+  BicgState* st;
+  OpP3 base;  // scalar epilogue shared with the fused schedule
+  double alpha, omega, momega;
+  int half;
+  __device__ bool begin() {
+    half = st->halfstep;
+    if (st->done && !half) return false;
+    alpha = st->alpha;
+    omega = st->omega;
+    momega = -omega;
+    base.half = half;
+    base.alpha = alpha;
+    base.omega = omega;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int i, double, double (&c)[2]) const {
+    if (half) {
+      x[i] = __fma_rn(alpha, __ldg(p + i), x[i]);
+      c[0] = 0.0;
+      c[1] = 0.0;
+      return;
+    }
+    const double s = __ldg(s_ + i);
+    x[i] = __fma_rn(omega, s, __fma_rn(alpha, __ldg(p + i), x[i]));
+    const double rr = __fma_rn(momega, __ldg(t + i), s);
+    r[i] = rr;
+    c[0] = __ldg(rh + i) * rr;
+    const double u = w ? __ldg(w + i) * rr : rr;
+    c[1] = u * u;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const { base.finish(s, lane); }
+};
+
 struct OpFinal {  // true residual ||b - A x|| (unweighted and weighted)
   static constexpr int D = 2;
   static constexpr bool kSpmv = true;
@@ -247,6 +395,8 @@ struct OpFinal {  // true residual ||b - A x|| (unweighted and weighted)
   }
 };
 
+static int passes_per_iter(const gsk_plan* P) { return P->bmode == 1 ? 3 : 5; }
+
 static int batch_size(const gsk_plan* P) {
   int K = P->poll;
   if (K <= 0) {
@@ -265,21 +415,41 @@ static int capture_bicg(gsk_plan* P, const double* b, double* x, int K, int copy
   cudaStream_t s = P->st;
   GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = GSK_OK;
+  auto probe = [&](int kind, int edge) {
+    return cudaEventRecordWithFlags(P->pev[kind][copy][edge], s, cudaEventRecordExternal);
+  };
   for (int k = 0; k < K && rc == GSK_OK; ++k) {
-    double *po = (k & 1) ? pb : pa, *vo = (k & 1) ? vb : va;
-    double *pn = (k & 1) ? pa : pb, *vn = (k & 1) ? va : vb;
-    OpP1 p1{r, po, vo, rh, pn, vn, P->bstate, 0, 0};
-    OpP2 p2{r, vn, w, t, P->hist_d, P->bstate, 0};
-    OpP3 p3{vn, pn, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0, 0, 0};
-    if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[0][copy][0], s, cudaEventRecordExternal));
-    rc = run_pass(P, p1, 1, s);
-    if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[0][copy][1], s, cudaEventRecordExternal));
-    if (rc == GSK_OK) {
-      if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[1][copy][0], s, cudaEventRecordExternal));
-      rc = run_pass(P, p2, 2, s);
-      if (k == 0) GSK_CUDA(cudaEventRecordWithFlags(P->pev[1][copy][1], s, cudaEventRecordExternal));
+    if (P->bmode == 1) {  // fused 3-pass schedule
+      double *po = (k & 1) ? pb : pa, *vo = (k & 1) ? vb : va;
+      double *pn = (k & 1) ? pa : pb, *vn = (k & 1) ? va : vb;
+      OpP1 p1{r, po, vo, rh, pn, vn, P->bstate, 0, 0};
+      OpP2 p2{r, vn, w, t, P->hist_d, P->bstate, 0};
+      OpP3 p3{vn, pn, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0, 0, 0};
+      if (k == 0 && probe(0, 0) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, p1, 1, s);
+      if (k == 0 && rc == GSK_OK && probe(0, 1) != cudaSuccess) rc = GSK_E_CUDA;
+      if (k == 0 && rc == GSK_OK && probe(1, 0) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, p2, 2, s);
+      if (k == 0 && rc == GSK_OK && probe(1, 1) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, p3, 3, s);
+    } else {  // split 5-pass schedule: p = pa, v = va, s = pb
+      double *p = pa, *v = va, *sv = pb;
+      OpS0 s0{r, v, p, P->bstate, 0, 0};
+      OpS1 s1{p, rh, v, P->bstate};
+      OpS2 s2{r, v, w, sv, P->hist_d, P->bstate, 0};
+      OpS3 s3{sv, t, P->bstate};
+      OpS4 s4{sv, p, t, rh, w, x, r, P->hist_d, P->bstate, OpP3{nullptr, nullptr, nullptr, nullptr, nullptr,
+              nullptr, nullptr, P->hist_d, P->bstate, 0, 0, 0, 0, 0}, 0, 0, 0, 0};
+      rc = run_pass(P, s0, 5, s);
+      if (k == 0 && rc == GSK_OK && probe(0, 0) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, s1, 1, s);
+      if (k == 0 && rc == GSK_OK && probe(0, 1) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, s2, 6, s);
+      if (k == 0 && rc == GSK_OK && probe(1, 0) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, s3, 2, s);
+      if (k == 0 && rc == GSK_OK && probe(1, 1) != cudaSuccess) rc = GSK_E_CUDA;
+      if (rc == GSK_OK) rc = run_pass(P, s4, 3, s);
     }
-    if (rc == GSK_OK) rc = run_pass(P, p3, 3, s);
   }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(s, &g);
@@ -298,7 +468,7 @@ static int capture_bicg(gsk_plan* P, const double* b, double* x, int K, int copy
     return GSK_E_CUDA;
   }
   // the launches recorded during capture are counted per replay instead
-  g_launches.fetch_sub(3LL * K);
+  g_launches.fetch_sub((long long)passes_per_iter(P) * K);
   return GSK_OK;
 }
 
@@ -346,7 +516,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   const long long maxb = (maxit + K - 1) / K + 1;
   long long nb = 0;
   GSK_CUDA(cudaGraphLaunch(P->bgraph[0], s));
-  g_launches.fetch_add(3LL * K);
+  g_launches.fetch_add((long long)passes_per_iter(P) * K);
   ++nb;
   cudaEvent_t ev;
   GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -357,7 +527,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
     const bool more = nb < maxb;
     if (more) {
       GSK_CUDA(cudaGraphLaunch(P->bgraph[nb & 1], s));
-      g_launches.fetch_add(3LL * K);
+      g_launches.fetch_add((long long)passes_per_iter(P) * K);
       ++nb;
     }
     GSK_CUDA(cudaEventSynchronize(ev));

@@ -91,7 +91,7 @@ struct OpArnoldi {
   __device__ double gather(int c) const { return __ldg(Wj + c) * invj; }
   __device__ void row(int i, double y, double (&c)[1]) const {
     Wn[i] = y;
-    c[0] = y * (W1[i] * inv1);
+    c[0] = y * (__ldg(W1 + i) * inv1);
   }
   __device__ void finish(const double (&s)[1], int lane) const {
     if (lane == 0) st->H[0 * st->m + (j - 1)] = s[0];
@@ -116,9 +116,9 @@ struct OpMgs {
   }
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int q, double, double (&c)[1]) const {
-    const double w = __fma_rn(mh, Wi[q] * invi, Wn[q]);
+    const double w = __fma_rn(mh, __ldg(Wi + q) * invi, Wn[q]);
     Wn[q] = w;
-    c[0] = w * (Wi1[q] * invi1);
+    c[0] = w * (__ldg(Wi1 + q) * invi1);
   }
   __device__ void finish(const double (&s)[1], int lane) const {
     if (lane == 0) st->H[i * st->m + (j - 1)] = s[0];
@@ -143,7 +143,7 @@ struct OpLast {
   }
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int q, double, double (&c)[1]) const {
-    const double w = __fma_rn(mh, Wj[q] * invj, Wn[q]);
+    const double w = __fma_rn(mh, __ldg(Wj + q) * invj, Wn[q]);
     Wn[q] = w;
     c[0] = w * w;
   }
@@ -249,7 +249,7 @@ struct OpXupd {
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int q, double, double (&)[1]) const {
     double xv = x[q];
-    for (int k = 0; k < K; ++k) xv = __fma_rn(__ldg(y + k), W[(size_t)k * n + q] * __ldg(inv + k + 1), xv);
+    for (int k = 0; k < K; ++k) xv = __fma_rn(__ldg(y + k), __ldg(W + (size_t)k * n + q) * __ldg(inv + k + 1), xv);
     x[q] = xv;
   }
 };

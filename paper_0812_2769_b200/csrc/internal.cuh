@@ -1,6 +1,7 @@
 // internal.cuh — host-side plumbing of libgsk: errors, launch accounting, geometry,
 // the plan object and the device-resident solver states.
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -32,10 +33,14 @@ extern std::atomic<int64_t> g_launches;
     }                                           \
   } while (0)
 
-// Tile geometry: sub-tiles of 256 rows, `sub` of them per CTA (pow2), chosen so that
-// the per-tile partials stay <= 8192 (one last-CTA pass reads them).
+// Tile geometry of one pass kind: CTAs of `rows` rows, groups of 256 tiles.
+struct TileGeo {
+  int rows = 0, ntiles = 0, ngroups = 0, gnp2 = 1;
+};
+// Vector passes use 2048-row tiles (SUB_V windows), SpMV passes 1024 (SUB_S).
 struct Geometry {
-  int n = 0, sub = 1, ntiles = 0, np2 = 1;
+  int n = 0;
+  TileGeo v, s;
 };
 Geometry make_geometry(int n);
 
@@ -63,6 +68,7 @@ struct gsk_plan {
   gsk_csr A{};
   int fmt = GSK_FMT_CSR;
   int poll = 0;
+  int bmode = 2;  // Bi-CGSTAB schedule: 1 fused, 2 split
   const double* weights = nullptr;
   gsk::Geometry geo;
   gsk::CsrView csr{};
@@ -75,8 +81,10 @@ struct gsk_plan {
   uint8_t* roff = nullptr;
   int64_t nchunks = 0, nslots = 0;
   // reduction scratch
+  static constexpr int NSLOT = 16;  // reduction slots (one per pass kind)
   double* part = nullptr;      // [MAXD][ntiles]
-  unsigned* tickets = nullptr; // [16]
+  double* gpart = nullptr;     // [MAXD][ngroups]
+  unsigned* tickets = nullptr; // [NSLOT] + [NSLOT][ngroups] group tickets
   double* scratch = nullptr;   // [n] (residual norms)
   cudaStream_t st = nullptr;
   int* h_flag = nullptr;       // pinned
@@ -115,16 +123,19 @@ namespace gsk {
 // Launch one fused pass over the plan's rows: Op::kSpmv selects an SpMV pass in the
 // plan's format (CSR or SELL) or a pure vector pass.
 template <class Op>
-int run_pass(gsk_plan* P, const Op& op, int ticket, cudaStream_t s) {
-  Red red{P->part, P->tickets + ticket, P->geo.ntiles, P->geo.np2};
-  Tiles tl{P->geo.n, P->geo.sub};
+int run_pass(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
+  const TileGeo& g = Op::kSpmv ? P->geo.s : P->geo.v;
+  const int gmax = std::max(P->geo.v.ngroups, P->geo.s.ngroups);
+  Red red{P->part, P->gpart, P->tickets + gsk_plan::NSLOT + (size_t)slot * gmax, P->tickets + slot,
+          g.ntiles, g.ngroups, g.gnp2};
+  Tiles tl{P->geo.n};
   if constexpr (!Op::kSpmv) {
-    fused_pass<0, Op><<<P->geo.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+    fused_pass<0, Op><<<g.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
   } else {
     if (P->fmt == GSK_FMT_SELL)
-      fused_pass<2, Op><<<P->geo.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+      fused_pass<2, Op><<<g.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
     else
-      fused_pass<1, Op><<<P->geo.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+      fused_pass<1, Op><<<g.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
   }
   GSK_LAUNCHED(1);
   return GSK_OK;

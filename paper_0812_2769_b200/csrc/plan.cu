@@ -21,16 +21,42 @@ void set_error(const char* fmt, ...) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+static TileGeo tile_geo(int n, int rows) {
+  TileGeo g;
+  g.rows = rows;
+  g.ntiles = (n + rows - 1) / rows;
+  g.ngroups = (g.ntiles + TB - 1) / TB;
+  g.gnp2 = 1;
+  while (g.gnp2 < g.ngroups) g.gnp2 <<= 1;
+  return g;
+}
+
 Geometry make_geometry(int n) {
   Geometry g;
   g.n = n;
-  const int nsub = (n + TB - 1) / TB;
-  g.sub = 1;
-  while ((nsub + g.sub - 1) / g.sub > 8192 && g.sub < MAX_SUB) g.sub <<= 1;
-  g.ntiles = (nsub + g.sub - 1) / g.sub;
-  g.np2 = 1;
-  while (g.np2 < g.ntiles) g.np2 <<= 1;
+  g.v = tile_geo(n, TB * SUB_V);
+  g.s = tile_geo(n, TB * SUB_S);
   return g;
+}
+
+// Reduction scratch of a geometry: tile and group partials, slot and group tickets.
+int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
+  const Geometry& geo = P->geo;
+  const size_t nt_max = std::max(geo.v.ntiles, geo.s.ntiles);
+  const size_t ng_max = std::max(geo.v.ngroups, geo.s.ngroups);
+  const size_t nt = sizeof(unsigned) * gsk_plan::NSLOT * (1 + ng_max);
+  if (async) {
+    GSK_CUDA(cudaMallocAsync(&P->part, sizeof(double) * MAXD * nt_max, s));
+    GSK_CUDA(cudaMallocAsync(&P->gpart, sizeof(double) * MAXD * ng_max, s));
+    GSK_CUDA(cudaMallocAsync(&P->tickets, nt, s));
+    GSK_CUDA(cudaMemsetAsync(P->tickets, 0, nt, s));
+  } else {
+    GSK_CUDA(cudaMalloc(&P->part, sizeof(double) * MAXD * nt_max));
+    GSK_CUDA(cudaMalloc(&P->gpart, sizeof(double) * MAXD * ng_max));
+    GSK_CUDA(cudaMalloc(&P->tickets, nt));
+    GSK_CUDA(cudaMemset(P->tickets, 0, nt));
+  }
+  return GSK_OK;
 }
 
 // ---- ops --------------------------------------------------------------------------
@@ -52,7 +78,7 @@ struct OpDot {
   double* out;
   __device__ bool begin() { return true; }
   __device__ double gather(int) const { return 0.0; }
-  __device__ void row(int i, double, double (&c)[1]) const { c[0] = a[i] * b[i]; }
+  __device__ void row(int i, double, double (&c)[1]) const { c[0] = __ldg(a + i) * __ldg(b + i); }
   __device__ void finish(const double (&s)[1], int lane) const {
     if (lane == 0) *out = s[0];
   }
@@ -80,9 +106,7 @@ struct OpResNorm {
 
 static int plan_alloc_common(gsk_plan* P) {
   P->geo = make_geometry(P->A.n);
-  GSK_CUDA(cudaMalloc(&P->part, sizeof(double) * MAXD * (size_t)P->geo.ntiles));
-  GSK_CUDA(cudaMalloc(&P->tickets, sizeof(unsigned) * 16));
-  GSK_CUDA(cudaMemset(P->tickets, 0, sizeof(unsigned) * 16));
+  GSK_TRY(alloc_reduction(P, nullptr, false));
   GSK_CUDA(cudaMalloc(&P->scratch, sizeof(double) * 8));
   GSK_CUDA(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
   GSK_CUDA(cudaMallocHost(&P->h_flag, sizeof(int) * 16));
@@ -158,6 +182,13 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
   P->fmt = fmt;
   P->poll = opts ? opts->poll : 0;
   P->weights = opts ? opts->weights : nullptr;
+  const int sched = opts ? opts->bicg_schedule : GSK_BICG_AUTO;
+  if (sched < 0 || sched > 2) {
+    delete P;
+    set_error("gsk_plan_create: unknown bicg_schedule %d", sched);
+    return GSK_E_INVALID;
+  }
+  P->bmode = sched == GSK_BICG_AUTO ? GSK_BICG_SPLIT : sched;
   int rc = plan_alloc_common(P);
   if (rc == GSK_OK && fmt == GSK_FMT_SELL) {
     cudaStream_t s = as_stream(stream);
@@ -192,7 +223,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
-  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->tickets, P->scratch,
+  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->gpart, P->tickets, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -253,19 +284,18 @@ int gsk_dot(int64_t n, const double* a, const double* b, double* result, void* s
   tmp.A.n = (int)n;
   tmp.geo = make_geometry((int)n);
   cudaStream_t s = as_stream(stream);
-  GSK_CUDA(cudaMallocAsync(&tmp.part, sizeof(double) * MAXD * (size_t)tmp.geo.ntiles, s));
-  GSK_CUDA(cudaMallocAsync(&tmp.tickets, sizeof(unsigned) * 16 + sizeof(double) * 2, s));
-  GSK_CUDA(cudaMemsetAsync(tmp.tickets, 0, sizeof(unsigned) * 16, s));
-  double* out = reinterpret_cast<double*>(tmp.tickets + 16);
+  GSK_TRY(alloc_reduction(&tmp, s, true));
+  double* out = nullptr;
+  GSK_CUDA(cudaMallocAsync(&out, sizeof(double), s));
   OpDot op{a, b, out};
   int rc = run_pass(&tmp, op, 0, s);
   double v = 0;
   if (rc == GSK_OK && cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     rc = GSK_E_CUDA;
   cudaFreeAsync(tmp.part, s);
+  cudaFreeAsync(tmp.gpart, s);
   cudaFreeAsync(tmp.tickets, s);
-  tmp.part = nullptr;
-  tmp.tickets = nullptr;
+  cudaFreeAsync(out, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) rc = GSK_E_CUDA;
   *result = v;
   return rc;

@@ -151,10 +151,11 @@ def system(name, N, scaling):
 @pytest.mark.parametrize("name,N", CASES)
 @pytest.mark.parametrize("scaling", ["none", 1, 2])
 @pytest.mark.parametrize("fmt", ["csr", "sell"])
-def test_bicgstab_parity(name, N, scaling, fmt):
+@pytest.mark.parametrize("schedule", ["fused", "split"])
+def test_bicgstab_parity(name, N, scaling, fmt, schedule):
     s, val, b, _ = system(name, N, scaling)
     maxit = 600
-    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt)
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt, schedule=schedule)
     g = P.bicgstab(b, tol=1e-8, maxit=maxit)
     o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-8, maxit)
     assert_same_solve(g, o)
@@ -164,13 +165,13 @@ def test_bicgstab_frame_weights():
     """Stopping in the GS(2) frame for an unscaled / GS(1) solve."""
     s = workloads.generate("P1", N=64)
     _, _, d2 = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
-    for p in ("none", 1):
+    for p, schedule in (("none", "fused"), ("none", "split"), (1, "fused"), (1, "split")):
         if p == "none":
             val, b, w = s["val"], s["b"], d2
         else:
             val, b, d1 = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 1)
             w = d2 / d1
-        P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), weights=w)
+        P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), weights=w, schedule=schedule)
         g = P.bicgstab(b, tol=1e-10, maxit=3000)
         o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-10, 3000, weights=w)
         assert_same_solve(g, o)
@@ -199,6 +200,8 @@ def test_solver_edge_cases():
     P = gsk.Plan(A)
     # A = I: Bi-CGSTAB half-step exit at iteration 1; GMRES 1 step (lucky)
     assert_same_solve(P.bicgstab(b, tol=1e-12, maxit=10), oracle.bicgstab(rp, col, ones, b, 1e-12, 10))
+    Pf = gsk.Plan(A, schedule="fused")
+    assert_same_solve(Pf.bicgstab(b, tol=1e-12, maxit=10), oracle.bicgstab(rp, col, ones, b, 1e-12, 10))
     assert_same_solve(P.gmres(b, m=5, tol=1e-12, maxit=10), oracle.gmres(rp, col, ones, b, 5, 1e-12, 10))
     # b = 0: converged at 0
     z = np.zeros(n)
@@ -217,9 +220,10 @@ def test_solver_edge_cases():
     c2 = np.array([1, 0], np.int32)
     v2 = np.array([1.0, -1.0])
     bb = np.array([1.0, 0.0])
-    g = gsk.Plan(gsk.CSR(rp2, c2, v2)).bicgstab(bb, tol=1e-10, maxit=10)
-    assert_same_solve(g, oracle.bicgstab(rp2, c2, v2, bb, 1e-10, 10))
-    assert g[2]["status"] == 2 and g[2]["breakdown_at"] == 1
+    for sched in ("fused", "split"):
+        g = gsk.Plan(gsk.CSR(rp2, c2, v2), schedule=sched).bicgstab(bb, tol=1e-10, maxit=10)
+        assert_same_solve(g, oracle.bicgstab(rp2, c2, v2, bb, 1e-10, 10))
+        assert g[2]["status"] == 2 and g[2]["breakdown_at"] == 1
     # maxit = 1 and m >= n
     s3 = workloads.generate("C1", N=6)
     P3 = gsk.Plan(gsk.CSR.from_system(s3))
