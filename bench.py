@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--impl", default="gsk", choices=["gsk", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--N", type=int, default=None, help="override grid size (debug only)")
-    ap.add_argument("--gmres-maxit", type=int, default=None)
+    ap.add_argument("--gmres-maxit", type=int, default=300,
+                    help="GMRES(30) iteration budget per step (10 restart cycles; DESIGN.md §7)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time-to-tol without GS / with GS(1)")
@@ -148,11 +149,24 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def reduce_over_ranks(ms, its, dist, device):
+    """Whole-job timing over ranks: the step time is the MAX over ranks, the work
+    (solver iterations) is the SUM (each rank solves its own replica)."""
+    import torch
+    t = torch.tensor([ms, float(its)], device=device, dtype=torch.float64)
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(tmax[0]), float(t[1])
+
+
 def config_desc(args, cfg, s):
     return {"workload": f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", "n": int(s["n"]),
             "nnz": int(s["nnz"]), "grid": f"{cfg.N if args.N is None else args.N}^{3 if cfg.cfg in (3, 4) else 2}",
             "format": "SELL-C-32-256" if cfg.sell else "CSR", "scaling": "GS(2)",
-            "solvers": ["Bi-CGSTAB", "GMRES(30)"], "tol": cfg.tol, "seed": cfg.seed,
+            "solvers": ["Bi-CGSTAB to tol (maxit %d)" % cfg.maxit,
+                        "GMRES(30) for %d iterations (or to tol)" % args.gmres_maxit],
+            "tol": cfg.tol, "seed": cfg.seed,
             "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % ((12 * s["nnz"] + 4 * s["n"]) / 1e9)}
 
 
@@ -175,7 +189,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = workloads.CONFIGS[args.config]
     m = 30
-    gmaxit = args.gmres_maxit or cfg.maxit
+    gmaxit = args.gmres_maxit
     s = workloads.generate(args.config, N=args.N)
     n, nnz = s["n"], s["nnz"]
     A0 = gsk.CSR.from_system(s)
@@ -218,11 +232,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     its = sum(r1["iterations"] + r2["iterations"] for r1, r2 in reps)
     if dist:
-        t = torch.tensor([ms, float(its)], device="cuda", dtype=torch.float64)
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        ms, its = float(tmax[0]), float(t[1])
+        ms, its = reduce_over_ranks(ms, its, dist, "cuda")
     value = its / (ms / 1e3)
 
     # dominant kernel: per-launch time from the CUDA-event probes inside the timed steps

@@ -24,6 +24,7 @@ constexpr int MAX_M = 128;
 // r = b - A x stored as basis slot 1; ||r||^2 and ||w o r||^2.
 struct OpGResid {
   static constexpr int D = 2;
+  static constexpr int NV = 2;
   static constexpr bool kSpmv = true;
   const double *x, *b, *w;
   double* W1;
@@ -31,12 +32,13 @@ struct OpGResid {
   GmresState* st;
   int init;
   __device__ bool begin() { return !st->done; }
+  __device__ const double* vin(int k) const { return k == 0 ? b : w; }
   __device__ double gather(int c) const { return __ldg(x + c); }
-  __device__ void row(int i, double y, double (&c)[2]) const {
-    const double ri = b[i] - y;
+  __device__ void row(int i, double y, const double (&v)[NV], double (&c)[2]) const {
+    const double ri = v[0] - y;
     W1[i] = ri;
     c[0] = ri * ri;
-    const double u = w ? w[i] * ri : ri;
+    const double u = w ? v[1] * ri : ri;
     c[1] = u * u;
   }
   __device__ void finish(const double (&s)[2], int lane) const {
@@ -76,6 +78,7 @@ struct OpGResid {
 // S_j: w = A v_j into slot j+1; h_1j = <w, v_1>
 struct OpArnoldi {
   static constexpr int D = 1;
+  static constexpr int NV = 1;
   static constexpr bool kSpmv = true;
   const double *Wj, *W1;
   double* Wn;
@@ -88,10 +91,11 @@ struct OpArnoldi {
     inv1 = st->inv[1];
     return true;
   }
+  __device__ const double* vin(int) const { return W1; }
   __device__ double gather(int c) const { return __ldg(Wj + c) * invj; }
-  __device__ void row(int i, double y, double (&c)[1]) const {
+  __device__ void row(int i, double y, const double (&v)[NV], double (&c)[1]) const {
     Wn[i] = y;
-    c[0] = y * (__ldg(W1 + i) * inv1);
+    c[0] = y * (v[0] * inv1);
   }
   __device__ void finish(const double (&s)[1], int lane) const {
     if (lane == 0) st->H[0 * st->m + (j - 1)] = s[0];
@@ -101,6 +105,7 @@ struct OpArnoldi {
 // M_{i,j}: w -= h_ij v_i; h_{i+1,j} = <w, v_{i+1}>
 struct OpMgs {
   static constexpr int D = 1;
+  static constexpr int NV = 3;
   static constexpr bool kSpmv = false;
   const double *Wi, *Wi1;
   double* Wn;
@@ -114,11 +119,12 @@ struct OpMgs {
     invi1 = st->inv[i + 1];
     return true;
   }
+  __device__ const double* vin(int k) const { return k == 0 ? Wi : k == 1 ? Wn : Wi1; }
   __device__ double gather(int) const { return 0.0; }
-  __device__ void row(int q, double, double (&c)[1]) const {
-    const double w = __fma_rn(mh, __ldg(Wi + q) * invi, Wn[q]);
+  __device__ void row(int q, double, const double (&v)[NV], double (&c)[1]) const {
+    const double w = __fma_rn(mh, v[0] * invi, v[1]);
     Wn[q] = w;
-    c[0] = w * (__ldg(Wi1 + q) * invi1);
+    c[0] = w * (v[2] * invi1);
   }
   __device__ void finish(const double (&s)[1], int lane) const {
     if (lane == 0) st->H[i * st->m + (j - 1)] = s[0];
@@ -128,6 +134,7 @@ struct OpMgs {
 // L_j: w -= h_jj v_j; ||w||^2 -> Givens update, history, stopping, back-solve.
 struct OpLast {
   static constexpr int D = 1;
+  static constexpr int NV = 2;
   static constexpr bool kSpmv = false;
   const double* Wj;
   double* Wn;
@@ -141,9 +148,10 @@ struct OpLast {
     invj = st->inv[j];
     return true;
   }
+  __device__ const double* vin(int k) const { return k == 0 ? Wj : Wn; }
   __device__ double gather(int) const { return 0.0; }
-  __device__ void row(int q, double, double (&c)[1]) const {
-    const double w = __fma_rn(mh, __ldg(Wj + q) * invj, Wn[q]);
+  __device__ void row(int q, double, const double (&v)[NV], double (&c)[1]) const {
+    const double w = __fma_rn(mh, v[0] * invj, v[1]);
     Wn[q] = w;
     c[0] = w * w;
   }
@@ -232,6 +240,7 @@ struct OpLast {
 // X: x += sum_{k=1..K} y_k v_k (k ascending)
 struct OpXupd {
   static constexpr int D = 0;
+  static constexpr int NV = 1;
   static constexpr bool kSpmv = false;
   const double* W;
   double* x;
@@ -246,9 +255,10 @@ struct OpXupd {
     inv = st->inv;
     return true;
   }
+  __device__ const double* vin(int) const { return x; }
   __device__ double gather(int) const { return 0.0; }
-  __device__ void row(int q, double, double (&)[1]) const {
-    double xv = x[q];
+  __device__ void row(int q, double, const double (&v)[NV], double (&)[1]) const {
+    double xv = v[0];
     for (int k = 0; k < K; ++k) xv = __fma_rn(__ldg(y + k), __ldg(W + (size_t)k * n + q) * __ldg(inv + k + 1), xv);
     x[q] = xv;
   }

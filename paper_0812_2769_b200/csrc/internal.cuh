@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include "common.cuh"
+#include "stream.cuh"
 #include "gsk.h"
 
 namespace gsk {
@@ -33,14 +34,8 @@ extern std::atomic<int64_t> g_launches;
     }                                           \
   } while (0)
 
-// Tile geometry of one pass kind: CTAs of `rows` rows, groups of 256 tiles.
-struct TileGeo {
-  int rows = 0, ntiles = 0, ngroups = 0, gnp2 = 1;
-};
-// Vector passes use 2048-row tiles (SUB_V windows), SpMV passes 1024 (SUB_S).
 struct Geometry {
   int n = 0;
-  TileGeo v, s;
 };
 Geometry make_geometry(int n);
 
@@ -82,9 +77,8 @@ struct gsk_plan {
   int64_t nchunks = 0, nslots = 0;
   // reduction scratch
   static constexpr int NSLOT = 16;  // reduction slots (one per pass kind)
-  double* part = nullptr;      // [MAXD][ntiles]
-  double* gpart = nullptr;     // [MAXD][ngroups]
-  unsigned* tickets = nullptr; // [NSLOT] + [NSLOT][ngroups] group tickets
+  double* part = nullptr;      // [MAXD][256] CTA partials
+  unsigned* tickets = nullptr; // [NSLOT]
   double* scratch = nullptr;   // [n] (residual norms)
   cudaStream_t st = nullptr;
   int* h_flag = nullptr;       // pinned
@@ -122,23 +116,38 @@ struct gsk_plan {
 namespace gsk {
 // Launch one fused pass over the plan's rows: Op::kSpmv selects an SpMV pass in the
 // plan's format (CSR or SELL) or a pure vector pass.
-template <class Op>
-int run_pass(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
-  const TileGeo& g = Op::kSpmv ? P->geo.s : P->geo.v;
-  const int gmax = std::max(P->geo.v.ngroups, P->geo.s.ngroups);
-  Red red{P->part, P->gpart, P->tickets + gsk_plan::NSLOT + (size_t)slot * gmax, P->tickets + slot,
-          g.ntiles, g.ngroups, g.gnp2};
-  Tiles tl{P->geo.n};
-  if constexpr (!Op::kSpmv) {
-    fused_pass<0, Op><<<g.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
-  } else {
-    if (P->fmt == GSK_FMT_SELL)
-      fused_pass<2, Op><<<g.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
-    else
-      fused_pass<1, Op><<<g.ntiles, TB, 0, s>>>(P->csr, P->sell, tl, op, red);
+int num_sms();
+
+// Launch one pass of the streaming engine: an SpMV pass in the plan's format (CSR
+// or SELL) or a vector pass; persistent grid of at most 2 CTAs per SM.
+template <int FMT, class Op>
+int launch_stream(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    GSK_CUDA(cudaFuncSetAttribute(stream_pass<FMT, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  st_dyn_smem()));
+    attr = true;
   }
+  const int n = P->geo.n;
+  const int rows = FMT == 0 ? VecTile<Op::NV>::W * TB : TB;
+  const int ntiles = (n + rows - 1) / rows;
+  int tpc = 1;  // tiles per CTA: pow2 with at most 256 CTAs (aligned blocks of the tree)
+  while ((ntiles + tpc - 1) / tpc > 256) tpc <<= 1;
+  const int grid = (ntiles + tpc - 1) / tpc;
+  Red red{P->part, P->tickets + slot, tpc, ntiles};
+  stream_pass<FMT, Op><<<grid, ST_THREADS, st_dyn_smem(), s>>>(P->csr, P->sell, n, ntiles, op, red);
   GSK_LAUNCHED(1);
   return GSK_OK;
+}
+
+template <class Op>
+int run_pass(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
+  if constexpr (!Op::kSpmv) {
+    return launch_stream<0>(P, op, slot, s);
+  } else {
+    if (P->fmt == GSK_FMT_SELL) return launch_stream<2>(P, op, slot, s);
+    return launch_stream<1>(P, op, slot, s);
+  }
 }
 #define GSK_TRY(x)              \
   do {                          \

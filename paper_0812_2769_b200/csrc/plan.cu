@@ -21,38 +21,32 @@ void set_error(const char* fmt, ...) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-static TileGeo tile_geo(int n, int rows) {
-  TileGeo g;
-  g.rows = rows;
-  g.ntiles = (n + rows - 1) / rows;
-  g.ngroups = (g.ntiles + TB - 1) / TB;
-  g.gnp2 = 1;
-  while (g.gnp2 < g.ngroups) g.gnp2 <<= 1;
-  return g;
-}
-
 Geometry make_geometry(int n) {
   Geometry g;
   g.n = n;
-  g.v = tile_geo(n, TB * SUB_V);
-  g.s = tile_geo(n, TB * SUB_S);
   return g;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
 }
 
 // Reduction scratch of a geometry: tile and group partials, slot and group tickets.
 int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
-  const Geometry& geo = P->geo;
-  const size_t nt_max = std::max(geo.v.ntiles, geo.s.ntiles);
-  const size_t ng_max = std::max(geo.v.ngroups, geo.s.ngroups);
-  const size_t nt = sizeof(unsigned) * gsk_plan::NSLOT * (1 + ng_max);
+  const size_t nt = sizeof(unsigned) * gsk_plan::NSLOT;
   if (async) {
-    GSK_CUDA(cudaMallocAsync(&P->part, sizeof(double) * MAXD * nt_max, s));
-    GSK_CUDA(cudaMallocAsync(&P->gpart, sizeof(double) * MAXD * ng_max, s));
+    GSK_CUDA(cudaMallocAsync(&P->part, sizeof(double) * MAXD * 256, s));
     GSK_CUDA(cudaMallocAsync(&P->tickets, nt, s));
     GSK_CUDA(cudaMemsetAsync(P->tickets, 0, nt, s));
   } else {
-    GSK_CUDA(cudaMalloc(&P->part, sizeof(double) * MAXD * nt_max));
-    GSK_CUDA(cudaMalloc(&P->gpart, sizeof(double) * MAXD * ng_max));
+    GSK_CUDA(cudaMalloc(&P->part, sizeof(double) * MAXD * 256));
     GSK_CUDA(cudaMalloc(&P->tickets, nt));
     GSK_CUDA(cudaMemset(P->tickets, 0, nt));
   }
@@ -62,23 +56,27 @@ int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
 // ---- ops --------------------------------------------------------------------------
 struct OpSpmv {
   static constexpr int D = 0;
+  static constexpr int NV = 0;
   static constexpr bool kSpmv = true;
   const double* x;
   double* y;
   __device__ bool begin() { return true; }
+  __device__ const double* vin(int) const { return nullptr; }
   __device__ double gather(int c) const { return __ldg(x + c); }
-  __device__ void row(int i, double v, double (&)[1]) const { y[i] = v; }
+  __device__ void row(int i, double v, const double (&)[1], double (&)[1]) const { y[i] = v; }
 };
 
 struct OpDot {
   static constexpr int D = 1;
+  static constexpr int NV = 2;
   static constexpr bool kSpmv = false;
   const double* a;
   const double* b;
   double* out;
   __device__ bool begin() { return true; }
+  __device__ const double* vin(int k) const { return k == 0 ? a : b; }
   __device__ double gather(int) const { return 0.0; }
-  __device__ void row(int i, double, double (&c)[1]) const { c[0] = __ldg(a + i) * __ldg(b + i); }
+  __device__ void row(int, double, const double (&v)[NV], double (&c)[1]) const { c[0] = v[0] * v[1]; }
   __device__ void finish(const double (&s)[1], int lane) const {
     if (lane == 0) *out = s[0];
   }
@@ -87,16 +85,18 @@ struct OpDot {
 // ||w o (b - A x)||^2
 struct OpResNorm {
   static constexpr int D = 1;
+  static constexpr int NV = 2;
   static constexpr bool kSpmv = true;
   const double* x;
   const double* b;
   const double* w;
   double* out;
   __device__ bool begin() { return true; }
+  __device__ const double* vin(int k) const { return k == 0 ? b : w; }
   __device__ double gather(int c) const { return __ldg(x + c); }
-  __device__ void row(int i, double y, double (&c)[1]) const {
-    const double r = b[i] - y;
-    const double u = w ? w[i] * r : r;
+  __device__ void row(int, double y, const double (&v)[NV], double (&c)[1]) const {
+    const double r = v[0] - y;
+    const double u = w ? v[1] * r : r;
     c[0] = u * u;
   }
   __device__ void finish(const double (&s)[1], int lane) const {
@@ -223,7 +223,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
-  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->gpart, P->tickets, P->scratch,
+  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->tickets, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -293,7 +293,6 @@ int gsk_dot(int64_t n, const double* a, const double* b, double* result, void* s
   if (rc == GSK_OK && cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     rc = GSK_E_CUDA;
   cudaFreeAsync(tmp.part, s);
-  cudaFreeAsync(tmp.gpart, s);
   cudaFreeAsync(tmp.tickets, s);
   cudaFreeAsync(out, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) rc = GSK_E_CUDA;

@@ -20,7 +20,7 @@ def main(rep):
     print("kernel".ljust(22), " ".join(s.rjust(9) for s in SHORT))
     for row in rows[2:]:
         name = row[idx["Kernel Name"]]
-        m = re.search(r"fused_pass<(\d), gsk::(\w+)>", name)
+        m = re.search(r"(?:fused|stream)_pass<(\d), gsk::(\w+)>", name)
         nm = f"{m.group(1)} {m.group(2)}" if m else name.split("(")[0][-22:]
         print(nm.ljust(22), " ".join(row[idx[c]][:9].rjust(9) if c in idx else "-".rjust(9) for c in WANT))
 
