@@ -106,9 +106,15 @@ class Clocks:
 
 
 def byte_model(n, nnz):
+    """Algorithmic bytes per launch; B_A = 12 nnz + 4(n+1)."""
     BA = 12 * nnz + 4 * (n + 1)
-    return {"spmv": BA + 16 * n, "bicg_p1": BA + 48 * n, "bicg_p2": BA + 24 * n,
-            "bicg_iter": 2 * BA + 17 * 8 * n, "gs": 16 * nnz + 4 * (n + 1) + 24 * n}
+    return {"spmv": BA + 16 * n, "gs": 16 * nnz + 4 * (n + 1) + 24 * n,
+            # fused schedule: P1 gathers r, p, v and writes p, v (+ r^ own row); P2 r, v -> t
+            "bicg_p1": BA + 48 * n, "bicg_p2": BA + 24 * n,
+            # split schedule: S1 v = A p (p gather, r^, v), S3 t = A s (s gather, t)
+            "bicg_s1": BA + 24 * n, "bicg_s3": BA + 16 * n,
+            "bicg_iter": 2 * BA + 17 * 8 * n, "bicg_iter_split": 2 * BA + 19 * 8 * n,
+            "gmres_mgs": 32 * n, "gmres_arnoldi": BA + 24 * n}
 
 
 def oracle_sample(sys_, cfg, m, kb=3, kg=3):
@@ -147,6 +153,11 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def plan_schedule(args):
+    """Bi-CGSTAB schedule the plan runs (auto = split)."""
+    return "fused" if args.schedule == "fused" else "split"
 
 
 def reduce_over_ranks(ms, its, dist, device):
@@ -246,11 +257,15 @@ def main():
     hbm, src = peaks()
     p1_ms = probes[0]
     roof = None
+    split = plan_schedule(args) == "split"
     if p1_ms:
-        ach = bm["bicg_p1"] / (p1_ms / 1e3) / 1e9
+        key = "bicg_s1" if split else "bicg_p1"
+        ach = bm[key] / (p1_ms / 1e3) / 1e9
+        kname = ("pass_kernel<SELL, OpS1> (v = A p, <r^,v>)" if split
+                 else "pass_kernel<SELL, OpP1> (p update at the gather, v = A p, <r^,v>)")
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": None, "kernel": "fused_pass<SELL, OpP1> (v = A p, <r^,v>)",
-                "bytes_per_launch": bm["bicg_p1"], "ms_per_launch": p1_ms, "peak_source": src}
+                "traffic": None, "kernel": kname, "bytes_per_launch": bm[key], "ms_per_launch": p1_ms,
+                "peak_source": src, "frac_of_8TBps": ach / 8000.0}
 
     # SpMV standalone roofline (same plan, 50 back-to-back launches)
     x = torch.tensor(workloads.uniform(n, 9, 9), device="cuda")
@@ -272,18 +287,25 @@ def main():
         "bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
                      "relres": r1["relres"], "true_relres": r1["true_relres"], "solve_ms": r1["solve_ms"],
                      "iters_per_s": r1["iterations"] / (r1["solve_ms"] / 1e3) if r1["solve_ms"] else None,
-                     "gbps_model": bm["bicg_iter"] * r1["iterations"] / (r1["solve_ms"] / 1e3) / 1e9
-                     if r1["solve_ms"] else None},
+                     "gbps_model": bm["bicg_iter_split" if split else "bicg_iter"] * r1["iterations"]
+                     / (r1["solve_ms"] / 1e3) / 1e9 if r1["solve_ms"] else None,
+                     "gbps_17vector_model": bm["bicg_iter"] * r1["iterations"] / (r1["solve_ms"] / 1e3) / 1e9
+                     if r1["solve_ms"] else None, "schedule": plan_schedule(args)},
         "gmres": {"m": m, "iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
                   "relres": r2["relres"], "true_relres": r2["true_relres"], "solve_ms": r2["solve_ms"],
                   "iters_per_s": r2["iterations"] / (r2["solve_ms"] / 1e3) if r2["solve_ms"] else None},
         "spmv": {"ms": spmv_ms, "gbps": spmv_gbps, "frac_of_hbm": spmv_gbps / hbm,
                  "frac_of_8TBps": spmv_gbps / 8000.0},
-        "probe_ms": {"bicg_p1": probes[0], "bicg_p2": probes[1], "gmres_mgs": probes[2],
+        "probe_ms": {"bicg_v_pass": probes[0], "bicg_t_pass": probes[1], "gmres_mgs": probes[2],
                      "gmres_arnoldi_spmv": probes[3]},
+        "probe_gbps": {"bicg_v_pass": bm["bicg_s1" if split else "bicg_p1"] / (probes[0] / 1e3) / 1e9
+                       if probes[0] else None,
+                       "bicg_t_pass": bm["bicg_s3" if split else "bicg_p2"] / (probes[1] / 1e3) / 1e9
+                       if probes[1] else None,
+                       "gmres_mgs": bm["gmres_mgs"] / (probes[2] / 1e3) / 1e9 if probes[2] else None,
+                       "gmres_arnoldi_spmv": bm["gmres_arnoldi"] / (probes[3] / 1e3) / 1e9
+                       if probes[3] else None},
     }
-    if roof:
-        extra["bicg_p1_frac_of_8TBps"] = roof["achieved"] / 8000.0
 
     e2e = None
     if not args.no_e2e:

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsk.so")
+LIB_PATH = os.environ.get("GSK_LIB") or os.path.join(_HERE, "libgsk.so")  # GSK_LIB: A/B builds
 
 GSK_OK, GSK_E_INVALID, GSK_E_ZERO_ROW, GSK_E_CUDA, GSK_E_NOMEM = 0, -1, -2, -3, -4
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}

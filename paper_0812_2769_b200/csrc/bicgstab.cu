@@ -415,8 +415,6 @@ struct OpFinal {  // true residual ||b - A x|| (unweighted and weighted)
   }
 };
 
-static int passes_per_iter(const gsk_plan* P) { return P->bmode == 1 ? 3 : 5; }
-
 static int batch_size(const gsk_plan* P) {
   int K = P->poll;
   if (K <= 0) {
@@ -426,7 +424,7 @@ static int batch_size(const gsk_plan* P) {
   return (K + 1) & ~1;  // even: p/v buffer parity repeats per replay
 }
 
-static int capture_bicg(gsk_plan* P, const double* b, double* x, int K, int copy, cudaGraphExec_t* out) {
+static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t* out) {
   const int n = P->A.n;
   double* V = P->bvec;
   double *r = V, *rh = V + (size_t)n, *pa = V + 2 * (size_t)n, *pb = V + 3 * (size_t)n,
@@ -434,24 +432,18 @@ static int capture_bicg(gsk_plan* P, const double* b, double* x, int K, int copy
   const double* w = P->weights;
   cudaStream_t s = P->st;
   GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  int rc = GSK_OK;
-  auto probe = [&](int kind, int edge) {
-    return cudaEventRecordWithFlags(P->pev[kind][copy][edge], s, cudaEventRecordExternal);
-  };
-  for (int k = 0; k < K && rc == GSK_OK; ++k) {
+  int rc = 0;
+  auto ev = [&](int kind, int edge, int k) { return k == 0 ? P->pev[kind][copy][edge] : nullptr; };
+  for (int k = 0; k < K && rc >= 0; ++k) {
     if (P->bmode == 1) {  // fused 3-pass schedule
       double *po = (k & 1) ? pb : pa, *vo = (k & 1) ? vb : va;
       double *pn = (k & 1) ? pa : pb, *vn = (k & 1) ? va : vb;
       OpP1 p1{r, po, vo, rh, pn, vn, P->bstate, 0, 0};
       OpP2 p2{r, vn, w, t, P->hist_d, P->bstate, 0};
       OpP3 p3{vn, pn, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0};
-      if (k == 0 && probe(0, 0) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, p1, 1, s);
-      if (k == 0 && rc == GSK_OK && probe(0, 1) != cudaSuccess) rc = GSK_E_CUDA;
-      if (k == 0 && rc == GSK_OK && probe(1, 0) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, p2, 2, s);
-      if (k == 0 && rc == GSK_OK && probe(1, 1) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, p3, 3, s);
+      rc = run_pass(P, p1, s, ev(0, 0, k), ev(0, 1, k));
+      if (rc >= 0) rc = run_pass(P, p2, s, ev(1, 0, k), ev(1, 1, k));
+      if (rc >= 0) rc = run_pass(P, p3, s);
     } else {  // split 5-pass schedule: p = pa, v = va, s = pb
       double *p = pa, *v = va, *sv = pb;
       OpS0 s0{r, v, p, P->bstate, 0, 0};
@@ -459,36 +451,14 @@ static int capture_bicg(gsk_plan* P, const double* b, double* x, int K, int copy
       OpS2 s2{r, v, w, sv, P->hist_d, P->bstate, 0};
       OpS3 s3{sv, t, P->bstate};
       OpS4 s4{sv, p, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0};
-      rc = run_pass(P, s0, 5, s);
-      if (k == 0 && rc == GSK_OK && probe(0, 0) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, s1, 1, s);
-      if (k == 0 && rc == GSK_OK && probe(0, 1) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, s2, 6, s);
-      if (k == 0 && rc == GSK_OK && probe(1, 0) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, s3, 2, s);
-      if (k == 0 && rc == GSK_OK && probe(1, 1) != cudaSuccess) rc = GSK_E_CUDA;
-      if (rc == GSK_OK) rc = run_pass(P, s4, 3, s);
+      rc = run_pass(P, s0, s);
+      if (rc >= 0) rc = run_pass(P, s1, s, ev(0, 0, k), ev(0, 1, k));
+      if (rc >= 0) rc = run_pass(P, s2, s);
+      if (rc >= 0) rc = run_pass(P, s3, s, ev(1, 0, k), ev(1, 1, k));
+      if (rc >= 0) rc = run_pass(P, s4, s);
     }
   }
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(s, &g);
-  if (rc != GSK_OK) {
-    if (g) cudaGraphDestroy(g);
-    return rc;
-  }
-  if (e != cudaSuccess) {
-    set_error("bicgstab graph capture: %s", cudaGetErrorString(e));
-    return GSK_E_CUDA;
-  }
-  e = cudaGraphInstantiate(out, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) {
-    set_error("bicgstab graph instantiate: %s", cudaGetErrorString(e));
-    return GSK_E_CUDA;
-  }
-  // the launches recorded during capture are counted per replay instead
-  g_launches.fetch_sub((long long)passes_per_iter(P) * K);
-  return GSK_OK;
+  return end_capture(s, rc, out, &P->bkernels, "bicgstab");
 }
 
 static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double tol, int maxit,
@@ -508,8 +478,8 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    GSK_TRY(capture_bicg(P, b, x, K, 0, &P->bgraph[0]));
-    GSK_TRY(capture_bicg(P, b, x, K, 1, &P->bgraph[1]));
+    GSK_TRY(capture_bicg(P, x, K, 0, &P->bgraph[0]));
+    GSK_TRY(capture_bicg(P, x, K, 1, &P->bgraph[1]));
     P->bkey_b = b;
     P->bkey_x = x;
     P->bK = K;
@@ -529,13 +499,13 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   GSK_CUDA(cudaMemcpyAsync(P->bstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   double* V = P->bvec;
   OpInit init{x, b, P->weights, V, V + (size_t)n, V + 2 * (size_t)n, V + 4 * (size_t)n, P->hist_d, P->bstate};
-  GSK_TRY(run_pass(P, init, 0, s));
+  if (run_pass(P, init, s) < 0) return GSK_E_CUDA;
   // batches of K iterations; the next batch is queued before the flag of the
   // previous one is read, so the GPU never idles on the host check
   const long long maxb = (maxit + K - 1) / K + 1;
   long long nb = 0;
   GSK_CUDA(cudaGraphLaunch(P->bgraph[0], s));
-  g_launches.fetch_add((long long)passes_per_iter(P) * K);
+  g_launches.fetch_add(P->bkernels);
   ++nb;
   cudaEvent_t ev;
   GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -546,7 +516,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
     const bool more = nb < maxb;
     if (more) {
       GSK_CUDA(cudaGraphLaunch(P->bgraph[nb & 1], s));
-      g_launches.fetch_add((long long)passes_per_iter(P) * K);
+      g_launches.fetch_add(P->bkernels);
       ++nb;
     }
     GSK_CUDA(cudaEventSynchronize(ev));
@@ -561,7 +531,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   }
   cudaEventDestroy(ev);
   OpFinal fin{x, b, P->weights, P->bstate};
-  GSK_TRY(run_pass(P, fin, 4, s));
+  if (run_pass(P, fin, s) < 0) return GSK_E_CUDA;
   GSK_CUDA(cudaEventRecord(P->t1, s));
   BicgState hs{};
   GSK_CUDA(cudaMemcpyAsync(&hs, P->bstate, sizeof hs, cudaMemcpyDeviceToHost, s));

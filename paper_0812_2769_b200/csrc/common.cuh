@@ -12,7 +12,7 @@ namespace gsk {
 constexpr int TB = 256;         // threads per CTA = rows per sub-tile = SELL sigma
 constexpr int SELL_C = 32;      // SELL chunk height (one warp)
 constexpr int SELL_SIGMA = 256; // SELL sorting window
-constexpr int CSR_CAP = 2048;   // entries of a 256-row CSR window staged in smem (GS)
+constexpr int CSR_CAP = 1792;   // entries of a 256-row CSR window staged in smem (7 per row)
 constexpr int MAXD = 3;         // max dot products fused into one pass
 
 struct CsrView {
@@ -29,17 +29,6 @@ struct SellView {
   const int* __restrict__ scol;     // [nslots], -1 = padding
   const double* __restrict__ sval;  // [nslots]
   const uint8_t* __restrict__ roff; // [nchunks*32] in-window row offset
-};
-
-// Reduction bookkeeping of one pass.  CTA b owns the contiguous tiles
-// [b*tpc, (b+1)*tpc) (tpc a power of two, at most 256 CTAs), so its partial is an
-// aligned power-of-two block of the canonical tree (AC-5); the last CTA to arrive
-// (ticket) reduces the CTA partials and runs the scalar epilogue on the device.
-struct Red {
-  double* part;      // [D][256] CTA partials
-  unsigned* ticket;  // arrival counter (self-resetting)
-  int tpc;           // tiles per CTA (pow2)
-  int ntiles;
 };
 
 __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }

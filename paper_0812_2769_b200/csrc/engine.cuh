@@ -1,0 +1,317 @@
+// engine.cuh — the row-pass engine of libgsk (sm_100a).
+//
+// Every hot pass of the solvers is `pass_kernel<FMT, Op>` followed, when it reduces
+// dot products, by `finish_kernel<Op>`:
+//
+//   pass_kernel   CTA of 256 threads owning `wpc` consecutive 256-row windows.
+//                 SpMV passes (FMT 1 CSR, 2 SELL) compute y for each window (CSR rows
+//                 staged through shared memory with coalesced loads; SELL chunks of
+//                 32 rows, one per warp, scattered back to canonical row order), then
+//                 the Op's row epilogue runs in canonical order (thread t <-> row t of
+//                 the window) and yields the dot-product leaves.  Vector passes
+//                 (FMT 0) give each thread one row of each window, all loads in
+//                 flight together.  Each window's leaves are reduced by warp
+//                 butterflies (= trees of 32 leaves); warp 0 finishes the trees of 8
+//                 warps and the tree over the CTA's windows, and writes ONE partial
+//                 per CTA.  No fences, no atomics: the CTA ends as soon as its stores
+//                 are issued.
+//   finish_kernel one CTA of 1024 threads reduces the CTA partials with the same
+//                 canonical tree (AC-5) and runs the Op's scalar
+//                 epilogue (alpha, omega, Givens, stopping tests, ...) on the device.
+//
+// Shared-memory scatter buffers and CSR stages are double-buffered by window parity,
+// so a window costs one __syncthreads.  Kernels are compiled with --fmad=false; every
+// FMA is an explicit __fma_rn (AC-2).
+#pragma once
+#include "common.cuh"
+
+namespace gsk {
+
+constexpr int FIN_THREADS = 1024;
+constexpr int FIN_LEAVES = 8;                          // partials per finish thread
+constexpr int FIN_ROUND = FIN_THREADS * FIN_LEAVES;    // 8192 partials per round
+
+struct CsrStage {
+  double v[CSR_CAP];
+  int c[CSR_CAP];
+};
+
+template <int FMT>
+struct PassSmem;
+template <>
+struct PassSmem<0> {
+  double wp[8 * MAXD * 8];  // [window][d][warp]
+};
+template <>
+struct PassSmem<1> {
+  CsrStage st[2];
+  double wp[8 * MAXD * 8];
+};
+template <>
+struct PassSmem<2> {
+  double sy[2][TB];
+  double wp[8 * MAXD * 8];
+};
+
+// Register budget per pass kind (CTAs per SM): SELL keeps 8 slots (col, val, x) in
+// flight per lane, vector passes RPT rows of NV operands; CSR is bounded by its
+// double-buffered 43 KB stage.
+// Rows per thread of a vector pass with NV own-row operands (all loads in flight).
+template <int NV>
+struct VecRpt {
+  static constexpr int value = NV <= 3 ? 8 : 4;
+};
+
+#ifndef GSK_SELL_MINB_DOT
+#define GSK_SELL_MINB_DOT 3
+#endif
+template <int FMT, int D>
+struct PassOcc {
+  // SELL: plain SpMV fits 64 registers (4 CTAs/SM, measured 93% of the copy peak);
+  // with a fused dot epilogue 64 registers spill, so 3 CTAs/SM unless overridden.
+  static constexpr int kMinBlocks = FMT == 1 ? 4 : FMT == 2 ? (D == 0 ? 4 : GSK_SELL_MINB_DOT) : 3;
+};
+
+// y for row r0 + t of a CSR window (AC-3 chain), staged through st.
+template <class G>
+__device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& g, CsrStage& st) {
+  const int t = threadIdx.x, r = r0 + t;
+  const int rend = min(r0 + TB, A.n);
+  const int s0 = A.rp[r0], s1 = A.rp[rend];
+  const int cnt = s1 - s0;
+  double acc = 0.0;
+  if (cnt <= CSR_CAP) {  // uniform over the CTA
+    for (int k = t; k < cnt; k += TB) {
+      st.v[k] = __ldcs(A.v + s0 + k);
+      st.c[k] = __ldcs(A.ci + s0 + k);
+    }
+    __syncthreads();
+    if (r < A.n) {
+      const int a = A.rp[r] - s0, b = A.rp[r + 1] - s0;
+      for (int k = a; k < b; ++k) acc = __fma_rn(st.v[k], g(st.c[k]), acc);
+    }
+  } else if (r < A.n) {
+    for (int k = A.rp[r]; k < A.rp[r + 1]; ++k) acc = __fma_rn(__ldcs(A.v + k), g(__ldcs(A.ci + k)), acc);
+  }
+  return acc;
+}
+
+// y for row r0 + t of a SELL window: lane l of warp w computes slot l of chunk
+// r0/32 + w; results are scattered to sy at the rows' in-window offsets.
+template <class G>
+__device__ __forceinline__ double sell_window(const SellView& A, int r0, const G& g, double* sy) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int c = (r0 >> 5) + warp;
+  if (c < A.nchunks) {
+    const int rl = A.roff[c * SELL_C + lane];
+    const int p0 = A.cptr[c], L = (A.cptr[c + 1] - p0) >> 5;
+    const int base = p0 + lane;
+    double acc = 0.0;
+    if (L <= 8) {
+      int cols[8];
+      double vals[8], xs[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L) {
+          cols[k] = __ldcs(A.scol + base + k * SELL_C);
+          vals[k] = __ldcs(A.sval + base + k * SELL_C);
+        }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L && cols[k] >= 0) xs[k] = g(cols[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L && cols[k] >= 0) acc = __fma_rn(vals[k], xs[k], acc);
+    } else {
+      for (int k = 0; k < L; ++k) {
+        const int col = __ldcs(A.scol + base + k * SELL_C);
+        if (col >= 0) acc = __fma_rn(__ldcs(A.sval + base + k * SELL_C), g(col), acc);
+      }
+    }
+    sy[rl] = acc;
+  }
+  __syncthreads();
+  return sy[t];
+}
+
+// Own-row operands of the Op for row i.
+template <class Op>
+__device__ __forceinline__ void load_vin(const Op& op, int i, double (&v)[Op::NV > 0 ? Op::NV : 1]) {
+#pragma unroll
+  for (int k = 0; k < Op::NV; ++k) {
+    const double* src = op.vin(k);
+    v[k] = src ? __ldg(src + i) : 0.0;
+  }
+}
+
+// Warp butterflies of one window's leaves (= trees of 32 leaves); lane 0 records the
+// warp's value.
+template <int D>
+__device__ __forceinline__ void warp_leaves(double (&c)[D], double* wp, int w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) c[d] = c[d] + __shfl_xor_sync(0xffffffffu, c[d], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) wp[(w * MAXD + d) * 8 + warp] = c[d];
+  }
+}
+
+// Warp 0, after a __syncthreads: trees of 8 warps per window, then the tree over the
+// CTA's windows; lane 0 writes the CTA partial.  Windows beyond nw (pow2 <= 8) enter
+// as +0 leaves: x + 0 = x, and the final + 0.0 of AC-5 canonicalises a zero's sign.
+template <int D>
+__device__ __forceinline__ void cta_partial(const double* wp, int nw, double* part, int stride) {
+  const int lane = threadIdx.x & 31;
+  double a[D][8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double u = (lane < 8 && w < nw) ? wp[(w * MAXD + d) * 8 + lane] : 0.0;
+      u = u + __shfl_xor_sync(0xffffffffu, u, 1);
+      u = u + __shfl_xor_sync(0xffffffffu, u, 2);
+      u = u + __shfl_xor_sync(0xffffffffu, u, 4);
+      a[d][w] = u;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double s = ((a[d][0] + a[d][1]) + (a[d][2] + a[d][3])) + ((a[d][4] + a[d][5]) + (a[d][6] + a[d][7]));
+      part[(size_t)d * stride + blockIdx.x] = s;
+    }
+  }
+}
+
+// FMT 0: vector pass, RPT windows (rows r0 + 256 w + t) per CTA, all loads in flight.
+// FMT 1/2: SpMV pass over wpc windows.
+template <int FMT, int RPT, class Op>
+__global__ void __launch_bounds__(TB, PassOcc<FMT, Op::D>::kMinBlocks)
+    pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
+  if (!op.begin()) return;
+  constexpr int D = Op::D;
+  constexpr int DD = D > 0 ? D : 1;
+  constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
+  __shared__ PassSmem<FMT> sm;
+  const int t = threadIdx.x, warp = t >> 5;
+  if constexpr (FMT == 0) {
+    const int r0 = blockIdx.x * (TB * RPT);
+    double v[RPT][NVA];
+#pragma unroll
+    for (int w = 0; w < RPT; ++w) {
+      const int i = r0 + w * TB + t;
+      if (i < n) load_vin(op, i, v[w]);
+    }
+    double cc[RPT][DD];
+#pragma unroll
+    for (int w = 0; w < RPT; ++w) {
+      const int i = r0 + w * TB + t;
+#pragma unroll
+      for (int d = 0; d < DD; ++d) cc[w][d] = 0.0;
+      if (i < n) op.row(i, 0.0, v[w], cc[w]);
+    }
+    if constexpr (D > 0) {
+#pragma unroll
+      for (int w = 0; w < RPT; ++w) warp_leaves<D>(cc[w], sm.wp, w);
+      __syncthreads();
+      if (warp == 0) cta_partial<D>(sm.wp, RPT, part, stride);
+    }
+  } else {
+    const int rb = blockIdx.x * wpc * TB;
+    for (int w = 0; w < wpc; ++w) {
+      const int r0 = rb + w * TB;
+      double cc[DD];
+#pragma unroll
+      for (int d = 0; d < DD; ++d) cc[d] = 0.0;
+      if (r0 < n) {  // uniform over the CTA
+        auto g = [&](int col) { return op.gather(col); };
+        const int i = r0 + t;
+        double v[NVA];
+        if (i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
+        double y;
+        if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
+        else y = sell_window(sell, r0, g, sm.sy[w & 1]);
+        if (i < n) op.row(i, y, v, cc);
+      }
+      if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);
+    }
+    if constexpr (D > 0) {
+      __syncthreads();
+      if (warp == 0) cta_partial<D>(sm.wp, wpc, part, stride);
+    }
+  }
+}
+
+// One CTA: canonical tree over ntiles CTA partials (pow2-padded with +0), + 0.0, then
+// the Op's scalar epilogue on warp 0.  Skipped exactly when the pass was skipped
+// (op.begin() reads the same device flags; only finish kernels change them).
+template <class Op>
+__global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double* part, int stride,
+                                                             int ntiles) {
+  if (!op.begin()) return;
+  constexpr int D = Op::D;
+  __shared__ double ws[D][32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double stk[D][24];
+  int lvl[24];
+  int sp = 0;
+  int np2 = 1;
+  while (np2 < ntiles) np2 <<= 1;
+  const int rounds = np2 > FIN_ROUND ? np2 / FIN_ROUND : 1;
+  const int per = np2 > FIN_ROUND ? FIN_LEAVES : (np2 + FIN_THREADS - 1) / FIN_THREADS;  // leaves per thread
+  for (int r = 0; r < rounds; ++r) {
+    double u[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      // leaves [base, base + per) of this thread: pairwise tree (per is 1, 2, 4 or 8)
+      const int base = r * FIN_ROUND + t * per;
+      double l[FIN_LEAVES];
+#pragma unroll
+      for (int q = 0; q < FIN_LEAVES; ++q) l[q] = (q < per && base + q < ntiles) ? part[(size_t)d * stride + base + q] : 0.0;
+      for (int len = per; len > 1; len >>= 1)
+        for (int q = 0; q < len / 2; ++q) l[q] = l[2 * q] + l[2 * q + 1];
+      u[d] = l[0];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) u[d] = u[d] + __shfl_xor_sync(0xffffffffu, u[d], off);
+    }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) ws[d][warp] = u[d];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double x = ws[d][lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) x = x + __shfl_xor_sync(0xffffffffu, x, off);
+        u[d] = x;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) stk[d][sp] = u[d];
+        lvl[sp] = 0;
+        ++sp;
+        while (sp >= 2 && lvl[sp - 1] == lvl[sp - 2]) {
+#pragma unroll
+          for (int d = 0; d < D; ++d) stk[d][sp - 2] = stk[d][sp - 2] + stk[d][sp - 1];
+          lvl[sp - 2] += 1;
+          --sp;
+        }
+      }
+    }
+  }
+  if (warp == 0) {
+    double s[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) s[d] = __shfl_sync(0xffffffffu, lane == 0 ? stk[d][0] : 0.0, 0) + 0.0;
+    op.finish(s, lane);
+  }
+}
+
+}  // namespace gsk

@@ -270,56 +270,28 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
   GmresState* st = P->gstate;
   auto slot = [&](int j) { return P->W + (size_t)(j - 1) * n; };
   GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  int rc = GSK_OK;
-  int nk = 0;
-  for (int j = 1; j <= m && rc == GSK_OK; ++j) {
+  int rc = 0;
+  for (int j = 1; j <= m && rc >= 0; ++j) {
     OpArnoldi a{slot(j), slot(1), slot(j + 1), st, j, 0, 0};
-    if (j == 1) GSK_CUDA(cudaEventRecordWithFlags(P->pev[3][copy][0], s, cudaEventRecordExternal));
-    rc = run_pass(P, a, 0, s);
-    if (j == 1) GSK_CUDA(cudaEventRecordWithFlags(P->pev[3][copy][1], s, cudaEventRecordExternal));
-    ++nk;
-    for (int i = 1; i < j && rc == GSK_OK; ++i) {
+    rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
+    for (int i = 1; i < j && rc >= 0; ++i) {
       OpMgs mg{slot(i), slot(i + 1), slot(j + 1), st, i, j, 0, 0, 0};
-      const bool probe = (j == 2 && i == 1);
-      if (probe) GSK_CUDA(cudaEventRecordWithFlags(P->pev[2][copy][0], s, cudaEventRecordExternal));
-      rc = run_pass(P, mg, 1, s);
-      if (probe) GSK_CUDA(cudaEventRecordWithFlags(P->pev[2][copy][1], s, cudaEventRecordExternal));
-      ++nk;
+      rc = (j == 2 && i == 1) ? run_pass(P, mg, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_pass(P, mg, s);
     }
-    if (rc == GSK_OK) {
+    if (rc >= 0) {
       OpLast l{slot(j), slot(j + 1), P->hist_d, st, j, 0, 0};
-      rc = run_pass(P, l, 2, s);
-      ++nk;
+      rc = run_pass(P, l, s);
     }
   }
-  if (rc == GSK_OK) {
+  if (rc >= 0) {
     OpXupd xu{P->W, x, st, n, 0, nullptr, nullptr};
-    rc = run_pass(P, xu, 3, s);
-    ++nk;
+    rc = run_pass(P, xu, s);
   }
-  if (rc == GSK_OK) {
+  if (rc >= 0) {
     OpGResid r{x, b, P->weights, slot(1), P->hist_d, st, 0};
-    rc = run_pass(P, r, 4, s);
-    ++nk;
+    rc = run_pass(P, r, s);
   }
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(s, &g);
-  if (rc != GSK_OK) {
-    if (g) cudaGraphDestroy(g);
-    return rc;
-  }
-  if (e != cudaSuccess) {
-    set_error("gmres graph capture: %s", cudaGetErrorString(e));
-    return GSK_E_CUDA;
-  }
-  e = cudaGraphInstantiate(out, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) {
-    set_error("gmres graph instantiate: %s", cudaGetErrorString(e));
-    return GSK_E_CUDA;
-  }
-  g_launches.fetch_sub(nk);
-  return GSK_OK;
+  return end_capture(s, rc, out, &P->gkernels, "gmres");
 }
 
 static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, double tol, int maxit,
@@ -361,7 +333,6 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
     P->gkey_m = m;
     P->gkey_h = P->hist_d;
   }
-  const long long kernels_per_cycle = (long long)m * (m + 3) / 2 + 2;
   cudaStream_t s = P->st;
   GSK_TRY(join_in(P, caller));
   GSK_CUDA(cudaEventRecord(P->t0, s));
@@ -384,11 +355,11 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 5 * MAX_M + 8), s));
   GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   OpGResid init{x, b, P->weights, P->W, P->hist_d, P->gstate, 1};
-  GSK_TRY(run_pass(P, init, 4, s));
+  if (run_pass(P, init, s) < 0) return GSK_E_CUDA;
   const long long maxc = (long long)maxit + 2;
   long long nc = 0;
   GSK_CUDA(cudaGraphLaunch(P->ggraph[0], s));
-  g_launches.fetch_add(kernels_per_cycle);
+  g_launches.fetch_add(P->gkernels);
   ++nc;
   cudaEvent_t ev;
   GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -399,7 +370,7 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
     const bool more = nc < maxc;
     if (more) {
       GSK_CUDA(cudaGraphLaunch(P->ggraph[nc & 1], s));
-      g_launches.fetch_add(kernels_per_cycle);
+      g_launches.fetch_add(P->gkernels);
       ++nc;
     }
     GSK_CUDA(cudaEventSynchronize(ev));

@@ -6,7 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include "common.cuh"
-#include "stream.cuh"
+#include "engine.cuh"
 #include "gsk.h"
 
 namespace gsk {
@@ -76,9 +76,8 @@ struct gsk_plan {
   uint8_t* roff = nullptr;
   int64_t nchunks = 0, nslots = 0;
   // reduction scratch
-  static constexpr int NSLOT = 16;  // reduction slots (one per pass kind)
-  double* part = nullptr;      // [MAXD][256] CTA partials
-  unsigned* tickets = nullptr; // [NSLOT]
+  double* part = nullptr;      // [MAXD][pstride] CTA partials of the current pass
+  int pstride = 0;             // >= number of CTAs of any pass (ceil(n/256))
   double* scratch = nullptr;   // [n] (residual norms)
   cudaStream_t st = nullptr;
   int* h_flag = nullptr;       // pinned
@@ -89,6 +88,8 @@ struct gsk_plan {
   const double* bkey_b = nullptr;
   const double* bkey_x = nullptr;
   int bK = 0;
+  long long bkernels = 0;  // kernel nodes per Bi-CGSTAB graph replay
+  long long gkernels = 0;  // kernel nodes per GMRES cycle replay
   const double* bkey_h = nullptr;
   // GMRES workspace
   double* W = nullptr;         // (m+1) n
@@ -118,36 +119,44 @@ namespace gsk {
 // plan's format (CSR or SELL) or a pure vector pass.
 int num_sms();
 
-// Launch one pass of the streaming engine: an SpMV pass in the plan's format (CSR
-// or SELL) or a vector pass; persistent grid of at most 2 CTAs per SM.
-template <int FMT, class Op>
-int launch_stream(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    GSK_CUDA(cudaFuncSetAttribute(stream_pass<FMT, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  st_dyn_smem()));
-    attr = true;
-  }
-  const int n = P->geo.n;
-  const int rows = FMT == 0 ? VecTile<Op::NV>::W * TB : TB;
-  const int ntiles = (n + rows - 1) / rows;
-  int tpc = 1;  // tiles per CTA: pow2 with at most 256 CTAs (aligned blocks of the tree)
-  while ((ntiles + tpc - 1) / tpc > 256) tpc <<= 1;
-  const int grid = (ntiles + tpc - 1) / tpc;
-  Red red{P->part, P->tickets + slot, tpc, ntiles};
-  stream_pass<FMT, Op><<<grid, ST_THREADS, st_dyn_smem(), s>>>(P->csr, P->sell, n, ntiles, op, red);
-  GSK_LAUNCHED(1);
-  return GSK_OK;
-}
-
+// Launch one pass: an SpMV pass in the plan's format (CSR or SELL) or a vector pass,
+// then (if it reduces dot products) the single-CTA finish kernel.  pe0/pe1: optional
+// probe events recorded around the pass kernel itself (graph capture: external
+// event nodes).  Returns the number of kernels launched (or a negative error).
 template <class Op>
-int run_pass(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
+int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullptr, cudaEvent_t pe1 = nullptr) {
+  const int n = P->geo.n;
+  const int sms = num_sms();
+  int ntiles;
+  if (pe0) GSK_CUDA(cudaEventRecordWithFlags(pe0, s, cudaEventRecordExternal));
   if constexpr (!Op::kSpmv) {
-    return launch_stream<0>(P, op, slot, s);
+    // RPT rows per thread when that still leaves >= 2 CTAs per SM, else 2
+    constexpr int R = VecRpt<Op::NV>::value;
+    if ((long long)n >= 2LL * TB * R * sms) {
+      ntiles = (n + TB * R - 1) / (TB * R);
+      pass_kernel<0, R, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, R, op, P->part, P->pstride);
+    } else {
+      ntiles = (n + TB * 2 - 1) / (TB * 2);
+      pass_kernel<0, 2, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, 2, op, P->part, P->pstride);
+    }
   } else {
-    if (P->fmt == GSK_FMT_SELL) return launch_stream<2>(P, op, slot, s);
-    return launch_stream<1>(P, op, slot, s);
+    const int windows = (n + TB - 1) / TB;
+    int wpc = 8;  // windows per CTA: as many as keep >= 3 CTAs per SM busy
+    while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
+    ntiles = (windows + wpc - 1) / wpc;
+    if (P->fmt == GSK_FMT_SELL)
+      pass_kernel<2, 1, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->part, P->pstride);
+    else
+      pass_kernel<1, 1, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->part, P->pstride);
   }
+  GSK_LAUNCHED(1);
+  if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
+  if constexpr (Op::D > 0) {
+    finish_kernel<Op><<<1, FIN_THREADS, 0, s>>>(op, P->part, P->pstride, ntiles);
+    GSK_LAUNCHED(1);
+    return 2;
+  }
+  return 1;
 }
 #define GSK_TRY(x)              \
   do {                          \
@@ -158,6 +167,9 @@ int run_pass(gsk_plan* P, const Op& op, int slot, cudaStream_t s) {
 int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
 int ensure_hist(gsk_plan* P, int maxit);
+// End a stream capture begun by the caller: instantiate the graph, count its kernel
+// nodes (returned in *kernels; launches made during capture are not counted).
+int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels, const char* what);
 int join_in(gsk_plan* P, cudaStream_t caller);
 int join_out(gsk_plan* P, cudaStream_t caller);
 }  // namespace gsk

@@ -3,6 +3,7 @@
 // gsk_plan_residual_norm, SELL copy-out, probes, diagnostics.
 #include <cstring>
 #include <string>
+#include <vector>
 #include "internal.cuh"
 
 namespace gsk {
@@ -38,18 +39,14 @@ int num_sms() {
   return sms;
 }
 
-// Reduction scratch of a geometry: tile and group partials, slot and group tickets.
+// Reduction scratch: CTA partials of one pass ([MAXD][pstride], pstride >= CTAs).
 int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
-  const size_t nt = sizeof(unsigned) * gsk_plan::NSLOT;
-  if (async) {
-    GSK_CUDA(cudaMallocAsync(&P->part, sizeof(double) * MAXD * 256, s));
-    GSK_CUDA(cudaMallocAsync(&P->tickets, nt, s));
-    GSK_CUDA(cudaMemsetAsync(P->tickets, 0, nt, s));
-  } else {
-    GSK_CUDA(cudaMalloc(&P->part, sizeof(double) * MAXD * 256));
-    GSK_CUDA(cudaMalloc(&P->tickets, nt));
-    GSK_CUDA(cudaMemset(P->tickets, 0, nt));
-  }
+  P->pstride = (P->geo.n + TB - 1) / TB;
+  const size_t bytes = sizeof(double) * MAXD * (size_t)P->pstride;
+  if (async)
+    GSK_CUDA(cudaMallocAsync(&P->part, bytes, s));
+  else
+    GSK_CUDA(cudaMalloc(&P->part, bytes));
   return GSK_OK;
 }
 
@@ -147,6 +144,37 @@ int join_out(gsk_plan* P, cudaStream_t caller) {
   return GSK_OK;
 }
 
+int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels, const char* what) {
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (rc < 0) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) {
+    set_error("%s graph capture: %s", what, cudaGetErrorString(e));
+    return GSK_E_CUDA;
+  }
+  size_t nn = 0;
+  cudaGraphGetNodes(g, nullptr, &nn);
+  std::vector<cudaGraphNode_t> nodes(nn);
+  cudaGraphGetNodes(g, nodes.data(), &nn);
+  long long k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++k;
+  }
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    set_error("%s graph instantiate: %s", what, cudaGetErrorString(e));
+    return GSK_E_CUDA;
+  }
+  g_launches.fetch_sub(k);  // counted per replay instead
+  *kernels = k;
+  return GSK_OK;
+}
+
 int ensure_hist(gsk_plan* P, int maxit) {
   if (P->hist_cap >= maxit + 1) return GSK_OK;
   if (P->hist_d) GSK_CUDA(cudaFree(P->hist_d));
@@ -223,7 +251,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
-  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->tickets, P->scratch,
+  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -246,7 +274,7 @@ int gsk_plan_spmv(gsk_plan* P, const double* x, double* y, void* stream) {
   }
   cudaStream_t s = as_stream(stream);
   OpSpmv op{x, y};
-  GSK_TRY(run_pass(P, op, 0, s));
+  if (run_pass(P, op, s) < 0) return GSK_E_CUDA;
   GSK_CUDA(cudaStreamSynchronize(s));
   return GSK_OK;
 }
@@ -267,7 +295,7 @@ int gsk_plan_residual_norm(gsk_plan* P, const double* b, const double* x, const 
   }
   cudaStream_t s = as_stream(stream);
   OpResNorm op{x, b, w, P->scratch};
-  GSK_TRY(run_pass(P, op, 1, s));
+  if (run_pass(P, op, s) < 0) return GSK_E_CUDA;
   double v = 0;
   GSK_CUDA(cudaMemcpyAsync(&v, P->scratch, sizeof(double), cudaMemcpyDeviceToHost, s));
   GSK_CUDA(cudaStreamSynchronize(s));
@@ -288,12 +316,11 @@ int gsk_dot(int64_t n, const double* a, const double* b, double* result, void* s
   double* out = nullptr;
   GSK_CUDA(cudaMallocAsync(&out, sizeof(double), s));
   OpDot op{a, b, out};
-  int rc = run_pass(&tmp, op, 0, s);
+  int rc = run_pass(&tmp, op, s) < 0 ? GSK_E_CUDA : GSK_OK;
   double v = 0;
   if (rc == GSK_OK && cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     rc = GSK_E_CUDA;
   cudaFreeAsync(tmp.part, s);
-  cudaFreeAsync(tmp.tickets, s);
   cudaFreeAsync(out, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) rc = GSK_E_CUDA;
   *result = v;
