@@ -91,6 +91,16 @@ typedef struct gsk_plan gsk_plan;
 int gsk_gs_scale(const gsk_csr *A, const double *b, int p, double *values_out,
                  double *b_out, double *d_out, int32_t *bad_row, void *stream);
 
+/* Two-sided scaling D^(1/2) A D^(1/2) y = D^(1/2) b, x = D^(1/2) y,
+ * D as in Eq. (2).  s_out [n] receives s_i = sqrt(1/||a_i||_p); values_out gets
+ * (a_ij * s_i) * s_j (same pattern), b_out (nullable) b_i * s_i.  Outputs must not
+ * alias the inputs.  Errors as gsk_gs_scale (zero rows are detected before any
+ * output is written). */
+int gsk_gs_scale_sym(const gsk_csr *A, const double *b, int p, double *values_out,
+                     double *b_out, double *s_out, int32_t *bad_row, void *stream);
+/* x_i = s_i * y_i: back to the original unknowns after a two-sided solve. */
+int gsk_gs_unscale(int64_t n, const double *s, const double *y, double *x, void *stream);
+
 /* y = A x (SPEC sparse-core spmv): y_i = sum_k val_k x_col_k, k ascending, one
  * fused multiply-add per entry from +0.  x and y must not overlap. */
 int gsk_spmv(const gsk_csr *A, const double *x, double *y, void *stream);

@@ -48,6 +48,10 @@ def _lib():
         lib.orc_spmv.restype = None
         lib.orc_gs_scale.argtypes = [i64, vp, vp, vp, i32, vp, vp, vp, vp]
         lib.orc_gs_scale.restype = i32
+        lib.orc_gs_scale_sym.argtypes = [i64, vp, vp, vp, vp, i32, vp, vp, vp, vp]
+        lib.orc_gs_scale_sym.restype = i32
+        lib.orc_unscale.argtypes = [i64, vp, vp, vp]
+        lib.orc_unscale.restype = None
         lib.orc_sell_size.argtypes = [i64, vp, i32, i32]
         lib.orc_sell_size.restype = i64
         lib.orc_sell_build.argtypes = [i64, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
@@ -118,6 +122,32 @@ def gs_scale(row_ptr, val, b, p):
     if rc == -2:
         raise ZeroRowError(bad.value)
     return vo, bo, d
+
+
+def gs_scale_sym(row_ptr, col, val, b, p):
+    """Two-sided scaling: returns (val', b', s) with
+    A' = D^1/2 A D^1/2, b' = D^1/2 b, s = diag(D^1/2)."""
+    row_ptr, col, val, b = _i32(row_ptr), _i32(col), _f64(val), _f64(b)
+    n = row_ptr.size - 1
+    vo = np.empty_like(val)
+    bo = None if b is None else np.empty_like(b)
+    sv = np.empty(n, np.float64)
+    bad = ctypes.c_int32(-1)
+    rc = _lib().orc_gs_scale_sym(n, _p(row_ptr), _p(col), _p(val), _p(b), int(p), _p(vo), _p(bo),
+                                 _p(sv), ctypes.addressof(bad))
+    if rc == -1:
+        raise ValueError("p must be >= 1")
+    if rc == -2:
+        raise ZeroRowError(bad.value)
+    return vo, bo, sv
+
+
+def unscale(s, y):
+    """x = D^1/2 y."""
+    s, y = _f64(s), _f64(y)
+    x = np.empty_like(y)
+    _lib().orc_unscale(y.size, _p(s), _p(y), _p(x))
+    return x
 
 
 def sell_build(row_ptr, col, val, C=32, sigma=256):

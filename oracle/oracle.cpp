@@ -148,6 +148,31 @@ int orc_gs_scale(int64_t n, const int32_t* rp, const double* val, const double* 
   return 0;
 }
 
+// ---- two-sided scaling D^(1/2) A D^(1/2) y = D^(1/2) b, x = D^(1/2) y --------------
+// PAPER.md:245-251 (the variant the authors also tried).  D = diag(1/||a_i||_p) as in
+// Eq. (2); reading S1: s_i = sqrt(d_i), a'_ij = (a_ij * s_i) * s_j
+// (left factor first), b'_i = b_i * s_i, and x_i = s_i * y_i.
+int orc_gs_scale_sym(int64_t n, const int32_t* rp, const int32_t* ci, const double* val,
+                     const double* b, int p, double* val_out, double* b_out, double* s_out,
+                     int32_t* bad_row) {
+  std::vector<double> d(n);
+  int rc = orc_gs_scale(n, rp, val, nullptr, p, std::vector<double>(rp[n]).data(), nullptr,
+                        d.data(), bad_row);
+  if (rc != 0) return rc;
+  std::vector<double> sq(n);
+  for (int64_t i = 0; i < n; ++i) sq[i] = std::sqrt(d[i]);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) val_out[k] = (val[k] * sq[i]) * sq[ci[k]];
+    if (b && b_out) b_out[i] = b[i] * sq[i];
+    if (s_out) s_out[i] = sq[i];
+  }
+  return 0;
+}
+
+void orc_unscale(int64_t n, const double* s, const double* y, double* x) {
+  for (int64_t i = 0; i < n; ++i) x[i] = s[i] * y[i];
+}
+
 // ---- SELL-C-sigma layout (BASELINE.json configs[3]) -------------------------------
 // Windows of sigma consecutive rows; inside a window rows are stably sorted by
 // descending length (ties keep row order); chunks of C sorted rows; chunk_len =

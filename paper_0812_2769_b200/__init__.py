@@ -6,7 +6,7 @@ hand-written sm_100a kernels behind the C-ABI of ``libgsk.so`` (include/gsk.h);
 this package is the thin ctypes binding (argument marshalling only).
 """
 from ._gsk import (CSR, Plan, GskError, STATUS, SYMBOLS, LIB_PATH, bicgstab_solve, dot,  # noqa: F401
-                   gmres_solve, gs_scale, launch_count, load, spmv)
+                   gmres_solve, gs_scale, gs_scale_sym, gs_unscale, launch_count, load, spmv)
 
 __all__ = ["CSR", "Plan", "GskError", "STATUS", "SYMBOLS", "LIB_PATH", "bicgstab_solve", "dot",
-           "gmres_solve", "gs_scale", "launch_count", "load", "spmv"]
+           "gmres_solve", "gs_scale", "gs_scale_sym", "gs_unscale", "launch_count", "load", "spmv"]

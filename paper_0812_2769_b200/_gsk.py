@@ -21,7 +21,7 @@ FMT = {"csr": 0, "sell": 1}
 SCHEDULE = {"auto": 0, "fused": 1, "split": 2}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
-SYMBOLS = ("gsk_gs_scale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
+SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
            "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_destroy",
            "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
            "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
@@ -71,6 +71,8 @@ def load(path: str = LIB_PATH):
     vp, i32, i64, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
     P = ctypes.POINTER
     lib.gsk_gs_scale.argtypes = [P(CsrStruct), vp, i32, vp, vp, vp, P(ctypes.c_int32), vp]
+    lib.gsk_gs_scale_sym.argtypes = [P(CsrStruct), vp, i32, vp, vp, vp, P(ctypes.c_int32), vp]
+    lib.gsk_gs_unscale.argtypes = [i64, vp, vp, vp, vp]
     lib.gsk_spmv.argtypes = [P(CsrStruct), vp, vp, vp]
     lib.gsk_dot.argtypes = [i64, vp, vp, P(d), vp]
     lib.gsk_plan_create.argtypes = [P(CsrStruct), P(Opts), P(vp), vp]
@@ -168,6 +170,31 @@ def gs_scale(A: CSR, b=None, p: int = 2, inplace: bool = False, out=None):
     if As is not A:
         As.row_ptr, As.col, As.val, As.n, As.nnz = A.row_ptr, A.col, vout, A.n, A.nnz
     return As, bout, d
+
+
+def gs_scale_sym(A: CSR, b=None, p: int = 2):
+    """Two-sided scaling: returns (A', b', s) with
+    A' = D^1/2 A D^1/2, b' = D^1/2 b and s = diag(D^1/2); solve A' y = b', then
+    x = gs_unscale(s, y)."""
+    lib = load()
+    b = _dev_f64(b, A.n)
+    vout = torch.empty_like(A.val)
+    bout = None if b is None else torch.empty_like(b)
+    sv = torch.empty(A.n, dtype=torch.float64, device="cuda")
+    bad = ctypes.c_int32(-1)
+    rc = lib.gsk_gs_scale_sym(ctypes.byref(A.struct()), _ptr(b), int(p), _ptr(vout), _ptr(bout), _ptr(sv),
+                              ctypes.byref(bad), _stream())
+    _check(rc, bad.value if rc == GSK_E_ZERO_ROW else None)
+    As = CSR.__new__(CSR)
+    As.row_ptr, As.col, As.val, As.n, As.nnz = A.row_ptr, A.col, vout, A.n, A.nnz
+    return As, bout, sv
+
+
+def gs_unscale(s, y):
+    s, y = _dev_f64(s), _dev_f64(y)
+    x = torch.empty_like(y)
+    _check(load().gsk_gs_unscale(y.numel(), _ptr(s), _ptr(y), _ptr(x), _stream()))
+    return x
 
 
 def spmv(A: CSR, x):

@@ -16,10 +16,12 @@ __device__ __forceinline__ double row_norm_term(double a, int p) {
   return t;
 }
 
+// norms_only: write s_i = sqrt(1/||a_i||_p) to dout and nothing else (two-sided
+// scaling, first pass).
 __global__ void __launch_bounds__(TB) gs_kernel(int n, const int* __restrict__ rp,
                                                 const double* vin, double* vout,
                                                 const double* b, double* bout, double* dout,
-                                                int p, int* bad) {
+                                                int p, int* bad, int norms_only) {
   __shared__ double sv[CSR_CAP];
   const int r0 = blockIdx.x * TB, t = threadIdx.x, r = r0 + t;
   const int rend = min(r0 + TB, n);
@@ -48,24 +50,94 @@ __global__ void __launch_bounds__(TB) gs_kernel(int n, const int* __restrict__ r
     } else {
       d = 1.0 / nrm;
     }
-    if (staged) {
+    if (norms_only) {
+      dout[r] = sqrt(d);
+    } else if (staged) {
       double* sg = sv + (a0 - s0);
       for (int k = 0; k < len; ++k) sg[k] = sg[k] * d;
     } else {
       for (int k = 0; k < len; ++k) vout[a0 + k] = vin[a0 + k] * d;
     }
-    if (b && bout) bout[r] = b[r] * d;
-    if (dout) dout[r] = d;
+    if (!norms_only) {
+      if (b && bout) bout[r] = b[r] * d;
+      if (dout) dout[r] = d;
+    }
   }
-  if (staged) {
+  if (staged && !norms_only) {
     __syncthreads();
     for (int k = t; k < cnt; k += TB) __stcs(vout + s0 + k, sv[k]);
   }
 }
 
+// a'_ij = (a_ij * s_i) * s_j, b'_i = b_i * s_i (reading S1)
+__global__ void __launch_bounds__(TB) sym_scale_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                       const double* vin, double* vout, const double* b,
+                                                       double* bout, const double* __restrict__ sv) {
+  const int r = blockIdx.x * TB + threadIdx.x;
+  if (r >= n) return;
+  const double si = sv[r];
+  for (int k = rp[r]; k < rp[r + 1]; ++k) vout[k] = (vin[k] * si) * __ldg(sv + ci[k]);
+  if (b && bout) bout[r] = b[r] * si;
+}
+
+__global__ void unscale_kernel(int64_t n, const double* s, const double* y, double* x) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = s[i] * y[i];
+}
+
 }  // namespace gsk
 
 using namespace gsk;
+
+extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double* values_out,
+                                double* b_out, double* s_out, int32_t* bad_row, void* stream) {
+  if (!A || A->n < 1 || A->nnz < 0 || !A->row_ptr || !s_out ||
+      (A->nnz > 0 && (!A->values || !values_out || !A->col_idx))) {
+    set_error("gsk_gs_scale_sym: invalid arguments");
+    return GSK_E_INVALID;
+  }
+  if (p < 1) {
+    set_error("gsk_gs_scale_sym: p must be >= 1 (got %d)", p);
+    return GSK_E_INVALID;
+  }
+  if (values_out == A->values || (b_out && b_out == b)) {
+    set_error("gsk_gs_scale_sym: outputs must not alias inputs (column scaling reads other rows)");
+    return GSK_E_INVALID;
+  }
+  cudaStream_t s = as_stream(stream);
+  int* dbad = nullptr;
+  GSK_CUDA(cudaMallocAsync(&dbad, sizeof(int), s));
+  const int big = 0x7fffffff;
+  GSK_CUDA(cudaMemcpyAsync(dbad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  const int grid = (A->n + TB - 1) / TB;
+  gs_kernel<<<grid, TB, 0, s>>>(A->n, A->row_ptr, A->values, nullptr, nullptr, nullptr, s_out, p, dbad, 1);
+  GSK_LAUNCHED(1);
+  int hbad = big;
+  GSK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaFreeAsync(dbad, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  if (hbad != big) {
+    if (bad_row) *bad_row = hbad;
+    set_error("gsk_gs_scale_sym: row %d has zero L_%d norm", hbad, p);
+    return GSK_E_ZERO_ROW;
+  }
+  sym_scale_kernel<<<grid, TB, 0, s>>>(A->n, A->row_ptr, A->col_idx, A->values, values_out, b, b_out, s_out);
+  GSK_LAUNCHED(1);
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
+
+extern "C" int gsk_gs_unscale(int64_t n, const double* s_in, const double* y, double* x, void* stream) {
+  if (n < 1 || !s_in || !y || !x) {
+    set_error("gsk_gs_unscale: invalid arguments");
+    return GSK_E_INVALID;
+  }
+  cudaStream_t s = as_stream(stream);
+  unscale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, s_in, y, x);
+  GSK_LAUNCHED(1);
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
 
 extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* values_out,
                             double* b_out, double* d_out, int32_t* bad_row, void* stream) {
@@ -87,7 +159,7 @@ extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* va
   const int big = 0x7fffffff;
   GSK_CUDA(cudaMemcpyAsync(dbad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
   const int grid = (A->n + TB - 1) / TB;
-  gs_kernel<<<grid, TB, 0, s>>>(A->n, A->row_ptr, A->values, values_out, b, b_out, d_out, p, dbad);
+  gs_kernel<<<grid, TB, 0, s>>>(A->n, A->row_ptr, A->values, values_out, b, b_out, d_out, p, dbad, 0);
   GSK_LAUNCHED(1);
   int hbad = big;
   GSK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -272,3 +272,19 @@ def test_full_size_parity(name):
     g = P.gmres(bs, m=30, tol=c.tol, maxit=32)
     o = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 30, c.tol, 32)
     assert_same_solve(g, o)
+
+
+@pytest.mark.parametrize("name,N", [("C1", None), ("C3", 20), ("C4", 24), ("C5", 96), ("P1", 64)])
+@pytest.mark.parametrize("p", [1, 2])
+def test_two_sided_scaling_parity(name, N, p):
+    """D^1/2 A D^1/2: scaled values, b, s bit-exact; a Bi-CGSTAB solve
+    of the scaled system and the unscaled x bit-exact."""
+    s = workloads.generate(name, N=N)
+    A = gsk.CSR.from_system(s)
+    As, bs, sv = gsk.gs_scale_sym(A, s["b"], p)
+    vo, bo, so = oracle.gs_scale_sym(s["row_ptr"], s["col"], s["val"], s["b"], p)
+    assert np.array_equal(cpu(As.val), vo) and np.array_equal(cpu(bs), bo) and np.array_equal(cpu(sv), so)
+    g = gsk.Plan(As).bicgstab(bs, tol=1e-9, maxit=500)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-9, 500)
+    assert_same_solve(g, o)
+    assert np.array_equal(cpu(gsk.gs_unscale(sv, g[0])), oracle.unscale(so, o[0]))

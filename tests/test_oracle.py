@@ -361,3 +361,26 @@ def test_zero_rhs_converges_immediately():
         assert rep["status"] == 0 and rep["iterations"] == 0 and np.all(x == 0)
     x, h, rep = oracle.gmres(s["row_ptr"], s["col"], s["val"], b, 5, 1e-8, 10)
     assert rep["status"] == 0 and rep["iterations"] == 0
+
+
+# ---------------------------------------------------------------- two-sided scaling
+def test_two_sided_scaling():
+    """D^1/2 A D^1/2 y = D^1/2 b, x = D^1/2 y: the solution is
+    unchanged, symmetry of A is kept (to 1 ulp: the two factors round in a fixed
+    order), and for p = 2 the entries are a_ij / sqrt(||a_i|| ||a_j||)."""
+    for name, N in [("P1", 14), ("C3", 6), ("lap2d", 9)]:
+        s = workloads.generate(name, N=N)
+        A = dense(s["row_ptr"], s["col"], s["val"], s["n"])
+        v2, b2, sv = oracle.gs_scale_sym(s["row_ptr"], s["col"], s["val"], s["b"], 2)
+        A2 = dense(s["row_ptr"], s["col"], v2, s["n"])
+        nrm = np.sqrt((A ** 2).sum(1))
+        assert np.allclose(sv, 1 / np.sqrt(nrm), rtol=1e-15, atol=0)
+        assert np.allclose(A2, A / np.sqrt(np.outer(nrm, nrm)), rtol=2e-15, atol=0)
+        y = np.linalg.solve(A2, b2)
+        x = oracle.unscale(sv, y)
+        xs = np.linalg.solve(A, s["b"])
+        assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs)
+        if name == "lap2d":
+            assert np.abs(A2 - A2.T).max() <= 2.3e-16 * np.abs(A2).max()
+    with pytest.raises(ValueError):
+        oracle.gs_scale_sym(s["row_ptr"], s["col"], s["val"], s["b"], 0)
