@@ -311,9 +311,23 @@ int orc_bicgstab(int64_t n, const int32_t* rp, const int32_t* ci, const double* 
 // ascending).  Iterations count inner Arnoldi steps (B6).  hist[it] is the
 // least-squares residual estimate |g_{j+1}|/||r0||.  w (nullable) only enters the
 // reported true_relres_w.
+// orth: 0 = modified Gram-Schmidt (north star), 1 = double classical Gram-Schmidt as
+// in AZTEC: h = V^T w; w -= V h; h' = V^T w; w -= V h';
+// H(:,j) = h + h' (each update an FMA chain over i ascending).
+int orc_gmres_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+                   const double* b, const double* x0, const double* w, int m, double tol, int maxit,
+                   int orth, double* x, double* hist, orc_report* rep);
+
 int orc_gmres(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
               const double* b, const double* x0, const double* w, int m, double tol, int maxit,
               double* x, double* hist, orc_report* rep) {
+  return orc_gmres_orth(n, rp, ci, v, b, x0, w, m, tol, maxit, 0, x, hist, rep);
+}
+
+int orc_gmres_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+                   const double* b, const double* x0, const double* w, int m, double tol, int maxit,
+                   int orth, double* x, double* hist, orc_report* rep) {
+  if (orth != 0 && orth != 1) return -1;
   if (n < 1 || maxit < 1 || m < 1 || !(tol > 0)) return -1;
   std::vector<double> r(n), ax(n), wv(n);
   std::vector<std::vector<double>> V(m + 1, std::vector<double>(n));
@@ -341,9 +355,20 @@ int orc_gmres(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
     for (int j = 0; j < m; ++j) {  // Arnoldi step j+1
       ++it;
       orc_spmv(n, rp, ci, v, V[j].data(), wv.data());
-      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
-        h(i, j) = orc_dot(n, wv.data(), V[i].data());
-        for (int64_t q = 0; q < n; ++q) wv[q] = std::fma(-h(i, j), V[i][q], wv[q]);
+      if (orth == 0) {
+        for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+          h(i, j) = orc_dot(n, wv.data(), V[i].data());
+          for (int64_t q = 0; q < n; ++q) wv[q] = std::fma(-h(i, j), V[i][q], wv[q]);
+        }
+      } else {
+        std::vector<double> c1(j + 1), c2(j + 1);
+        for (int i = 0; i <= j; ++i) c1[i] = orc_dot(n, wv.data(), V[i].data());
+        for (int64_t q = 0; q < n; ++q)
+          for (int i = 0; i <= j; ++i) wv[q] = std::fma(-c1[i], V[i][q], wv[q]);
+        for (int i = 0; i <= j; ++i) c2[i] = orc_dot(n, wv.data(), V[i].data());
+        for (int64_t q = 0; q < n; ++q)
+          for (int i = 0; i <= j; ++i) wv[q] = std::fma(-c2[i], V[i][q], wv[q]);
+        for (int i = 0; i <= j; ++i) h(i, j) = c1[i] + c2[i];
       }
       double hn = std::sqrt(orc_dot(n, wv.data(), wv.data()));
       h(j + 1, j) = hn;

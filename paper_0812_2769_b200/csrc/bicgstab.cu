@@ -81,6 +81,7 @@ struct OpInit {  // r = b - A x; r^ = r; p_old = v_old = 0
 
 // ---- fused schedule (3 passes; p and s recomputed at the gather) ---------------------
 struct OpP1 {
+  static constexpr int kSellMinBlocks = 3;  // see SellTuning (engine.cuh)
   static constexpr int D = 1;
   static constexpr int NV = 4;
   static constexpr bool kSpmv = true;
@@ -142,6 +143,7 @@ __device__ __forceinline__ void set_omega(BicgState* st, double ts, double tt) {
 }
 
 struct OpP2 {
+  static constexpr int kSellMinBlocks = 3;  // see SellTuning (engine.cuh)
   static constexpr int D = 3;
   static constexpr int NV = 3;
   static constexpr bool kSpmv = true;

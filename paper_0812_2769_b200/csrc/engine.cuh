@@ -23,12 +23,13 @@
 // so a window costs one __syncthreads.  Kernels are compiled with --fmad=false; every
 // FMA is an explicit __fma_rn (AC-2).
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace gsk {
 
 constexpr int FIN_THREADS = 1024;
-constexpr int FIN_LEAVES = 8;                          // partials per finish thread
+constexpr int FIN_LEAVES = 8;                          // partials per finish thread (fixed)
 constexpr int FIN_ROUND = FIN_THREADS * FIN_LEAVES;    // 8192 partials per round
 
 struct CsrStage {
@@ -62,14 +63,23 @@ struct VecRpt {
   static constexpr int value = NV <= 3 ? 8 : 4;
 };
 
-#ifndef GSK_SELL_MINB_DOT
-#define GSK_SELL_MINB_DOT 3
-#endif
-template <int FMT, int D>
+// SELL register budget per Op: 64 registers (4 CTAs/SM) unless the Op declares
+// kSellMinBlocks = 3; only then are its own-row operands loaded before the SpMV
+// (prefetching them at 64 registers spills).  Measured at C4: plain SpMV and the
+// Bi-CGSTAB passes are fastest at 4 CTAs/SM, the GMRES Arnoldi pass at 3.
+template <class Op, class = void>
+struct SellTuning {
+  static constexpr int minb = 4;
+};
+template <class Op>
+struct SellTuning<Op, std::void_t<decltype(Op::kSellMinBlocks)>> {
+  static constexpr int minb = Op::kSellMinBlocks;
+};
+
+template <int FMT, class Op>
 struct PassOcc {
-  // SELL: plain SpMV fits 64 registers (4 CTAs/SM, measured 93% of the copy peak);
-  // with a fused dot epilogue 64 registers spill, so 3 CTAs/SM unless overridden.
-  static constexpr int kMinBlocks = FMT == 1 ? 4 : FMT == 2 ? (D == 0 ? 4 : GSK_SELL_MINB_DOT) : 3;
+  static constexpr int kMinBlocks = FMT == 1 ? 4 : FMT == 2 ? SellTuning<Op>::minb : 3;
+  static constexpr bool kPrefetch = FMT == 1 || (FMT == 2 && SellTuning<Op>::minb < 4);
 };
 
 // y for row r0 + t of a CSR window (AC-3 chain), staged through st.
@@ -190,7 +200,7 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 // FMT 0: vector pass, RPT windows (rows r0 + 256 w + t) per CTA, all loads in flight.
 // FMT 1/2: SpMV pass over wpc windows.
 template <int FMT, int RPT, class Op>
-__global__ void __launch_bounds__(TB, PassOcc<FMT, Op::D>::kMinBlocks)
+__global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
   if (!op.begin()) return;
   constexpr int D = Op::D;
@@ -231,10 +241,12 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op::D>::kMinBlocks)
         auto g = [&](int col) { return op.gather(col); };
         const int i = r0 + t;
         double v[NVA];
-        if (i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
+        constexpr bool kPre = PassOcc<FMT, Op>::kPrefetch;
+        if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
         if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
         else y = sell_window(sell, r0, g, sm.sy[w & 1]);
+        if (!kPre && i < n) load_vin(op, i, v);
         if (i < n) op.row(i, y, v, cc);
       }
       if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);
@@ -246,9 +258,14 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op::D>::kMinBlocks)
   }
 }
 
-// One CTA: canonical tree over ntiles CTA partials (pow2-padded with +0), + 0.0, then
-// the Op's scalar epilogue on warp 0.  Skipped exactly when the pass was skipped
-// (op.begin() reads the same device flags; only finish kernels change them).
+// One CTA: canonical tree over ntiles CTA partials, + 0.0, then the Op's scalar
+// epilogue on warp 0.  The partials are zero-padded to a multiple of 8192 (trailing
+// +0 leaves never change a tree value beyond the sign of a zero, which the final
+// + 0.0 canonicalises): thread t owns leaves [8t, 8t+8) of each 8192-leaf round
+// (four 16-byte loads), a register tree of 8, warp butterflies, a tree of 32
+// warps, and a binary counter joins the rounds in order.  Skipped exactly when the
+// pass was skipped (op.begin() reads the same device flags; only finish kernels
+// change them).
 template <class Op>
 __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double* part, int stride,
                                                              int ntiles) {
@@ -256,25 +273,31 @@ __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double
   constexpr int D = Op::D;
   __shared__ double ws[D][32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  double stk[D][24];
-  int lvl[24];
+  double stk[D][12];
+  int lvl[12];
   int sp = 0;
-  int np2 = 1;
-  while (np2 < ntiles) np2 <<= 1;
-  const int rounds = np2 > FIN_ROUND ? np2 / FIN_ROUND : 1;
-  const int per = np2 > FIN_ROUND ? FIN_LEAVES : (np2 + FIN_THREADS - 1) / FIN_THREADS;  // leaves per thread
-  for (int r = 0; r < rounds; ++r) {
+  const int rounds = (ntiles + FIN_ROUND - 1) / FIN_ROUND;
+  int rp2 = 1;  // rounds padded to a power of two (zero rounds contribute +0)
+  while (rp2 < rounds) rp2 <<= 1;
+  for (int r = 0; r < rp2; ++r) {
     double u[D];
+    const int base = r * FIN_ROUND + t * FIN_LEAVES;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      // leaves [base, base + per) of this thread: pairwise tree (per is 1, 2, 4 or 8)
-      const int base = r * FIN_ROUND + t * per;
       double l[FIN_LEAVES];
+      if (base + FIN_LEAVES <= ntiles) {
+        const double2* q = reinterpret_cast<const double2*>(part + (size_t)d * stride + base);
 #pragma unroll
-      for (int q = 0; q < FIN_LEAVES; ++q) l[q] = (q < per && base + q < ntiles) ? part[(size_t)d * stride + base + q] : 0.0;
-      for (int len = per; len > 1; len >>= 1)
-        for (int q = 0; q < len / 2; ++q) l[q] = l[2 * q] + l[2 * q + 1];
-      u[d] = l[0];
+        for (int h = 0; h < FIN_LEAVES / 2; ++h) {
+          const double2 x = q[h];
+          l[2 * h] = x.x;
+          l[2 * h + 1] = x.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < FIN_LEAVES; ++q) l[q] = base + q < ntiles ? part[(size_t)d * stride + base + q] : 0.0;
+      }
+      u[d] = ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) u[d] = u[d] + __shfl_xor_sync(0xffffffffu, u[d], off);
     }
@@ -292,7 +315,10 @@ __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double
         for (int off = 1; off < 32; off <<= 1) x = x + __shfl_xor_sync(0xffffffffu, x, off);
         u[d] = x;
       }
-      if (lane == 0) {
+      if (rp2 == 1) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) stk[d][0] = u[d];
+      } else if (lane == 0) {
 #pragma unroll
         for (int d = 0; d < D; ++d) stk[d][sp] = u[d];
         lvl[sp] = 0;
@@ -309,7 +335,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double
   if (warp == 0) {
     double s[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) s[d] = __shfl_sync(0xffffffffu, lane == 0 ? stk[d][0] : 0.0, 0) + 0.0;
+    for (int d = 0; d < D; ++d) s[d] = __shfl_sync(0xffffffffu, stk[d][0], 0) + 0.0;
     op.finish(s, lane);
   }
 }

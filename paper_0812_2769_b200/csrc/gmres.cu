@@ -77,6 +77,7 @@ struct OpGResid {
 
 // S_j: w = A v_j into slot j+1; h_1j = <w, v_1>
 struct OpArnoldi {
+  static constexpr int kSellMinBlocks = 3;  // see SellTuning (engine.cuh)
   static constexpr int D = 1;
   static constexpr int NV = 1;
   static constexpr bool kSpmv = true;

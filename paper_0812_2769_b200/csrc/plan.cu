@@ -41,7 +41,7 @@ int num_sms() {
 
 // Reduction scratch: CTA partials of one pass ([MAXD][pstride], pstride >= CTAs).
 int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
-  P->pstride = (P->geo.n + TB - 1) / TB;
+  P->pstride = ((P->geo.n + TB - 1) / TB + 7) & ~7;  // multiple of 8: 16-byte aligned rows
   const size_t bytes = sizeof(double) * MAXD * (size_t)P->pstride;
   if (async)
     GSK_CUDA(cudaMallocAsync(&P->part, bytes, s));

@@ -268,6 +268,8 @@ def test_solvers_match_dense_lu(seed):
     xs = np.linalg.solve(A, b)
     x, h, rep = oracle.gmres(rp, col, val, b, n, 1e-14, 5 * n)
     assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs)
+    x, h, rep = oracle.gmres(rp, col, val, b, 15, 1e-14, 20 * n, orth="cgs2")
+    assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs)
     x, h, rep = oracle.bicgstab(rp, col, val, b, 1e-14, 20 * n)
     assert rep["status"] == 0
     assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs) * 10
@@ -300,14 +302,16 @@ def test_finite_termination_diagonal():
     assert np.allclose(x, b / d, rtol=1e-10)
 
 
-def test_gmres_is_krylov_least_squares():
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_gmres_is_krylov_least_squares(orth):
     """hist[j] * ||r0|| = min over x in x0 + K_j(A, r0) of ||b - A x|| (GMRES's
     defining property, Saad & Schultz 1986); checked by brute-force least squares
-    on an orthonormalised explicit Krylov basis."""
+    on an orthonormalised explicit Krylov basis.  Holds for either orthogonalisation
+    (MGS, or AZTEC's double classical Gram-Schmidt)."""
     n = 60
     A, b = small_system(n, 11, kappa=10.0)
     rp, col, val = csr_from_dense(A)
-    x, h, rep = oracle.gmres(rp, col, val, b, n, 1e-15, n)
+    x, h, rep = oracle.gmres(rp, col, val, b, n, 1e-15, n, orth=orth)
     beta0 = np.linalg.norm(b)
     K = [b / beta0]
     for j in range(1, 30):  # K_j = span{r0, A r0, ..., A^{j-1} r0}

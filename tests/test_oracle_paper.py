@@ -48,11 +48,13 @@ def test_tbl1_problem1_bicgstab():
 
 
 @pytest.mark.slow
-def test_tbl1_problem1_gmres():
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_tbl1_problem1_gmres(orth):
     """Table 1: GMRES(10) stalls near 3.8e-2 unscaled; with GS(2)
-    it reaches 1e-4 at 265 and stalls at 1.1e-5."""
+    it reaches 1e-4 at 265 and stalls at 1.1e-5 — with MGS and with the paper's own
+    double classical Gram-Schmidt."""
     s, vo, bo, d = scaled("P1")
-    _, h, rep = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 10, 1e-10, 10000)
+    _, h, rep = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 10, 1e-10, 10000, orth=orth)
     assert first_crossings(h)[0] == GOLD["tbl1"]["gmres10_gs2"][0]
     stall = rep["best_relres"]
     assert first_crossings(h)[1] is None
@@ -67,8 +69,9 @@ def test_tbl1a_continuous_problem1():
     """Table tbl1a, a = b = 1000 everywhere."""
     s, vo, bo, d = scaled("P1cont")
     g = GOLD["tbl1a"]
-    _, h, _ = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 10, 1e-10, 7000)
-    check(first_crossings(h), g["gmres10_gs2"], 0.02)
+    for orth in ("mgs", "cgs2"):
+        _, h, _ = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 10, 1e-10, 7000, orth=orth)
+        check(first_crossings(h), g["gmres10_gs2"], 0.02)
     _, h, _ = oracle.gmres(s["row_ptr"], s["col"], s["val"], s["b"], 10, 1e-10, 7000)
     check(first_crossings(h), g["gmres10_unscaled"], 0.02)
     _, h, _ = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-10, 10000)
