@@ -33,6 +33,7 @@ def run(name, maxit_gmres=None):
     fmt = "sell" if c.sell else "csr"
     A0 = gsk.CSR.from_system(s)
     _, _, d2 = gsk.gs_scale(A0, s["b"], 2)
+    gsk.gs_scale(A0, s["b"], 1)  # warm-up: module load / allocator pools out of the timings
     rows = []
     tols = c.tols or (c.tol,)
     for scaling in ("none", 1, 2):

@@ -73,6 +73,7 @@ PAPER = {
     "P1": Config("P1", 11, 128, 0, 1e-10, 10000, 10, param=1e3),
     "P1cont": Config("P1cont", 12, 128, 0, 1e-10, 10000, 10, param=1e3),
     "P4": Config("P4", 14, 80, 0, 1e-10, 10000, 10, param=1e4),
+    "P4conv": Config("P4conv", 15, 40, 0, 1e-10, 10000, 10, param=100.0),
 }
 
 

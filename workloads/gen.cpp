@@ -297,15 +297,18 @@ bool make_problem(int cfg, int N, uint64_t seed, double param, Problem& P) {
       P.vel = [](double x, double y, double, double* v) { v[0] = 10.0 * (x + y); v[1] = 10.0 * (x - y); v[2] = 0; };
       return true;
     }
-    case 14: {  // paper P4: a = D inside (1/3,2/3)^3, d=e=f=100
+    case 14: case 15: {  // paper P4: a = D inside (1/3,2/3)^3
+      // 14: d=e=f=100, D = param; 15: D = 1e4, d=e=f = param (Table "limit",
+      // PAPER.md:1099-1147, convection sweep 100/200/500/1000)
       P.dim = 3; P.scheme = CENTRED; P.bc_z0_one = true;
       int64_t L = 2 * (int64_t)(N + 1);
-      double D = param > 0 ? param : 1e4;
+      double D = (cfg == 14 && param > 0) ? param : 1e4;
+      const double cv = (cfg == 15 && param > 0) ? param : 100.0;
       P.kface = [L, D](int64_t mx, int64_t my, int64_t mz) {
         auto in = [L](int64_t m) { return (L < 3 * m) && (3 * m < 2 * L); };
         return (in(mx) && in(my) && in(mz)) ? D : 1.0;
       };
-      P.vel = [](double, double, double, double* v) { v[0] = 100; v[1] = 100; v[2] = 100; };
+      P.vel = [cv](double, double, double, double* v) { v[0] = cv; v[1] = cv; v[2] = cv; };
       return true;
     }
     case 20: case 21: {  // Laplacian, k = 1, no convection
@@ -328,7 +331,7 @@ int gen_dims(int cfg, int N, int64_t* n, int64_t* nnz) {
   Problem P;
   P.N = N;
   if (cfg == 1 || cfg == 2 || cfg == 5 || cfg == 11 || cfg == 12 || cfg == 20) P.dim = 2;
-  else if (cfg == 3 || cfg == 4 || cfg == 14 || cfg == 21) P.dim = 3;
+  else if (cfg == 3 || cfg == 4 || cfg == 14 || cfg == 15 || cfg == 21) P.dim = 3;
   else return -1;
   if (N < 2) return -1;
   int64_t NN = N;
@@ -361,7 +364,7 @@ int gen_fill(int cfg, int N, uint64_t seed, double param, int32_t* row_ptr, int3
     assemble_row(P, I, J, K, col + row_ptr[r], val + row_ptr[r], &rhs_bc[r]);
   }
   // x*
-  const bool is_p1 = (cfg == 11 || cfg == 12), is_p4 = (cfg == 14);
+  const bool is_p1 = (cfg == 11 || cfg == 12), is_p4 = (cfg == 14 || cfg == 15);
   #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i)
     xstar[i] = is_p1 ? 1.0 : (is_p4 ? 0.0 : 2.0 * u01(seed, 1, i) - 1.0);
