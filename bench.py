@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time-to-tol without GS / with GS(1)")
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
+    ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
+                    help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
     return ap.parse_args()
 
 
@@ -210,7 +212,7 @@ def main():
     dbuf = torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
     fmt = "sell" if cfg.sell else "csr"
-    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule)
+    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth)
     x1 = torch.empty(n, dtype=torch.float64, device="cuda")
     x2 = torch.empty(n, dtype=torch.float64, device="cuda")
 
@@ -291,7 +293,7 @@ def main():
                      / (r1["solve_ms"] / 1e3) / 1e9 if r1["solve_ms"] else None,
                      "gbps_17vector_model": bm["bicg_iter"] * r1["iterations"] / (r1["solve_ms"] / 1e3) / 1e9
                      if r1["solve_ms"] else None, "schedule": plan_schedule(args)},
-        "gmres": {"m": m, "iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
+        "gmres": {"m": m, "orth": args.orth, "iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
                   "relres": r2["relres"], "true_relres": r2["true_relres"], "solve_ms": r2["solve_ms"],
                   "iters_per_s": r2["iterations"] / (r2["solve_ms"] / 1e3) if r2["solve_ms"] else None},
         "spmv": {"ms": spmv_ms, "gbps": spmv_gbps, "frac_of_hbm": spmv_gbps / hbm,

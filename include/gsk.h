@@ -72,10 +72,14 @@ typedef struct gsk_opts {
   int32_t poll;
   const double *weights;
   int32_t bicg_schedule;
-  int32_t reserved_;
+  int32_t gmres_orth;
 } gsk_opts;
 
 enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2 };
+/* gmres_orth: GSK_ORTH_MGS (modified Gram-Schmidt, j+1 passes per Arnoldi step; the
+ * north star's choice) or GSK_ORTH_CGS2 (double classical Gram-Schmidt as in AZTEC,
+ * three passes per step, H(:,j) = h + h'; m <= 64). */
+enum { GSK_ORTH_MGS = 0, GSK_ORTH_CGS2 = 1 };
 
 typedef struct gsk_plan gsk_plan;
 

@@ -19,6 +19,7 @@ GSK_OK, GSK_E_INVALID, GSK_E_ZERO_ROW, GSK_E_CUDA, GSK_E_NOMEM = 0, -1, -2, -3, 
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}
 FMT = {"csr": 0, "sell": 1}
 SCHEDULE = {"auto": 0, "fused": 1, "split": 2}
+ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
 SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
@@ -47,7 +48,7 @@ class Report(ctypes.Structure):
 
 class Opts(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("poll", ctypes.c_int32), ("weights", ctypes.c_void_p),
-                ("bicg_schedule", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
+                ("bicg_schedule", ctypes.c_int32), ("gmres_orth", ctypes.c_int32)]
 
 
 class GskError(RuntimeError):
@@ -218,12 +219,13 @@ def launch_count() -> int:
 class Plan:
     """gsk_plan: SELL build, workspace and captured graphs reused across solves."""
 
-    def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto"):
+    def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
+                 orth: str = "mgs"):
         lib = load()
         self.A = A
         self.weights = _dev_f64(weights, A.n)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE[schedule], 0)
+                    SCHEDULE[schedule], ORTH[orth])
         self._csr = A.struct()
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))

@@ -340,4 +340,137 @@ __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Multi-dot passes (GMRES with double classical Gram-Schmidt): J
+// dot products per row, J known at launch (<= MDOT_MAX).  CTA = 256 threads x wpc
+// windows; per window each dot's leaves go through warp butterflies, lane 0 of each
+// warp parks the warp value in smem, threads t < J finish the trees of 8 warps and,
+// after the CTA's windows, the tree over windows (zero-padded to 8).  Op provides
+//   bool begin(); int nd; double gather(int) (SpMV ops);
+//   double value(int i, double y, double* cache)  -> the row's w (may fill cache[d*TB])
+//   double operand(int i, int d, const double* cache) -> v_d at row i
+// The per-dot finish is mdot_finish<Op> with J CTAs.
+constexpr int MDOT_MAX = 64;
+constexpr int MDOT_CACHE = 48;  // operands cached in smem when J <= this
+
+template <class Op>
+struct MdotSmem {
+  double sy[2][TB];
+  double wp[2][MDOT_MAX * 8];  // [window parity][dot][warp]
+  double winp[8][MDOT_MAX];    // [window][dot]
+};
+
+template <int FMT, class Op>
+__global__ void __launch_bounds__(TB, 2)
+    mdot_pass(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
+  if (!op.begin()) return;
+  extern __shared__ __align__(16) double cache[];  // [J][TB] when op caches operands
+  __shared__ MdotSmem<Op> sm;
+  const int J = op.nd;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int rb = blockIdx.x * wpc * TB;
+  for (int w = 0; w < wpc; ++w) {
+    const int r0 = rb + w * TB;
+    const int i = r0 + t;
+    double* wp = sm.wp[w & 1];
+    if (r0 < n) {  // uniform over the CTA
+      double y = 0.0;
+      if constexpr (FMT == 1) {
+        // CSR rows are short here (stencils); read directly (L1/L2-served gathers)
+        if (i < n)
+          for (int k = csr.rp[i]; k < csr.rp[i + 1]; ++k) y = __fma_rn(__ldcs(csr.v + k), op.gather(__ldcs(csr.ci + k)), y);
+      } else if constexpr (FMT == 2) {
+        const int c = (r0 >> 5) + warp;
+        if (c < sell.nchunks) {
+          const int rl = sell.roff[c * SELL_C + lane];
+          const int p0 = sell.cptr[c], L = (sell.cptr[c + 1] - p0) >> 5;
+          double acc = 0.0;
+          for (int k = 0; k < L; ++k) {
+            const int col = __ldcs(sell.scol + p0 + lane + k * SELL_C);
+            if (col >= 0) acc = __fma_rn(__ldcs(sell.sval + p0 + lane + k * SELL_C), op.gather(col), acc);
+          }
+          sm.sy[w & 1][rl] = acc;
+        }
+        __syncthreads();
+        y = sm.sy[w & 1][t];
+      }
+      const double u = i < n ? op.value(i, y, cache + t) : 0.0;
+      for (int d = 0; d < J; ++d) {
+        double q = i < n ? u * op.operand(i, d, cache + t) : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) q = q + __shfl_xor_sync(0xffffffffu, q, off);
+        if (lane == 0) wp[d * 8 + warp] = q;
+      }
+    } else {
+      for (int d = lane; d < J; d += 32)
+        if (warp == 0) wp[d * 8 + 0] = 0.0;
+    }
+    __syncthreads();
+    if (t < J) {
+      const double* v = wp + t * 8;
+      sm.winp[w][t] = (r0 < n) ? ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])) : 0.0;
+    }
+  }
+  __syncthreads();
+  if (t < J) {
+    double a[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) a[w] = w < wpc ? sm.winp[w][t] : 0.0;
+    part[(size_t)t * stride + blockIdx.x] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  }
+}
+
+// Tree of one CTA over ntiles partials p[0..ntiles) (as finish_kernel), result in warp 0.
+__device__ __forceinline__ double cta_tree(const double* p, int ntiles) {
+  __shared__ double ws[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double stk[12];
+  int lvl[12];
+  int sp = 0;
+  const int rounds = (ntiles + FIN_ROUND - 1) / FIN_ROUND;
+  int rp2 = 1;
+  while (rp2 < rounds) rp2 <<= 1;
+  double res = 0.0;
+  for (int r = 0; r < rp2; ++r) {
+    const int base = r * FIN_ROUND + t * FIN_LEAVES;
+    double l[FIN_LEAVES];
+#pragma unroll
+    for (int q = 0; q < FIN_LEAVES; ++q) l[q] = base + q < ntiles ? p[base + q] : 0.0;
+    double u = ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+    __syncthreads();
+    if (lane == 0) ws[warp] = u;
+    __syncthreads();
+    if (warp == 0) {
+      double x = ws[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) x = x + __shfl_xor_sync(0xffffffffu, x, off);
+      if (rp2 == 1) {
+        res = x;
+      } else if (lane == 0) {
+        stk[sp] = x;
+        lvl[sp] = 0;
+        ++sp;
+        while (sp >= 2 && lvl[sp - 1] == lvl[sp - 2]) {
+          stk[sp - 2] = stk[sp - 2] + stk[sp - 1];
+          lvl[sp - 2] += 1;
+          --sp;
+        }
+      }
+    }
+  }
+  if (warp == 0 && rp2 > 1) res = __shfl_sync(0xffffffffu, lane == 0 ? stk[0] : 0.0, 0);
+  return res + 0.0;  // AC-5
+}
+
+// Dot d = blockIdx.x of a multi-dot pass: canonical tree over the CTA partials, then
+// op.store(d, value) by thread 0.
+template <class Op>
+__global__ void __launch_bounds__(FIN_THREADS) mdot_finish(Op op, const double* part, int stride, int ntiles) {
+  if (!op.begin()) return;
+  const double v = cta_tree(part + (size_t)blockIdx.x * stride, ntiles);
+  if (threadIdx.x == 0) op.store(blockIdx.x, v);
+}
+
 }  // namespace gsk

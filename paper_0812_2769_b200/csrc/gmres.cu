@@ -132,6 +132,92 @@ struct OpMgs {
   }
 };
 
+// End of Arnoldi step j (1-based; warp 0 of the finishing CTA): h_{j+1,j} = sqrt(hn2),
+// the previous Givens rotations on column j, the new rotation, g, the history entry,
+// the stopping tests and, when the cycle ends, the column-oriented
+// back substitution R y = g in one warp (AC-7).
+__device__ void arnoldi_finish(GmresState* S, double* hist, int j, double hn2, int lane, int cgs2) {
+  const int m = S->m, col = j - 1;
+  double* H = S->H;
+  __shared__ int need_bs;
+  if (lane == 0) {
+    const double hn = sqrt(hn2);
+    if (cgs2)  // H(:, j) = h + h' of the two classical projections
+      for (int i = 0; i < j; ++i) H[i * m + col] = S->c1[i] + S->c2[i];
+    H[j * m + col] = hn;
+    for (int i = 0; i < col; ++i) {  // previous rotations on column j
+      const double a = H[i * m + col], b = H[(i + 1) * m + col];
+      H[i * m + col] = __fma_rn(S->cs[i], a, S->sn[i] * b);
+      H[(i + 1) * m + col] = __fma_rn(-S->sn[i], a, S->cs[i] * b);
+    }
+    const double a = H[col * m + col], b = H[j * m + col];
+    const double delta = sqrt(__fma_rn(a, a, b * b));
+    const double cj = a / delta, sj = b / delta;
+    S->cs[col] = cj;
+    S->sn[col] = sj;
+    H[col * m + col] = delta;
+    H[j * m + col] = 0.0;
+    const double gj = S->g[col];
+    S->g[col + 1] = -sj * gj;
+    S->g[col] = cj * gj;
+    const double rel = fabs(S->g[col + 1]) / S->beta0;
+    const int it = S->it + 1;
+    S->it = it;
+    hist[it] = rel;
+    S->hist_len = it + 1;
+    S->k = j;
+    int stop = 0;
+    if (!isfinite(rel)) {
+      S->diverged = 1;
+      S->skip_x = 1;
+      S->final_ = 1;
+      stop = 1;
+    } else if (rel < S->tol) {
+      S->conv = 1;
+      S->final_ = 1;
+      stop = 1;
+    } else if (hn == 0.0 || it == S->maxit) {
+      if (it == S->maxit) S->final_ = 1;
+      stop = 1;
+    } else {
+      S->inv[j + 1] = 1.0 / hn;
+    }
+    S->cycle_stop = stop;
+    need_bs = (stop && !S->skip_x) || (j == m);
+  }
+  __syncwarp();
+  if (need_bs) {
+    // column-oriented back substitution R y = g (AC-7), lanes own rows
+    const int k = j;
+    double acc[MAX_M / 32];
+#pragma unroll
+    for (int q = 0; q < MAX_M / 32; ++q) {
+      const int l = lane + 32 * q;
+      acc[q] = l < k ? S->g[l] : 0.0;
+    }
+    bool fin = true;
+    for (int kk = k - 1; kk >= 0; --kk) {
+      const int owner = kk & 31, qo = kk >> 5;
+      double mine = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAX_M / 32; ++q)
+        if (q == qo) mine = acc[q];
+      const double ykk = __shfl_sync(0xffffffffu, mine, owner) / H[kk * m + kk];
+      fin = fin && isfinite(ykk);
+      if (lane == 0) S->y[kk] = ykk;
+#pragma unroll
+      for (int q = 0; q < MAX_M / 32; ++q) {
+        const int l = lane + 32 * q;
+        if (l < kk) acc[q] = __fma_rn(-H[l * m + kk], ykk, acc[q]);
+      }
+    }
+    if (lane == 0 && !fin) {
+      S->diverged = 1;
+      S->final_ = 1;
+    }
+  }
+}
+
 // L_j: w -= h_jj v_j; ||w||^2 -> Givens update, history, stopping, back-solve.
 struct OpLast {
   static constexpr int D = 1;
@@ -156,86 +242,100 @@ struct OpLast {
     Wn[q] = w;
     c[0] = w * w;
   }
-  __device__ void finish(const double (&s)[1], int lane) const {
-    GmresState* S = st;
-    const int m = S->m, col = j - 1;
-    double* H = S->H;
-    __shared__ int need_bs;
-    if (lane == 0) {
-      const double hn = sqrt(s[0]);
-      H[j * m + col] = hn;
-      for (int i = 0; i < col; ++i) {  // previous rotations on column j
-        const double a = H[i * m + col], b = H[(i + 1) * m + col];
-        H[i * m + col] = __fma_rn(S->cs[i], a, S->sn[i] * b);
-        H[(i + 1) * m + col] = __fma_rn(-S->sn[i], a, S->cs[i] * b);
-      }
-      const double a = H[col * m + col], b = H[j * m + col];
-      const double delta = sqrt(__fma_rn(a, a, b * b));
-      const double cj = a / delta, sj = b / delta;
-      S->cs[col] = cj;
-      S->sn[col] = sj;
-      H[col * m + col] = delta;
-      H[j * m + col] = 0.0;
-      const double gj = S->g[col];
-      S->g[col + 1] = -sj * gj;
-      S->g[col] = cj * gj;
-      const double rel = fabs(S->g[col + 1]) / S->beta0;
-      const int it = S->it + 1;
-      S->it = it;
-      hist[it] = rel;
-      S->hist_len = it + 1;
-      S->k = j;
-      int stop = 0;
-      if (!isfinite(rel)) {
-        S->diverged = 1;
-        S->skip_x = 1;
-        S->final_ = 1;
-        stop = 1;
-      } else if (rel < S->tol) {
-        S->conv = 1;
-        S->final_ = 1;
-        stop = 1;
-      } else if (hn == 0.0 || it == S->maxit) {
-        if (it == S->maxit) S->final_ = 1;
-        stop = 1;
-      } else {
-        S->inv[j + 1] = 1.0 / hn;
-      }
-      S->cycle_stop = stop;
-      need_bs = (stop && !S->skip_x) || (j == m);
-    }
-    __syncwarp();
-    if (need_bs) {
-      // column-oriented back substitution R y = g (AC-7), lanes own rows
-      const int k = j;
-      double acc[MAX_M / 32];
-#pragma unroll
-      for (int q = 0; q < MAX_M / 32; ++q) {
-        const int l = lane + 32 * q;
-        acc[q] = l < k ? S->g[l] : 0.0;
-      }
-      bool fin = true;
-      for (int kk = k - 1; kk >= 0; --kk) {
-        const int owner = kk & 31, qo = kk >> 5;
-        double mine = 0.0;
-#pragma unroll
-        for (int q = 0; q < MAX_M / 32; ++q)
-          if (q == qo) mine = acc[q];
-        const double ykk = __shfl_sync(0xffffffffu, mine, owner) / H[kk * m + kk];
-        fin = fin && isfinite(ykk);
-        if (lane == 0) S->y[kk] = ykk;
-#pragma unroll
-        for (int q = 0; q < MAX_M / 32; ++q) {
-          const int l = lane + 32 * q;
-          if (l < kk) acc[q] = __fma_rn(-H[l * m + kk], ykk, acc[q]);
-        }
-      }
-      if (lane == 0 && !fin) {
-        S->diverged = 1;
-        S->final_ = 1;
-      }
-    }
+  __device__ void finish(const double (&s)[1], int lane) const { arnoldi_finish(st, hist, j, s[0], lane, 0); }
+};
+
+// ---- double classical Gram-Schmidt (AZTEC's orthogonalisation) ----
+// Step j = three passes: A  w = A v_j, c1_d = <w, v_d>;  B  w -= sum_d c1_d v_d,
+// c2_d = <w, v_d>;  C  w -= sum_d c2_d v_d, ||w||^2 -> H(:, j) = c1 + c2, Givens.
+// Each update is an FMA chain over d ascending (oracle orc_gmres_orth, orth = 1).
+struct OpCgsA {
+  static constexpr bool kSpmv = true;
+  const double* W;
+  size_t n;
+  const double* Wj;
+  double* Wn;
+  GmresState* st;
+  int j;
+  int nd;
+  double invj;
+  const double* inv;
+  __device__ bool begin() {
+    if (st->done || st->cycle_stop) return false;
+    invj = st->inv[j];
+    inv = st->inv;
+    nd = j;
+    return true;
   }
+  __device__ double gather(int c) const { return __ldg(Wj + c) * invj; }
+  __device__ double value(int i, double y, double*) const {
+    Wn[i] = y;
+    return y;
+  }
+  __device__ double operand(int i, int d, const double*) const { return __ldg(W + d * n + i) * inv[d + 1]; }
+  __device__ void store(int d, double v) const { st->c1[d] = v; }
+};
+
+struct OpCgsB {
+  static constexpr bool kSpmv = false;
+  const double* W;
+  size_t n;
+  double* Wn;
+  GmresState* st;
+  int j;
+  int nd;
+  const double *inv, *c1;
+  __device__ bool begin() {
+    if (st->done || st->cycle_stop) return false;
+    inv = st->inv;
+    c1 = st->c1;
+    nd = j;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ double value(int i, double, double* cache) const {
+    double w = Wn[i];
+    const bool cached = nd <= MDOT_CACHE;
+    for (int d = 0; d < nd; ++d) {
+      const double v = __ldg(W + d * n + i) * inv[d + 1];
+      if (cached) cache[d * TB] = v;
+      w = __fma_rn(-c1[d], v, w);
+    }
+    Wn[i] = w;
+    return w;
+  }
+  __device__ double operand(int i, int d, const double* cache) const {
+    return nd <= MDOT_CACHE ? cache[d * TB] : __ldg(W + d * n + i) * inv[d + 1];
+  }
+  __device__ void store(int d, double v) const { st->c2[d] = v; }
+};
+
+struct OpCgsC {
+  static constexpr int D = 1;
+  static constexpr int NV = 1;
+  static constexpr bool kSpmv = false;
+  const double* W;
+  size_t n;
+  double* Wn;
+  double* hist;
+  GmresState* st;
+  int j;
+  const double *inv, *c2;
+  __device__ bool begin() {
+    if (st->done || st->cycle_stop) return false;
+    inv = st->inv;
+    c2 = st->c2;
+    return true;
+  }
+  __device__ const double* vin(int) const { return Wn; }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int q, double, const double (&v)[NV], double (&c)[1]) const {
+    double w = v[0];
+    for (int d = 0; d < j; ++d) w = __fma_rn(-c2[d], __ldg(W + d * n + q) * inv[d + 1], w);
+    Wn[q] = w;
+    c[0] = w * w;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const { arnoldi_finish(st, hist, j, s[0], lane, 1); }
 };
 
 // X: x += sum_{k=1..K} y_k v_k (k ascending)
@@ -272,7 +372,15 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
   auto slot = [&](int j) { return P->W + (size_t)(j - 1) * n; };
   GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
-  for (int j = 1; j <= m && rc >= 0; ++j) {
+  for (int j = 1; j <= m && rc >= 0 && P->orth == 1; ++j) {
+    OpCgsA a{P->W, n, slot(j), slot(j + 1), st, j, 0, 0, nullptr};
+    OpCgsB bpass{P->W, n, slot(j + 1), st, j, 0, nullptr, nullptr};
+    OpCgsC c{P->W, n, slot(j + 1), P->hist_d, st, j, nullptr, nullptr};
+    rc = j == 1 ? run_mdot(P, a, j, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_mdot(P, a, j, s);
+    if (rc >= 0) rc = j == 2 ? run_mdot(P, bpass, j, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_mdot(P, bpass, j, s);
+    if (rc >= 0) rc = run_pass(P, c, s);
+  }
+  for (int j = 1; j <= m && rc >= 0 && P->orth == 0; ++j) {
     OpArnoldi a{slot(j), slot(1), slot(j + 1), st, j, 0, 0};
     rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
     for (int i = 1; i < j && rc >= 0; ++i) {
@@ -318,10 +426,17 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
         g = nullptr;
       }
   }
+  if (P->orth == 1 && m > MDOT_MAX) {
+    set_error("gmres: double classical Gram-Schmidt supports m <= %d", MDOT_MAX);
+    return GSK_E_INVALID;
+  }
+  if (P->orth == 1 && !P->mpart)
+    GSK_CUDA(cudaMalloc(&P->mpart, sizeof(double) * MDOT_MAX * (size_t)P->pstride));
   if (!P->gstate) GSK_CUDA(cudaMalloc(&P->gstate, sizeof(GmresState)));
-  if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 5 * MAX_M + 8)));
+  if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8)));
   GSK_TRY(ensure_hist(P, maxit));
-  if (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d) {
+  if (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d ||
+      P->gkey_orth != P->orth) {
     for (auto& g : P->ggraph)
       if (g) {
         cudaGraphExecDestroy(g);
@@ -333,6 +448,7 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
     P->gkey_x = x;
     P->gkey_m = m;
     P->gkey_h = P->hist_d;
+    P->gkey_orth = P->orth;
   }
   cudaStream_t s = P->st;
   GSK_TRY(join_in(P, caller));
@@ -350,10 +466,12 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   h.g = h.sn + MAX_M;
   h.y = h.g + MAX_M + 1;
   h.inv = h.y + MAX_M;
+  h.c1 = h.inv + MAX_M + 2;
+  h.c2 = h.c1 + MAX_M;
   h.tol = tol;
   h.maxit = maxit;
   h.m = m;
-  GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 5 * MAX_M + 8), s));
+  GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8), s));
   GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   OpGResid init{x, b, P->weights, P->W, P->hist_d, P->gstate, 1};
   if (run_pass(P, init, s) < 0) return GSK_E_CUDA;

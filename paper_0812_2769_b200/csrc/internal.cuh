@@ -51,6 +51,7 @@ struct BicgState {
 struct GmresState {
   double beta0, n0w, tol, true_rel, true_rel_w;
   double *H, *cs, *sn, *g, *y, *inv;
+  double *c1, *c2;  // CGS2: the two classical projections of the current step
   int it, maxit, m, k, cycle_stop, final_, conv, diverged, skip_x, done, status, restarts,
       hist_len, pad;
 };
@@ -64,6 +65,7 @@ struct gsk_plan {
   int fmt = GSK_FMT_CSR;
   int poll = 0;
   int bmode = 2;  // Bi-CGSTAB schedule: 1 fused, 2 split
+  int orth = 0;   // GMRES orthogonalisation: 0 MGS, 1 double classical Gram-Schmidt
   const double* weights = nullptr;
   gsk::Geometry geo;
   gsk::CsrView csr{};
@@ -101,6 +103,8 @@ struct gsk_plan {
   const double* gkey_x = nullptr;
   int gkey_m = 0;
   const double* gkey_h = nullptr;
+  int gkey_orth = -1;
+  double* mpart = nullptr;     // [MDOT_MAX][pstride] partials of multi-dot passes
   // history (device)
   double* hist_d = nullptr;
   int hist_cap = 0;
@@ -158,6 +162,39 @@ int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullpt
   }
   return 1;
 }
+// Launch a multi-dot pass (J dots per row) and its J-CTA finish.
+template <class Op>
+int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 = nullptr,
+             cudaEvent_t pe1 = nullptr) {
+  const int n = P->geo.n;
+  const int sms = num_sms();
+  const int windows = (n + TB - 1) / TB;
+  int wpc = 8;
+  while (wpc > 1 && (long long)windows < (long long)wpc * 2 * sms) wpc >>= 1;
+  const int ntiles = (windows + wpc - 1) / wpc;
+  const size_t dyn = (!Op::kSpmv && J <= MDOT_CACHE) ? sizeof(double) * J * TB : 0;
+  static bool attr = false;
+  if constexpr (!Op::kSpmv) {
+    if (!attr) {
+      GSK_CUDA(cudaFuncSetAttribute(mdot_pass<0, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double) * MDOT_CACHE * TB)));
+      attr = true;
+    }
+  }
+  if (pe0) GSK_CUDA(cudaEventRecordWithFlags(pe0, s, cudaEventRecordExternal));
+  if constexpr (!Op::kSpmv)
+    mdot_pass<0, Op><<<ntiles, TB, dyn, s>>>(P->csr, P->sell, n, wpc, op, P->mpart, P->pstride);
+  else if (P->fmt == GSK_FMT_SELL)
+    mdot_pass<2, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->mpart, P->pstride);
+  else
+    mdot_pass<1, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->mpart, P->pstride);
+  GSK_LAUNCHED(1);
+  if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
+  mdot_finish<Op><<<J, FIN_THREADS, 0, s>>>(op, P->mpart, P->pstride, ntiles);
+  GSK_LAUNCHED(1);
+  return 2;
+}
+
 #define GSK_TRY(x)              \
   do {                          \
     int rc_ = (x);              \

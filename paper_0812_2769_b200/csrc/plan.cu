@@ -217,6 +217,13 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
     return GSK_E_INVALID;
   }
   P->bmode = sched == GSK_BICG_AUTO ? GSK_BICG_SPLIT : sched;
+  const int orth = opts ? opts->gmres_orth : GSK_ORTH_MGS;
+  if (orth != GSK_ORTH_MGS && orth != GSK_ORTH_CGS2) {
+    delete P;
+    set_error("gsk_plan_create: unknown gmres_orth %d", orth);
+    return GSK_E_INVALID;
+  }
+  P->orth = orth;
   int rc = plan_alloc_common(P);
   if (rc == GSK_OK && fmt == GSK_FMT_SELL) {
     cudaStream_t s = as_stream(stream);
@@ -252,7 +259,7 @@ void gsk_plan_destroy(gsk_plan* P) {
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->scratch,
-                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d};
+                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (P->h_flag) cudaFreeHost(P->h_flag);

@@ -180,14 +180,26 @@ def test_bicgstab_frame_weights():
 @pytest.mark.parametrize("name,N", CASES)
 @pytest.mark.parametrize("scaling", ["none", 2])
 @pytest.mark.parametrize("m", [1, 20, 30, 50])
-def test_gmres_parity(name, N, scaling, m):
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_gmres_parity(name, N, scaling, m, orth):
     s, val, b, _ = system(name, N, scaling)
     maxit = 400
     fmt = "sell" if name == "C4" else "csr"
-    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt)
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt, orth=orth)
     g = P.gmres(b, m=m, tol=1e-8, maxit=maxit)
-    o = oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-8, maxit)
+    o = oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-8, maxit, orth=orth)
     assert_same_solve(g, o)
+
+
+def test_gmres_cgs2_paper_problem1():
+    """GS(2) + GMRES(10) with the paper's own orthogonalisation on
+    Problem 1 128x128: bit-exact with the oracle; 265 steps to 1e-4 (Table 1)."""
+    s, val, b, _ = system("P1", None, 2)
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), orth="cgs2")
+    g = P.gmres(b, m=10, tol=1e-10, maxit=600)
+    o = oracle.gmres(s["row_ptr"], s["col"], val, b, 10, 1e-10, 600, orth="cgs2")
+    assert_same_solve(g, o)
+    assert int(np.flatnonzero(g[1] < 1e-4)[0]) == 265
 
 
 def test_solver_edge_cases():
@@ -272,6 +284,11 @@ def test_full_size_parity(name):
     g = P.gmres(bs, m=30, tol=c.tol, maxit=32)
     o = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 30, c.tol, 32)
     assert_same_solve(g, o)
+    if name in ("C2", "C4"):
+        Pc = gsk.Plan(As, fmt="sell" if c.sell else "csr", orth="cgs2")
+        g = Pc.gmres(bs, m=30, tol=c.tol, maxit=32)
+        o = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 30, c.tol, 32, orth="cgs2")
+        assert_same_solve(g, o)
 
 
 @pytest.mark.parametrize("name,N", [("C1", None), ("C3", 20), ("C4", 24), ("C5", 96), ("P1", 64)])
