@@ -231,17 +231,23 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = Clocks(local)
+    clocks = Clocks(local) if os.environ.get("GSK_BENCH_NO_CLOCKS") != "1" else None
     launches0 = gsk.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     reps = []
+    sev = []
     for _ in range(args.steps):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        sev.append(e)
         reps.append(step())
     ev1.record()
     torch.cuda.synchronize()
+    sev.append(ev1)
+    step_ms = [sev[k].elapsed_time(sev[k + 1]) for k in range(args.steps)]
     launches = gsk.launch_count() - launches0
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
     ms = ev0.elapsed_time(ev1)
     its = sum(r1["iterations"] + r2["iterations"] for r1, r2 in reps)
     if dist:
@@ -296,6 +302,8 @@ def main():
         "gmres": {"m": m, "orth": args.orth, "iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
                   "relres": r2["relres"], "true_relres": r2["true_relres"], "solve_ms": r2["solve_ms"],
                   "iters_per_s": r2["iterations"] / (r2["solve_ms"] / 1e3) if r2["solve_ms"] else None},
+        "steps_ms": [{"step": round(t, 2), "bicgstab": round(r1["solve_ms"], 2), "gmres": round(r2["solve_ms"], 2),
+                      "rest": round(t - r1["solve_ms"] - r2["solve_ms"], 2)} for t, (r1, r2) in zip(step_ms, reps)],
         "spmv": {"ms": spmv_ms, "gbps": spmv_gbps, "frac_of_hbm": spmv_gbps / hbm,
                  "frac_of_8TBps": spmv_gbps / 8000.0},
         "probe_ms": {"bicg_v_pass": probes[0], "bicg_t_pass": probes[1], "gmres_mgs": probes[2],

@@ -421,7 +421,7 @@ static int batch_size(const gsk_plan* P) {
   int K = P->poll;
   if (K <= 0) {
     const long long n = P->A.n;
-    K = (int)std::min<long long>(64, std::max<long long>(2, (1LL << 23) / n));
+    K = (int)std::min<long long>(64, std::max<long long>(4, (1LL << 26) / n));  // ~4+ ms batches at C4
   }
   return (K + 1) & ~1;  // even: p/v buffer parity repeats per replay
 }
@@ -480,8 +480,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    GSK_TRY(capture_bicg(P, x, K, 0, &P->bgraph[0]));
-    GSK_TRY(capture_bicg(P, x, K, 1, &P->bgraph[1]));
+    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_bicg(P, x, K, c, &P->bgraph[c]));
     P->bkey_b = b;
     P->bkey_x = x;
     P->bK = K;
@@ -505,33 +504,8 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   // batches of K iterations; the next batch is queued before the flag of the
   // previous one is read, so the GPU never idles on the host check
   const long long maxb = (maxit + K - 1) / K + 1;
-  long long nb = 0;
-  GSK_CUDA(cudaGraphLaunch(P->bgraph[0], s));
-  g_launches.fetch_add(P->bkernels);
-  ++nb;
-  cudaEvent_t ev;
-  GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  for (;;) {
-    const int copy = (int)((nb - 1) & 1);
-    GSK_CUDA(cudaMemcpyAsync(P->h_flag, &P->bstate->done, sizeof(int), cudaMemcpyDeviceToHost, s));
-    GSK_CUDA(cudaEventRecord(ev, s));
-    const bool more = nb < maxb;
-    if (more) {
-      GSK_CUDA(cudaGraphLaunch(P->bgraph[nb & 1], s));
-      g_launches.fetch_add(P->bkernels);
-      ++nb;
-    }
-    GSK_CUDA(cudaEventSynchronize(ev));
-    for (int kind = 0; kind < 2; ++kind) {
-      float ms = 0;
-      if (cudaEventElapsedTime(&ms, P->pev[kind][copy][0], P->pev[kind][copy][1]) == cudaSuccess) {
-        P->probe_ms[kind] += ms;
-        P->probe_n[kind] += 1;
-      }
-    }
-    if (P->h_flag[0] || !more) break;
-  }
-  cudaEventDestroy(ev);
+  const int kinds[2] = {0, 1};
+  GSK_TRY(run_batches(P, P->bgraph, maxb, P->bkernels, &P->bstate->done, kinds, 2));
   OpFinal fin{x, b, P->weights, P->bstate};
   if (run_pass(P, fin, s) < 0) return GSK_E_CUDA;
   GSK_CUDA(cudaEventRecord(P->t1, s));

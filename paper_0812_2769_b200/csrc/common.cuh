@@ -31,6 +31,15 @@ struct SellView {
   const uint8_t* __restrict__ roff; // [nchunks*32] in-window row offset
 };
 
+// Programmatic dependent launch (PDL): every pass / finish kernel waits for the
+// previous kernel's completion (and memory) at entry, then lets the next kernel of the
+// stream begin launching, so launch latency overlaps the tail of the previous grid.
+// Both are no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ldcs(const int* p) { return __ldcs(p); }
 

@@ -202,6 +202,7 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 template <int FMT, int RPT, class Op>
 __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
+  pdl_enter();
   if (!op.begin()) return;
   constexpr int D = Op::D;
   constexpr int DD = D > 0 ? D : 1;
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
 template <class Op>
 __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double* part, int stride,
                                                              int ntiles) {
+  pdl_enter();
   if (!op.begin()) return;
   constexpr int D = Op::D;
   __shared__ double ws[D][32];
@@ -363,6 +365,7 @@ struct MdotSmem {
 template <int FMT, class Op>
 __global__ void __launch_bounds__(TB, 2)
     mdot_pass(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
+  pdl_enter();
   if (!op.begin()) return;
   extern __shared__ __align__(16) double cache[];  // [J][TB] when op caches operands
   __shared__ MdotSmem<Op> sm;
@@ -468,6 +471,7 @@ __device__ __forceinline__ double cta_tree(const double* p, int ntiles) {
 // op.store(d, value) by thread 0.
 template <class Op>
 __global__ void __launch_bounds__(FIN_THREADS) mdot_finish(Op op, const double* part, int stride, int ntiles) {
+  pdl_enter();
   if (!op.begin()) return;
   const double v = cta_tree(part + (size_t)blockIdx.x * stride, ntiles);
   if (threadIdx.x == 0) op.store(blockIdx.x, v);

@@ -442,8 +442,7 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    GSK_TRY(capture_cycle(P, b, x, m, 0, &P->ggraph[0]));
-    GSK_TRY(capture_cycle(P, b, x, m, 1, &P->ggraph[1]));
+    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_cycle(P, b, x, m, c, &P->ggraph[c]));
     P->gkey_b = b;
     P->gkey_x = x;
     P->gkey_m = m;
@@ -476,34 +475,8 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   OpGResid init{x, b, P->weights, P->W, P->hist_d, P->gstate, 1};
   if (run_pass(P, init, s) < 0) return GSK_E_CUDA;
   const long long maxc = (long long)maxit + 2;
-  long long nc = 0;
-  GSK_CUDA(cudaGraphLaunch(P->ggraph[0], s));
-  g_launches.fetch_add(P->gkernels);
-  ++nc;
-  cudaEvent_t ev;
-  GSK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  for (;;) {
-    const int copy = (int)((nc - 1) & 1);
-    GSK_CUDA(cudaMemcpyAsync(P->h_flag, &P->gstate->done, sizeof(int), cudaMemcpyDeviceToHost, s));
-    GSK_CUDA(cudaEventRecord(ev, s));
-    const bool more = nc < maxc;
-    if (more) {
-      GSK_CUDA(cudaGraphLaunch(P->ggraph[nc & 1], s));
-      g_launches.fetch_add(P->gkernels);
-      ++nc;
-    }
-    GSK_CUDA(cudaEventSynchronize(ev));
-    for (int kind = 2; kind < 4; ++kind) {
-      if (kind == 2 && m < 2) continue;
-      float ms = 0;
-      if (cudaEventElapsedTime(&ms, P->pev[kind][copy][0], P->pev[kind][copy][1]) == cudaSuccess) {
-        P->probe_ms[kind] += ms;
-        P->probe_n[kind] += 1;
-      }
-    }
-    if (P->h_flag[0] || !more) break;
-  }
-  cudaEventDestroy(ev);
+  const int kinds[2] = {2, 3};
+  GSK_TRY(run_batches(P, P->ggraph, maxc, P->gkernels, &P->gstate->done, kinds, 2));
   GSK_CUDA(cudaEventRecord(P->t1, s));
   GmresState hs{};
   GSK_CUDA(cudaMemcpyAsync(&hs, P->gstate, sizeof hs, cudaMemcpyDeviceToHost, s));

@@ -85,6 +85,18 @@ __global__ void unscale_kernel(int64_t n, const double* s, const double* y, doub
   if (i < n) x[i] = s[i] * y[i];
 }
 
+// Per-process device word for the zero-row flag (avoids a stream-ordered allocation
+// per call; calls are serialised by the stream synchronisation they end with).
+static int* zero_row_flag(cudaStream_t s, int* err) {
+  static int* flag = nullptr;
+  if (!flag && cudaMalloc(&flag, sizeof(int)) != cudaSuccess) {
+    *err = 1;
+    return nullptr;
+  }
+  (void)s;
+  return flag;
+}
+
 }  // namespace gsk
 
 using namespace gsk;
@@ -105,8 +117,12 @@ extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double
     return GSK_E_INVALID;
   }
   cudaStream_t s = as_stream(stream);
-  int* dbad = nullptr;
-  GSK_CUDA(cudaMallocAsync(&dbad, sizeof(int), s));
+  int ferr = 0;
+  int* dbad = zero_row_flag(s, &ferr);
+  if (ferr) {
+    set_error("gs: cannot allocate the zero-row flag");
+    return GSK_E_NOMEM;
+  }
   const int big = 0x7fffffff;
   GSK_CUDA(cudaMemcpyAsync(dbad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
   const int grid = (A->n + TB - 1) / TB;
@@ -114,7 +130,6 @@ extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double
   GSK_LAUNCHED(1);
   int hbad = big;
   GSK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GSK_CUDA(cudaFreeAsync(dbad, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   if (hbad != big) {
     if (bad_row) *bad_row = hbad;
@@ -154,8 +169,12 @@ extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* va
     return GSK_E_INVALID;
   }
   cudaStream_t s = as_stream(stream);
-  int* dbad = nullptr;
-  GSK_CUDA(cudaMallocAsync(&dbad, sizeof(int), s));
+  int ferr = 0;
+  int* dbad = zero_row_flag(s, &ferr);
+  if (ferr) {
+    set_error("gs: cannot allocate the zero-row flag");
+    return GSK_E_NOMEM;
+  }
   const int big = 0x7fffffff;
   GSK_CUDA(cudaMemcpyAsync(dbad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
   const int grid = (A->n + TB - 1) / TB;
@@ -163,7 +182,6 @@ extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* va
   GSK_LAUNCHED(1);
   int hbad = big;
   GSK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GSK_CUDA(cudaFreeAsync(dbad, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   if (hbad != big) {
     if (bad_row) *bad_row = hbad;

@@ -3,6 +3,7 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include "common.cuh"
@@ -86,7 +87,8 @@ struct gsk_plan {
   // Bi-CGSTAB workspace
   double* bvec = nullptr;      // 7 vectors: r, rhat, pa, pb, va, vb, t
   gsk::BicgState* bstate = nullptr;
-  cudaGraphExec_t bgraph[2] = {nullptr, nullptr};
+  static constexpr int NQ = 3;  // graph copies = batches in flight (host checks lag)
+  cudaGraphExec_t bgraph[NQ] = {};
   const double* bkey_b = nullptr;
   const double* bkey_x = nullptr;
   int bK = 0;
@@ -98,7 +100,7 @@ struct gsk_plan {
   int Wm = 0;
   gsk::GmresState* gstate = nullptr;
   double* garr = nullptr;      // H, cs, sn, g, y, inv
-  cudaGraphExec_t ggraph[2] = {nullptr, nullptr};
+  cudaGraphExec_t ggraph[NQ] = {};
   const double* gkey_b = nullptr;
   const double* gkey_x = nullptr;
   int gkey_m = 0;
@@ -112,7 +114,8 @@ struct gsk_plan {
   // kinds: 0 Bi-CGSTAB v = A p pass, 1 Bi-CGSTAB t = A s pass, 2 GMRES MGS pass,
   // 3 GMRES Arnoldi SpMV pass; [graph copy][start/stop]
   static constexpr int NPROBE = 4;
-  cudaEvent_t pev[NPROBE][2][2] = {};
+  cudaEvent_t pev[NPROBE][NQ][2] = {};
+  cudaEvent_t qev[NQ] = {};
   double probe_ms[NPROBE] = {};
   int64_t probe_n[NPROBE] = {};
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -122,6 +125,24 @@ namespace gsk {
 // Launch one fused pass over the plan's rows: Op::kSpmv selects an SpMV pass in the
 // plan's format (CSR or SELL) or a pure vector pass.
 int num_sms();
+bool pdl_enabled();  // GSK_PDL=0 in the environment disables programmatic launches
+
+// Kernel launch with the programmatic-stream-serialization attribute (PDL).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // Launch one pass: an SpMV pass in the plan's format (CSR or SELL) or a vector pass,
 // then (if it reduces dot products) the single-CTA finish kernel.  pe0/pe1: optional
@@ -138,10 +159,10 @@ int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullpt
     constexpr int R = VecRpt<Op::NV>::value;
     if ((long long)n >= 2LL * TB * R * sms) {
       ntiles = (n + TB * R - 1) / (TB * R);
-      pass_kernel<0, R, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, R, op, P->part, P->pstride);
+      GSK_CUDA(launch_k(pass_kernel<0, R, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, R, op, P->part, P->pstride));
     } else {
       ntiles = (n + TB * 2 - 1) / (TB * 2);
-      pass_kernel<0, 2, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, 2, op, P->part, P->pstride);
+      GSK_CUDA(launch_k(pass_kernel<0, 2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, 2, op, P->part, P->pstride));
     }
   } else {
     const int windows = (n + TB - 1) / TB;
@@ -149,14 +170,14 @@ int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullpt
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
     if (P->fmt == GSK_FMT_SELL)
-      pass_kernel<2, 1, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->part, P->pstride);
+      GSK_CUDA(launch_k(pass_kernel<2, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
     else
-      pass_kernel<1, 1, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->part, P->pstride);
+      GSK_CUDA(launch_k(pass_kernel<1, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
   }
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
   if constexpr (Op::D > 0) {
-    finish_kernel<Op><<<1, FIN_THREADS, 0, s>>>(op, P->part, P->pstride, ntiles);
+    GSK_CUDA(launch_k(finish_kernel<Op>, 1, FIN_THREADS, 0, s, op, P->part, P->pstride, ntiles));
     GSK_LAUNCHED(1);
     return 2;
   }
@@ -183,14 +204,14 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
   }
   if (pe0) GSK_CUDA(cudaEventRecordWithFlags(pe0, s, cudaEventRecordExternal));
   if constexpr (!Op::kSpmv)
-    mdot_pass<0, Op><<<ntiles, TB, dyn, s>>>(P->csr, P->sell, n, wpc, op, P->mpart, P->pstride);
+    GSK_CUDA(launch_k(mdot_pass<0, Op>, ntiles, TB, dyn, s, P->csr, P->sell, n, wpc, op, P->mpart, P->pstride));
   else if (P->fmt == GSK_FMT_SELL)
-    mdot_pass<2, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->mpart, P->pstride);
+    GSK_CUDA(launch_k(mdot_pass<2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->mpart, P->pstride));
   else
-    mdot_pass<1, Op><<<ntiles, TB, 0, s>>>(P->csr, P->sell, n, wpc, op, P->mpart, P->pstride);
+    GSK_CUDA(launch_k(mdot_pass<1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->mpart, P->pstride));
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
-  mdot_finish<Op><<<J, FIN_THREADS, 0, s>>>(op, P->mpart, P->pstride, ntiles);
+  GSK_CUDA(launch_k(mdot_finish<Op>, J, FIN_THREADS, 0, s, op, P->mpart, P->pstride, ntiles));
   GSK_LAUNCHED(1);
   return 2;
 }
@@ -208,5 +229,10 @@ int ensure_hist(gsk_plan* P, int maxit);
 // nodes (returned in *kernels; launches made during capture are not counted).
 int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels, const char* what);
 int join_in(gsk_plan* P, cudaStream_t caller);
+// Replay graphs[b % NQ] for batch b until the device flag *done_dev is set (checked on
+// the host one batch behind, NQ batches in flight) or maxb batches ran; accumulates
+// the probe events of the kinds listed.
+int run_batches(gsk_plan* P, cudaGraphExec_t* graphs, long long maxb, long long kernels, const int* done_dev,
+                const int* kinds, int nkinds);
 int join_out(gsk_plan* P, cudaStream_t caller);
 }  // namespace gsk

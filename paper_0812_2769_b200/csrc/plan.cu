@@ -28,6 +28,15 @@ Geometry make_geometry(int n) {
   return g;
 }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("GSK_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -107,6 +116,7 @@ static int plan_alloc_common(gsk_plan* P) {
   GSK_CUDA(cudaMalloc(&P->scratch, sizeof(double) * 8));
   GSK_CUDA(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
   GSK_CUDA(cudaMallocHost(&P->h_flag, sizeof(int) * 16));
+  for (int q = 0; q < 16; ++q) P->h_flag[q] = 0;
   GSK_CUDA(cudaEventCreate(&P->t0));
   GSK_CUDA(cudaEventCreate(&P->t1));
   for (auto& k : P->pev)
@@ -114,6 +124,7 @@ static int plan_alloc_common(gsk_plan* P) {
       GSK_CUDA(cudaEventCreate(&e[0]));
       GSK_CUDA(cudaEventCreate(&e[1]));
     }
+  for (auto& e : P->qev) GSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   P->csr = CsrView{P->A.n, P->A.row_ptr, P->A.col_idx, P->A.values};
   return GSK_OK;
 }
@@ -172,6 +183,51 @@ int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels
   }
   g_launches.fetch_sub(k);  // counted per replay instead
   *kernels = k;
+  return GSK_OK;
+}
+
+int run_batches(gsk_plan* P, cudaGraphExec_t* graphs, long long maxb, long long kernels, const int* done_dev,
+                const int* kinds, int nkinds) {
+  constexpr int NQ = gsk_plan::NQ;
+  cudaStream_t s = P->st;
+  // batches in flight: 3 for large systems (a late host check never idles the GPU);
+  // 1 for small ones, where a queued batch that returns at once costs as much as a
+  // real one
+  const int depth = P->A.n >= (1 << 20) ? NQ : 1;
+  long long launched = 0, checked = 0;
+  auto launch = [&]() -> int {
+    const int c = (int)(launched % NQ);
+    GSK_CUDA(cudaGraphLaunch(graphs[c], s));
+    g_launches.fetch_add(kernels);
+    GSK_CUDA(cudaMemcpyAsync(P->h_flag + c, done_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaEventRecord(P->qev[c], s));
+    ++launched;
+    return GSK_OK;
+  };
+  while (launched < depth && launched < maxb) GSK_TRY(launch());
+  for (;;) {
+    const int c = (int)(checked % NQ);
+    GSK_CUDA(cudaEventSynchronize(P->qev[c]));
+    for (int q = 0; q < nkinds; ++q) {
+      const int kind = kinds[q];
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, P->pev[kind][c][0], P->pev[kind][c][1]) == cudaSuccess) {
+        P->probe_ms[kind] += ms;
+        P->probe_n[kind] += 1;
+      } else {
+        (void)cudaGetLastError();  // probe not recorded in this graph (e.g. GMRES m = 1)
+      }
+    }
+    const int done = P->h_flag[c];
+    ++checked;
+    if (done) break;
+    if (launched < maxb)
+      GSK_TRY(launch());
+    else if (checked == launched)
+      break;
+  }
+  // drain the batches still queued (they return at once: the done flag is set)
+  GSK_CUDA(cudaStreamSynchronize(s));
   return GSK_OK;
 }
 
@@ -268,6 +324,8 @@ void gsk_plan_destroy(gsk_plan* P) {
       if (e[0]) cudaEventDestroy(e[0]);
       if (e[1]) cudaEventDestroy(e[1]);
     }
+  for (auto e : P->qev)
+    if (e) cudaEventDestroy(e);
   if (P->t0) cudaEventDestroy(P->t0);
   if (P->t1) cudaEventDestroy(P->t1);
   if (P->st) cudaStreamDestroy(P->st);
