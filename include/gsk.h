@@ -73,6 +73,11 @@ typedef struct gsk_opts {
   const double *weights;
   int32_t bicg_schedule;
   int32_t gmres_orth;
+  int32_t sell_index;   /* SELL column indices: 0 = plain int32 (default), 1 = uint8
+                           index into a per-chunk dictionary of col - row deltas when
+                           every chunk has <= 32 of them (25% fewer matrix bytes, but
+                           slower on B200 at C4: DESIGN.md §5) */
+  int32_t reserved_;
 } gsk_opts;
 
 enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2 };
@@ -123,6 +128,11 @@ int gsk_plan_spmv(gsk_plan *plan, const double *x, double *y, void *stream);
 int gsk_plan_sell_info(gsk_plan *plan, int64_t *nchunks, int64_t *nslots);
 int gsk_plan_sell_copy(gsk_plan *plan, int32_t *chunk_ptr, int32_t *chunk_len,
                        int32_t *scol, double *sval, uint8_t *roff, void *stream);
+/* SELL column-index dictionary (SELL-D): per chunk the ascending distinct
+ * deltas col - row of its real slots (<= 32), per slot a uint8 index into them (255 =
+ * padding).  *ndict = -1 when the plan uses plain int32 columns.  Outputs nullable. */
+int gsk_plan_sell_dict(gsk_plan *plan, int64_t *ndict, int32_t *dict_ptr, int32_t *dict,
+                       uint8_t *sidx, void *stream);
 void gsk_plan_destroy(gsk_plan *plan);
 
 /* Bi-CGSTAB (van der Vorst 1992) on A x = b.

@@ -56,6 +56,10 @@ def _lib():
         lib.orc_sell_size.restype = i64
         lib.orc_sell_build.argtypes = [i64, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
         lib.orc_sell_build.restype = i32
+        lib.orc_sell_dict_size.argtypes = [i64, i32, i32, vp, vp, vp]
+        lib.orc_sell_dict_size.restype = i64
+        lib.orc_sell_dict.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, vp]
+        lib.orc_sell_dict.restype = i32
         lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, vp, d, i32, vp, vp,
                                      ctypes.POINTER(Report)]
         lib.orc_bicgstab.restype = i32
@@ -165,6 +169,24 @@ def sell_build(row_ptr, col, val, C=32, sigma=256):
                                *(_p(out[k]) for k in ("chunk_ptr", "chunk_len", "scol", "sval", "roff")))
     if rc != 0:
         raise ValueError("bad SELL parameters")
+    return out
+
+
+def sell_dict(n, S, C=32, sigma=256):
+    """Delta-dictionary encoding of a SELL layout's column indices (None if some chunk
+    has more than 32 distinct col - row deltas)."""
+    cp, sc, ro = _i32(S["chunk_ptr"]), _i32(S["scol"]), np.ascontiguousarray(S["roff"], np.uint8)
+    tot = _lib().orc_sell_dict_size(n, C, sigma, _p(cp), _p(sc), _p(ro))
+    if tot < 0:
+        return None
+    nch = (n + C - 1) // C
+    out = {"dict_ptr": np.zeros(nch + 1, np.int32), "dict": np.zeros(max(tot, 1), np.int32),
+           "sidx": np.zeros(sc.size, np.uint8)}
+    rc = _lib().orc_sell_dict(n, C, sigma, _p(cp), _p(sc), _p(ro), _p(out["dict_ptr"]), _p(out["dict"]),
+                              _p(out["sidx"]))
+    if rc != 0:
+        return None
+    out["dict"] = out["dict"][:tot]
     return out
 
 

@@ -229,6 +229,66 @@ int orc_sell_build(int64_t n, const int32_t* rp, const int32_t* ci, const double
   return 0;
 }
 
+// ---- SELL column-index dictionary (storage format of the GPU path) ----
+// Per chunk c: D_c = ascending distinct deltas (col - row) over the chunk's real slots;
+// idx[slot] = position of the slot's delta in D_c, 255 for padding.  Valid only when
+// every |D_c| <= 32 (returns 0), else returns 1 (format not applicable).
+int64_t orc_sell_dict_size(int64_t n, int C, int sigma, const int32_t* chunk_ptr, const int32_t* scol,
+                           const uint8_t* roff) {
+  int64_t nch = (n + C - 1) / C, tot = 0;
+  for (int64_t c = 0; c < nch; ++c) {
+    std::vector<int32_t> d;
+    int64_t w0 = (c * C) / sigma * sigma;
+    int32_t L = (chunk_ptr[c + 1] - chunk_ptr[c]) / C;
+    for (int lane = 0; lane < C; ++lane) {
+      int64_t row = w0 + roff[c * C + lane];
+      for (int32_t k = 0; k < L; ++k) {
+        int32_t col = scol[chunk_ptr[c] + (int64_t)k * C + lane];
+        if (col >= 0) d.push_back((int32_t)(col - row));
+      }
+    }
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    if (d.size() > 32) return -1;
+    tot += (int64_t)d.size();
+  }
+  return tot;
+}
+
+int orc_sell_dict(int64_t n, int C, int sigma, const int32_t* chunk_ptr, const int32_t* scol,
+                  const uint8_t* roff, int32_t* dict_ptr, int32_t* dict, uint8_t* sidx) {
+  int64_t nch = (n + C - 1) / C;
+  dict_ptr[0] = 0;
+  for (int64_t c = 0; c < nch; ++c) {
+    std::vector<int32_t> d;
+    int64_t w0 = (c * C) / sigma * sigma;
+    int32_t L = (chunk_ptr[c + 1] - chunk_ptr[c]) / C;
+    for (int lane = 0; lane < C; ++lane) {
+      int64_t row = w0 + roff[c * C + lane];
+      for (int32_t k = 0; k < L; ++k) {
+        int32_t col = scol[chunk_ptr[c] + (int64_t)k * C + lane];
+        if (col >= 0) d.push_back((int32_t)(col - row));
+      }
+    }
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    if (d.size() > 32) return 1;
+    for (size_t u = 0; u < d.size(); ++u) dict[dict_ptr[c] + u] = d[u];
+    dict_ptr[c + 1] = dict_ptr[c] + (int32_t)d.size();
+    for (int lane = 0; lane < C; ++lane) {
+      int64_t row = w0 + roff[c * C + lane];
+      for (int32_t k = 0; k < L; ++k) {
+        int64_t slot = chunk_ptr[c] + (int64_t)k * C + lane;
+        int32_t col = scol[slot];
+        if (col < 0) { sidx[slot] = 255; continue; }
+        int32_t delta = (int32_t)(col - row);
+        sidx[slot] = (uint8_t)(std::lower_bound(d.begin(), d.end(), delta) - d.begin());
+      }
+    }
+  }
+  return 0;
+}
+
 // ---- Bi-CGSTAB (van der Vorst 1992, cited PAPER.md:102) ----------------------------
 // DESIGN.md §4 algorithm B, arithmetic AC-6; stopping PAPER.md:302-307 (reading B1/B2:
 // strict <, frame weights w optional); breakdown exact-zero tests (PAPER.md:315-321,

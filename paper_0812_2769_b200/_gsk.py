@@ -23,7 +23,7 @@ ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
 SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
-           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_destroy",
+           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_destroy",
            "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
            "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
            "gsk_last_error", "gsk_launch_count", "gsk_version")
@@ -48,7 +48,8 @@ class Report(ctypes.Structure):
 
 class Opts(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("poll", ctypes.c_int32), ("weights", ctypes.c_void_p),
-                ("bicg_schedule", ctypes.c_int32), ("gmres_orth", ctypes.c_int32)]
+                ("bicg_schedule", ctypes.c_int32), ("gmres_orth", ctypes.c_int32),
+                ("sell_index", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
 
 class GskError(RuntimeError):
@@ -81,6 +82,7 @@ def load(path: str = LIB_PATH):
     lib.gsk_plan_spmv.argtypes = [vp, vp, vp, vp]
     lib.gsk_plan_sell_info.argtypes = [vp, P(i64), P(i64)]
     lib.gsk_plan_sell_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    lib.gsk_plan_sell_dict.argtypes = [vp, P(i64), vp, vp, vp, vp]
     lib.gsk_plan_destroy.argtypes = [vp]
     lib.gsk_plan_destroy.restype = None
     lib.gsk_bicgstab_solve.argtypes = [P(CsrStruct), vp, vp, d, i32, vp, vp, P(Report), vp]
@@ -220,12 +222,12 @@ class Plan:
     """gsk_plan: SELL build, workspace and captured graphs reused across solves."""
 
     def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
-                 orth: str = "mgs"):
+                 orth: str = "mgs", sell_index: str = "plain"):
         lib = load()
         self.A = A
         self.weights = _dev_f64(weights, A.n)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE[schedule], ORTH[orth])
+                    SCHEDULE[schedule], ORTH[orth], {"plain": 0, "dict": 1}[sell_index], 0)
         self._csr = A.struct()
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))
@@ -273,6 +275,25 @@ class Plan:
         res = {k: v.cpu().numpy() for k, v in out.items()}
         res["scol"] = res["scol"][:nsl.value]
         res["sval"] = res["sval"][:nsl.value]
+        return res
+
+    def sell_dict(self):
+        """The plan's SELL column dictionary (None when it uses plain int32 columns)."""
+        lib = load()
+        nd = ctypes.c_int64()
+        _check(lib.gsk_plan_sell_dict(self.h, ctypes.byref(nd), None, None, None, _stream()))
+        if nd.value < 0:
+            return None
+        nch, nsl = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.gsk_plan_sell_info(self.h, ctypes.byref(nch), ctypes.byref(nsl)))
+        out = {"dict_ptr": torch.empty(nch.value + 1, dtype=torch.int32, device="cuda"),
+               "dict": torch.empty(max(nd.value, 1), dtype=torch.int32, device="cuda"),
+               "sidx": torch.empty(max(nsl.value, 1), dtype=torch.uint8, device="cuda")}
+        _check(lib.gsk_plan_sell_dict(self.h, ctypes.byref(nd), _ptr(out["dict_ptr"]), _ptr(out["dict"]),
+                                      _ptr(out["sidx"]), _stream()))
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res["dict"] = res["dict"][:nd.value]
+        res["sidx"] = res["sidx"][:nsl.value]
         return res
 
     def probe(self, kind: int):

@@ -29,6 +29,11 @@ struct SellView {
   const int* __restrict__ scol;     // [nslots], -1 = padding
   const double* __restrict__ sval;  // [nslots]
   const uint8_t* __restrict__ roff; // [nchunks*32] in-window row offset
+  // optional column-index dictionary (null: scol is used): per slot a uint8 index into
+  // the chunk's ascending distinct deltas col - row (255 = padding)
+  const uint8_t* __restrict__ sidx;  // [nslots]
+  const int* __restrict__ dptr;      // [nchunks+1]
+  const int* __restrict__ dict;      // [ndict]
 };
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the

@@ -53,6 +53,8 @@ struct PassSmem<2> {
   double sy[2][TB];
   double wp[8 * MAXD * 8];
 };
+template <>
+struct PassSmem<3> : PassSmem<2> {};
 
 // Register budget per pass kind (CTAs per SM): SELL keeps 8 slots (col, val, x) in
 // flight per lane, vector passes RPT rows of NV operands; CSR is bounded by its
@@ -76,10 +78,16 @@ struct SellTuning<Op, std::void_t<decltype(Op::kSellMinBlocks)>> {
   static constexpr int minb = Op::kSellMinBlocks;
 };
 
+#ifndef GSK_SELLD_DOT_MINB
+#define GSK_SELLD_DOT_MINB 4
+#endif
 template <int FMT, class Op>
 struct PassOcc {
-  static constexpr int kMinBlocks = FMT == 1 ? 4 : FMT == 2 ? SellTuning<Op>::minb : 3;
-  static constexpr bool kPrefetch = FMT == 1 || (FMT == 2 && SellTuning<Op>::minb < 4);
+  static constexpr int kMinBlocks = FMT == 1 ? 4
+                                  : FMT == 3 ? (Op::D > 0 && SellTuning<Op>::minb == 4 ? GSK_SELLD_DOT_MINB
+                                                                                       : SellTuning<Op>::minb)
+                                  : FMT == 2 ? SellTuning<Op>::minb : 3;
+  static constexpr bool kPrefetch = FMT == 1 || (FMT >= 2 && SellTuning<Op>::minb < 4);
 };
 
 // y for row r0 + t of a CSR window (AC-3 chain), staged through st.
@@ -108,7 +116,7 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
 
 // y for row r0 + t of a SELL window: lane l of warp w computes slot l of chunk
 // r0/32 + w; results are scattered to sy at the rows' in-window offsets.
-template <class G>
+template <bool DICT, class G>
 __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G& g, double* sy) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int c = (r0 >> 5) + warp;
@@ -117,7 +125,32 @@ __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G
     const int p0 = A.cptr[c], L = (A.cptr[c + 1] - p0) >> 5;
     const int base = p0 + lane;
     double acc = 0.0;
-    if (L <= 8) {
+    if (DICT && L <= 8) {
+      // SELL-D: col = row + dict_c[idx] (1-byte index per slot instead of 4)
+      const int d0 = A.dptr[c], U = A.dptr[c + 1] - d0;
+      const int dv = lane < U ? __ldg(A.dict + d0 + lane) : 0;
+      const int row = r0 + rl;
+      int cols[8];
+      double vals[8], xs[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)  // all slot loads first (shuffles would serialise them)
+        if (k < L) {
+          cols[k] = __ldcs(A.sidx + base + k * SELL_C);
+          vals[k] = __ldcs(A.sval + base + k * SELL_C);
+        }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L) {
+          const int delta = __shfl_sync(0xffffffffu, dv, cols[k] & 31);
+          cols[k] = cols[k] == 255 ? -1 : row + delta;
+        }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L && cols[k] >= 0) xs[k] = g(cols[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L && cols[k] >= 0) acc = __fma_rn(vals[k], xs[k], acc);
+    } else if (L <= 8) {
       int cols[8];
       double vals[8], xs[8];
 #pragma unroll
@@ -133,7 +166,7 @@ __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G
       for (int k = 0; k < 8; ++k)
         if (k < L && cols[k] >= 0) acc = __fma_rn(vals[k], xs[k], acc);
     } else {
-      for (int k = 0; k < L; ++k) {
+      for (int k = 0; k < L; ++k) {  // long chunks: plain int32 columns (kept in every plan)
         const int col = __ldcs(A.scol + base + k * SELL_C);
         if (col >= 0) acc = __fma_rn(__ldcs(A.sval + base + k * SELL_C), g(col), acc);
       }
@@ -198,7 +231,7 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 }
 
 // FMT 0: vector pass, RPT windows (rows r0 + 256 w + t) per CTA, all loads in flight.
-// FMT 1/2: SpMV pass over wpc windows.
+// FMT 1/2/3: SpMV pass over wpc windows (CSR, SELL, SELL with column dictionary).
 template <int FMT, int RPT, class Op>
 __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
@@ -246,7 +279,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
         if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
         if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
-        else y = sell_window(sell, r0, g, sm.sy[w & 1]);
+        else y = sell_window<FMT == 3>(sell, r0, g, sm.sy[w & 1]);
         if (!kPre && i < n) load_vin(op, i, v);
         if (i < n) op.row(i, y, v, cc);
       }

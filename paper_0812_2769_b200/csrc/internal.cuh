@@ -78,6 +78,11 @@ struct gsk_plan {
   double* sval = nullptr;
   uint8_t* roff = nullptr;
   int64_t nchunks = 0, nslots = 0;
+  uint8_t* sidx = nullptr;  // column-index dictionary (SELL-D); null = plain int32 columns
+  int* dptr = nullptr;
+  int* dict = nullptr;
+  int64_t ndict = 0;
+  int sell_index = 0;       // 0 auto (dictionary when applicable), 1 plain
   // reduction scratch
   double* part = nullptr;      // [MAXD][pstride] CTA partials of the current pass
   int pstride = 0;             // >= number of CTAs of any pass (ceil(n/256))
@@ -169,7 +174,9 @@ int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullpt
     int wpc = 8;  // windows per CTA: as many as keep >= 3 CTAs per SM busy
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
-    if (P->fmt == GSK_FMT_SELL)
+    if (P->fmt == GSK_FMT_SELL && P->sell.dict)
+      GSK_CUDA(launch_k(pass_kernel<3, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
+    else if (P->fmt == GSK_FMT_SELL)
       GSK_CUDA(launch_k(pass_kernel<2, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
     else
       GSK_CUDA(launch_k(pass_kernel<1, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
@@ -224,6 +231,7 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
 
 int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
+int sell_dict_build(gsk_plan* P, cudaStream_t s);
 int ensure_hist(gsk_plan* P, int maxit);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).

@@ -280,11 +280,18 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
     return GSK_E_INVALID;
   }
   P->orth = orth;
+  P->sell_index = opts ? opts->sell_index : 0;
+  if (P->sell_index != 0 && P->sell_index != 1) {
+    delete P;
+    set_error("gsk_plan_create: unknown sell_index %d", opts->sell_index);
+    return GSK_E_INVALID;
+  }
   int rc = plan_alloc_common(P);
   if (rc == GSK_OK && fmt == GSK_FMT_SELL) {
     cudaStream_t s = as_stream(stream);
     rc = join_in(P, s);
     if (rc == GSK_OK) rc = sell_build(P, P->st);
+    if (rc == GSK_OK && P->sell_index == 1) rc = sell_dict_build(P, P->st);
     if (rc == GSK_OK) rc = join_out(P, s);
     if (rc == GSK_OK && cudaStreamSynchronize(P->st) != cudaSuccess) rc = GSK_E_CUDA;
   }
@@ -315,7 +322,7 @@ void gsk_plan_destroy(gsk_plan* P) {
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->scratch,
-                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart};
+                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (P->h_flag) cudaFreeHost(P->h_flag);
@@ -415,6 +422,25 @@ int gsk_plan_sell_copy(gsk_plan* P, int32_t* chunk_ptr, int32_t* chunk_len, int3
   if (scol) GSK_CUDA(cudaMemcpyAsync(scol, P->scol, sizeof(int) * P->nslots, cudaMemcpyDeviceToDevice, s));
   if (sval) GSK_CUDA(cudaMemcpyAsync(sval, P->sval, sizeof(double) * P->nslots, cudaMemcpyDeviceToDevice, s));
   if (roff) GSK_CUDA(cudaMemcpyAsync(roff, P->roff, P->nchunks * SELL_C, cudaMemcpyDeviceToDevice, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
+
+int gsk_plan_sell_dict(gsk_plan* P, int64_t* ndict, int32_t* dict_ptr, int32_t* dict, uint8_t* sidx,
+                       void* stream) {
+  if (!P || P->fmt != GSK_FMT_SELL) {
+    set_error("gsk_plan_sell_dict: plan is not SELL");
+    return GSK_E_INVALID;
+  }
+  if (!P->dict) {
+    if (ndict) *ndict = -1;
+    return GSK_OK;
+  }
+  if (ndict) *ndict = P->ndict;
+  cudaStream_t s = as_stream(stream);
+  if (dict_ptr) GSK_CUDA(cudaMemcpyAsync(dict_ptr, P->dptr, sizeof(int) * (P->nchunks + 1), cudaMemcpyDeviceToDevice, s));
+  if (dict) GSK_CUDA(cudaMemcpyAsync(dict, P->dict, sizeof(int) * P->ndict, cudaMemcpyDeviceToDevice, s));
+  if (sidx) GSK_CUDA(cudaMemcpyAsync(sidx, P->sidx, P->nslots, cudaMemcpyDeviceToDevice, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   return GSK_OK;
 }

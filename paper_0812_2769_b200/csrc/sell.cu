@@ -5,6 +5,7 @@
 //   2. chunk_ptr = exclusive scan of 32 * chunk_len (one CTA);
 //   3. fill: slot (k, lane) of chunk c at chunk_ptr[c] + 32 k + lane, CSR order kept,
 //      padding col = -1, val = 0 (predicated off in the SpMV, AC-3).
+#include <climits>
 #include "internal.cuh"
 
 namespace gsk {
@@ -33,13 +34,13 @@ __global__ void __launch_bounds__(TB) sell_rank_kernel(int n, int nchunks, const
 }
 
 // exclusive scan of 32*clen into cptr[0..nchunks] (single CTA, one-off)
-__global__ void __launch_bounds__(1024) sell_scan_kernel(int nchunks, const int* __restrict__ clen, int* cptr) {
+__global__ void __launch_bounds__(1024) sell_scan_kernel(int nchunks, const int* __restrict__ clen, int* cptr, int mult) {
   __shared__ long long part[1024];
   const int t = threadIdx.x;
   const int per = (nchunks + 1023) / 1024;
   const int a = t * per, b = min(nchunks, a + per);
   long long s = 0;
-  for (int i = a; i < b; ++i) s += (long long)clen[i] * SELL_C;
+  for (int i = a; i < b; ++i) s += (long long)clen[i] * mult;
   part[t] = s;
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(1024) sell_scan_kernel(int nchunks, const int*
   long long run = t ? part[t - 1] : 0;
   for (int i = a; i < b; ++i) {
     cptr[i] = (int)run;
-    run += (long long)clen[i] * SELL_C;
+    run += (long long)clen[i] * mult;
   }
   if (t == 1023) cptr[nchunks] = (int)part[1023];
 }
@@ -88,7 +89,7 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&P->roff, (size_t)P->nchunks * SELL_C));
   sell_rank_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->roff, P->clen);
   GSK_LAUNCHED(1);
-  sell_scan_kernel<<<1, 1024, 0, s>>>((int)P->nchunks, P->clen, P->cptr);
+  sell_scan_kernel<<<1, 1024, 0, s>>>((int)P->nchunks, P->clen, P->cptr, SELL_C);
   GSK_LAUNCHED(1);
   int tot = 0;
   GSK_CUDA(cudaMemcpyAsync(&tot, P->cptr + P->nchunks, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -99,7 +100,102 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
                                        P->cptr, P->roff, P->scol, P->sval, false);
   GSK_LAUNCHED(1);
-  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff};
+  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr};
+  return GSK_OK;
+}
+
+// ---- column-index dictionary ("SELL-D") ---------------------------------
+// One warp per chunk.  The chunk's distinct deltas col - row (real slots only) are
+// extracted in ascending order by repeated warp minima; a chunk with more than 32
+// deltas makes the format inapplicable (*fail = 1).  Pass 0 counts, pass 1 writes the
+// dictionary and the per-slot uint8 index (255 = padding).
+__global__ void __launch_bounds__(TB) sell_dict_kernel(int nchunks, const int* __restrict__ cptr,
+                                                       const int* __restrict__ scol, const uint8_t* __restrict__ roff,
+                                                       int* ucount, const int* __restrict__ dptr, int* dict,
+                                                       uint8_t* sidx, int* fail, int pass) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (TB / 32) + (threadIdx.x >> 5);
+  if (c >= nchunks) return;
+  const long long row = (long long)(c * SELL_C) / SELL_SIGMA * SELL_SIGMA + roff[c * SELL_C + lane];
+  const int p0 = cptr[c], L = (cptr[c + 1] - p0) / SELL_C;
+  long long last = LLONG_MIN;
+  int U = 0;
+  int dv = 0;  // lane u < U holds dictionary entry u
+  for (;;) {
+    long long mine = LLONG_MAX;
+    for (int k = 0; k < L; ++k) {
+      const int col = scol[p0 + k * SELL_C + lane];
+      if (col >= 0) {
+        const long long d = (long long)col - row;
+        if (d > last && d < mine) mine = d;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const long long o = __shfl_xor_sync(0xffffffffu, mine, off);
+      mine = o < mine ? o : mine;
+    }
+    if (mine == LLONG_MAX) break;
+    if (U < 32 && lane == U) dv = (int)mine;
+    ++U;
+    last = mine;
+    if (U > 32) break;
+  }
+  if (pass == 0) {
+    if (lane == 0) {
+      ucount[c] = U;
+      if (U > 32) atomicExch(fail, 1);
+    }
+    return;
+  }
+  if (lane < U) dict[dptr[c] + lane] = dv;
+  for (int k = 0; k < L; ++k) {
+    const int slot = p0 + k * SELL_C + lane;
+    const int col = scol[slot];
+    const int d = (int)((long long)col - row);
+    int pos = 0;
+    for (int u = 0; u < U; ++u) pos += __shfl_sync(0xffffffffu, dv, u) < d;  // lower bound
+    sidx[slot] = col >= 0 ? (uint8_t)pos : (uint8_t)255;
+  }
+}
+
+int sell_dict_build(gsk_plan* P, cudaStream_t s) {
+  const int nch = (int)P->nchunks;
+  const int grid = (nch + TB / 32 - 1) / (TB / 32);
+  int* ucount = nullptr;
+  int* fail = nullptr;
+  GSK_CUDA(cudaMalloc(&ucount, sizeof(int) * (nch + 1)));
+  GSK_CUDA(cudaMalloc(&fail, sizeof(int)));
+  GSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
+  GSK_CUDA(cudaMalloc(&P->dptr, sizeof(int) * (nch + 1)));
+  sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, nullptr, nullptr, nullptr, fail, 0);
+  GSK_LAUNCHED(1);
+  int hfail = 0;
+  GSK_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  if (hfail) {  // some chunk has > 32 distinct deltas: keep plain int32 columns
+    cudaFree(ucount);
+    cudaFree(fail);
+    cudaFree(P->dptr);
+    P->dptr = nullptr;
+    return GSK_OK;
+  }
+  sell_scan_kernel<<<1, 1024, 0, s>>>(nch, ucount, P->dptr, 1);
+  GSK_LAUNCHED(1);
+  int tot = 0;
+  GSK_CUDA(cudaMemcpyAsync(&tot, P->dptr + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  P->ndict = tot;
+  GSK_CUDA(cudaMalloc(&P->dict, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_CUDA(cudaMalloc(&P->sidx, (size_t)(P->nslots > 0 ? P->nslots : 1)));
+  sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, P->dptr, P->dict, P->sidx, fail, 1);
+  GSK_LAUNCHED(1);
+  GSK_CUDA(cudaStreamSynchronize(s));
+  cudaFree(ucount);
+  cudaFree(fail);
+  P->sell.sidx = P->sidx;
+  P->sell.dptr = P->dptr;
+  P->sell.dict = P->dict;
   return GSK_OK;
 }
 

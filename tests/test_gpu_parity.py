@@ -132,6 +132,30 @@ def test_sell_layout_parity(name, N):
         assert np.array_equal(g[k], o[k]), k
 
 
+@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 100), ("C3", 20), ("C4", None), ("C5", 64)])
+def test_sell_dict_parity(name, N):
+    """Column-index dictionary built on the device == the oracle's encoding (integer
+    bit-exact); C5's permuted system keeps plain int32 columns on both sides."""
+    s = workloads.generate(name, N=N)
+    P = gsk.Plan(gsk.CSR.from_system(s), fmt="sell", sell_index="dict")
+    g = P.sell_dict()
+    o = oracle.sell_dict(s["n"], oracle.sell_build(s["row_ptr"], s["col"], s["val"], 32, 256))
+    if o is None:
+        assert g is None
+        return
+    for k in ("dict_ptr", "dict", "sidx"):
+        assert np.array_equal(g[k], o[k]), k
+    # plain-index plan gives the same SpMV bits
+    x = workloads.uniform(s["n"], 5, 5)
+    Pp = gsk.Plan(gsk.CSR.from_system(s), fmt="sell")
+    assert Pp.sell_dict() is None
+    assert np.array_equal(cpu(P.spmv(x)), cpu(Pp.spmv(x)))
+    vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    Pd = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], vo), fmt="sell", sell_index="dict")
+    assert_same_solve(Pd.bicgstab(bo, tol=1e-8, maxit=200), oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 200))
+    assert_same_solve(Pd.gmres(bo, m=20, tol=1e-8, maxit=60), oracle.gmres(s["row_ptr"], s["col"], vo, bo, 20, 1e-8, 60))
+
+
 @pytest.mark.parametrize("n", [1, 3, 255, 256, 257, 4097, 65536, 65537, 1000003, 3000001])
 def test_dot_parity(n):
     a = workloads.uniform(n, 5, 11) * np.exp(workloads.uniform(n, 6, 11, -20, 20))

@@ -388,3 +388,29 @@ def test_two_sided_scaling():
             assert np.abs(A2 - A2.T).max() <= 2.3e-16 * np.abs(A2).max()
     with pytest.raises(ValueError):
         oracle.gs_scale_sym(s["row_ptr"], s["col"], s["val"], s["b"], 0)
+
+
+def test_sell_dict_round_trip():
+    """SELL-D (the GPU's column-index dictionary): decoding row + dict_c[idx] gives back
+    every column of the SELL layout; padding stays marked; dictionaries are ascending
+    and unique; the permuted C5 system (random deltas) is rejected."""
+    for name, N in [("C4", 16), ("C3", 12), ("C2", 40), ("C1", None)]:
+        s = workloads.generate(name, N=N)
+        S = oracle.sell_build(s["row_ptr"], s["col"], s["val"])
+        D = oracle.sell_dict(s["n"], S)
+        assert D is not None
+        nch = S["chunk_len"].size
+        for c in range(nch):
+            dct = D["dict"][D["dict_ptr"][c]:D["dict_ptr"][c + 1]]
+            assert np.all(np.diff(dct) > 0) and dct.size <= 32
+            w0 = (c * 32) // 256 * 256
+            for k in range(S["chunk_len"][c]):
+                for lane in range(32):
+                    slot = S["chunk_ptr"][c] + 32 * k + lane
+                    idx = int(D["sidx"][slot])
+                    if S["scol"][slot] < 0:
+                        assert idx == 255
+                    else:
+                        assert w0 + int(S["roff"][c * 32 + lane]) + dct[idx] == S["scol"][slot]
+    s = workloads.generate("C5", N=64)
+    assert oracle.sell_dict(s["n"], oracle.sell_build(s["row_ptr"], s["col"], s["val"])) is None
