@@ -112,6 +112,8 @@ struct gsk_plan {
   const double* gkey_h = nullptr;
   int gkey_orth = -1;
   double* mpart = nullptr;     // [MDOT_MAX][pstride] partials of multi-dot passes
+  double* cpart = nullptr;     // cooperative kernel partials [2][MAXD][256] + barrier words
+  int coop = 1;                // 0: cooperative kernel for small systems (GSK_COOP=1), 1: never
   // history (device)
   double* hist_d = nullptr;
   int hist_cap = 0;
@@ -232,6 +234,7 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
 int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
 int sell_dict_build(gsk_plan* P, cudaStream_t s);
+int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);
 int ensure_hist(gsk_plan* P, int maxit);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).

@@ -281,6 +281,12 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
   }
   P->orth = orth;
   P->sell_index = opts ? opts->sell_index : 0;
+  {
+    // cooperative single-launch Bi-CGSTAB (coop.cu): opt-in with GSK_COOP=1 — measured
+    // no faster than the graph path on C1/C2 (L2 round trips per barrier dominate)
+    const char* e = std::getenv("GSK_COOP");
+    P->coop = (e && e[0] == '1') ? 0 : 1;
+  }
   if (P->sell_index != 0 && P->sell_index != 1) {
     delete P;
     set_error("gsk_plan_create: unknown sell_index %d", opts->sell_index);
@@ -322,7 +328,8 @@ void gsk_plan_destroy(gsk_plan* P) {
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->scratch,
-                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict};
+                  P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
+                  P->cpart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (P->h_flag) cudaFreeHost(P->h_flag);
