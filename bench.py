@@ -157,6 +157,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
+    capture (profiles/r01_ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            k = json.load(f)["kernels"].get(kernel)
+        return k["bytes_per_launch"] if k else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def plan_schedule(args):
     """Bi-CGSTAB schedule the plan runs (auto = split)."""
     return "fused" if args.schedule == "fused" else "split"
@@ -272,7 +283,8 @@ def main():
         kname = ("pass_kernel<SELL, OpS1> (v = A p, <r^,v>)" if split
                  else "pass_kernel<SELL, OpP1> (p update at the gather, v = A p, <r^,v>)")
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": None, "kernel": kname, "bytes_per_launch": bm[key], "ms_per_launch": p1_ms,
+                "traffic": ncu_traffic("pass_kernel<2,1,OpS1>" if split else "pass_kernel<2,1,OpP1>"),
+                "kernel": kname, "bytes_per_launch": bm[key], "ms_per_launch": p1_ms,
                 "peak_source": src, "frac_of_8TBps": ach / 8000.0}
 
     # SpMV standalone roofline (same plan, 50 back-to-back launches)

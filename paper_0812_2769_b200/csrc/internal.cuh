@@ -133,6 +133,7 @@ namespace gsk {
 // plan's format (CSR or SELL) or a pure vector pass.
 int num_sms();
 bool pdl_enabled();  // GSK_PDL=0 in the environment disables programmatic launches
+int spmv_wpc_max();  // windows per CTA of SpMV passes (8; GSK_WPC overrides, pow2 <= 8)
 
 // Kernel launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KArgs, typename... Args>
@@ -173,7 +174,7 @@ int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullpt
     }
   } else {
     const int windows = (n + TB - 1) / TB;
-    int wpc = 8;  // windows per CTA: as many as keep >= 3 CTAs per SM busy
+    int wpc = spmv_wpc_max();  // windows per CTA: as many as keep >= 3 CTAs per SM busy
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
     if (P->fmt == GSK_FMT_SELL && P->sell.dict)

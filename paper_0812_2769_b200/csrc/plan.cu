@@ -37,6 +37,16 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+int spmv_wpc_max() {
+  static int w = 0;
+  if (!w) {
+    const char* e = std::getenv("GSK_WPC");
+    w = e ? std::atoi(e) : 8;
+    if (w != 1 && w != 2 && w != 4 && w != 8) w = 8;
+  }
+  return w;
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
