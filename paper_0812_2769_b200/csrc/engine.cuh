@@ -431,11 +431,20 @@ __global__ void __launch_bounds__(TB, 2)
         y = sm.sy[w & 1][t];
       }
       const double u = i < n ? op.value(i, y, cache + t) : 0.0;
-      for (int d = 0; d < J; ++d) {
-        double q = i < n ? u * op.operand(i, d, cache + t) : 0.0;
+      for (int d0 = 0; d0 < J; d0 += 8) {  // 8 dots at a time: loads and butterflies interleave
+        double q[8];
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) q = q + __shfl_xor_sync(0xffffffffu, q, off);
-        if (lane == 0) wp[d * 8 + warp] = q;
+        for (int e = 0; e < 8; ++e) q[e] = (i < n && d0 + e < J) ? u * op.operand(i, d0 + e, cache + t) : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) q[e] = q[e] + __shfl_xor_sync(0xffffffffu, q[e], off);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (d0 + e < J) wp[(d0 + e) * 8 + warp] = q[e];
+        }
       }
     } else {
       for (int d = lane; d < J; d += 32)

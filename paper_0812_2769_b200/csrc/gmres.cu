@@ -296,10 +296,16 @@ struct OpCgsB {
   __device__ double value(int i, double, double* cache) const {
     double w = Wn[i];
     const bool cached = nd <= MDOT_CACHE;
-    for (int d = 0; d < nd; ++d) {
-      const double v = __ldg(W + d * n + i) * inv[d + 1];
-      if (cached) cache[d * TB] = v;
-      w = __fma_rn(-c1[d], v, w);
+    for (int d0 = 0; d0 < nd; d0 += 8) {  // 8 basis loads in flight, chain in d order
+      double vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) vv[u] = d0 + u < nd ? __ldg(W + (d0 + u) * n + i) * inv[d0 + u + 1] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (d0 + u < nd) {
+          if (cached) cache[(d0 + u) * TB] = vv[u];
+          w = __fma_rn(-c1[d0 + u], vv[u], w);
+        }
     }
     Wn[i] = w;
     return w;
@@ -331,7 +337,14 @@ struct OpCgsC {
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int q, double, const double (&v)[NV], double (&c)[1]) const {
     double w = v[0];
-    for (int d = 0; d < j; ++d) w = __fma_rn(-c2[d], __ldg(W + d * n + q) * inv[d + 1], w);
+    for (int d0 = 0; d0 < j; d0 += 8) {
+      double vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) vv[u] = d0 + u < j ? __ldg(W + (d0 + u) * n + q) * inv[d0 + u + 1] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (d0 + u < j) w = __fma_rn(-c2[d0 + u], vv[u], w);
+    }
     Wn[q] = w;
     c[0] = w * w;
   }
@@ -360,7 +373,14 @@ struct OpXupd {
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int q, double, const double (&v)[NV], double (&)[1]) const {
     double xv = v[0];
-    for (int k = 0; k < K; ++k) xv = __fma_rn(__ldg(y + k), __ldg(W + (size_t)k * n + q) * __ldg(inv + k + 1), xv);
+    for (int k0 = 0; k0 < K; k0 += 8) {  // batches of 8 basis loads in flight, chain in k order
+      double wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = k0 + u < K ? __ldg(W + (size_t)(k0 + u) * n + q) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u < K) xv = __fma_rn(__ldg(y + k0 + u), wv[u] * __ldg(inv + k0 + u + 1), xv);
+    }
     x[q] = xv;
   }
 };
