@@ -77,8 +77,18 @@ typedef struct gsk_opts {
                            index into a per-chunk dictionary of col - row deltas when
                            every chunk has <= 32 of them (25% fewer matrix bytes, but
                            slower on B200 at C4: DESIGN.md §5) */
-  int32_t reserved_;
+  int32_t engine;       /* how the solvers run (all engines give bit-identical results):
+                           GSK_ENGINE_AUTO (default) = the on-chip single-CTA solver (one
+                           launch for the whole solve) where it is measured faster
+                           (Bi-CGSTAB n <= 2048, GMRES with MGS n <= GSK_SMALL_NMAX),
+                           else graph-replayed passes; GSK_ENGINE_GRAPH = always the
+                           passes; GSK_ENGINE_COOP = cooperative multi-CTA Bi-CGSTAB for
+                           n <= 2^19 (opt-in); GSK_ENGINE_SMALL = the on-chip solver
+                           whenever n <= GSK_SMALL_NMAX. */
 } gsk_opts;
+
+enum { GSK_ENGINE_AUTO = 0, GSK_ENGINE_GRAPH = 1, GSK_ENGINE_COOP = 2, GSK_ENGINE_SMALL = 3 };
+#define GSK_SMALL_NMAX 4096
 
 enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2 };
 /* gmres_orth: GSK_ORTH_MGS (modified Gram-Schmidt, j+1 passes per Arnoldi step; the

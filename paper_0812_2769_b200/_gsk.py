@@ -19,6 +19,7 @@ GSK_OK, GSK_E_INVALID, GSK_E_ZERO_ROW, GSK_E_CUDA, GSK_E_NOMEM = 0, -1, -2, -3, 
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}
 FMT = {"csr": 0, "sell": 1}
 SCHEDULE = {"auto": 0, "fused": 1, "split": 2}
+ENGINE = {"auto": 0, "graph": 1, "coop": 2, "small": 3}
 ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
@@ -49,7 +50,7 @@ class Report(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("poll", ctypes.c_int32), ("weights", ctypes.c_void_p),
                 ("bicg_schedule", ctypes.c_int32), ("gmres_orth", ctypes.c_int32),
-                ("sell_index", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
+                ("sell_index", ctypes.c_int32), ("engine", ctypes.c_int32)]
 
 
 class GskError(RuntimeError):
@@ -222,12 +223,15 @@ class Plan:
     """gsk_plan: SELL build, workspace and captured graphs reused across solves."""
 
     def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
-                 orth: str = "mgs", sell_index: str = "plain"):
+                 orth: str = "mgs", sell_index: str = "plain", engine: str = "auto"):
+        """engine: "auto" (on-chip single-CTA solver where measured faster: Bi-CGSTAB
+        n <= 2048, GMRES/MGS n <= 4096; else graph passes), "graph" (always the passes),
+        "coop" (cooperative multi-CTA Bi-CGSTAB) or "small" (on-chip for n <= 4096)."""
         lib = load()
         self.A = A
         self.weights = _dev_f64(weights, A.n)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE[schedule], ORTH[orth], {"plain": 0, "dict": 1}[sell_index], 0)
+                    SCHEDULE[schedule], ORTH[orth], {"plain": 0, "dict": 1}[sell_index], ENGINE[engine])
         self._csr = A.struct()
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))

@@ -8,6 +8,7 @@ namespace gsk {
 
 // Every op names its own-row operands (vin(k); the engine stages them through
 // shared memory with TMA and hands the values to row() as v[k]).
+template <class L = LdNC>
 struct OpInit {  // r = b - A x; r^ = r; p_old = v_old = 0
   static constexpr int D = 2;
   static constexpr int NV = 2;
@@ -19,7 +20,7 @@ struct OpInit {  // r = b - A x; r^ = r; p_old = v_old = 0
   BicgState* st;
   __device__ bool begin() { return true; }
   __device__ const double* vin(int k) const { return k == 0 ? b : w; }
-  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ double gather(int c) const { return L::ld(x + c); }
   __device__ void row(int i, double y, const double (&v)[NV], double (&c)[2]) const {
     const double ri = v[0] - y;
     r[i] = ri;
@@ -63,6 +64,7 @@ struct OpInit {  // r = b - A x; r^ = r; p_old = v_old = 0
 };
 
 // ---- fused schedule (3 passes; p and s recomputed at the gather) ---------------------
+template <class L = LdNC>
 struct OpP1 {
   static constexpr int kSellMinBlocks = 3;  // see SellTuning (engine.cuh)
   static constexpr int D = 1;
@@ -80,7 +82,7 @@ struct OpP1 {
   }
   __device__ const double* vin(int k) const { return k == 0 ? vo : k == 1 ? po : k == 2 ? r : rh; }
   __device__ double gather(int c) const {
-    return __fma_rn(beta, __fma_rn(momega, __ldg(vo + c), __ldg(po + c)), __ldg(r + c));
+    return __fma_rn(beta, __fma_rn(momega, L::ld(vo + c), L::ld(po + c)), L::ld(r + c));
   }
   __device__ void row(int i, double y, const double (&v)[NV], double (&c)[1]) const {
     pn[i] = __fma_rn(beta, __fma_rn(momega, v[0], v[1]), v[2]);
@@ -125,6 +127,7 @@ __device__ __forceinline__ void set_omega(BicgState* st, double ts, double tt) {
   st->omega = ts / tt;
 }
 
+template <class L = LdNC>
 struct OpP2 {
   static constexpr int kSellMinBlocks = 3;  // see SellTuning (engine.cuh)
   static constexpr int D = 3;
@@ -140,7 +143,7 @@ struct OpP2 {
     return true;
   }
   __device__ const double* vin(int k) const { return k == 0 ? vn : k == 1 ? r : w; }
-  __device__ double gather(int c) const { return __fma_rn(malpha, __ldg(vn + c), __ldg(r + c)); }
+  __device__ double gather(int c) const { return __fma_rn(malpha, L::ld(vn + c), L::ld(r + c)); }
   __device__ void row(int i, double y, const double (&v)[NV], double (&c)[3]) const {
     const double s = __fma_rn(malpha, v[0], v[1]);
     t[i] = y;
@@ -264,6 +267,7 @@ struct OpS0 {
   }
 };
 
+template <class L = LdNC>
 struct OpS1 {
   static constexpr int D = 1;
   static constexpr int NV = 1;
@@ -273,7 +277,7 @@ struct OpS1 {
   BicgState* st;
   __device__ bool begin() { return !st->done; }
   __device__ const double* vin(int) const { return rh; }
-  __device__ double gather(int c) const { return __ldg(p + c); }
+  __device__ double gather(int c) const { return L::ld(p + c); }
   __device__ void row(int i, double y, const double (&x)[NV], double (&c)[1]) const {
     v[i] = y;
     c[0] = x[0] * y;
@@ -317,6 +321,7 @@ struct OpS2 {
   }
 };
 
+template <class L = LdNC>
 struct OpS3 {
   static constexpr int D = 2;
   static constexpr int NV = 1;
@@ -326,7 +331,7 @@ struct OpS3 {
   BicgState* st;
   __device__ bool begin() { return !st->done; }
   __device__ const double* vin(int) const { return s_; }
-  __device__ double gather(int c) const { return __ldg(s_ + c); }
+  __device__ double gather(int c) const { return L::ld(s_ + c); }
   __device__ void row(int i, double y, const double (&x)[NV], double (&c)[2]) const {
     t[i] = y;
     c[0] = y * x[0];
@@ -378,6 +383,7 @@ struct OpS4 {
   }
 };
 
+template <class L = LdNC>
 struct OpFinal {  // true residual ||b - A x|| (unweighted and weighted)
   static constexpr int D = 2;
   static constexpr int NV = 2;
@@ -386,7 +392,7 @@ struct OpFinal {  // true residual ||b - A x|| (unweighted and weighted)
   BicgState* st;
   __device__ bool begin() { return true; }
   __device__ const double* vin(int k) const { return k == 0 ? b : w; }
-  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ double gather(int c) const { return L::ld(x + c); }
   __device__ void row(int i, double y, const double (&v)[NV], double (&c)[2]) const {
     const double ri = v[0] - y;
     c[0] = ri * ri;

@@ -46,8 +46,8 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
     if (P->bmode == 1) {  // fused 3-pass schedule
       double *po = (k & 1) ? pb : pa, *vo = (k & 1) ? vb : va;
       double *pn = (k & 1) ? pa : pb, *vn = (k & 1) ? va : vb;
-      OpP1 p1{r, po, vo, rh, pn, vn, P->bstate, 0, 0};
-      OpP2 p2{r, vn, w, t, P->hist_d, P->bstate, 0};
+      OpP1<> p1{r, po, vo, rh, pn, vn, P->bstate, 0, 0};
+      OpP2<> p2{r, vn, w, t, P->hist_d, P->bstate, 0};
       OpP3 p3{vn, pn, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0};
       rc = run_pass(P, p1, s, ev(0, 0, k), ev(0, 1, k));
       if (rc >= 0) rc = run_pass(P, p2, s, ev(1, 0, k), ev(1, 1, k));
@@ -55,9 +55,9 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
     } else {  // split 5-pass schedule: p = pa, v = va, s = pb
       double *p = pa, *v = va, *sv = pb;
       OpS0 s0{r, v, p, P->bstate, 0, 0};
-      OpS1 s1{p, rh, v, P->bstate};
+      OpS1<> s1{p, rh, v, P->bstate};
       OpS2 s2{r, v, w, sv, P->hist_d, P->bstate, 0};
-      OpS3 s3{sv, t, P->bstate};
+      OpS3<> s3{sv, t, P->bstate};
       OpS4 s4{sv, p, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0};
       rc = run_pass(P, s0, s);
       if (rc >= 0) rc = run_pass(P, s1, s, ev(0, 0, k), ev(0, 1, k));
@@ -107,11 +107,13 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   if (!P->bvec) GSK_CUDA(cudaMalloc(&P->bvec, sizeof(double) * 7 * (size_t)n));
   if (!P->bstate) GSK_CUDA(cudaMalloc(&P->bstate, sizeof(BicgState)));
   GSK_TRY(ensure_hist(P, maxit));
-  // small systems: one cooperative launch runs the whole iteration loop (coop.cu)
-  if (P->coop == 0 && P->bmode == 2) {
-    if (!P->bvec) GSK_CUDA(cudaMalloc(&P->bvec, sizeof(double) * 7 * (size_t)n));
-    if (!P->bstate) GSK_CUDA(cudaMalloc(&P->bstate, sizeof(BicgState)));
-    GSK_TRY(ensure_hist(P, maxit));
+  // small systems: one launch runs the whole iteration loop — on one SM with the
+  // vectors in shared memory (small.cu; by default for n <= 2048, where
+  // it is measured faster: 6.7 vs 31 us per iteration at n = 1024), or on a
+  // cooperative grid (coop.cu, opt-in).  Same operators, bit-identical results.
+  const bool small = (P->engine == GSK_ENGINE_AUTO && n <= 2048) ||
+                     (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX);
+  if (small || P->engine == GSK_ENGINE_COOP) {
     cudaStream_t s = P->st;
     GSK_TRY(join_in(P, caller));
     GSK_CUDA(cudaEventRecord(P->t0, s));
@@ -120,8 +122,11 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
     } else {
       GSK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     }
-    int used = 0;
-    GSK_TRY(coop_bicgstab_run(P, b, tol, maxit, x, &used));
+    int used = 1;
+    if (small)
+      GSK_TRY(small_bicgstab_run(P, b, tol, maxit, x));
+    else
+      GSK_TRY(coop_bicgstab_run(P, b, tol, maxit, x, &used));
     if (used) {
       GSK_CUDA(cudaEventRecord(P->t1, s));
       return bicgstab_report(P, hist, rep, caller);
@@ -153,14 +158,14 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   h.maxit = maxit;
   GSK_CUDA(cudaMemcpyAsync(P->bstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   double* V = P->bvec;
-  OpInit init{x, b, P->weights, V, V + (size_t)n, V + 2 * (size_t)n, V + 4 * (size_t)n, P->hist_d, P->bstate};
+  OpInit<> init{x, b, P->weights, V, V + (size_t)n, V + 2 * (size_t)n, V + 4 * (size_t)n, P->hist_d, P->bstate};
   if (run_pass(P, init, s) < 0) return GSK_E_CUDA;
   // batches of K iterations; the next batch is queued before the flag of the
   // previous one is read, so the GPU never idles on the host check
   const long long maxb = (maxit + K - 1) / K + 1;
   const int kinds[2] = {0, 1};
   GSK_TRY(run_batches(P, P->bgraph, maxb, P->bkernels, &P->bstate->done, kinds, 2));
-  OpFinal fin{x, b, P->weights, P->bstate};
+  OpFinal<> fin{x, b, P->weights, P->bstate};
   if (run_pass(P, fin, s) < 0) return GSK_E_CUDA;
   GSK_CUDA(cudaEventRecord(P->t1, s));
   return bicgstab_report(P, hist, rep, caller);

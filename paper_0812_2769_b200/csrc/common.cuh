@@ -45,6 +45,20 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Gather-load policy of the ops that gather a vector at neighbouring columns.  The
+// graph passes read vectors written by an EARLIER kernel: the read-only path is valid.
+// A kernel that writes and re-reads its vectors (coop.cu across CTAs, small.cu in one
+// CTA) must use a coherent load instead.
+struct LdNC {
+  static __device__ __forceinline__ double ld(const double* p) { return __ldg(p); }
+};
+struct LdCG {  // L2 (coherent across SMs after the grid barrier's release/acquire)
+  static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+};
+struct LdPlain {  // generic load: shared or global memory, coherent within a CTA
+  static __device__ __forceinline__ double ld(const double* p) { return *p; }
+};
+
 __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ldcs(const int* p) { return __ldcs(p); }
 

@@ -112,7 +112,11 @@ __device__ __forceinline__ void coop_pass(const CoopArgs& a, Op op, double* sy, 
         }
         if (i < a.n) {
           double v[NVA];
-          load_vin(op, i, v);
+#pragma unroll
+          for (int k = 0; k < Op::NV; ++k) {  // coherent (L2) loads: written in this launch
+            const double* src = op.vin(k);
+            v[k] = src ? __ldcg(src + i) : 0.0;
+          }
           op.row(i, y, v, cc);
         }
       }
@@ -155,12 +159,12 @@ __global__ void __launch_bounds__(TB) coop_bicgstab(CoopArgs a) {
   }
   __syncthreads();
   int par = 0;
-  OpInit init{a.x, a.b, a.w, a.r, a.rh, a.p, a.v, a.hist, &st};
+  OpInit<LdCG> init{a.x, a.b, a.w, a.r, a.rh, a.p, a.v, a.hist, &st};
   coop_pass<FMT>(a, init, sy, wp, red, par);
   OpS0 s0{a.r, a.v, a.p, &st, 0, 0};
-  OpS1 s1{a.p, a.rh, a.v, &st};
+  OpS1<LdCG> s1{a.p, a.rh, a.v, &st};
   OpS2 s2{a.r, a.v, a.w, a.s, a.hist, &st, 0};
-  OpS3 s3{a.s, a.t, &st};
+  OpS3<LdCG> s3{a.s, a.t, &st};
   OpS4 s4{a.s, a.p, a.t, a.rh, a.w, a.x, a.r, a.hist, &st, 0, 0, 0};
   for (;;) {
     if (st.done && !st.halfstep) break;
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(TB) coop_bicgstab(CoopArgs a) {
     coop_pass<FMT>(a, s3, sy, wp, red, par);
     coop_pass<0>(a, s4, sy, wp, red, par);
   }
-  OpFinal fin{a.x, a.b, a.w, &st};
+  OpFinal<LdCG> fin{a.x, a.b, a.w, &st};
   coop_pass<FMT>(a, fin, sy, wp, red, par);
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.st_out = st;
 }

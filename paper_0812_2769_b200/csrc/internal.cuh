@@ -113,7 +113,7 @@ struct gsk_plan {
   int gkey_orth = -1;
   double* mpart = nullptr;     // [MDOT_MAX][pstride] partials of multi-dot passes
   double* cpart = nullptr;     // cooperative kernel partials [2][MAXD][256] + barrier words
-  int coop = 1;                // 0: cooperative kernel for small systems (GSK_COOP=1), 1: never
+  int engine = GSK_ENGINE_AUTO; // on-chip single-CTA solver / graph passes / cooperative
   // history (device)
   double* hist_d = nullptr;
   int hist_cap = 0;
@@ -236,6 +236,10 @@ int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
 int sell_dict_build(gsk_plan* P, cudaStream_t s);
 int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);
+// On-chip single-CTA solvers (small.cu) for n <= GSK_SMALL_NMAX: one launch runs the
+// whole solve; the caller has set x = x0 and zeroed/initialised the state.
+int small_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x);
+int small_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h);
 int ensure_hist(gsk_plan* P, int maxit);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).

@@ -291,11 +291,11 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
   }
   P->orth = orth;
   P->sell_index = opts ? opts->sell_index : 0;
-  {
-    // cooperative single-launch Bi-CGSTAB (coop.cu): opt-in with GSK_COOP=1 — measured
-    // no faster than the graph path on C1/C2 (L2 round trips per barrier dominate)
-    const char* e = std::getenv("GSK_COOP");
-    P->coop = (e && e[0] == '1') ? 0 : 1;
+  P->engine = opts ? opts->engine : GSK_ENGINE_AUTO;
+  if (P->engine < GSK_ENGINE_AUTO || P->engine > GSK_ENGINE_SMALL) {
+    delete P;
+    set_error("gsk_plan_create: unknown engine %d", opts->engine);
+    return GSK_E_INVALID;
   }
   if (P->sell_index != 0 && P->sell_index != 1) {
     delete P;

@@ -226,17 +226,18 @@ def test_gmres_cgs2_paper_problem1():
     assert int(np.flatnonzero(g[1] < 1e-4)[0]) == 265
 
 
-def test_solver_edge_cases():
+@pytest.mark.parametrize("engine", ["auto", "graph", "coop", "small"])
+def test_solver_edge_cases(engine):
     n = 300
     rp = np.arange(n + 1, dtype=np.int32)
     col = np.arange(n, dtype=np.int32)
     ones = np.ones(n)
     b = workloads.uniform(n, 1, 2)
     A = gsk.CSR(rp, col, ones)
-    P = gsk.Plan(A)
+    P = gsk.Plan(A, engine=engine)
     # A = I: Bi-CGSTAB half-step exit at iteration 1; GMRES 1 step (lucky)
     assert_same_solve(P.bicgstab(b, tol=1e-12, maxit=10), oracle.bicgstab(rp, col, ones, b, 1e-12, 10))
-    Pf = gsk.Plan(A, schedule="fused")
+    Pf = gsk.Plan(A, schedule="fused", engine=engine)
     assert_same_solve(Pf.bicgstab(b, tol=1e-12, maxit=10), oracle.bicgstab(rp, col, ones, b, 1e-12, 10))
     assert_same_solve(P.gmres(b, m=5, tol=1e-12, maxit=10), oracle.gmres(rp, col, ones, b, 5, 1e-12, 10))
     # b = 0: converged at 0
@@ -246,7 +247,7 @@ def test_solver_edge_cases():
     # nonzero x0
     s = workloads.generate("C2", N=50)
     x0 = workloads.uniform(s["n"], 3, 4)
-    P2 = gsk.Plan(gsk.CSR.from_system(s))
+    P2 = gsk.Plan(gsk.CSR.from_system(s), engine=engine)
     assert_same_solve(P2.bicgstab(s["b"], x0=x0, tol=1e-9, maxit=300),
                       oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-9, 300, x0=x0))
     assert_same_solve(P2.gmres(s["b"], x0=x0, m=7, tol=1e-9, maxit=300),
@@ -257,16 +258,48 @@ def test_solver_edge_cases():
     v2 = np.array([1.0, -1.0])
     bb = np.array([1.0, 0.0])
     for sched in ("fused", "split"):
-        g = gsk.Plan(gsk.CSR(rp2, c2, v2), schedule=sched).bicgstab(bb, tol=1e-10, maxit=10)
+        g = gsk.Plan(gsk.CSR(rp2, c2, v2), schedule=sched, engine=engine).bicgstab(bb, tol=1e-10, maxit=10)
         assert_same_solve(g, oracle.bicgstab(rp2, c2, v2, bb, 1e-10, 10))
         assert g[2]["status"] == 2 and g[2]["breakdown_at"] == 1
     # maxit = 1 and m >= n
     s3 = workloads.generate("C1", N=6)
-    P3 = gsk.Plan(gsk.CSR.from_system(s3))
+    P3 = gsk.Plan(gsk.CSR.from_system(s3), engine=engine)
     assert_same_solve(P3.bicgstab(s3["b"], tol=1e-14, maxit=1),
                       oracle.bicgstab(s3["row_ptr"], s3["col"], s3["val"], s3["b"], 1e-14, 1))
     assert_same_solve(P3.gmres(s3["b"], m=40, tol=1e-14, maxit=100),
                       oracle.gmres(s3["row_ptr"], s3["col"], s3["val"], s3["b"], 40, 1e-14, 100))
+
+
+SMALL = [("C1", None), ("C1", 20), ("C2", 40), ("C2", 64), ("C3", 12), ("C3", 16), ("C4", 10), ("C5", 50),
+         ("P1", 64)]
+
+
+@pytest.mark.parametrize("name,N", SMALL)
+@pytest.mark.parametrize("scaling", ["none", 2])
+def test_small_engine_parity(name, N, scaling):
+    """The on-chip single-CTA solvers (small.cu; n <= 4096, ragged n included) against
+    the oracle and against the graph-replayed passes: Bi-CGSTAB (both schedules, SELL
+    and CSR plans, frame weights) and GMRES(m) with MGS for m in {1, 20, 30}."""
+    s, val, b, _ = system(name, N, scaling)
+    assert s["n"] <= 4096
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 800)
+    for fmt in ("csr", "sell"):
+        for schedule in ("split", "fused"):
+            P = gsk.Plan(A, fmt=fmt, schedule=schedule, engine="small")
+            assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=800), o)
+    assert_same_solve(gsk.Plan(A, engine="graph").bicgstab(b, tol=1e-9, maxit=800), o)
+    w = workloads.uniform(s["n"], 5, 6) + 1.5
+    assert_same_solve(gsk.Plan(A, weights=w, engine="small").bicgstab(b, tol=1e-9, maxit=800),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 800, weights=w))
+    for m in (1, 20, 30):
+        o = oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-9, 300)
+        assert_same_solve(gsk.Plan(A, engine="small").gmres(b, m=m, tol=1e-9, maxit=300), o)
+        if m == 20:
+            assert_same_solve(gsk.Plan(A, engine="graph").gmres(b, m=m, tol=1e-9, maxit=300), o)
+            assert_same_solve(gsk.Plan(A, fmt="sell").gmres(b, m=m, tol=1e-9, maxit=300), o)
+            assert_same_solve(gsk.Plan(A, weights=w).gmres(b, m=m, tol=1e-9, maxit=300),
+                              oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-9, 300, weights=w))
 
 
 def test_plan_less_entry_points():
