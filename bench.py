@@ -302,6 +302,18 @@ def main():
     spmv_ms = e0.elapsed_time(e1) / 50
     spmv_gbps = bm["spmv"] / (spmv_ms / 1e3) / 1e9
 
+    # GS(2) standalone roofline (row a2): each call is flag reset + gs_kernel + flag
+    # read + stream sync; events bracket one call, best of 10
+    gs_times = []
+    for _ in range(10):
+        e0.record()
+        gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
+        e1.record()
+        torch.cuda.synchronize()
+        gs_times.append(e0.elapsed_time(e1))
+    gs_ms = min(gs_times)
+    gs_gbps = bm["gs"] / (gs_ms / 1e3) / 1e9
+
     r1, r2 = reps[-1]
     extra = {
         "bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
@@ -318,6 +330,8 @@ def main():
                       "rest": round(t - r1["solve_ms"] - r2["solve_ms"], 2)} for t, (r1, r2) in zip(step_ms, reps)],
         "spmv": {"ms": spmv_ms, "gbps": spmv_gbps, "frac_of_hbm": spmv_gbps / hbm,
                  "frac_of_8TBps": spmv_gbps / 8000.0},
+        "gs2": {"ms": gs_ms, "gbps": gs_gbps, "bytes": bm["gs"], "frac_of_hbm": gs_gbps / hbm,
+                "frac_of_8TBps": gs_gbps / 8000.0},
         "probe_ms": {"bicg_v_pass": probes[0], "bicg_t_pass": probes[1], "gmres_mgs": probes[2],
                      "gmres_arnoldi_spmv": probes[3]},
         "probe_gbps": {"bicg_v_pass": bm["bicg_s1" if split else "bicg_p1"] / (probes[0] / 1e3) / 1e9

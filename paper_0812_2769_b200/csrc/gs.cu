@@ -16,35 +16,58 @@ __device__ __forceinline__ double row_norm_term(double a, int p) {
   return t;
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS): no register round trip, so all
+// of a thread's staging loads are in flight at once.
+__device__ __forceinline__ void cp_async8(double* smem, const double* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+
 // norms_only: write s_i = sqrt(1/||a_i||_p) to dout and nothing else (two-sided
 // scaling, first pass).
-__global__ void __launch_bounds__(TB) gs_kernel(int n, const int* __restrict__ rp,
+// PP: 1, 2 (specialised) or 0 (any p >= 3, passed in p)
+template <int PP>
+__global__ void __launch_bounds__(TB, 8) gs_kernel(int n, const int* __restrict__ rp,
                                                 const double* vin, double* vout,
                                                 const double* b, double* bout, double* dout,
                                                 int p, int* bad, int norms_only) {
   __shared__ double sv[CSR_CAP];
   const int r0 = blockIdx.x * TB, t = threadIdx.x, r = r0 + t;
   const int rend = min(r0 + TB, n);
-  const int s0 = rp[r0], s1 = rp[rend], cnt = s1 - s0;
+  const int s0 = __ldg(rp + r0), s1 = __ldg(rp + rend), cnt = s1 - s0;
   const bool staged = cnt <= CSR_CAP;
   if (staged) {
-    for (int k = t; k < cnt; k += TB) sv[k] = __ldcs(vin + s0 + k);
+    for (int k = t; k < cnt; k += TB) cp_async8(sv + k, vin + s0 + k);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // own-row operands while the segment is in flight
+  int a0 = 0, a1 = 0;
+  double bi = 0.0;
+  if (r < n) {
+    a0 = __ldg(rp + r);
+    a1 = __ldg(rp + r + 1);
+    if (b && bout && !norms_only) bi = __ldcs(b + r);
+  }
+  if (staged) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
   }
   double d = 0.0;
   if (r < n) {
-    const int a0 = rp[r], a1 = rp[r + 1];
     const double* seg = staged ? sv + (a0 - s0) : vin + a0;
     const int len = a1 - a0;
     double acc = 0.0;
-    if (p == 2) {
+    double nrm;
+    if constexpr (PP == 2) {
       for (int k = 0; k < len; ++k) acc = __fma_rn(seg[k], seg[k], acc);
-    } else if (p == 1) {
+      nrm = sqrt(acc);
+    } else if constexpr (PP == 1) {
       for (int k = 0; k < len; ++k) acc = acc + fabs(seg[k]);
+      nrm = acc;
     } else {
       for (int k = 0; k < len; ++k) acc = acc + row_norm_term(seg[k], p);
+      nrm = pow(acc, 1.0 / p);
     }
-    const double nrm = (p == 1) ? acc : (p == 2 ? sqrt(acc) : pow(acc, 1.0 / p));
     if (nrm == 0.0) {
       atomicMin(bad, r);
     } else {
@@ -59,8 +82,8 @@ __global__ void __launch_bounds__(TB) gs_kernel(int n, const int* __restrict__ r
       for (int k = 0; k < len; ++k) vout[a0 + k] = vin[a0 + k] * d;
     }
     if (!norms_only) {
-      if (b && bout) bout[r] = b[r] * d;
-      if (dout) dout[r] = d;
+      if (b && bout) __stcs(bout + r, bi * d);
+      if (dout) __stcs(dout + r, d);
     }
   }
   if (staged && !norms_only) {
@@ -83,6 +106,17 @@ __global__ void __launch_bounds__(TB) sym_scale_kernel(int n, const int* __restr
 __global__ void unscale_kernel(int64_t n, const double* s, const double* y, double* x) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = s[i] * y[i];
+}
+
+static int launch_gs(int grid, cudaStream_t s, int n, const int* rp, const double* vin, double* vout,
+                     const double* b, double* bout, double* dout, int p, int* bad, int norms_only) {
+  if (p == 2)
+    gs_kernel<2><<<grid, TB, 0, s>>>(n, rp, vin, vout, b, bout, dout, p, bad, norms_only);
+  else if (p == 1)
+    gs_kernel<1><<<grid, TB, 0, s>>>(n, rp, vin, vout, b, bout, dout, p, bad, norms_only);
+  else
+    gs_kernel<0><<<grid, TB, 0, s>>>(n, rp, vin, vout, b, bout, dout, p, bad, norms_only);
+  return GSK_OK;
 }
 
 // Per-process device word for the zero-row flag (avoids a stream-ordered allocation
@@ -123,10 +157,10 @@ extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double
     set_error("gs: cannot allocate the zero-row flag");
     return GSK_E_NOMEM;
   }
-  const int big = 0x7fffffff;
-  GSK_CUDA(cudaMemcpyAsync(dbad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  const int big = 0x7f7f7f7f;  // > any row index; set by a byte memset (no host copy)
+  GSK_CUDA(cudaMemsetAsync(dbad, 0x7f, sizeof(int), s));
   const int grid = (A->n + TB - 1) / TB;
-  gs_kernel<<<grid, TB, 0, s>>>(A->n, A->row_ptr, A->values, nullptr, nullptr, nullptr, s_out, p, dbad, 1);
+  GSK_TRY(launch_gs(grid, s, A->n, A->row_ptr, A->values, nullptr, nullptr, nullptr, s_out, p, dbad, 1));
   GSK_LAUNCHED(1);
   int hbad = big;
   GSK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -175,10 +209,10 @@ extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* va
     set_error("gs: cannot allocate the zero-row flag");
     return GSK_E_NOMEM;
   }
-  const int big = 0x7fffffff;
-  GSK_CUDA(cudaMemcpyAsync(dbad, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  const int big = 0x7f7f7f7f;  // > any row index; set by a byte memset (no host copy)
+  GSK_CUDA(cudaMemsetAsync(dbad, 0x7f, sizeof(int), s));
   const int grid = (A->n + TB - 1) / TB;
-  gs_kernel<<<grid, TB, 0, s>>>(A->n, A->row_ptr, A->values, values_out, b, b_out, d_out, p, dbad, 0);
+  GSK_TRY(launch_gs(grid, s, A->n, A->row_ptr, A->values, values_out, b, b_out, d_out, p, dbad, 0));
   GSK_LAUNCHED(1);
   int hbad = big;
   GSK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
