@@ -59,6 +59,16 @@ struct LdPlain {  // generic load: shared or global memory, coherent within a CT
   static __device__ __forceinline__ double ld(const double* p) { return *p; }
 };
 
+// 8-byte asynchronous global -> shared copy (LDGSTS): no register round trip, so all
+// of a thread's loads can be in flight at once; completion via cp_async_wait<N>.
+__device__ __forceinline__ void cp_async8(double* smem, const double* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ldcs(const int* p) { return __ldcs(p); }
 

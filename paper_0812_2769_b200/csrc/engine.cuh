@@ -43,6 +43,7 @@ template <>
 struct PassSmem<0> {
   double wp[8 * MAXD * 8];  // [window][d][warp]
 };
+constexpr int ASYNC_NV = 2;  // own-row operands prefetched with cp.async (SpMV passes)
 template <>
 struct PassSmem<1> {
   CsrStage st[2];
@@ -52,6 +53,7 @@ template <>
 struct PassSmem<2> {
   double sy[2][TB];
   double wp[8 * MAXD * 8];
+  double vin[2][ASYNC_NV][TB];
 };
 template <>
 struct PassSmem<3> : PassSmem<2> {};
@@ -88,6 +90,9 @@ struct PassOcc {
                                                                                        : SellTuning<Op>::minb)
                                   : FMT == 2 ? SellTuning<Op>::minb : 3;
   static constexpr bool kPrefetch = FMT == 1 || (FMT >= 2 && SellTuning<Op>::minb < 4);
+  // otherwise (SELL at 4 CTAs/SM, no registers to spare) up to ASYNC_NV own-row
+  // operands of window w+1 are copied into shared memory with cp.async during window w
+  static constexpr bool kAsync = !kPrefetch && FMT >= 2 && Op::NV >= 1 && Op::NV <= ASYNC_NV;
 };
 
 // y for row r0 + t of a CSR window (AC-3 chain), staged through st.
@@ -266,21 +271,45 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     }
   } else {
     const int rb = blockIdx.x * wpc * TB;
+    constexpr bool kPre = PassOcc<FMT, Op>::kPrefetch;
+    constexpr bool kAsync = PassOcc<FMT, Op>::kAsync;
+    // own-row operands of window w -> sm.vin[w & 1] (one commit group per window; each
+    // thread copies and later reads only its own slots, so no barrier is involved)
+    auto issue = [&](int w) {
+      if constexpr (kAsync) {
+        const int i = rb + w * TB + t;
+        if (w < wpc && i < n) {
+#pragma unroll
+          for (int k = 0; k < Op::NV; ++k) {
+            const double* src = op.vin(k);
+            if (src) cp_async8(&sm.vin[w & 1][k][t], src + i);
+          }
+        }
+        cp_async_commit();
+      }
+    };
+    issue(0);
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       double cc[DD];
 #pragma unroll
       for (int d = 0; d < DD; ++d) cc[d] = 0.0;
+      issue(w + 1);
       if (r0 < n) {  // uniform over the CTA
         auto g = [&](int col) { return op.gather(col); };
         const int i = r0 + t;
         double v[NVA];
-        constexpr bool kPre = PassOcc<FMT, Op>::kPrefetch;
         if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
         if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
         else y = sell_window<FMT == 3>(sell, r0, g, sm.sy[w & 1]);
-        if (!kPre && i < n) load_vin(op, i, v);
+        if constexpr (kAsync) {
+          cp_async_wait<1>();  // all groups but window w+1's are complete
+#pragma unroll
+          for (int k = 0; k < Op::NV; ++k) v[k] = (i < n && op.vin(k)) ? sm.vin[w & 1][k][t] : 0.0;
+        } else if (!kPre && i < n) {
+          load_vin(op, i, v);
+        }
         if (i < n) op.row(i, y, v, cc);
       }
       if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);

@@ -16,13 +16,6 @@ __device__ __forceinline__ double row_norm_term(double a, int p) {
   return t;
 }
 
-// 8-byte asynchronous global -> shared copy (LDGSTS): no register round trip, so all
-// of a thread's staging loads are in flight at once.
-__device__ __forceinline__ void cp_async8(double* smem, const double* g) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
-}
-
 // norms_only: write s_i = sqrt(1/||a_i||_p) to dout and nothing else (two-sided
 // scaling, first pass).
 // PP: 1, 2 (specialised) or 0 (any p >= 3, passed in p)
@@ -38,7 +31,7 @@ __global__ void __launch_bounds__(TB, 8) gs_kernel(int n, const int* __restrict_
   const bool staged = cnt <= CSR_CAP;
   if (staged) {
     for (int k = t; k < cnt; k += TB) cp_async8(sv + k, vin + s0 + k);
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    cp_async_commit();
   }
   // own-row operands while the segment is in flight
   int a0 = 0, a1 = 0;
@@ -49,7 +42,7 @@ __global__ void __launch_bounds__(TB, 8) gs_kernel(int n, const int* __restrict_
     if (b && bout && !norms_only) bi = __ldcs(b + r);
   }
   if (staged) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    cp_async_wait<0>();
     __syncthreads();
   }
   double d = 0.0;
