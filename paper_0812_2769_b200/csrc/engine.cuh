@@ -119,10 +119,10 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
   return acc;
 }
 
-// y for row r0 + t of a SELL window: lane l of warp w computes slot l of chunk
-// r0/32 + w; results are scattered to sy at the rows' in-window offsets.
+// SELL window core: lane l of warp w computes slot l of chunk r0/32 + w and scatters
+// the row's y to sy at its in-window offset (no barrier).
 template <bool DICT, class G>
-__device__ __forceinline__ double sell_window(const SellView& A, int r0, const G& g, double* sy) {
+__device__ __forceinline__ void sell_window_store(const SellView& A, int r0, const G& g, double* sy) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int c = (r0 >> 5) + warp;
   if (c < A.nchunks) {
@@ -178,8 +178,14 @@ __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G
     }
     sy[rl] = acc;
   }
+}
+
+// y for row r0 + t of a SELL window (scatter through sy, one barrier).
+template <bool DICT, class G>
+__device__ __forceinline__ double sell_window(const SellView& A, int r0, const G& g, double* sy) {
+  sell_window_store<DICT>(A, r0, g, sy);
   __syncthreads();
-  return sy[t];
+  return sy[threadIdx.x];
 }
 
 // Own-row operands of the Op for row i.
@@ -406,91 +412,146 @@ __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double
 
 // ---------------------------------------------------------------------------------
 // Multi-dot passes (GMRES with double classical Gram-Schmidt): J
-// dot products per row, J known at launch (<= MDOT_MAX).  CTA = 256 threads x wpc
-// windows; per window each dot's leaves go through warp butterflies, lane 0 of each
-// warp parks the warp value in smem, threads t < J finish the trees of 8 warps and,
-// after the CTA's windows, the tree over windows (zero-padded to 8).  Op provides
+// dot products per row, J known at launch (<= MDOT_MAX).  A CTA owns tpc tiles of
+// 2048 rows; in a tile thread t owns the 8 CONSECUTIVE rows 8t .. 8t+7, so each dot's
+// 8 leaves of a thread are a canonical subtree reduced in registers, the warp
+// butterfly extends it to 256 rows and warps' values (parked in smem) to 2048 — one
+// butterfly per dot per 2048 rows instead of per 256, and every operand access is a
+// 64-byte contiguous run per thread (16-byte loads).  SpMV ops scatter the SELL
+// windows of the tile through smem first.  Op provides
 //   bool begin(); int nd; double gather(int) (SpMV ops);
-//   double value(int i, double y, double* cache)  -> the row's w (may fill cache[d*TB])
-//   double operand(int i, int d, const double* cache) -> v_d at row i
+//   void value8(int i0, int cnt, const double (&y)[8], double (&u)[8])  rows i0.. (+cnt valid):
+//        stores the rows' new w, returns u = w (0 for invalid rows)
+//   void operand8(int i0, int cnt, int d, u, double (&v)[8])  -> operand d at rows i0..i0+7
+//   void store(int d, double value)  or, with kWarpFinish, finish_warp(value, lane)
 // The per-dot finish is mdot_finish<Op> with J CTAs.
 constexpr int MDOT_MAX = 64;
-constexpr int MDOT_CACHE = 48;  // operands cached in smem when J <= this
+#ifndef GSK_MDOT_MINB
+#define GSK_MDOT_MINB 5
+#endif
+#ifndef GSK_MDOT_G
+#define GSK_MDOT_G 1
+#endif
+constexpr int MDOT_MINB = GSK_MDOT_MINB;  // CTAs per SM (register budget)
+constexpr int MDOT_G = GSK_MDOT_G;        // dots whose operand loads are in flight together
+constexpr int MD_R = 8;                   // consecutive rows per thread
+constexpr int MD_TILE = TB * MD_R;        // rows per tile (2048)
 
-template <class Op>
+// 8 consecutive doubles at p (cnt of them valid): four 16-byte loads when possible.
+__device__ __forceinline__ void ld8(const double* p, int cnt, double (&v)[8]) {
+  if (cnt == 8 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const double2 x = __ldg(q + h);
+      v[2 * h] = x.x;
+      v[2 * h + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = k < cnt ? __ldg(p + k) : 0.0;
+  }
+}
+__device__ __forceinline__ void st8(double* p, int cnt, const double (&v)[8]) {
+  if (cnt == 8 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) q[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < cnt) p[k] = v[k];
+  }
+}
+__device__ __forceinline__ double tree8(const double (&a)[8]) {
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 struct MdotSmem {
-  double sy[2][TB];
-  double wp[2][MDOT_MAX * 8];  // [window parity][dot][warp]
-  double winp[8][MDOT_MAX];    // [window][dot]
+  double sy[MD_TILE];        // SpMV results of the tile in row order
+  double wp[MDOT_MAX * 8];   // [dot][warp]
+  double tp[8 * MDOT_MAX];   // [tile][dot]
 };
 
 template <int FMT, class Op>
-__global__ void __launch_bounds__(TB, 2)
-    mdot_pass(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
+__global__ void __launch_bounds__(TB, MDOT_MINB)
+    mdot_pass(CsrView csr, SellView sell, int n, int tpc, Op op, double* part, int stride) {
   pdl_enter();
   if (!op.begin()) return;
-  extern __shared__ __align__(16) double cache[];  // [J][TB] when op caches operands
-  __shared__ MdotSmem<Op> sm;
+  __shared__ __align__(16) MdotSmem sm;
   const int J = op.nd;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int rb = blockIdx.x * wpc * TB;
-  for (int w = 0; w < wpc; ++w) {
-    const int r0 = rb + w * TB;
-    const int i = r0 + t;
-    double* wp = sm.wp[w & 1];
-    if (r0 < n) {  // uniform over the CTA
-      double y = 0.0;
-      if constexpr (FMT == 1) {
-        // CSR rows are short here (stencils); read directly (L1/L2-served gathers)
-        if (i < n)
-          for (int k = csr.rp[i]; k < csr.rp[i + 1]; ++k) y = __fma_rn(__ldcs(csr.v + k), op.gather(__ldcs(csr.ci + k)), y);
-      } else if constexpr (FMT == 2) {
-        const int c = (r0 >> 5) + warp;
-        if (c < sell.nchunks) {
-          const int rl = sell.roff[c * SELL_C + lane];
-          const int p0 = sell.cptr[c], L = (sell.cptr[c + 1] - p0) >> 5;
-          double acc = 0.0;
-          for (int k = 0; k < L; ++k) {
-            const int col = __ldcs(sell.scol + p0 + lane + k * SELL_C);
-            if (col >= 0) acc = __fma_rn(__ldcs(sell.sval + p0 + lane + k * SELL_C), op.gather(col), acc);
-          }
-          sm.sy[w & 1][rl] = acc;
-        }
+  for (int tl = 0; tl < tpc; ++tl) {
+    const int r0 = (blockIdx.x * tpc + tl) * MD_TILE;
+    if (r0 >= n) {  // uniform: an all-padding tile
+      for (int d = t; d < J; d += TB) sm.tp[tl * MDOT_MAX + d] = 0.0;
+      continue;
+    }
+    const int i0 = r0 + MD_R * t;
+    const int cnt = max(0, min(MD_R, n - i0));
+    double y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) y[k] = 0.0;
+    if constexpr (Op::kSpmv) {
+      auto g = [&](int col) { return op.gather(col); };
+      if constexpr (FMT == 2) {
+        for (int w = 0; w < MD_R; ++w)
+          if (r0 + w * TB < n) sell_window_store<false>(sell, r0 + w * TB, g, sm.sy + w * TB);
         __syncthreads();
-        y = sm.sy[w & 1][t];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y[k] = sm.sy[MD_R * t + k];
+      } else {  // CSR (stencils: short rows), AC-3 chain per row
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < cnt) {
+            const int i = i0 + k;
+            double acc = 0.0;
+            for (int q = csr.rp[i]; q < csr.rp[i + 1]; ++q) acc = __fma_rn(__ldcs(csr.v + q), g(__ldcs(csr.ci + q)), acc);
+            y[k] = acc;
+          }
       }
-      const double u = i < n ? op.value(i, y, cache + t) : 0.0;
-      for (int d0 = 0; d0 < J; d0 += 8) {  // 8 dots at a time: loads and butterflies interleave
-        double q[8];
+    }
+    double u[8];
+    op.value8(i0, cnt, y, u);
+    for (int d0 = 0; d0 < J; d0 += MDOT_G) {
+      double q[MDOT_G];
+      double v[MDOT_G][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) q[e] = (i < n && d0 + e < J) ? u * op.operand(i, d0 + e, cache + t) : 0.0;
+      for (int e = 0; e < MDOT_G; ++e)  // MDOT_G operand runs in flight
+        if (d0 + e < J) op.operand8(i0, cnt, d0 + e, u, v[e]);
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
+      for (int e = 0; e < MDOT_G; ++e) {
+        double pr[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) q[e] = q[e] + __shfl_xor_sync(0xffffffffu, q[e], off);
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (d0 + e < J) wp[(d0 + e) * 8 + warp] = q[e];
-        }
+        for (int k = 0; k < 8; ++k) pr[k] = u[k] * v[e][k];
+        q[e] = d0 + e < J ? tree8(pr) : 0.0;
       }
-    } else {
-      for (int d = lane; d < J; d += 32)
-        if (warp == 0) wp[d * 8 + 0] = 0.0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+        for (int e = 0; e < MDOT_G; ++e)
+          if (d0 + e < J) q[e] = q[e] + __shfl_xor_sync(0xffffffffu, q[e], off);  // J uniform
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int e = 0; e < MDOT_G; ++e)
+          if (d0 + e < J) sm.wp[(d0 + e) * 8 + warp] = q[e];
+      }
     }
     __syncthreads();
-    if (t < J) {
-      const double* v = wp + t * 8;
-      sm.winp[w][t] = (r0 < n) ? ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])) : 0.0;
+    for (int d = t; d < J; d += TB) {
+      double a[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) a[w] = sm.wp[d * 8 + w];
+      sm.tp[tl * MDOT_MAX + d] = tree8(a);
     }
+    __syncthreads();  // sy / wp are rewritten by the next tile
   }
-  __syncthreads();
-  if (t < J) {
+  for (int d = t; d < J; d += TB) {
     double a[8];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) a[w] = w < wpc ? sm.winp[w][t] : 0.0;
-    part[(size_t)t * stride + blockIdx.x] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    for (int w = 0; w < 8; ++w) a[w] = w < tpc ? sm.tp[w * MDOT_MAX + d] : 0.0;
+    part[(size_t)d * stride + blockIdx.x] = tree8(a);
   }
 }
 
@@ -538,14 +599,23 @@ __device__ __forceinline__ double cta_tree(const double* p, int ntiles) {
   return res + 0.0;  // AC-5
 }
 
+template <class Op, class = void>
+struct MdotWarpFinish : std::false_type {};
+template <class Op>
+struct MdotWarpFinish<Op, std::void_t<decltype(Op::kWarpFinish)>> : std::true_type {};
+
 // Dot d = blockIdx.x of a multi-dot pass: canonical tree over the CTA partials, then
-// op.store(d, value) by thread 0.
+// op.store(d, value) by thread 0 (or the Op's warp-wide epilogue).
 template <class Op>
 __global__ void __launch_bounds__(FIN_THREADS) mdot_finish(Op op, const double* part, int stride, int ntiles) {
   pdl_enter();
   if (!op.begin()) return;
   const double v = cta_tree(part + (size_t)blockIdx.x * stride, ntiles);
-  if (threadIdx.x == 0) op.store(blockIdx.x, v);
+  if constexpr (MdotWarpFinish<Op>::value) {
+    if (threadIdx.x < 32) op.finish_warp(v, threadIdx.x);  // valid in warp 0
+  } else if (threadIdx.x == 0) {
+    op.store(blockIdx.x, v);
+  }
 }
 
 }  // namespace gsk

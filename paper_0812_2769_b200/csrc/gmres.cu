@@ -27,12 +27,17 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
   GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
   for (int j = 1; j <= m && rc >= 0 && P->orth == 1; ++j) {
-    OpCgsA a{P->W, n, slot(j), slot(j + 1), st, j, 0, 0, nullptr};
-    OpCgsB bpass{P->W, n, slot(j + 1), st, j, 0, nullptr, nullptr};
-    OpCgsC c{P->W, n, slot(j + 1), P->hist_d, st, j, nullptr, nullptr};
-    rc = j == 1 ? run_mdot(P, a, j, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_mdot(P, a, j, s);
-    if (rc >= 0) rc = j == 2 ? run_mdot(P, bpass, j, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_mdot(P, bpass, j, s);
-    if (rc >= 0) rc = run_pass(P, c, s);
+    OpCgsS sp{slot(j), slot(j + 1), st, j, 0};
+    OpCgsA a{};
+    a.W = P->W, a.n = n, a.Wn = slot(j + 1), a.st = st, a.j = j;
+    OpCgsB bp{};
+    bp.W = P->W, bp.n = n, bp.Wn = slot(j + 1), bp.st = st, bp.j = j;
+    OpCgsC c{};
+    c.W = P->W, c.n = n, c.Wn = slot(j + 1), c.st = st, c.j = j, c.hist = P->hist_d;
+    rc = j == 1 ? run_pass(P, sp, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, sp, s);
+    if (rc >= 0) rc = run_mdot(P, a, j, s);
+    if (rc >= 0) rc = j == 2 ? run_mdot(P, bp, j, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_mdot(P, bp, j, s);
+    if (rc >= 0) rc = run_mdot(P, c, 1, s);
   }
   for (int j = 1; j <= m && rc >= 0 && P->orth == 0; ++j) {
     OpArnoldi<> a{slot(j), slot(1), slot(j + 1), st, j, 0, 0};

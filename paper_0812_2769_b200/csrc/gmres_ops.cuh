@@ -236,109 +236,120 @@ struct OpLast {
 };
 
 // ---- double classical Gram-Schmidt (AZTEC's orthogonalisation) ----
-// Step j = three passes: A  w = A v_j, c1_d = <w, v_d>;  B  w -= sum_d c1_d v_d,
-// c2_d = <w, v_d>;  C  w -= sum_d c2_d v_d, ||w||^2 -> H(:, j) = c1 + c2, Givens.
-// Each update is an FMA chain over d ascending (oracle orc_gmres_orth, orth = 1).
-struct OpCgsA {
-  static constexpr bool kSpmv = true;
+// Step j = four passes: S  w = A v_j (SpMV pass);  A  c1_d = <w, v_d>;
+// B  w -= sum_d c1_d v_d, c2_d = <w, v_d>;  C  w -= sum_d c2_d v_d, ||w||^2 ->
+// H(:, j) = c1 + c2, Givens.  A, B, C are tile passes (mdot_pass: 8 consecutive rows
+// per thread, 16-byte loads).  Each update is an FMA chain over d ascending (oracle
+// orc_gmres_orth, orth = 1); v_d = RN(w_d * inv_d) as everywhere (AC-7).
+#ifndef GSK_CGS_UNROLL
+#define GSK_CGS_UNROLL 1
+#endif
+constexpr int kCgsUnroll = GSK_CGS_UNROLL;
+struct CgsBase {
   const double* W;
   size_t n;
+  double* Wn;
+  GmresState* st;
+  int j;
+  int nd;
+  const double* inv;
+  __device__ bool live() const { return !(st->done || st->cycle_stop); }
+  __device__ void basis8(int i0, int cnt, int d, double (&v)[8]) const {
+    ld8(W + d * n + i0, cnt, v);
+    const double s = inv[d + 1];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = v[k] * s;
+  }
+  // w -= sum_d c_d v_d over d < j (8 rows' chains interleaved); returns w (0 past cnt)
+  __device__ void update8(int i0, int cnt, const double* c, double (&u)[8]) const {
+    double w[8];
+    ld8(Wn + i0, cnt, w);
+#pragma unroll kCgsUnroll
+    for (int d = 0; d < j; ++d) {
+      double v[8];
+      basis8(i0, cnt, d, v);
+      const double mc = -c[d];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = __fma_rn(mc, v[k], w[k]);
+    }
+    st8(Wn + i0, cnt, w);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) u[k] = k < cnt ? w[k] : 0.0;
+  }
+};
+
+struct OpCgsS {  // S: w = A v_j (no reduction)
+  static constexpr int D = 0;
+  static constexpr int NV = 0;
+  static constexpr bool kSpmv = true;
   const double* Wj;
   double* Wn;
   GmresState* st;
   int j;
-  int nd;
   double invj;
-  const double* inv;
   __device__ bool begin() {
     if (st->done || st->cycle_stop) return false;
     invj = st->inv[j];
-    inv = st->inv;
-    nd = j;
     return true;
   }
+  __device__ const double* vin(int) const { return nullptr; }
   __device__ double gather(int c) const { return __ldg(Wj + c) * invj; }
-  __device__ double value(int i, double y, double*) const {
-    Wn[i] = y;
-    return y;
-  }
-  __device__ double operand(int i, int d, const double*) const { return __ldg(W + d * n + i) * inv[d + 1]; }
-  __device__ void store(int d, double v) const { st->c1[d] = v; }
+  __device__ void row(int i, double y, const double (&)[1], double (&)[1]) const { Wn[i] = y; }
 };
 
-struct OpCgsB {
+struct OpCgsA : CgsBase {  // A: c1 = V^T w
   static constexpr bool kSpmv = false;
-  const double* W;
-  size_t n;
-  double* Wn;
-  GmresState* st;
-  int j;
-  int nd;
-  const double *inv, *c1;
   __device__ bool begin() {
-    if (st->done || st->cycle_stop) return false;
+    if (!live()) return false;
     inv = st->inv;
-    c1 = st->c1;
     nd = j;
     return true;
   }
   __device__ double gather(int) const { return 0.0; }
-  __device__ double value(int i, double, double* cache) const {
-    double w = Wn[i];
-    const bool cached = nd <= MDOT_CACHE;
-    for (int d0 = 0; d0 < nd; d0 += 8) {  // 8 basis loads in flight, chain in d order
-      double vv[8];
+  __device__ void value8(int i0, int cnt, const double (&)[8], double (&u)[8]) const {
+    ld8(Wn + i0, cnt, u);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) vv[u] = d0 + u < nd ? __ldg(W + (d0 + u) * n + i) * inv[d0 + u + 1] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (d0 + u < nd) {
-          if (cached) cache[(d0 + u) * TB] = vv[u];
-          w = __fma_rn(-c1[d0 + u], vv[u], w);
-        }
-    }
-    Wn[i] = w;
-    return w;
+    for (int k = 0; k < 8; ++k) u[k] = k < cnt ? u[k] : 0.0;
   }
-  __device__ double operand(int i, int d, const double* cache) const {
-    return nd <= MDOT_CACHE ? cache[d * TB] : __ldg(W + d * n + i) * inv[d + 1];
+  __device__ void operand8(int i0, int cnt, int d, const double (&)[8], double (&v)[8]) const {
+    basis8(i0, cnt, d, v);
+  }
+  __device__ void store(int d, double v) const { st->c1[d] = v; }
+};
+
+struct OpCgsB : CgsBase {  // B: w -= V c1, c2 = V^T w
+  static constexpr bool kSpmv = false;
+  __device__ bool begin() {
+    if (!live()) return false;
+    inv = st->inv;
+    nd = j;
+    return true;
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void value8(int i0, int cnt, const double (&)[8], double (&u)[8]) const { update8(i0, cnt, st->c1, u); }
+  __device__ void operand8(int i0, int cnt, int d, const double (&)[8], double (&v)[8]) const {
+    basis8(i0, cnt, d, v);
   }
   __device__ void store(int d, double v) const { st->c2[d] = v; }
 };
 
-struct OpCgsC {
-  static constexpr int D = 1;
-  static constexpr int NV = 1;
+struct OpCgsC : CgsBase {  // C: w -= V c2, ||w||^2 -> Givens etc. (warp finish)
   static constexpr bool kSpmv = false;
-  const double* W;
-  size_t n;
-  double* Wn;
+  static constexpr bool kWarpFinish = true;
   double* hist;
-  GmresState* st;
-  int j;
-  const double *inv, *c2;
   __device__ bool begin() {
-    if (st->done || st->cycle_stop) return false;
+    if (!live()) return false;
     inv = st->inv;
-    c2 = st->c2;
+    nd = 1;
     return true;
   }
-  __device__ const double* vin(int) const { return Wn; }
   __device__ double gather(int) const { return 0.0; }
-  __device__ void row(int q, double, const double (&v)[NV], double (&c)[1]) const {
-    double w = v[0];
-    for (int d0 = 0; d0 < j; d0 += 8) {
-      double vv[8];
+  __device__ void value8(int i0, int cnt, const double (&)[8], double (&u)[8]) const { update8(i0, cnt, st->c2, u); }
+  __device__ void operand8(int, int, int, const double (&u)[8], double (&v)[8]) const {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) vv[u] = d0 + u < j ? __ldg(W + (d0 + u) * n + q) * inv[d0 + u + 1] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (d0 + u < j) w = __fma_rn(-c2[d0 + u], vv[u], w);
-    }
-    Wn[q] = w;
-    c[0] = w * w;
+    for (int k = 0; k < 8; ++k) v[k] = u[k];
   }
-  __device__ void finish(const double (&s)[1], int lane) const { arnoldi_finish(st, hist, j, s[0], lane, 1); }
+  __device__ void finish_warp(double hn2, int lane) const { arnoldi_finish(st, hist, j, hn2, lane, 1); }
 };
 
 // X: x += sum_{k=1..K} y_k v_k (k ascending)

@@ -199,26 +199,17 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
              cudaEvent_t pe1 = nullptr) {
   const int n = P->geo.n;
   const int sms = num_sms();
-  const int windows = (n + TB - 1) / TB;
-  int wpc = 8;
-  while (wpc > 1 && (long long)windows < (long long)wpc * 2 * sms) wpc >>= 1;
-  const int ntiles = (windows + wpc - 1) / wpc;
-  const size_t dyn = (!Op::kSpmv && J <= MDOT_CACHE) ? sizeof(double) * J * TB : 0;
-  static bool attr = false;
-  if constexpr (!Op::kSpmv) {
-    if (!attr) {
-      GSK_CUDA(cudaFuncSetAttribute(mdot_pass<0, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(sizeof(double) * MDOT_CACHE * TB)));
-      attr = true;
-    }
-  }
+  const int tiles = (n + MD_TILE - 1) / MD_TILE;
+  int tpc = 8;  // tiles per CTA: as many as still leave >= 2 waves of CTAs
+  while (tpc > 1 && (long long)tiles < (long long)tpc * MDOT_MINB * sms * 2) tpc >>= 1;
+  const int ntiles = (tiles + tpc - 1) / tpc;
   if (pe0) GSK_CUDA(cudaEventRecordWithFlags(pe0, s, cudaEventRecordExternal));
   if constexpr (!Op::kSpmv)
-    GSK_CUDA(launch_k(mdot_pass<0, Op>, ntiles, TB, dyn, s, P->csr, P->sell, n, wpc, op, P->mpart, P->pstride));
+    GSK_CUDA(launch_k(mdot_pass<0, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride));
   else if (P->fmt == GSK_FMT_SELL)
-    GSK_CUDA(launch_k(mdot_pass<2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->mpart, P->pstride));
+    GSK_CUDA(launch_k(mdot_pass<2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride));
   else
-    GSK_CUDA(launch_k(mdot_pass<1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->mpart, P->pstride));
+    GSK_CUDA(launch_k(mdot_pass<1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride));
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
   GSK_CUDA(launch_k(mdot_finish<Op>, J, FIN_THREADS, 0, s, op, P->mpart, P->pstride, ntiles));
