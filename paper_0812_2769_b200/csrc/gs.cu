@@ -86,14 +86,54 @@ __global__ void __launch_bounds__(TB, 8) gs_kernel(int n, const int* __restrict_
 }
 
 // a'_ij = (a_ij * s_i) * s_j, b'_i = b_i * s_i (reading S1)
+__device__ __forceinline__ void cp_async4(int* smem, const int* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
+}
+
+// Staged like gs_kernel: the 256-row window's values and columns arrive in shared
+// memory with cp.async, each thread scales its row there (the column factor is a
+// gather of s), and the window is written back coalesced.
 __global__ void __launch_bounds__(TB) sym_scale_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                                                        const double* vin, double* vout, const double* b,
                                                        double* bout, const double* __restrict__ sv) {
-  const int r = blockIdx.x * TB + threadIdx.x;
-  if (r >= n) return;
-  const double si = sv[r];
-  for (int k = rp[r]; k < rp[r + 1]; ++k) vout[k] = (vin[k] * si) * __ldg(sv + ci[k]);
-  if (b && bout) bout[r] = b[r] * si;
+  __shared__ double sval[CSR_CAP];
+  __shared__ int scol[CSR_CAP];
+  const int r0 = blockIdx.x * TB, t = threadIdx.x, r = r0 + t;
+  const int rend = min(r0 + TB, n);
+  const int s0 = __ldg(rp + r0), s1 = __ldg(rp + rend), cnt = s1 - s0;
+  const bool staged = cnt <= CSR_CAP;
+  if (staged) {
+    for (int k = t; k < cnt; k += TB) {
+      cp_async8(sval + k, vin + s0 + k);
+      cp_async4(scol + k, ci + s0 + k);
+    }
+    cp_async_commit();
+  }
+  int a0 = 0, a1 = 0;
+  double si = 0.0, bi = 0.0;
+  if (r < n) {
+    a0 = __ldg(rp + r);
+    a1 = __ldg(rp + r + 1);
+    si = sv[r];
+    if (b && bout) bi = __ldcs(b + r);
+  }
+  if (staged) {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  if (r < n) {
+    if (staged) {
+      for (int k = a0 - s0; k < a1 - s0; ++k) sval[k] = (sval[k] * si) * __ldg(sv + scol[k]);
+    } else {
+      for (int k = a0; k < a1; ++k) vout[k] = (vin[k] * si) * __ldg(sv + ci[k]);
+    }
+    if (b && bout) __stcs(bout + r, bi * si);
+  }
+  if (staged) {
+    __syncthreads();
+    for (int k = t; k < cnt; k += TB) __stcs(vout + s0 + k, sval[k]);
+  }
 }
 
 __global__ void unscale_kernel(int64_t n, const double* s, const double* y, double* x) {

@@ -20,3 +20,9 @@ for p in (2, 2, 2, 1):
     e1.record()
     torch.cuda.synchronize()
     print("GS(%d) %.3f ms" % (p, e0.elapsed_time(e1)))
+for _ in range(3):
+    e0.record()
+    gsk.gs_scale_sym(A, b, 2)
+    e1.record()
+    torch.cuda.synchronize()
+    print("two-sided GS(2) %.3f ms" % e0.elapsed_time(e1))

@@ -1,4 +1,5 @@
-"""Run every BASELINE.json config on the GPU: {none, GS(1), GS(2)} x {Bi-CGSTAB, GMRES(m)}.
+"""Run every BASELINE.json config on the GPU: {none, GS(1), GS(2), two-sided D^1/2 A D^1/2
+with p = 2} x {Bi-CGSTAB, GMRES(m)}.
 
 For each run: iterations to each tolerance (first crossing of the history), verdict,
 best relative residual, device time of the solve and time to the tightest tolerance
@@ -36,14 +37,22 @@ def run(name, maxit_gmres=None):
     gsk.gs_scale(A0, s["b"], 1)  # warm-up: module load / allocator pools out of the timings
     rows = []
     tols = c.tols or (c.tol,)
-    for scaling in ("none", 1, 2):
+    for scaling in ("none", 1, 2, "sym2"):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         A = gsk.CSR.from_system(s)
         b = torch.tensor(s["b"], device="cuda")
         w = d2
         gs_ms = 0.0
-        if scaling != "none":
+        if scaling == "sym2":  # PAPER.md:245-251; GS(2) frame: D r = D^1/2 r_sym -> w = s
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            A, b, sv = gsk.gs_scale_sym(A, b, 2)
+            e1.record()
+            torch.cuda.synchronize()
+            gs_ms = e0.elapsed_time(e1)
+            w = sv
+        elif scaling != "none":
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             A, b, dp = gsk.gs_scale(A, b, scaling, inplace=True)
