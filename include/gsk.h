@@ -175,6 +175,51 @@ int gsk_plan_residual_norm(gsk_plan *plan, const double *b, const double *x, con
  * pass.  Returns samples in *count. */
 int gsk_plan_probe(gsk_plan *plan, int kind, double *avg_ms, int64_t *count);
 
+/* ---- Row-block sharding ------------------
+ * The global system is split into P contiguous row blocks: with N = 2^ceil(log2 n) and
+ * B = N / P, shard r owns rows [r B, min((r+1) B, n)).  Each block is an aligned
+ * power-of-two subtree of the canonical reduction tree (AC-5), so a sharded solve is
+ * bit-identical to the unsharded one.  SpMV reads boundary rows of the neighbouring
+ * shards (the halo): a halo may reach only into the adjacent shards (banded / stencil
+ * matrices; a randomly permuted system such as C5 is rejected).  Dot products: each
+ * shard reduces its own block, the P values are gathered (device copies on one GPU,
+ * ncclAllGather across processes) and joined by the top levels of the same tree. */
+typedef struct gsk_shard_opts {
+  int32_t nshards;   /* P: a power of two, 1..32 */
+  int32_t first;     /* first shard held by this process */
+  int32_t count;     /* shards held by this process: P (all of them, one GPU) or 1
+                        (one shard per process, one process per GPU) */
+  int32_t pad_;
+  void *nccl_comm;   /* ncclComm_t over the P processes when count == 1 < P, else NULL
+                        (gsk_nccl_comm_create); not owned by the plan */
+} gsk_shard_opts;
+
+/* Host-only layout helpers (no GPU needed).  Rows of shard r; GSK_E_INVALID if P is not
+ * a power of two in [1, 32], r is out of range or the shard would be empty. */
+int gsk_shard_rows(int64_t n, int32_t nshards, int32_t r, int64_t *lo, int64_t *hi);
+/* Halo widths of shard r from a [host] CSR with global columns: *hl = lo - min col,
+ * *hr = max col - (hi - 1) (0 when inside).  GSK_E_INVALID if a halo reaches beyond an
+ * adjacent shard. */
+int gsk_shard_halo_host(int64_t n, const int32_t *row_ptr, const int32_t *col, int32_t nshards, int32_t r,
+                        int32_t *hl, int32_t *hr);
+
+/* Plan over this process's shards of the GLOBAL matrix A (device, global columns;
+ * every process passes the whole matrix).  Each shard gets its own CSR (rebased row
+ * pointers, columns relative to its first row) and, for GSK_FMT_SELL, its own SELL
+ * layout; values are read from A->values (gsk_plan_refresh after rescaling).  Solves
+ * on the plan (gsk_bicgstab_solve_plan, gsk_gmres_solve_plan) take b, x0, x and the
+ * weights as this process's rows [lo(first), hi(first + count - 1)) (device) and
+ * return the global history.  The split Bi-CGSTAB schedule and MGS GMRES are used;
+ * opts->engine is ignored. */
+int gsk_plan_create_sharded(const gsk_csr *A, const gsk_opts *opts, const gsk_shard_opts *sh,
+                            gsk_plan **plan, void *stream);
+/* NCCL communicator for sharded plans across processes (libnccl.so.2 is loaded at run
+ * time; GSK_E_INVALID if it cannot be).  id: 128 bytes from gsk_nccl_unique_id on one
+ * rank, shared with the others by the caller. */
+int gsk_nccl_unique_id(char *id);
+int gsk_nccl_comm_create(const char *id, int32_t nranks, int32_t rank, void **comm);
+int gsk_nccl_comm_destroy(void *comm);
+
 /* Diagnostics. */
 const char *gsk_last_error(void);
 int64_t gsk_launch_count(void);   /* kernels launched by this library so far */

@@ -5,8 +5,10 @@ systems with discontinuous coefficients" (arXiv 0812.2769).  The hot path runs i
 hand-written sm_100a kernels behind the C-ABI of ``libgsk.so`` (include/gsk.h);
 this package is the thin ctypes binding (argument marshalling only).
 """
-from ._gsk import (CSR, Plan, GskError, STATUS, SYMBOLS, LIB_PATH, bicgstab_solve, dot,  # noqa: F401
-                   gmres_solve, gs_scale, gs_scale_sym, gs_unscale, launch_count, load, spmv)
+from ._gsk import (CSR, NcclComm, Plan, ShardedPlan, GskError, STATUS, SYMBOLS, LIB_PATH,  # noqa: F401
+                   bicgstab_solve, dot, gmres_solve, gs_scale, gs_scale_sym, gs_unscale, launch_count, load,
+                   shard_halo, shard_rows, spmv)
 
-__all__ = ["CSR", "Plan", "GskError", "STATUS", "SYMBOLS", "LIB_PATH", "bicgstab_solve", "dot",
-           "gmres_solve", "gs_scale", "gs_scale_sym", "gs_unscale", "launch_count", "load", "spmv"]
+__all__ = ["CSR", "NcclComm", "Plan", "ShardedPlan", "GskError", "STATUS", "SYMBOLS", "LIB_PATH",
+           "bicgstab_solve", "dot", "gmres_solve", "gs_scale", "gs_scale_sym", "gs_unscale", "launch_count", "load",
+           "shard_halo", "shard_rows", "spmv"]

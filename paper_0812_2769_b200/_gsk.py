@@ -27,6 +27,8 @@ SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gs
            "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_destroy",
            "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
            "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
+           "gsk_shard_rows", "gsk_shard_halo_host", "gsk_plan_create_sharded", "gsk_nccl_unique_id",
+           "gsk_nccl_comm_create", "gsk_nccl_comm_destroy",
            "gsk_last_error", "gsk_launch_count", "gsk_version")
 
 
@@ -51,6 +53,11 @@ class Opts(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("poll", ctypes.c_int32), ("weights", ctypes.c_void_p),
                 ("bicg_schedule", ctypes.c_int32), ("gmres_orth", ctypes.c_int32),
                 ("sell_index", ctypes.c_int32), ("engine", ctypes.c_int32)]
+
+
+class ShardOpts(ctypes.Structure):
+    _fields_ = [("nshards", ctypes.c_int32), ("first", ctypes.c_int32), ("count", ctypes.c_int32),
+                ("pad_", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p)]
 
 
 class GskError(RuntimeError):
@@ -92,6 +99,12 @@ def load(path: str = LIB_PATH):
     lib.gsk_gmres_solve_plan.argtypes = [vp, vp, vp, i32, d, i32, vp, vp, P(Report), vp]
     lib.gsk_plan_residual_norm.argtypes = [vp, vp, vp, vp, P(d), vp]
     lib.gsk_plan_probe.argtypes = [vp, i32, P(d), P(i64)]
+    lib.gsk_shard_rows.argtypes = [i64, i32, i32, P(i64), P(i64)]
+    lib.gsk_shard_halo_host.argtypes = [i64, vp, vp, i32, i32, P(ctypes.c_int32), P(ctypes.c_int32)]
+    lib.gsk_plan_create_sharded.argtypes = [P(CsrStruct), P(Opts), P(ShardOpts), P(vp), vp]
+    lib.gsk_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    lib.gsk_nccl_comm_create.argtypes = [ctypes.c_char_p, i32, i32, P(vp)]
+    lib.gsk_nccl_comm_destroy.argtypes = [vp]
     lib.gsk_last_error.restype = ctypes.c_char_p
     lib.gsk_launch_count.restype = i64
     for name in SYMBOLS:
@@ -237,6 +250,7 @@ class Plan:
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))
         self.h = h
         self.fmt = fmt
+        self.nloc = A.n
 
     def close(self):
         if getattr(self, "h", None):
@@ -307,9 +321,9 @@ class Plan:
 
     def _solve(self, which, b, x0, tol, maxit, m=None, x=None, hist=True):
         lib = load()
-        b = _dev_f64(b, self.A.n)
-        x0 = _dev_f64(x0, self.A.n)
-        x = torch.empty(self.A.n, dtype=torch.float64, device="cuda") if x is None else x
+        b = _dev_f64(b, self.nloc)
+        x0 = _dev_f64(x0, self.nloc)
+        x = torch.empty(self.nloc, dtype=torch.float64, device="cuda") if x is None else x
         H = np.empty(maxit + 1, np.float64) if hist else None
         rep = Report()
         hp = None if H is None else H.ctypes.data_as(ctypes.c_void_p)
@@ -330,6 +344,78 @@ class Plan:
     def gmres(self, b, x0=None, m=30, tol=1e-8, maxit=10000, x=None, hist=True):
         """Restarted GMRES(m) on the plan's system; returns (x, hist, report)."""
         return self._solve("gmres", b, x0, tol, maxit, m=m, x=x, hist=hist)
+
+
+def shard_rows(n: int, nshards: int, r: int):
+    """Rows [lo, hi) of shard r of n rows in nshards row blocks (host only)."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().gsk_shard_rows(int(n), int(nshards), int(r), ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def shard_halo(row_ptr, col, nshards: int, r: int):
+    """Halo widths (left, right) of shard r from a host CSR with global columns."""
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    ci = np.ascontiguousarray(col, np.int32)
+    hl, hr = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().gsk_shard_halo_host(rp.size - 1, rp.ctypes.data_as(ctypes.c_void_p),
+                                      ci.ctypes.data_as(ctypes.c_void_p), int(nshards), int(r),
+                                      ctypes.byref(hl), ctypes.byref(hr)))
+    return hl.value, hr.value
+
+
+class NcclComm:
+    """NCCL communicator over the ranks of a torch.distributed process group (one GPU
+    per rank); rank 0's unique id is broadcast through the group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        lib = load()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        buf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib.gsk_nccl_unique_id(buf))
+        obj = [bytes(buf.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        h = ctypes.c_void_p()
+        _check(lib.gsk_nccl_comm_create(ctypes.c_char_p(obj[0]), self.world, self.rank, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            load().gsk_nccl_comm_destroy(self.h)
+            self.h = None
+
+
+class ShardedPlan(Plan):
+    """Row-block sharded plan: `shards` row blocks of the GLOBAL matrix A.
+    On one GPU (comm=None) this process holds all shards; with an NcclComm each rank
+    holds shard `comm.rank` of `comm.world`.  Solves take and return this process's
+    rows; the history is global.  Bit-identical to the unsharded solvers."""
+
+    def __init__(self, A: CSR, shards: int = 2, fmt: str = "csr", weights=None, poll: int = 0,
+                 comm: "NcclComm" = None):
+        lib = load()
+        self.A = A
+        if comm is None:
+            first, count, ch = 0, int(shards), None
+        else:
+            shards, first, count, ch = comm.world, comm.rank, 1, comm.h
+        lo, _ = shard_rows(A.n, shards, first)
+        _, hi = shard_rows(A.n, shards, first + count - 1)
+        self.rows = (lo, hi)
+        self.nloc = hi - lo
+        self.weights = _dev_f64(weights, self.nloc)
+        opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
+                    SCHEDULE["split"], ORTH["mgs"], 0, ENGINE["graph"])
+        so = ShardOpts(int(shards), int(first), int(count), 0, ch)
+        self._csr = A.struct()
+        h = ctypes.c_void_p()
+        _check(lib.gsk_plan_create_sharded(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(so),
+                                           ctypes.byref(h), _stream()))
+        self.h = h
+        self.fmt = fmt
+        self.shards = shards
 
 
 def bicgstab_solve(A: CSR, b, x0=None, tol=1e-8, maxit=10000):

@@ -70,7 +70,7 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
 }
 
 // Copy the device state and history out into the report (after t1 was recorded).
-static int bicgstab_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller) {
+int bicgstab_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller) {
   cudaStream_t s = P->st;
   BicgState hs{};
   GSK_CUDA(cudaMemcpyAsync(&hs, P->bstate, sizeof hs, cudaMemcpyDeviceToHost, s));
@@ -103,6 +103,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
     set_error("bicgstab: invalid arguments (b, x, rep non-null; tol > 0; maxit >= 1)");
     return GSK_E_INVALID;
   }
+  if (P->shards) return shard_bicgstab_run(P, b, x0, tol, maxit, x, hist, rep, caller);
   const int n = P->A.n;
   if (!P->bvec) GSK_CUDA(cudaMalloc(&P->bvec, sizeof(double) * 7 * (size_t)n));
   if (!P->bstate) GSK_CUDA(cudaMalloc(&P->bstate, sizeof(BicgState)));

@@ -34,6 +34,8 @@ struct SellView {
   const uint8_t* __restrict__ sidx;  // [nslots]
   const int* __restrict__ dptr;      // [nchunks+1]
   const int* __restrict__ dict;      // [ndict]
+  int pad;  // column value of padding slots: -1, or INT_MIN in a shard plan, whose
+            // remapped columns may be negative (left halo)
 };
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the

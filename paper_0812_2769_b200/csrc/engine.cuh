@@ -147,14 +147,14 @@ __device__ __forceinline__ void sell_window_store(const SellView& A, int r0, con
       for (int k = 0; k < 8; ++k)
         if (k < L) {
           const int delta = __shfl_sync(0xffffffffu, dv, cols[k] & 31);
-          cols[k] = cols[k] == 255 ? -1 : row + delta;
+          cols[k] = cols[k] == 255 ? A.pad : row + delta;
         }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (k < L && cols[k] >= 0) xs[k] = g(cols[k]);
+        if (k < L && cols[k] != A.pad) xs[k] = g(cols[k]);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (k < L && cols[k] >= 0) acc = __fma_rn(vals[k], xs[k], acc);
+        if (k < L && cols[k] != A.pad) acc = __fma_rn(vals[k], xs[k], acc);
     } else if (L <= 8) {
       int cols[8];
       double vals[8], xs[8];
@@ -166,14 +166,14 @@ __device__ __forceinline__ void sell_window_store(const SellView& A, int r0, con
         }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (k < L && cols[k] >= 0) xs[k] = g(cols[k]);
+        if (k < L && cols[k] != A.pad) xs[k] = g(cols[k]);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (k < L && cols[k] >= 0) acc = __fma_rn(vals[k], xs[k], acc);
+        if (k < L && cols[k] != A.pad) acc = __fma_rn(vals[k], xs[k], acc);
     } else {
       for (int k = 0; k < L; ++k) {  // long chunks: plain int32 columns (kept in every plan)
         const int col = __ldcs(A.scol + base + k * SELL_C);
-        if (col >= 0) acc = __fma_rn(__ldcs(A.sval + base + k * SELL_C), g(col), acc);
+        if (col != A.pad) acc = __fma_rn(__ldcs(A.sval + base + k * SELL_C), g(col), acc);
       }
     }
     sy[rl] = acc;
@@ -335,12 +335,10 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
 // warps, and a binary counter joins the rounds in order.  Skipped exactly when the
 // pass was skipped (op.begin() reads the same device flags; only finish kernels
 // change them).
-template <class Op>
-__global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double* part, int stride,
-                                                             int ntiles) {
-  pdl_enter();
-  if (!op.begin()) return;
-  constexpr int D = Op::D;
+// Canonical tree of D dot products over ntiles CTA partials (+ 0.0), valid in warp 0
+// (every lane).  Body of the finish kernels; blockDim = FIN_THREADS.
+template <int D>
+__device__ __forceinline__ void fin_tree(const double* part, int stride, int ntiles, double (&s)[D]) {
   __shared__ double ws[D][32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   double stk[D][12];
@@ -403,11 +401,52 @@ __global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double
     }
   }
   if (warp == 0) {
-    double s[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) s[d] = __shfl_sync(0xffffffffu, stk[d][0], 0) + 0.0;
-    op.finish(s, lane);
   }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(FIN_THREADS) finish_kernel(Op op, const double* part, int stride,
+                                                             int ntiles) {
+  pdl_enter();
+  if (!op.begin()) return;
+  double s[Op::D];
+  fin_tree<Op::D>(part, stride, ntiles, s);
+  if (threadIdx.x < 32) op.finish(s, threadIdx.x);
+}
+
+// Row-block shards: each shard's finish writes its canonical subtree
+// values (the shard's rows are an aligned power-of-two block of the global tree) ...
+template <class Op>
+__global__ void __launch_bounds__(FIN_THREADS) finish_local_kernel(Op op, const double* part, int stride,
+                                                                   int ntiles, double* out) {
+  pdl_enter();
+  if (!op.begin()) return;
+  double s[Op::D];
+  fin_tree<Op::D>(part, stride, ntiles, s);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int d = 0; d < Op::D; ++d) out[d] = s[d];
+  }
+}
+
+// ... and one warp joins the P shard values (gath[r * MAXD + d], P a power of two <= 32)
+// with the top levels of the same tree, + 0.0, then runs the Op's scalar epilogue.
+template <class Op>
+__global__ void __launch_bounds__(32) finish_global_kernel(Op op, const double* gath, int P) {
+  pdl_enter();
+  if (!op.begin()) return;
+  const int lane = threadIdx.x;
+  double s[Op::D];
+#pragma unroll
+  for (int d = 0; d < Op::D; ++d) {
+    double u = lane < P ? gath[lane * MAXD + d] : 0.0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+    s[d] = u + 0.0;
+  }
+  op.finish(s, lane);
 }
 
 // ---------------------------------------------------------------------------------

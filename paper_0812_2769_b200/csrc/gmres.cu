@@ -62,12 +62,41 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
   return end_capture(s, rc, out, &P->gkernels, "gmres");
 }
 
+// Copy the device state and history out into the report (after t1 was recorded).
+int gmres_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller) {
+  cudaStream_t s = P->st;
+  GmresState hs{};
+  GSK_CUDA(cudaMemcpyAsync(&hs, P->gstate, sizeof hs, cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  std::vector<double> H(hs.hist_len);
+  GSK_CUDA(cudaMemcpy(H.data(), P->hist_d, sizeof(double) * hs.hist_len, cudaMemcpyDeviceToHost));
+  if (hist) std::copy(H.begin(), H.end(), hist);
+  float ms = 0;
+  GSK_CUDA(cudaEventElapsedTime(&ms, P->t0, P->t1));
+  rep->status = hs.status;
+  rep->iterations = hs.it;
+  rep->restarts = hs.restarts;
+  rep->history_len = hs.hist_len;
+  rep->breakdown_at = 0;
+  rep->pad_ = 0;
+  rep->relres = H.back();
+  rep->true_relres = hs.true_rel;
+  rep->true_relres_w = hs.true_rel_w;
+  double best = H[0];
+  for (double v : H) best = std::min(best, v);
+  rep->best_relres = best;
+  rep->solve_ms = ms;
+  GSK_TRY(join_out(P, caller));
+  return GSK_OK;
+}
+
 static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, double tol, int maxit,
                      double* x, double* hist, gsk_report* rep, cudaStream_t caller) {
   if (!b || !x || !rep || !(tol > 0) || maxit < 1 || m < 1 || m > MAX_M) {
     set_error("gmres: invalid arguments (b, x, rep non-null; tol > 0; maxit >= 1; 1 <= m <= %d)", MAX_M);
     return GSK_E_INVALID;
   }
+  if (P->shards) return shard_gmres_run(P, b, x0, m, tol, maxit, x, hist, rep, caller);
   const size_t n = (size_t)P->A.n;
   if (P->Wm < m) {
     if (P->W) GSK_CUDA(cudaFree(P->W));
@@ -144,29 +173,7 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
     GSK_TRY(run_batches(P, P->ggraph, maxc, P->gkernels, &P->gstate->done, kinds, 2));
   }
   GSK_CUDA(cudaEventRecord(P->t1, s));
-  GmresState hs{};
-  GSK_CUDA(cudaMemcpyAsync(&hs, P->gstate, sizeof hs, cudaMemcpyDeviceToHost, s));
-  GSK_CUDA(cudaStreamSynchronize(s));
-  std::vector<double> H(hs.hist_len);
-  GSK_CUDA(cudaMemcpy(H.data(), P->hist_d, sizeof(double) * hs.hist_len, cudaMemcpyDeviceToHost));
-  if (hist) std::copy(H.begin(), H.end(), hist);
-  float ms = 0;
-  GSK_CUDA(cudaEventElapsedTime(&ms, P->t0, P->t1));
-  rep->status = hs.status;
-  rep->iterations = hs.it;
-  rep->restarts = hs.restarts;
-  rep->history_len = hs.hist_len;
-  rep->breakdown_at = 0;
-  rep->pad_ = 0;
-  rep->relres = H.back();
-  rep->true_relres = hs.true_rel;
-  rep->true_relres_w = hs.true_rel_w;
-  double best = H[0];
-  for (double v : H) best = std::min(best, v);
-  rep->best_relres = best;
-  rep->solve_ms = ms;
-  GSK_TRY(join_out(P, caller));
-  return GSK_OK;
+  return gmres_report(P, hist, rep, caller);
 }
 
 }  // namespace gsk

@@ -35,6 +35,12 @@ extern std::atomic<int64_t> g_launches;
     }                                           \
   } while (0)
 
+#define GSK_TRY(x)              \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_ != GSK_OK) return rc_; \
+  } while (0)
+
 struct Geometry {
   int n = 0;
 };
@@ -58,6 +64,8 @@ struct GmresState {
 };
 
 cudaStream_t as_stream(void* s);
+struct ShardSet;  // row-block shards of a plan (shard.cu)
+void shard_destroy(ShardSet* S);
 
 }  // namespace gsk
 
@@ -83,6 +91,7 @@ struct gsk_plan {
   int* dict = nullptr;
   int64_t ndict = 0;
   int sell_index = 0;       // 0 auto (dictionary when applicable), 1 plain
+  int sell_pad = -1;        // padding column value (INT_MIN in shard plans)
   // reduction scratch
   double* part = nullptr;      // [MAXD][pstride] CTA partials of the current pass
   int pstride = 0;             // >= number of CTAs of any pass (ceil(n/256))
@@ -126,6 +135,7 @@ struct gsk_plan {
   double probe_ms[NPROBE] = {};
   int64_t probe_n[NPROBE] = {};
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  gsk::ShardSet* shards = nullptr;  // non-null: a row-block sharded plan (shard.cu)
 };
 
 namespace gsk {
@@ -152,12 +162,12 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-// Launch one pass: an SpMV pass in the plan's format (CSR or SELL) or a vector pass,
-// then (if it reduces dot products) the single-CTA finish kernel.  pe0/pe1: optional
-// probe events recorded around the pass kernel itself (graph capture: external
-// event nodes).  Returns the number of kernels launched (or a negative error).
+// Launch one pass kernel: an SpMV pass in the plan's format (CSR or SELL) or a vector
+// pass; *ntiles_out receives its CTA count (= CTA partials per dot).  pe0/pe1: optional
+// probe events recorded around the kernel (graph capture: external event nodes).
 template <class Op>
-int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullptr, cudaEvent_t pe1 = nullptr) {
+int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cudaEvent_t pe0 = nullptr,
+                cudaEvent_t pe1 = nullptr) {
   const int n = P->geo.n;
   const int sms = num_sms();
   int ntiles;
@@ -186,6 +196,16 @@ int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullpt
   }
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
+  *ntiles_out = ntiles;
+  return GSK_OK;
+}
+
+// One pass and, when it reduces dot products, the single-CTA finish kernel.  Returns
+// the number of kernels launched (or a negative error).
+template <class Op>
+int run_pass(gsk_plan* P, const Op& op, cudaStream_t s, cudaEvent_t pe0 = nullptr, cudaEvent_t pe1 = nullptr) {
+  int ntiles = 0;
+  GSK_TRY(launch_pass(P, op, s, &ntiles, pe0, pe1));
   if constexpr (Op::D > 0) {
     GSK_CUDA(launch_k(finish_kernel<Op>, 1, FIN_THREADS, 0, s, op, P->part, P->pstride, ntiles));
     GSK_LAUNCHED(1);
@@ -217,12 +237,6 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
   return 2;
 }
 
-#define GSK_TRY(x)              \
-  do {                          \
-    int rc_ = (x);              \
-    if (rc_ != GSK_OK) return rc_; \
-  } while (0)
-
 int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
 int sell_dict_build(gsk_plan* P, cudaStream_t s);
@@ -232,6 +246,14 @@ int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, doubl
 int small_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x);
 int small_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h);
 int ensure_hist(gsk_plan* P, int maxit);
+int bicgstab_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller);
+int gmres_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller);
+int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_plan** plan, cudaStream_t s);
+int shard_bicgstab_run(gsk_plan* P, const double* b, const double* x0, double tol, int maxit, double* x,
+                       double* hist, gsk_report* rep, cudaStream_t caller);
+int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, double tol, int maxit, double* x,
+                    double* hist, gsk_report* rep, cudaStream_t caller);
+int shard_refresh(gsk_plan* P, cudaStream_t s);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).
 int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels, const char* what);

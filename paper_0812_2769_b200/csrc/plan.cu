@@ -261,6 +261,13 @@ int64_t gsk_launch_count(void) { return g_launches.load(); }
 int gsk_version(void) { return 1; }
 
 int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, void* stream) {
+  return plan_create_impl(A, opts, -1, plan, as_stream(stream));
+}
+
+}  // extern "C"
+
+namespace gsk {
+int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_plan** plan, cudaStream_t stream) {
   GSK_TRY(check_csr(A, "gsk_plan_create"));
   if (!plan) {
     set_error("gsk_plan_create: plan is NULL");
@@ -274,6 +281,7 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
   gsk_plan* P = new gsk_plan();
   P->A = *A;
   P->fmt = fmt;
+  P->sell_pad = sell_pad;
   P->poll = opts ? opts->poll : 0;
   P->weights = opts ? opts->weights : nullptr;
   const int sched = opts ? opts->bicg_schedule : GSK_BICG_AUTO;
@@ -304,7 +312,7 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
   }
   int rc = plan_alloc_common(P);
   if (rc == GSK_OK && fmt == GSK_FMT_SELL) {
-    cudaStream_t s = as_stream(stream);
+    cudaStream_t s = stream;
     rc = join_in(P, s);
     if (rc == GSK_OK) rc = sell_build(P, P->st);
     if (rc == GSK_OK && P->sell_index == 1) rc = sell_dict_build(P, P->st);
@@ -318,9 +326,13 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
   *plan = P;
   return GSK_OK;
 }
+}  // namespace gsk
+
+extern "C" {
 
 int gsk_plan_refresh(gsk_plan* P, void* stream) {
   if (!P) return GSK_E_INVALID;
+  if (P->shards) return shard_refresh(P, as_stream(stream));
   if (P->fmt != GSK_FMT_SELL) return GSK_OK;
   cudaStream_t s = as_stream(stream);
   GSK_TRY(join_in(P, s));
@@ -333,6 +345,7 @@ int gsk_plan_refresh(gsk_plan* P, void* stream) {
 void gsk_plan_destroy(gsk_plan* P) {
   if (!P) return;
   if (P->st) cudaStreamSynchronize(P->st);
+  if (P->shards) shard_destroy(P->shards);
   for (auto g : P->bgraph)
     if (g) cudaGraphExecDestroy(g);
   for (auto g : P->ggraph)
@@ -357,6 +370,10 @@ void gsk_plan_destroy(gsk_plan* P) {
 }
 
 int gsk_plan_spmv(gsk_plan* P, const double* x, double* y, void* stream) {
+  if (P && P->shards) {
+    set_error("gsk_plan_spmv: not available on a sharded plan (use the per-shard solvers)");
+    return GSK_E_INVALID;
+  }
   if (!P || !x || !y) {
     set_error("gsk_plan_spmv: NULL argument");
     return GSK_E_INVALID;
@@ -378,6 +395,10 @@ int gsk_spmv(const gsk_csr* A, const double* x, double* y, void* stream) {
 
 int gsk_plan_residual_norm(gsk_plan* P, const double* b, const double* x, const double* w,
                            double* result, void* stream) {
+  if (P && P->shards) {
+    set_error("gsk_plan_residual_norm: not available on a sharded plan (use the per-shard solvers)");
+    return GSK_E_INVALID;
+  }
   if (!P || !b || !x || !result) {
     set_error("gsk_plan_residual_norm: NULL argument");
     return GSK_E_INVALID;
@@ -417,6 +438,10 @@ int gsk_dot(int64_t n, const double* a, const double* b, double* result, void* s
 }
 
 int gsk_plan_sell_info(gsk_plan* P, int64_t* nchunks, int64_t* nslots) {
+  if (P && P->shards) {
+    set_error("gsk_plan_sell_info: not available on a sharded plan (use the per-shard solvers)");
+    return GSK_E_INVALID;
+  }
   if (!P || P->fmt != GSK_FMT_SELL) {
     set_error("gsk_plan_sell_info: plan is not SELL");
     return GSK_E_INVALID;
@@ -428,6 +453,10 @@ int gsk_plan_sell_info(gsk_plan* P, int64_t* nchunks, int64_t* nslots) {
 
 int gsk_plan_sell_copy(gsk_plan* P, int32_t* chunk_ptr, int32_t* chunk_len, int32_t* scol,
                        double* sval, uint8_t* roff, void* stream) {
+  if (P && P->shards) {
+    set_error("gsk_plan_sell_copy: not available on a sharded plan (use the per-shard solvers)");
+    return GSK_E_INVALID;
+  }
   if (!P || P->fmt != GSK_FMT_SELL) {
     set_error("gsk_plan_sell_copy: plan is not SELL");
     return GSK_E_INVALID;
@@ -445,6 +474,10 @@ int gsk_plan_sell_copy(gsk_plan* P, int32_t* chunk_ptr, int32_t* chunk_len, int3
 
 int gsk_plan_sell_dict(gsk_plan* P, int64_t* ndict, int32_t* dict_ptr, int32_t* dict, uint8_t* sidx,
                        void* stream) {
+  if (P && P->shards) {
+    set_error("gsk_plan_sell_dict: not available on a sharded plan (use the per-shard solvers)");
+    return GSK_E_INVALID;
+  }
   if (!P || P->fmt != GSK_FMT_SELL) {
     set_error("gsk_plan_sell_dict: plan is not SELL");
     return GSK_E_INVALID;

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(1024) sell_scan_kernel(int nchunks, const int*
 __global__ void __launch_bounds__(TB) sell_fill_kernel(int n, int nchunks, const int* __restrict__ rp,
                                                        const int* __restrict__ ci, const double* __restrict__ v,
                                                        const int* __restrict__ cptr, const uint8_t* __restrict__ roff,
-                                                       int* scol, double* sval, bool values_only) {
+                                                       int* scol, double* sval, bool values_only, int pad) {
   const int w = blockIdx.x, t = threadIdx.x, lane = t & 31;
   const int c = w * (TB / SELL_C) + (t >> 5);
   if (c >= nchunks) return;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(TB) sell_fill_kernel(int n, int nchunks, const
       if (!values_only) scol[slot] = ci[a + k];
       sval[slot] = v[a + k];
     } else {
-      if (!values_only) scol[slot] = -1;
+      if (!values_only) scol[slot] = pad;
       sval[slot] = 0.0;
     }
   }
@@ -98,9 +98,9 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&P->scol, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
   GSK_CUDA(cudaMalloc(&P->sval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
-                                       P->cptr, P->roff, P->scol, P->sval, false);
+                                       P->cptr, P->roff, P->scol, P->sval, false, P->sell_pad);
   GSK_LAUNCHED(1);
-  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr};
+  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr, P->sell_pad};
   return GSK_OK;
 }
 
@@ -112,7 +112,7 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
 __global__ void __launch_bounds__(TB) sell_dict_kernel(int nchunks, const int* __restrict__ cptr,
                                                        const int* __restrict__ scol, const uint8_t* __restrict__ roff,
                                                        int* ucount, const int* __restrict__ dptr, int* dict,
-                                                       uint8_t* sidx, int* fail, int pass) {
+                                                       uint8_t* sidx, int* fail, int pass, int pad) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (TB / 32) + (threadIdx.x >> 5);
   if (c >= nchunks) return;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(TB) sell_dict_kernel(int nchunks, const int* _
     long long mine = LLONG_MAX;
     for (int k = 0; k < L; ++k) {
       const int col = scol[p0 + k * SELL_C + lane];
-      if (col >= 0) {
+      if (col != pad) {
         const long long d = (long long)col - row;
         if (d > last && d < mine) mine = d;
       }
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(TB) sell_dict_kernel(int nchunks, const int* _
     const int d = (int)((long long)col - row);
     int pos = 0;
     for (int u = 0; u < U; ++u) pos += __shfl_sync(0xffffffffu, dv, u) < d;  // lower bound
-    sidx[slot] = col >= 0 ? (uint8_t)pos : (uint8_t)255;
+    sidx[slot] = col != pad ? (uint8_t)pos : (uint8_t)255;
   }
 }
 
@@ -168,7 +168,7 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&fail, sizeof(int)));
   GSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
   GSK_CUDA(cudaMalloc(&P->dptr, sizeof(int) * (nch + 1)));
-  sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, nullptr, nullptr, nullptr, fail, 0);
+  sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, nullptr, nullptr, nullptr, fail, 0, P->sell_pad);
   GSK_LAUNCHED(1);
   int hfail = 0;
   GSK_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -188,7 +188,7 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
   P->ndict = tot;
   GSK_CUDA(cudaMalloc(&P->dict, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
   GSK_CUDA(cudaMalloc(&P->sidx, (size_t)(P->nslots > 0 ? P->nslots : 1)));
-  sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, P->dptr, P->dict, P->sidx, fail, 1);
+  sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, P->dptr, P->dict, P->sidx, fail, 1, P->sell_pad);
   GSK_LAUNCHED(1);
   GSK_CUDA(cudaStreamSynchronize(s));
   cudaFree(ucount);
@@ -203,7 +203,7 @@ int sell_fill_values(gsk_plan* P, cudaStream_t s) {
   const int n = P->A.n;
   const int nwin = (n + TB - 1) / TB;
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
-                                       P->cptr, P->roff, P->scol, P->sval, true);
+                                       P->cptr, P->roff, P->scol, P->sval, true, P->sell_pad);
   GSK_LAUNCHED(1);
   return GSK_OK;
 }

@@ -362,3 +362,63 @@ def test_two_sided_scaling_parity(name, N, p):
     o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-9, 500)
     assert_same_solve(g, o)
     assert np.array_equal(cpu(gsk.gs_unscale(sv, g[0])), oracle.unscale(so, o[0]))
+
+
+# ---------------------------------------------------------------- row-block shards (f4)
+SHARDED = [("C1", None, 2), ("C1", None, 8), ("C2", 64, 4), ("C3", 16, 4), ("C4", 24, 2), ("C4", 24, 4),
+           ("C5", 64, 2), ("P1", 64, 8)]
+
+
+@pytest.mark.parametrize("name,N,P", SHARDED)
+def test_sharded_parity(name, N, P):
+    """All P shards on this GPU (halo exchange by device copies, shard values gathered
+    and joined by the top of the canonical tree): Bi-CGSTAB and MGS
+    GMRES bit-identical to the oracle, CSR and SELL shards, weights and x0."""
+    s, val, b, _ = system(name, N, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    ob = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 500)
+    og = oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 200)
+    for fmt in ("csr", "sell"):
+        SP = gsk.ShardedPlan(A, shards=P, fmt=fmt)
+        assert_same_solve(SP.bicgstab(b, tol=1e-9, maxit=500), ob)
+        assert_same_solve(SP.gmres(b, m=20, tol=1e-9, maxit=200), og)
+        SP.close()
+    w = workloads.uniform(s["n"], 5, 6) + 1.5
+    x0 = workloads.uniform(s["n"], 7, 8)
+    SP = gsk.ShardedPlan(A, shards=P, weights=w)
+    assert_same_solve(SP.bicgstab(b, x0=x0, tol=1e-9, maxit=500),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 500, x0=x0, weights=w))
+    assert_same_solve(SP.gmres(b, x0=x0, m=7, tol=1e-9, maxit=200),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, 7, 1e-9, 200, x0=x0, weights=w))
+
+
+def test_sharded_rejections():
+    s = workloads.generate("C5", N=64)
+    with pytest.raises(gsk.GskError):  # permuted: halos beyond the adjacent shards
+        gsk.ShardedPlan(gsk.CSR.from_system(s), shards=8)
+    s = workloads.generate("C1")
+    SP = gsk.ShardedPlan(gsk.CSR.from_system(s), shards=2)
+    SP.close()
+    with pytest.raises(gsk.GskError):
+        gsk.ShardedPlan(gsk.CSR.from_system(s), shards=3)
+
+
+def test_sharded_full_c4_matches_unsharded():
+    """C4 at full size in 8 SELL shards on one GPU: the first 30 Bi-CGSTAB iterations
+    and 35 GMRES(30) steps are bit-identical to the unsharded plan (itself bit-exact
+    with the oracle, test_full_size_parity)."""
+    s = workloads.generate("C4")
+    A0 = gsk.CSR.from_system(s)
+    As, bs, _ = gsk.gs_scale(A0, s["b"], 2)
+    P1 = gsk.Plan(As, fmt="sell")
+    g1 = P1.bicgstab(bs, tol=1e-8, maxit=30)
+    h1 = P1.gmres(bs, m=30, tol=1e-8, maxit=35)
+    P1.close()
+    SP = gsk.ShardedPlan(As, shards=8, fmt="sell")
+    g8 = SP.bicgstab(bs, tol=1e-8, maxit=30)
+    h8 = SP.gmres(bs, m=30, tol=1e-8, maxit=35)
+    for a, c in ((g1, g8), (h1, h8)):
+        assert np.array_equal(a[1], c[1])
+        assert torch.equal(a[0], c[0])
+        for k in ("status", "iterations", "relres", "true_relres"):
+            assert a[2][k] == c[2][k]
