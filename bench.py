@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
     ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
                     help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
+    ap.add_argument("--shards", type=int, default=0,
+                    help="row-block sharded solve (DESIGN.md §8): with one process, P shards emulated on "
+                         "one GPU (the cost of sharding); under torchrun, one shard per rank over NCCL "
+                         "(strong scaling).  0 = the default replicated step")
     return ap.parse_args()
 
 
@@ -201,6 +205,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+
+    if args.shards:
+        run_sharded(args, rank, world, local)
         return
 
     import torch
@@ -365,6 +373,106 @@ def main():
             "clocks": clk, "extra": extra,
         }
         print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_sharded(args, rank, world, local):
+    """--shards: ONE system split into row blocks.  world == 1: all
+    shards on this GPU (halo exchange by device copies); world > 1: one shard per rank,
+    halos and reductions over NCCL, timing max over ranks, value = iterations of the one
+    solve per second ("scaling": "strong")."""
+    import torch
+    import paper_0812_2769_b200 as gsk
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = world if world > 1 else args.shards
+    cfg = workloads.CONFIGS[args.config]
+    m, gmaxit = 30, args.gmres_maxit
+    s = workloads.generate(args.config, N=args.N)
+    A0 = gsk.CSR.from_system(s)
+    b0 = torch.tensor(s["b"], device="cuda")
+    vbuf, bbuf, dbuf = torch.empty_like(A0.val), torch.empty_like(b0), torch.empty_like(b0)
+    As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
+    fmt = "sell" if cfg.sell else "csr"
+    comm = gsk.NcclComm() if world > 1 else None
+    SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
+    lo, hi = SP.rows
+    bl = bbuf[lo:hi]
+    x1 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+    x2 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+
+    def step():
+        gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
+        SP.refresh()
+        _, _, r1 = SP.bicgstab(bl, tol=cfg.tol, maxit=cfg.maxit, x=x1, hist=False)
+        _, _, r2 = SP.gmres(bl, m=m, tol=cfg.tol, maxit=gmaxit, x=x2, hist=False)
+        return r1["iterations"] + r2["iterations"], r1, r2
+
+    for _ in range(args.warmup):
+        step()
+    probes0 = [SP.probe(k) for k in range(4)]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks(local) if os.environ.get("GSK_BENCH_NO_CLOCKS") != "1" else None
+    launches0 = gsk.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its, reps = 0, []
+    for _ in range(args.steps):
+        k, r1, r2 = step()
+        its += k
+        reps.append((r1, r2))
+    e1.record()
+    torch.cuda.synchronize()
+    launches = gsk.launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    # roofline: shard 0's v = A p pass (probe 0) against its own rows' bytes
+    l0, h0 = gsk.shard_rows(s["n"], P, rank if world > 1 else 0)
+    nnz0 = int(s["row_ptr"][h0] - s["row_ptr"][l0])
+    tot, cnt = SP.probe(0)
+    t0, c0 = probes0[0]
+    p_ms = (tot * cnt - t0 * c0) / (cnt - c0) if cnt > c0 else None
+    bm = byte_model(h0 - l0, nnz0)
+    hbm, src = peaks()
+    roof = None
+    if p_ms:
+        ach = bm["bicg_s1"] / (p_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "kernel": "pass_kernel<SELL, OpS1> of one shard (v = A p, <r^,v>)", "bytes_per_launch": bm["bicg_s1"],
+                "ms_per_launch": p_ms, "peak_source": src}
+    if rank == 0:
+        r1, r2 = reps[-1]
+        line = {
+            "metric": "solver iters/s (GS(2)+Bi-CGSTAB+GMRES(30) step, C4 256^3, row-block sharded)",
+            "value": its / (ms / 1e3), "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "none (emulated shards on one GPU)",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**config_desc(args, cfg, s), "parallelism": f"rows/{P}", "shards": P,
+                       "placement": f"{world} GPUs, NCCL halos + all-gathers" if world > 1
+                       else "all shards on one GPU (device-copy halos)"},
+            "roofline": roof, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk,
+            "extra": {"bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
+                                   "solve_ms": r1["solve_ms"]},
+                      "gmres": {"iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
+                                "solve_ms": r2["solve_ms"]}},
+        }
+        print(json.dumps(line), flush=True)
+    SP.close()
+    if comm:
+        comm.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
