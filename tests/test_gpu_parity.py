@@ -422,3 +422,16 @@ def test_sharded_full_c4_matches_unsharded():
         assert torch.equal(a[0], c[0])
         for k in ("status", "iterations", "relres", "true_relres"):
             assert a[2][k] == c[2][k]
+
+
+def test_nccl_plumbing_single_rank():
+    """The NCCL entry points the multi-process shards use (libnccl.so.2 loaded at run
+    time next to torch's): unique id, a 1-rank communicator, destroy."""
+    import ctypes
+    lib = gsk.load()
+    buf = ctypes.create_string_buffer(128)
+    assert lib.gsk_nccl_unique_id(buf) == 0
+    h = ctypes.c_void_p()
+    assert lib.gsk_nccl_comm_create(ctypes.c_char_p(bytes(buf.raw)), 1, 0, ctypes.byref(h)) == 0
+    assert h.value
+    assert lib.gsk_nccl_comm_destroy(h) == 0
