@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
     ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
                     help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
+    ap.add_argument("--fmt", default="sell", choices=["csr", "sell"],
+                    help="plan layout built on the device from the CSR input (SELL-C-32-256 is faster "
+                         "on every config: DESIGN.md §7)")
     ap.add_argument("--shards", type=int, default=0,
                     help="row-block sharded solve (DESIGN.md §8): with one process, P shards emulated on "
                          "one GPU (the cost of sharding); under torchrun, one shard per rank over NCCL "
@@ -191,7 +194,8 @@ def reduce_over_ranks(ms, its, dist, device):
 def config_desc(args, cfg, s):
     return {"workload": f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", "n": int(s["n"]),
             "nnz": int(s["nnz"]), "grid": f"{cfg.N if args.N is None else args.N}^{3 if cfg.cfg in (3, 4) else 2}",
-            "format": "SELL-C-32-256" if cfg.sell else "CSR", "scaling": "GS(2)",
+            "format": ("SELL-C-32-256" if getattr(args, "fmt", "sell") == "sell" else "CSR")
+            + " (built on the device from the CSR input)", "scaling": "GS(2)",
             "solvers": ["Bi-CGSTAB to tol (maxit %d)" % cfg.maxit,
                         "GMRES(30) for %d iterations (or to tol)" % args.gmres_maxit],
             "tol": cfg.tol, "seed": cfg.seed,
@@ -230,7 +234,7 @@ def main():
     bbuf = torch.empty_like(b0)
     dbuf = torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
-    fmt = "sell" if cfg.sell else "csr"
+    fmt = args.fmt
     plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth)
     x1 = torch.empty(n, dtype=torch.float64, device="cuda")
     x2 = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -399,7 +403,7 @@ def run_sharded(args, rank, world, local):
     b0 = torch.tensor(s["b"], device="cuda")
     vbuf, bbuf, dbuf = torch.empty_like(A0.val), torch.empty_like(b0), torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
-    fmt = "sell" if cfg.sell else "csr"
+    fmt = args.fmt
     comm = gsk.NcclComm() if world > 1 else None
     SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
     lo, hi = SP.rows

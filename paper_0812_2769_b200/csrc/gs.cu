@@ -86,10 +86,6 @@ __global__ void __launch_bounds__(TB, 8) gs_kernel(int n, const int* __restrict_
 }
 
 // a'_ij = (a_ij * s_i) * s_j, b'_i = b_i * s_i (reading S1)
-__device__ __forceinline__ void cp_async4(int* smem, const int* g) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
-}
 
 // Staged like gs_kernel: the 256-row window's values and columns arrive in shared
 // memory with cp.async, each thread scales its row there (the column factor is a
