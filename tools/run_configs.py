@@ -64,7 +64,7 @@ def run(name, maxit_gmres=None):
             if solver == "gmres" and m == 30 and c.m == 30 and any(r["solver"] == "gmres(30)" and
                                                                    r["scaling"] == str(scaling) for r in rows):
                 continue
-            P = gsk.Plan(A, fmt=fmt, weights=w if solver == "bicgstab" else None)
+            P = gsk.Plan(A, fmt="sell", weights=w if solver == "bicgstab" else None)
             maxit = c.maxit if solver == "bicgstab" else (maxit_gmres or c.maxit)
             if solver == "bicgstab":
                 x, h, rep = P.bicgstab(b, tol=min(tols), maxit=maxit)
@@ -73,7 +73,7 @@ def run(name, maxit_gmres=None):
             tr2 = None
             if solver == "gmres" and scaling != 2:
                 # report the GS(2)-frame true residual
-                Pw = gsk.Plan(A, fmt=fmt)
+                Pw = gsk.Plan(A, fmt="sell")
                 r0 = Pw.residual_norm(b, torch.zeros_like(b), w)
                 tr2 = Pw.residual_norm(b, x, w) / r0
             its = {str(t): first(h, t) for t in tols}
