@@ -52,7 +52,8 @@ def parse():
                     help="GMRES(30) iteration budget per step (10 restart cycles; DESIGN.md §7)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extras", action="store_true", help="also time-to-tol without GS / with GS(1)")
+    ap.add_argument("--no-time-to-tol", action="store_true",
+                    help="skip the time-to-tolerance runs (Bi-CGSTAB: none / GS(1) / GS(2) / two-sided, ~15 s)")
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
     ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
                     help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
@@ -363,7 +364,7 @@ def main():
         v, its_c, dt, cores = oracle_sample(s, cfg, m)
         cpu = {"value": v, "unit": "iters/s", "cores": cores, "kind": "oracle",
                "sample": f"GS(2) + 8 Bi-CGSTAB its + 8 GMRES(30) steps of {cfg.name} ({dt:.1f} s)"}
-    if args.extras and rank == 0:
+    if not args.no_time_to_tol and rank == 0:
         extra["time_to_tol"] = time_to_tol(gsk, torch, s, cfg, fmt)
 
     if rank == 0:
@@ -521,23 +522,27 @@ def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args):
 
 
 def time_to_tol(gsk, torch, s, cfg, fmt):
-    """Time to cfg.tol with and without GS (north-star metric), Bi-CGSTAB, stopping
-    measured in the GS(2) frame."""
+    """Time to cfg.tol with and without GS (north-star metric): Bi-CGSTAB from the
+    device-resident unscaled system — scaling + plan (SELL build) + solve, CUDA events;
+    stopping measured in the GS(2) frame for every variant."""
     out = {}
     A0 = gsk.CSR.from_system(s)
-    _, _, d2 = gsk.gs_scale(A0, s["b"], 2)
-    for name, p in (("none", None), ("GS1", 1), ("GS2", 2)):
+    b0 = torch.tensor(s["b"], device="cuda")
+    _, _, d2 = gsk.gs_scale(A0, b0, 2)
+    for name, p in (("none", None), ("GS1", 1), ("GS2", 2), ("two-sided GS2", "sym")):
+        A = gsk.CSR(A0.row_ptr, A0.col, A0.val.clone())
+        b = b0.clone()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        A = gsk.CSR.from_system(s)
-        b = torch.tensor(s["b"], device="cuda")
         w = d2
-        if p is not None:
+        if p == "sym":
+            A, b, w = gsk.gs_scale_sym(A, b, 2)  # GS(2) frame: D r = D^1/2 r_sym
+        elif p is not None:
             A, b, dp = gsk.gs_scale(A, b, p, inplace=True)
             w = None if p == 2 else d2 / dp
         P = gsk.Plan(A, fmt=fmt, weights=w)
-        _, h, r = P.bicgstab(b, tol=cfg.tol, maxit=cfg.maxit)
+        _, h, r = P.bicgstab(b, tol=cfg.tol, maxit=cfg.maxit, hist=False)
         e1.record()
         torch.cuda.synchronize()
         out[name] = {"ms": e0.elapsed_time(e1), "iterations": r["iterations"],
