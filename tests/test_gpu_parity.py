@@ -435,3 +435,23 @@ def test_nccl_plumbing_single_rank():
     assert lib.gsk_nccl_comm_create(ctypes.c_char_p(bytes(buf.raw)), 1, 0, ctypes.byref(h)) == 0
     assert h.value
     assert lib.gsk_nccl_comm_destroy(h) == 0
+
+
+def test_bench_sharded_line():
+    """bench.py --shards (emulated on one GPU): one JSON line, the sharded solve converges
+    with the unsharded iteration count."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GSK_BENCH_NO_CLOCKS="1")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "C3", "--N", "32",
+                          "--shards", "4", "--steps", "1", "--warmup", "1"], capture_output=True, text=True,
+                         check=True, timeout=600, env=env).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    assert line["config"]["shards"] == 4 and line["value"] > 0 and line["gpu_launches"] > 0
+    s = workloads.generate("C3", N=32)
+    _, vo, bo, _ = system("C3", 32, 2)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, workloads.CONFIGS["C3"].tol, 10000)
+    assert line["extra"]["bicgstab"]["iterations"] == o[2]["iterations"]
