@@ -124,7 +124,8 @@ def byte_model(n, nnz):
             # split schedule: S1 v = A p (p gather, r^, v), S3 t = A s (s gather, t)
             "bicg_s1": BA + 24 * n, "bicg_s3": BA + 16 * n,
             "bicg_iter": 2 * BA + 17 * 8 * n, "bicg_iter_split": 2 * BA + 19 * 8 * n,
-            "gmres_mgs": 32 * n, "gmres_arnoldi": BA + 24 * n}
+            # GMRES S_j: w = A v_j as a plain SpMV pass (its h_1j dot is a separate pass)
+            "gmres_mgs": 32 * n, "gmres_arnoldi": BA + 16 * n}
 
 
 def oracle_sample(sys_, cfg, m, kb=8, kg=8):

@@ -40,8 +40,10 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
     if (rc >= 0) rc = run_mdot(P, c, 1, s);
   }
   for (int j = 1; j <= m && rc >= 0 && P->orth == 0; ++j) {
-    OpArnoldi<> a{slot(j), slot(1), slot(j + 1), st, j, 0, 0};
+    // S_j as a plain SpMV pass (w = A v_j) + the h_1j dot pass (OpH1)
+    OpCgsS a{slot(j), slot(j + 1), st, j, 0};
     rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
+    if (rc >= 0) rc = run_pass(P, OpH1{slot(j + 1), slot(1), st, j, 0}, s);
     for (int i = 1; i < j && rc >= 0; ++i) {
       OpMgs mg{slot(i), slot(i + 1), slot(j + 1), st, i, j, 0, 0, 0};
       rc = (j == 2 && i == 1) ? run_pass(P, mg, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_pass(P, mg, s);
