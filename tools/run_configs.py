@@ -78,6 +78,14 @@ def run(name, maxit_gmres=None):
                 tr2 = Pw.residual_norm(b, x, w) / r0
             its = {str(t): first(h, t) for t in tols}
             ms = rep["solve_ms"]
+            n, nnz = s["n"], s["nnz"]
+            ba = 12 * nnz + 4 * (n + 1)
+            # algorithmic bytes per iteration: Bi-CGSTAB split schedule 2 B_A + 19 vectors;
+            # MGS GMRES(m) averaged over a cycle: step j moves B_A + (4j + 3) vectors (S_j, h_1j, j-1 M, L),
+            # the restart (X, R) B_A + (m + 5) vectors per m steps
+            bpi = (2 * ba + 19 * 8 * n) if solver == "bicgstab" else \
+                (ba * (1 + 1 / m) + (2 * (m + 1) + 3 + (m + 5) / m) * 8 * n)
+            its_done = max(rep["iterations"], 1)
             rows.append({
                 "config": name, "scaling": str(scaling), "solver": f"{solver}" + (f"({m})" if m else ""),
                 "status": gsk.STATUS[rep["status"]], "iterations": rep["iterations"], "its_to_tol": its,
@@ -85,6 +93,7 @@ def run(name, maxit_gmres=None):
                 "true_relres_gs2_frame": tr2 if tr2 is not None else rep["true_relres_w"],
                 "solve_ms": ms, "gs_ms": gs_ms,
                 "ms_per_iter": ms / max(rep["iterations"], 1),
+                "gbps_model": bpi * its_done / (ms / 1e3) / 1e9 if ms else None,
                 "time_to_tightest_ms": (gs_ms + ms) if rep["status"] == 0 else None,
             })
             print(json.dumps(rows[-1]), flush=True)
@@ -93,12 +102,13 @@ def run(name, maxit_gmres=None):
 
 
 def markdown(rows):
-    out = ["| config | scaling | solver | verdict | its to tol | best rel-res | solve ms | ms/it | GS ms |",
-           "|---|---|---|---|---|---|---|---|---|"]
+    out = ["| config | scaling | solver | verdict | its to tol | best rel-res | solve ms | ms/it | GB/s (model) | GS ms |",
+           "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         its = ", ".join(f"{k}: {v if v is not None else '—'}" for k, v in r["its_to_tol"].items())
         out.append(f"| {r['config']} | {r['scaling']} | {r['solver']} | {r['status']} ({r['iterations']}) | {its} | "
-                   f"{r['best_relres']:.2e} | {r['solve_ms']:.1f} | {r['ms_per_iter']:.3f} | {r['gs_ms']:.2f} |")
+                   f"{r['best_relres']:.2e} | {r['solve_ms']:.1f} | {r['ms_per_iter']:.3f} | {r['gbps_model']:.0f} | "
+                   f"{r['gs_ms']:.2f} |")
     return "\n".join(out) + "\n"
 
 
