@@ -41,18 +41,18 @@ template <int FMT>
 struct PassSmem;
 template <>
 struct PassSmem<0> {
-  double wp[8 * MAXD * 8];  // [window][d][warp]
+  double wp[16 * MAXD * 8];  // [window][d][warp]
 };
 constexpr int ASYNC_NV = 2;  // own-row operands prefetched with cp.async (SpMV passes)
 template <>
 struct PassSmem<1> {
   CsrStage st[2];
-  double wp[8 * MAXD * 8];
+  double wp[16 * MAXD * 8];
 };
 template <>
 struct PassSmem<2> {
   double sy[2][TB];
-  double wp[8 * MAXD * 8];
+  double wp[16 * MAXD * 8];
   double vin[2][ASYNC_NV][TB];
 };
 template <>
@@ -199,45 +199,51 @@ __device__ __forceinline__ void load_vin(const Op& op, int i, double (&v)[Op::NV
 }
 
 // Warp butterflies of one window's leaves (= trees of 32 leaves); lane 0 records the
-// warp's value.
+// warp's value.  Two dots share the first level: even lanes keep dot 0, odd lanes dot
+// 1 (each lane adds its partner's value of the dot it keeps: the same pairs (2i, 2i+1)
+// and IEEE addition commutes), so a pair costs 6 shuffles instead of 10.
 template <int D>
 __device__ __forceinline__ void warp_leaves(double (&c)[D], double* wp, int w) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (D == 2) {
+    const bool odd = lane & 1;
+    const double give = odd ? c[0] : c[1];
+    const double keep = odd ? c[1] : c[0];
+    double u = keep + __shfl_xor_sync(0xffffffffu, give, 1);
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
+    for (int off = 2; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+    if (lane < 2) wp[(w * MAXD + lane) * 8 + warp] = u;
+  } else {
 #pragma unroll
-    for (int d = 0; d < D; ++d) c[d] = c[d] + __shfl_xor_sync(0xffffffffu, c[d], off);
-  }
-  if (lane == 0) {
+    for (int off = 1; off < 32; off <<= 1) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) wp[(w * MAXD + d) * 8 + warp] = c[d];
+      for (int d = 0; d < D; ++d) c[d] = c[d] + __shfl_xor_sync(0xffffffffu, c[d], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) wp[(w * MAXD + d) * 8 + warp] = c[d];
+    }
   }
 }
 
-// Warp 0, after a __syncthreads: trees of 8 warps per window, then the tree over the
-// CTA's windows; lane 0 writes the CTA partial.  Windows beyond nw (pow2 <= 8) enter
-// as +0 leaves: x + 0 = x, and the final + 0.0 of AC-5 canonicalises a zero's sign.
+// Warp 0, after a __syncthreads: lane w builds window w's tree over its 8 warp values,
+// a butterfly over lanes 0..WMAX-1 joins the windows pairwise, lane 0 writes the CTA
+// partial.  Windows beyond nw (pow2 <= WMAX) enter as +0 leaves: x + 0 = x, and the
+// final + 0.0 of AC-5 canonicalises a zero's sign.
+constexpr int WMAX = 16;  // windows per CTA (SpMV passes, GSK_WPC)
 template <int D>
 __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* part, int stride) {
   const int lane = threadIdx.x & 31;
-  double a[D][8];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      double u = (lane < 8 && w < nw) ? wp[(w * MAXD + d) * 8 + lane] : 0.0;
-      u = u + __shfl_xor_sync(0xffffffffu, u, 1);
-      u = u + __shfl_xor_sync(0xffffffffu, u, 2);
-      u = u + __shfl_xor_sync(0xffffffffu, u, 4);
-      a[d][w] = u;
+  for (int d = 0; d < D; ++d) {
+    double u = 0.0;
+    if (lane < nw) {
+      const double* v = wp + (lane * MAXD + d) * 8;
+      u = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
     }
-  }
-  if (lane == 0) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const double s = ((a[d][0] + a[d][1]) + (a[d][2] + a[d][3])) + ((a[d][4] + a[d][5]) + (a[d][6] + a[d][7]));
-      part[(size_t)d * stride + blockIdx.x] = s;
-    }
+    for (int off = 1; off < WMAX; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+    if (lane == 0) part[(size_t)d * stride + blockIdx.x] = u;
   }
 }
 
@@ -337,8 +343,58 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
 // change them).
 // Canonical tree of D dot products over ntiles CTA partials (+ 0.0), valid in warp 0
 // (every lane).  Body of the finish kernels; blockDim = FIN_THREADS.
+// One round of LV partials per thread over the canonical tree (no round loop):
+// thread t's LV leaves, a register tree, warp butterflies, the tree of 32 warps.
+template <int D, int LV>
+__device__ __forceinline__ void fin_one_round(const double* part, int stride, int ntiles, double (&s)[D]) {
+  __shared__ double wsr[D][32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int base = t * LV;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double l[LV];
+    if (base + LV <= ntiles) {
+      const double2* q = reinterpret_cast<const double2*>(part + (size_t)d * stride + base);
+#pragma unroll
+      for (int h = 0; h < LV / 2; ++h) {
+        const double2 x = q[h];
+        l[2 * h] = x.x;
+        l[2 * h + 1] = x.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < LV; ++q) l[q] = base + q < ntiles ? part[(size_t)d * stride + base + q] : 0.0;
+    }
+#pragma unroll
+    for (int len = LV; len > 1; len >>= 1) {
+#pragma unroll
+      for (int q = 0; q < len / 2; ++q) l[q] = l[2 * q] + l[2 * q + 1];
+    }
+    double u = l[0];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+    if (lane == 0) wsr[d][warp] = u;
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double x = wsr[d][lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) x = x + __shfl_xor_sync(0xffffffffu, x, off);
+      s[d] = x + 0.0;
+    }
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void fin_tree(const double* part, int stride, int ntiles, double (&s)[D]) {
+  // up to 16384 partials (vector passes with 4 rows per thread at C4): one round of
+  // 16 leaves per thread instead of two rounds joined by the binary counter
+  if (ntiles > FIN_ROUND && ntiles <= 2 * FIN_ROUND) {
+    fin_one_round<D, 2 * FIN_LEAVES>(part, stride, ntiles, s);
+    return;
+  }
   __shared__ double ws[D][32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   double stk[D][12];

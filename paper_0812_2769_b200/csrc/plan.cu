@@ -42,7 +42,7 @@ int spmv_wpc_max() {
   if (!w) {
     const char* e = std::getenv("GSK_WPC");
     w = e ? std::atoi(e) : 8;
-    if (w != 1 && w != 2 && w != 4 && w != 8) w = 8;
+    if (w != 1 && w != 2 && w != 4 && w != 8 && w != 16) w = 8;
   }
   return w;
 }
