@@ -226,6 +226,44 @@ __device__ __forceinline__ void warp_leaves(double (&c)[D], double* wp, int w) {
   }
 }
 
+// The same warp trees for all RPT x D leaves of a vector pass at once, as a
+// reduce-scatter: at level l (partner lane ^ 2^l) every lane keeps half of its
+// remaining values and adds its partner's copies of them (the canonical pairs, IEEE
+// addition commutes), so K = RPT * D values cost K/2 + K/4 + ... + 1 shuffles, then the
+// remaining levels one each, instead of 5 K.  Afterwards lane l (l < K) holds value
+// bitreverse(l) of the K (window-major, dot-minor), which it records.
+template <int RPT, int D>
+__device__ __forceinline__ void warp_leaves_multi(double (&c)[RPT][D], double* wp) {
+  constexpr int K0 = RPT * D;
+  constexpr int K = K0 <= 1 ? 1 : K0 <= 2 ? 2 : K0 <= 4 ? 4 : K0 <= 8 ? 8 : K0 <= 16 ? 16 : 32;
+  static_assert(K0 <= 32, "at most 32 leaves per lane");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) v[q] = q < K0 ? c[q / D][q % D] : 0.0;
+  int off = 1;
+#pragma unroll
+  for (int len = K; len > 1; len >>= 1, off <<= 1) {
+    const bool hi = lane & off;
+#pragma unroll
+    for (int q = 0; q < len / 2; ++q) {
+      const double send = hi ? v[q] : v[q + len / 2];
+      const double keep = hi ? v[q + len / 2] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  double u = v[0];
+#pragma unroll
+  for (; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+  if (lane < K) {
+    int idx = 0;  // the value this lane kept: bit l of the lane selects the upper half at level l
+#pragma unroll
+    for (int b = 0, h = K / 2; h >= 1; ++b, h >>= 1)
+      if (lane & (1 << b)) idx += h;
+    if (idx < K0) wp[((idx / D) * MAXD + idx % D) * 8 + warp] = u;
+  }
+}
+
 // Warp 0, after a __syncthreads: lane w builds window w's tree over its 8 warp values,
 // a butterfly over lanes 0..WMAX-1 joins the windows pairwise, lane 0 writes the CTA
 // partial.  Windows beyond nw (pow2 <= WMAX) enter as +0 leaves: x + 0 = x, and the
@@ -276,8 +314,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       if (i < n) op.row(i, 0.0, v[w], cc[w]);
     }
     if constexpr (D > 0) {
-#pragma unroll
-      for (int w = 0; w < RPT; ++w) warp_leaves<D>(cc[w], sm.wp, w);
+      warp_leaves_multi<RPT, D>(cc, sm.wp);
       __syncthreads();
       if (warp == 0) cta_partial<D>(sm.wp, RPT, part, stride);
     }
