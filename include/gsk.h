@@ -209,7 +209,8 @@ int gsk_shard_halo_host(int64_t n, const int32_t *row_ptr, const int32_t *col, i
  * layout; values are read from A->values (gsk_plan_refresh after rescaling).  Solves
  * on the plan (gsk_bicgstab_solve_plan, gsk_gmres_solve_plan) take b, x0, x and the
  * weights as this process's rows [lo(first), hi(first + count - 1)) (device) and
- * return the global history.  The split Bi-CGSTAB schedule and MGS GMRES are used;
+ * return the global history; gsk_plan_spmv takes and returns this process's rows of x
+ * and y = A x (halo exchanged).  The split Bi-CGSTAB schedule and MGS GMRES are used;
  * opts->engine is ignored. */
 int gsk_plan_create_sharded(const gsk_csr *A, const gsk_opts *opts, const gsk_shard_opts *sh,
                             gsk_plan **plan, void *stream);

@@ -267,7 +267,7 @@ class Plan:
         _check(load().gsk_plan_refresh(self.h, _stream()))
 
     def spmv(self, x, y=None):
-        x = _dev_f64(x, self.A.n)
+        x = _dev_f64(x, self.nloc)
         y = torch.empty_like(x) if y is None else y
         _check(load().gsk_plan_spmv(self.h, _ptr(x), _ptr(y), _stream()))
         return y

@@ -254,6 +254,7 @@ int shard_bicgstab_run(gsk_plan* P, const double* b, const double* x0, double to
 int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, double tol, int maxit, double* x,
                     double* hist, gsk_report* rep, cudaStream_t caller);
 int shard_refresh(gsk_plan* P, cudaStream_t s);
+int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).
 int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels, const char* what);

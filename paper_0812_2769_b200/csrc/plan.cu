@@ -370,10 +370,7 @@ void gsk_plan_destroy(gsk_plan* P) {
 }
 
 int gsk_plan_spmv(gsk_plan* P, const double* x, double* y, void* stream) {
-  if (P && P->shards) {
-    set_error("gsk_plan_spmv: not available on a sharded plan (use the per-shard solvers)");
-    return GSK_E_INVALID;
-  }
+  if (P && P->shards && x && y) return shard_spmv(P, x, y, as_stream(stream));
   if (!P || !x || !y) {
     set_error("gsk_plan_spmv: NULL argument");
     return GSK_E_INVALID;

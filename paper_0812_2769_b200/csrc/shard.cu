@@ -443,6 +443,33 @@ int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doubl
   return gmres_report(P, hist, rep, caller);
 }
 
+// ---- y = A x on this process's rows (halo-exchanged x) -----------------------------------
+struct OpShardSpmv {
+  static constexpr int D = 0;
+  static constexpr int NV = 0;
+  static constexpr bool kSpmv = true;
+  const double* x;
+  double* y;
+  __device__ bool begin() { return true; }
+  __device__ const double* vin(int) const { return nullptr; }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int i, double v, const double (&)[1], double (&)[1]) const { y[i] = v; }
+};
+
+int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller) {
+  ShardSet* S = P->shards;
+  for (auto& d : S->sh)
+    if (!d.bvec) GSK_CUDA(cudaMalloc(&d.bvec, sizeof(double) * 7 * d.pitch));
+  cudaStream_t s = P->st;
+  GSK_TRY(join_in(P, caller));
+  GSK_TRY(shard_x_in(P, x, bicg_x, s));
+  GSK_TRY(shard_halo(P, [&](int i) { return bicg_x(S->sh[i]); }, s));
+  GSK_TRY(shard_pass(P, [&](int i) { return OpShardSpmv{bicg_x(S->sh[i]), y + (S->sh[i].lo - S->rows0)}; }, s));
+  GSK_TRY(join_out(P, caller));
+  GSK_CUDA(cudaStreamSynchronize(caller));
+  return GSK_OK;
+}
+
 int shard_refresh(gsk_plan* P, cudaStream_t caller) {
   for (auto& d : P->shards->sh) GSK_TRY(gsk_plan_refresh(d.sub, caller));
   return GSK_OK;

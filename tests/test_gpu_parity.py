@@ -455,3 +455,14 @@ def test_bench_sharded_line():
     _, vo, bo, _ = system("C3", 32, 2)
     o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, workloads.CONFIGS["C3"].tol, 10000)
     assert line["extra"]["bicgstab"]["iterations"] == o[2]["iterations"]
+
+
+@pytest.mark.parametrize("name,N,P", [("C3", 16, 4), ("C4", 24, 2), ("C1", None, 8)])
+def test_sharded_spmv(name, N, P):
+    s = workloads.generate(name, N=N)
+    x = workloads.uniform(s["n"], 9, 9)
+    y = oracle.spmv(s["row_ptr"], s["col"], s["val"], x)
+    for fmt in ("csr", "sell"):
+        SP = gsk.ShardedPlan(gsk.CSR.from_system(s), shards=P, fmt=fmt)
+        assert np.array_equal(cpu(SP.spmv(x)), y)
+        SP.close()
