@@ -1,5 +1,5 @@
 // common.cuh — shared definitions of libgsk (sm_100a): matrix views, reduction
-// bookkeeping and small helpers.  The pass engine itself is stream.cuh.
+// bookkeeping and small helpers.  The pass engine itself is engine.cuh.
 // Everything is memory-bound fp64 (no tensor cores: nothing is a dense
 // contraction).  Kernels are compiled with --fmad=false; every FMA is an explicit
 // __fma_rn (arithmetic contract AC-2).

@@ -10,14 +10,18 @@
 //                 the Op's row epilogue runs in canonical order (thread t <-> row t of
 //                 the window) and yields the dot-product leaves.  Vector passes
 //                 (FMT 0) give each thread one row of each window, all loads in
-//                 flight together.  Each window's leaves are reduced by warp
-//                 butterflies (= trees of 32 leaves); warp 0 finishes the trees of 8
-//                 warps and the tree over the CTA's windows, and writes ONE partial
-//                 per CTA.  No fences, no atomics: the CTA ends as soon as its stores
-//                 are issued.
+//                 flight together.  Warp trees of 32 leaves: per window in SpMV
+//                 passes (two dots share the first level), one reduce-scatter over
+//                 all of a thread's leaves in vector passes; warp 0 finishes the trees
+//                 of 8 warps and the tree over the CTA's windows, and writes ONE
+//                 partial per CTA.  No fences, no atomics: the CTA ends as soon as its
+//                 stores are issued.  SpMV passes prefetch the next window's own-row
+//                 operands into shared memory with cp.async.
 //   finish_kernel one CTA of 1024 threads reduces the CTA partials with the same
 //                 canonical tree (AC-5) and runs the Op's scalar
 //                 epilogue (alpha, omega, Givens, stopping tests, ...) on the device.
+//   mdot_pass     the CGS2 tile engine (thread = 8 consecutive rows), further below;
+//                 finish_local/global_kernel: the shard-split finish (shard.cu).
 //
 // Shared-memory scatter buffers and CSR stages are double-buffered by window parity,
 // so a window costs one __syncthreads.  Kernels are compiled with --fmad=false; every

@@ -143,7 +143,7 @@ namespace gsk {
 // plan's format (CSR or SELL) or a pure vector pass.
 int num_sms();
 bool pdl_enabled();  // GSK_PDL=0 in the environment disables programmatic launches
-int spmv_wpc_max();  // windows per CTA of SpMV passes (8; GSK_WPC overrides, pow2 <= 8)
+int spmv_wpc_max();  // windows per CTA of SpMV passes (8; GSK_WPC overrides, pow2 <= 16)
 
 // Kernel launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KArgs, typename... Args>
