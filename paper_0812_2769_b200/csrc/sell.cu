@@ -33,28 +33,88 @@ __global__ void __launch_bounds__(TB) sell_rank_kernel(int n, int nchunks, const
   }
 }
 
-// exclusive scan of 32*clen into cptr[0..nchunks] (single CTA, one-off)
-__global__ void __launch_bounds__(1024) sell_scan_kernel(int nchunks, const int* __restrict__ clen, int* cptr, int mult) {
-  __shared__ long long part[1024];
+// exclusive scan of mult*clen into cptr[0..nchunks] in three launches (integer work,
+// order-free): per-block sums of SCAN_B chunks, one CTA scans the block sums, each
+// block scans its chunks from its offset.
+constexpr int SCAN_T = 1024;
+constexpr int SCAN_B = 4 * SCAN_T;  // chunks per block
+
+__device__ __forceinline__ long long block_excl_scan(long long v, long long* sh, long long* total) {
   const int t = threadIdx.x;
-  const int per = (nchunks + 1023) / 1024;
-  const int a = t * per, b = min(nchunks, a + per);
-  long long s = 0;
-  for (int i = a; i < b; ++i) s += (long long)clen[i] * mult;
-  part[t] = s;
+  sh[t] = v;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    long long v = t >= off ? part[t - off] : 0;
+  for (int off = 1; off < SCAN_T; off <<= 1) {
+    const long long u = t >= off ? sh[t - off] : 0;
     __syncthreads();
-    part[t] += v;
+    sh[t] += u;
     __syncthreads();
   }
-  long long run = t ? part[t - 1] : 0;
-  for (int i = a; i < b; ++i) {
-    cptr[i] = (int)run;
-    run += (long long)clen[i] * mult;
+  const long long incl = sh[t];
+  if (total) *total = sh[SCAN_T - 1];
+  __syncthreads();
+  return incl - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) sell_scan_sums(int nchunks, const int* __restrict__ clen, long long* bsum,
+                                                       int mult) {
+  __shared__ long long sh[SCAN_T];
+  const int b0 = blockIdx.x * SCAN_B, t = threadIdx.x;
+  long long v = 0;
+  for (int k = 0; k < SCAN_B / SCAN_T; ++k) {
+    const int c = b0 + k * SCAN_T + t;
+    if (c < nchunks) v += (long long)clen[c] * mult;
   }
-  if (t == 1023) cptr[nchunks] = (int)part[1023];
+  long long tot = 0;
+  block_excl_scan(v, sh, &tot);
+  if (t == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_T) sell_scan_offsets(int nblocks, long long* bsum) {
+  __shared__ long long sh[SCAN_T];
+  long long carry = 0;
+  for (int base = 0; base < nblocks; base += SCAN_T) {
+    const int i = base + threadIdx.x;
+    const long long v = i < nblocks ? bsum[i] : 0;
+    long long tot = 0;
+    const long long ex = block_excl_scan(v, sh, &tot);
+    if (i < nblocks) bsum[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_T) sell_scan_final(int nchunks, const int* __restrict__ clen,
+                                                        const long long* __restrict__ boff, int* cptr, int mult) {
+  __shared__ long long sh[SCAN_T];
+  const int b0 = blockIdx.x * SCAN_B, t = threadIdx.x;
+  constexpr int PER = SCAN_B / SCAN_T;  // thread t owns chunks b0 + PER t .. + PER-1
+  long long loc[PER];
+  long long v = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = b0 + PER * t + k;
+    loc[k] = c < nchunks ? (long long)clen[c] * mult : 0;
+    v += loc[k];
+  }
+  long long run = boff[blockIdx.x] + block_excl_scan(v, sh, nullptr);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int c = b0 + PER * t + k;
+    if (c < nchunks) cptr[c] = (int)run;
+    run += loc[k];
+    if (c == nchunks - 1) cptr[nchunks] = (int)run;
+  }
+}
+
+static int sell_scan(int nchunks, const int* clen, int* cptr, int mult, cudaStream_t s) {
+  const int nb = (nchunks + SCAN_B - 1) / SCAN_B;
+  long long* bsum = nullptr;
+  GSK_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (nb > 0 ? nb : 1), s));
+  sell_scan_sums<<<nb, SCAN_T, 0, s>>>(nchunks, clen, bsum, mult);
+  sell_scan_offsets<<<1, SCAN_T, 0, s>>>(nb, bsum);
+  sell_scan_final<<<nb, SCAN_T, 0, s>>>(nchunks, clen, bsum, cptr, mult);
+  GSK_LAUNCHED(3);
+  GSK_CUDA(cudaFreeAsync(bsum, s));
+  return GSK_OK;
 }
 
 __global__ void __launch_bounds__(TB) sell_fill_kernel(int n, int nchunks, const int* __restrict__ rp,
@@ -89,8 +149,7 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&P->roff, (size_t)P->nchunks * SELL_C));
   sell_rank_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->roff, P->clen);
   GSK_LAUNCHED(1);
-  sell_scan_kernel<<<1, 1024, 0, s>>>((int)P->nchunks, P->clen, P->cptr, SELL_C);
-  GSK_LAUNCHED(1);
+  GSK_TRY(sell_scan((int)P->nchunks, P->clen, P->cptr, SELL_C, s));
   int tot = 0;
   GSK_CUDA(cudaMemcpyAsync(&tot, P->cptr + P->nchunks, sizeof(int), cudaMemcpyDeviceToHost, s));
   GSK_CUDA(cudaStreamSynchronize(s));
@@ -180,8 +239,7 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
     P->dptr = nullptr;
     return GSK_OK;
   }
-  sell_scan_kernel<<<1, 1024, 0, s>>>(nch, ucount, P->dptr, 1);
-  GSK_LAUNCHED(1);
+  GSK_TRY(sell_scan(nch, ucount, P->dptr, 1, s));
   int tot = 0;
   GSK_CUDA(cudaMemcpyAsync(&tot, P->dptr + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
   GSK_CUDA(cudaStreamSynchronize(s));
