@@ -466,3 +466,24 @@ def test_sharded_spmv(name, N, P):
         SP = gsk.ShardedPlan(gsk.CSR.from_system(s), shards=P, fmt=fmt)
         assert np.array_equal(cpu(SP.spmv(x)), y)
         SP.close()
+
+
+def test_solver_argument_errors():
+    """API errors are negative returns with a message (include/gsk.h), never a crash:
+    tol <= 0, maxit < 1, m out of range, CGS2 beyond its m limit, unknown options; a
+    failed call leaves the plan usable."""
+    s = workloads.generate("C2", N=40)
+    A = gsk.CSR.from_system(s)
+    P = gsk.Plan(A)
+    bad = [lambda: P.bicgstab(s["b"], tol=0.0), lambda: P.bicgstab(s["b"], maxit=0),
+           lambda: P.gmres(s["b"], m=0), lambda: P.gmres(s["b"], m=129), lambda: P.gmres(s["b"], tol=-1.0),
+           lambda: gsk.Plan(A, orth="cgs2", engine="graph").gmres(s["b"], m=65, maxit=10)]
+    for f in bad:
+        with pytest.raises(gsk.GskError) as ei:
+            f()
+        assert ei.value.code == -1 and str(ei.value)
+    for kw in ({"fmt": "dia"}, {"schedule": "x"}, {"orth": "x"}, {"engine": "x"}):
+        with pytest.raises(KeyError):
+            gsk.Plan(A, **kw)
+    assert_same_solve(P.bicgstab(s["b"], tol=1e-9, maxit=300),
+                      oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-9, 300))
