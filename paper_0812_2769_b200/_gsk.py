@@ -19,7 +19,7 @@ GSK_OK, GSK_E_INVALID, GSK_E_ZERO_ROW, GSK_E_CUDA, GSK_E_NOMEM = 0, -1, -2, -3, 
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}
 FMT = {"csr": 0, "sell": 1}
 SCHEDULE = {"auto": 0, "fused": 1, "split": 2}
-ENGINE = {"auto": 0, "graph": 1, "coop": 2, "small": 3}
+ENGINE = {"auto": 0, "graph": 1, "coop": 2, "small": 3, "cluster": 4}
 ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
@@ -237,9 +237,10 @@ class Plan:
 
     def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
                  orth: str = "mgs", sell_index: str = "plain", engine: str = "auto"):
-        """engine: "auto" (on-chip single-CTA solver where measured faster: Bi-CGSTAB
-        n <= 2048, GMRES/MGS n <= 4096; else graph passes), "graph" (always the passes),
-        "coop" (cooperative multi-CTA Bi-CGSTAB) or "small" (on-chip for n <= 4096)."""
+        """engine: "auto" (one launch per solve on one CTA for n <= 2048 or on one
+        thread-block cluster for n <= 16384, where measured faster; else graph passes),
+        "graph" (always the passes), "coop" (cooperative multi-CTA Bi-CGSTAB), "small"
+        (one CTA for n <= 4096) or "cluster" (one cluster for n <= 16384)."""
         lib = load()
         self.A = A
         self.weights = _dev_f64(weights, A.n)

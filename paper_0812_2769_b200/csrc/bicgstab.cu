@@ -114,7 +114,10 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   // cooperative grid (coop.cu, opt-in).  Same operators, bit-identical results.
   const bool small = (P->engine == GSK_ENGINE_AUTO && n <= 2048) ||
                      (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX);
-  if (small || P->engine == GSK_ENGINE_COOP) {
+  // one thread-block cluster (cluster.cu) above that, up to 16384 rows: 12-15 vs 25-27
+  // us per iteration on the graph passes
+  const bool clus = (P->engine == GSK_ENGINE_CLUSTER || P->engine == GSK_ENGINE_AUTO) && !small && n <= 16384;
+  if (small || clus || P->engine == GSK_ENGINE_COOP) {
     cudaStream_t s = P->st;
     GSK_TRY(join_in(P, caller));
     GSK_CUDA(cudaEventRecord(P->t0, s));
@@ -126,6 +129,8 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
     int used = 1;
     if (small)
       GSK_TRY(small_bicgstab_run(P, b, tol, maxit, x));
+    else if (clus)
+      GSK_TRY(cluster_bicgstab_run(P, b, tol, maxit, x, &used));
     else
       GSK_TRY(coop_bicgstab_run(P, b, tol, maxit, x, &used));
     if (used) {

@@ -1,0 +1,272 @@
+// cluster.cu — on-chip solvers on one thread-block cluster: the
+// single-CTA solvers of small.cu spread over CS <= 16 CTAs of a cluster, for systems
+// of up to 16 x 1024 rows (the paper's Problem 1 at 128 x 128 is 16384 rows).
+//
+// CTA c of the cluster owns the aligned row block [c B, (c+1) B) (B = 1024 / 512 / ...,
+// a power of two), one row per thread.  A pass: the rows (SpMV gathers read the
+// vectors from global memory through L2: they were written by other CTAs), a warp
+// butterfly per 32 rows and the CTA's tree over its warps (a canonical subtree, the
+// block being aligned), the CTA value parked in shared memory, ONE cluster barrier
+// (hardware, release/acquire at cluster scope: vectors and CTA values visible), then
+// every CTA reads the CS CTA values through distributed shared memory, joins them
+// with the top of the same tree (+ 0.0, AC-5) and runs the operator's scalar epilogue
+// on its own shared-memory copy of the state — every CTA takes the same decisions
+// without another barrier.  Operators are the graph path's (bicg_ops.cuh,
+// gmres_ops.cuh): results are bit-identical to it and to the oracle.  GMRES keeps
+// its small dense arrays (H, Givens, g, y, 1/norms) per CTA in shared memory, so the
+// replicated epilogues never race on global memory.
+#include <cooperative_groups.h>
+#include "bicg_ops.cuh"
+#include "gmres_ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gsk {
+
+constexpr int CL_T = 1024;      // threads per CTA = max rows per CTA
+constexpr int CL_MAX = 16;      // CTAs per cluster (non-portable size)
+constexpr int CL_NMAX = CL_T * CL_MAX;
+constexpr int CL_MMAX = 40;     // GMRES restart length with its arrays in shared memory
+
+struct ClusterRed {
+  double wsum[MAXD][32];
+  double cpart[2][MAXD];  // this CTA's block value, double-buffered by reducing pass
+};
+
+template <class Op>
+__device__ __forceinline__ void cluster_pass(const CsrView& A, int n, int r0, int B, Op op, ClusterRed& R,
+                                             int& par) {
+  constexpr int D = Op::D;
+  constexpr int DD = D > 0 ? D : 1;
+  constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int i = r0 + t;
+  const bool mine = t < B && i < n;
+  const bool run = op.begin();  // the shared state copy: identical in every CTA
+  double cc[DD];
+#pragma unroll
+  for (int d = 0; d < DD; ++d) cc[d] = 0.0;
+  if (run && mine) {
+    double y = 0.0;
+    if constexpr (Op::kSpmv) {  // AC-3 chain in CSR order
+      const int e = __ldg(A.rp + i + 1);
+      for (int q = __ldg(A.rp + i); q < e; ++q) y = __fma_rn(__ldg(A.v + q), op.gather(__ldg(A.ci + q)), y);
+    }
+    double v[NVA];
+#pragma unroll
+    for (int k = 0; k < Op::NV; ++k) {
+      const double* src = op.vin(k);
+      v[k] = src ? src[i] : 0.0;  // own rows: written by this thread only
+    }
+    op.row(i, y, v, cc);
+  }
+  if constexpr (D > 0) {
+    if (run) {
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) cc[d] = cc[d] + __shfl_xor_sync(0xffffffffu, cc[d], off);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) R.wsum[d][warp] = cc[d];
+      }
+    }
+    __syncthreads();
+    if (run && warp == 0) {
+      const int nw = B >= 32 ? B / 32 : 1;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double u = lane < nw ? R.wsum[d][lane] : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+        if (lane == 0) R.cpart[par][d] = u;
+      }
+    }
+  }
+  cluster.sync();  // the pass's vectors and the CTA values, cluster-wide
+  if constexpr (D > 0) {
+    if (run && warp == 0) {
+      const int cs = (int)cluster.num_blocks();
+      double q[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double u = lane < cs ? *cluster.map_shared_rank(&R.cpart[par][d], lane) : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+        q[d] = u + 0.0;  // AC-5
+      }
+      op.finish(q, lane);
+    }
+    // the next reducing pass writes the other buffer; this one is rewritten only after
+    // the next pass's cluster barrier, i.e. after every CTA has read it
+    par ^= 1;
+    __syncthreads();
+  }
+}
+
+// ---- Bi-CGSTAB: split schedule, vectors in global memory (L2) ---------------------------
+struct ClusterBicgArgs {
+  CsrView csr;
+  int n, B;
+  const double *b, *w;
+  double *x, *hist, *V;  // V: r, r^, p, -, v, -, t and s at V + 3n (the graph path's layout)
+  BicgState* st_out;
+  double tol;
+  int maxit;
+};
+
+__global__ void __launch_bounds__(CL_T, 1) cluster_bicgstab(ClusterBicgArgs a) {
+  __shared__ BicgState st;
+  __shared__ ClusterRed R;
+  const int n = a.n, r0 = (int)cg::this_cluster().block_rank() * a.B;
+  const size_t nn = (size_t)n;
+  double *r = a.V, *rh = a.V + nn, *p = a.V + 2 * nn, *s = a.V + 3 * nn, *v = a.V + 4 * nn, *t = a.V + 6 * nn;
+  if (threadIdx.x == 0) {
+    st = BicgState{};
+    st.tol = a.tol;
+    st.maxit = a.maxit;
+  }
+  __syncthreads();
+  int par = 0;
+  cluster_pass(a.csr, n, r0, a.B, OpInit<LdCG>{a.x, a.b, a.w, r, rh, p, v, a.hist, &st}, R, par);
+  while (!(st.done && !st.halfstep)) {
+    cluster_pass(a.csr, n, r0, a.B, OpS0{r, v, p, &st, 0, 0}, R, par);
+    cluster_pass(a.csr, n, r0, a.B, OpS1<LdCG>{p, rh, v, &st}, R, par);
+    cluster_pass(a.csr, n, r0, a.B, OpS2{r, v, a.w, s, a.hist, &st, 0}, R, par);
+    cluster_pass(a.csr, n, r0, a.B, OpS3<LdCG>{s, t, &st}, R, par);
+    cluster_pass(a.csr, n, r0, a.B, OpS4{s, p, t, rh, a.w, a.x, r, a.hist, &st, 0, 0, 0}, R, par);
+  }
+  cluster_pass(a.csr, n, r0, a.B, OpFinal<LdCG>{a.x, a.b, a.w, &st}, R, par);
+  if (cg::this_cluster().block_rank() == 0 && threadIdx.x == 0) *a.st_out = st;
+}
+
+// Cluster geometry for n rows: CS CTAs (power of two, <= 16) of B rows (power of two,
+// <= 1024); 0 if n is too large.
+static int cluster_geometry(int n, int* B) {
+  int cs = 1;
+  while (cs * CL_T < n) cs <<= 1;
+  if (cs > CL_MAX) return 0;
+  int b = CL_T;
+  while (b / 2 * cs >= n && b > 32) b >>= 1;
+  *B = b;
+  return cs;
+}
+
+static cudaError_t launch_cluster(const void* kern, int cs, void** args, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(CL_T);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, kern, args);
+}
+
+int cluster_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used) {
+  *used = 0;
+  const int n = P->A.n;
+  int B = 0;
+  const int cs = cluster_geometry(n, &B);
+  if (!cs) return GSK_OK;
+  static bool attr = false;
+  if (!attr) {
+    GSK_CUDA(cudaFuncSetAttribute(cluster_bicgstab, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  ClusterBicgArgs a{P->csr, n, B, b, P->weights, x, P->hist_d, P->bvec, P->bstate, tol, maxit};
+  void* args[] = {&a};
+  GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_bicgstab), cs, args, P->st));
+  GSK_LAUNCHED(1);
+  *used = 1;
+  return GSK_OK;
+}
+
+// ---- GMRES(m) with MGS: the cycle of gmres.cu on the cluster ------------------------------
+struct ClusterGmresArgs {
+  CsrView csr;
+  int n, B;
+  const double *b, *w;
+  double *x, *W, *hist;
+  GmresState h;  // initial scalars (the arrays are replaced by shared-memory copies)
+  GmresState* st_out;
+};
+
+__global__ void __launch_bounds__(CL_T, 1) cluster_gmres(ClusterGmresArgs a) {
+  __shared__ GmresState st;
+  __shared__ ClusterRed R;
+  constexpr int M = CL_MMAX;
+  constexpr int NARR = (M + 1) * M + 7 * M + 8;
+  __shared__ double arr[NARR];
+  const int n = a.n, r0 = (int)cg::this_cluster().block_rank() * a.B;
+  const int m = a.h.m;
+  for (int k = threadIdx.x; k < NARR; k += blockDim.x) arr[k] = 0.0;
+  if (threadIdx.x == 0) {
+    st = a.h;
+    st.H = arr;  // (m+1) x m row-major with stride m, as in gmres.cu
+    st.cs = arr + (M + 1) * M;
+    st.sn = st.cs + M;
+    st.g = st.sn + M;
+    st.y = st.g + M + 1;
+    st.inv = st.y + M;
+    st.c1 = st.inv + M + 2;
+    st.c2 = st.c1 + M;
+  }
+  __syncthreads();
+  auto slot = [&](int j) { return a.W + (size_t)(j - 1) * n; };
+  int par = 0;
+  cluster_pass(a.csr, n, r0, a.B, OpGResid<LdCG>{a.x, a.b, a.w, a.W, a.hist, &st, 1}, R, par);
+  const long long maxc = (long long)st.maxit + 2;
+  for (long long c = 0; c < maxc && !st.done; ++c) {
+    for (int j = 1; j <= m && !st.done && !st.cycle_stop; ++j) {
+      cluster_pass(a.csr, n, r0, a.B, OpCgsS<LdCG>{slot(j), slot(j + 1), &st, j, 0}, R, par);
+      cluster_pass(a.csr, n, r0, a.B, OpH1{slot(j + 1), slot(1), &st, j, 0}, R, par);
+      for (int i = 1; i < j; ++i)
+        cluster_pass(a.csr, n, r0, a.B, OpMgs{slot(i), slot(i + 1), slot(j + 1), &st, i, j, 0, 0, 0}, R, par);
+      cluster_pass(a.csr, n, r0, a.B, OpLast{slot(j), slot(j + 1), a.hist, &st, j, 0, 0}, R, par);
+    }
+    cluster_pass(a.csr, n, r0, a.B, OpXupd<LdPlain>{a.W, a.x, &st, (size_t)n, 0, nullptr, nullptr}, R, par);
+    cluster_pass(a.csr, n, r0, a.B, OpGResid<LdCG>{a.x, a.b, a.w, a.W, a.hist, &st, 0}, R, par);
+  }
+  if (cg::this_cluster().block_rank() == 0) {
+    if (threadIdx.x == 0) {  // scalars only (the report reads no arrays)
+      GmresState o = st;
+      o.H = a.h.H;
+      o.cs = a.h.cs;
+      o.sn = a.h.sn;
+      o.g = a.h.g;
+      o.y = a.h.y;
+      o.inv = a.h.inv;
+      o.c1 = a.h.c1;
+      o.c2 = a.h.c2;
+      *a.st_out = o;
+    }
+  }
+}
+
+int cluster_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h, int* used) {
+  *used = 0;
+  const int n = P->A.n;
+  int B = 0;
+  const int cs = cluster_geometry(n, &B);
+  if (!cs || h.m > CL_MMAX) return GSK_OK;
+  static bool attr = false;
+  if (!attr) {
+    GSK_CUDA(cudaFuncSetAttribute(cluster_gmres, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  ClusterGmresArgs a{P->csr, n, B, b, P->weights, x, P->W, P->hist_d, h, P->gstate};
+  void* args[] = {&a};
+  GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_gmres), cs, args, P->st));
+  GSK_LAUNCHED(1);
+  *used = 1;
+  return GSK_OK;
+}
+
+}  // namespace gsk

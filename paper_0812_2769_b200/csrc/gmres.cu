@@ -27,7 +27,7 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
   GSK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
   for (int j = 1; j <= m && rc >= 0 && P->orth == 1; ++j) {
-    OpCgsS sp{slot(j), slot(j + 1), st, j, 0};
+    OpCgsS<> sp{slot(j), slot(j + 1), st, j, 0};
     OpCgsA a{};
     a.W = P->W, a.n = n, a.Wn = slot(j + 1), a.st = st, a.j = j;
     OpCgsB bp{};
@@ -41,7 +41,7 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
   }
   for (int j = 1; j <= m && rc >= 0 && P->orth == 0; ++j) {
     // S_j as a plain SpMV pass (w = A v_j) + the h_1j dot pass (OpH1)
-    OpCgsS a{slot(j), slot(j + 1), st, j, 0};
+    OpCgsS<> a{slot(j), slot(j + 1), st, j, 0};
     rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
     if (rc >= 0) rc = run_pass(P, OpH1{slot(j + 1), slot(1), st, j, 0}, s);
     for (int i = 1; i < j && rc >= 0; ++i) {
@@ -126,9 +126,13 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8)));
   GSK_TRY(ensure_hist(P, maxit));
   // small systems: the whole solve in one launch on one SM (small.cu), MGS only
-  const bool small = (P->engine == GSK_ENGINE_AUTO || P->engine == GSK_ENGINE_SMALL) && n <= GSK_SMALL_NMAX &&
+  // (default for n <= 2048), or on one thread-block cluster (cluster.cu) up to 16384
+  // rows and m <= 40 (2-2.2x faster than the graph passes there)
+  const bool small = ((P->engine == GSK_ENGINE_AUTO && n <= 2048) || (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX)) &&
                      P->orth == 0;
-  if (!small && (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d ||
+  const bool clus = (P->engine == GSK_ENGINE_CLUSTER || P->engine == GSK_ENGINE_AUTO) && !small && P->orth == 0 &&
+                    n <= 16384 && m <= 40;
+  if (!small && !clus && (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d ||
       P->gkey_orth != P->orth)) {
     for (auto& g : P->ggraph)
       if (g) {
@@ -165,8 +169,11 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   h.m = m;
   GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8), s));
   GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  int cused = 0;
+  if (clus) GSK_TRY(cluster_gmres_run(P, b, x, h, &cused));
   if (small) {
     GSK_TRY(small_gmres_run(P, b, x, h));
+  } else if (cused) {
   } else {
     OpGResid<> init{x, b, P->weights, P->W, P->hist_d, P->gstate, 1};
     if (run_pass(P, init, s) < 0) return GSK_E_CUDA;

@@ -303,6 +303,7 @@ struct CgsBase {
   }
 };
 
+template <class L = LdNC>
 struct OpCgsS {  // S: w = A v_j (no reduction)
   static constexpr int D = 0;
   static constexpr int NV = 0;
@@ -318,7 +319,7 @@ struct OpCgsS {  // S: w = A v_j (no reduction)
     return true;
   }
   __device__ const double* vin(int) const { return nullptr; }
-  __device__ double gather(int c) const { return __ldg(Wj + c) * invj; }
+  __device__ double gather(int c) const { return L::ld(Wj + c) * invj; }
   __device__ void row(int i, double y, const double (&)[1], double (&)[1]) const { Wn[i] = y; }
 };
 

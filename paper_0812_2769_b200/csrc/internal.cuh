@@ -245,6 +245,10 @@ int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, doubl
 // whole solve; the caller has set x = x0 and zeroed/initialised the state.
 int small_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x);
 int small_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h);
+// On-chip solvers on one thread-block cluster (cluster.cu) for n <= 16384; *used = 0
+// when the system does not fit (the caller then runs the graph path).
+int cluster_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);
+int cluster_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h, int* used);
 int ensure_hist(gsk_plan* P, int maxit);
 int bicgstab_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller);
 int gmres_report(gsk_plan* P, double* hist, gsk_report* rep, cudaStream_t caller);

@@ -347,7 +347,7 @@ static int shard_capture_cycle(gsk_plan* P, const double* b, int m, int copy, cu
   for (int j = 1; j <= m && rc == GSK_OK; ++j) {
     rc = shard_halo(P, [&](int i) { return slot(i, j); }, s);
     if (rc == GSK_OK) {
-      auto mk = [&](int i) { return OpCgsS{slot(i, j), slot(i, j + 1), st, j, 0}; };
+      auto mk = [&](int i) { return OpCgsS<>{slot(i, j), slot(i, j + 1), st, j, 0}; };
       rc = j == 1 ? shard_pass(P, mk, s, P->pev[3][copy][0], P->pev[3][copy][1]) : shard_pass(P, mk, s);
       if (rc == GSK_OK) rc = shard_pass(P, [&](int i) { return OpH1{slot(i, j + 1), slot(i, 1), st, j, 0}; }, s);
     }

@@ -179,7 +179,7 @@ def system(name, N, scaling):
 def test_bicgstab_parity(name, N, scaling, fmt, schedule):
     s, val, b, _ = system(name, N, scaling)
     maxit = 600
-    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt, schedule=schedule)
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt, schedule=schedule, engine="graph")
     g = P.bicgstab(b, tol=1e-8, maxit=maxit)
     o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-8, maxit)
     assert_same_solve(g, o)
@@ -195,7 +195,7 @@ def test_bicgstab_frame_weights():
         else:
             val, b, d1 = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 1)
             w = d2 / d1
-        P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), weights=w, schedule=schedule)
+        P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), weights=w, schedule=schedule, engine="graph")
         g = P.bicgstab(b, tol=1e-10, maxit=3000)
         o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-10, 3000, weights=w)
         assert_same_solve(g, o)
@@ -209,7 +209,7 @@ def test_gmres_parity(name, N, scaling, m, orth):
     s, val, b, _ = system(name, N, scaling)
     maxit = 400
     fmt = "sell" if name == "C4" else "csr"
-    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt, orth=orth)
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt=fmt, orth=orth, engine="graph")
     g = P.gmres(b, m=m, tol=1e-8, maxit=maxit)
     o = oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-8, maxit, orth=orth)
     assert_same_solve(g, o)
@@ -226,7 +226,7 @@ def test_gmres_cgs2_paper_problem1():
     assert int(np.flatnonzero(g[1] < 1e-4)[0]) == 265
 
 
-@pytest.mark.parametrize("engine", ["auto", "graph", "coop", "small"])
+@pytest.mark.parametrize("engine", ["auto", "graph", "coop", "small", "cluster"])
 def test_solver_edge_cases(engine):
     n = 300
     rp = np.arange(n + 1, dtype=np.int32)
@@ -313,7 +313,7 @@ def test_plan_less_entry_points():
 
 def test_repeat_solves_are_deterministic():
     s = workloads.generate("C3", N=16)
-    P = gsk.Plan(gsk.CSR.from_system(s), fmt="sell")
+    P = gsk.Plan(gsk.CSR.from_system(s), fmt="sell", engine="graph")
     a = P.bicgstab(s["b"], tol=1e-9, maxit=500)
     b = P.bicgstab(s["b"], tol=1e-9, maxit=500)
     assert np.array_equal(a[1], b[1]) and np.array_equal(cpu(a[0]), cpu(b[0]))
@@ -487,3 +487,28 @@ def test_solver_argument_errors():
             gsk.Plan(A, **kw)
     assert_same_solve(P.bicgstab(s["b"], tol=1e-9, maxit=300),
                       oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-9, 300))
+
+
+CLUSTER = [("C1", None), ("C2", 50), ("C3", 16), ("C5", 96), ("P1", None), ("C4", 24)]
+
+
+@pytest.mark.parametrize("name,N", CLUSTER)
+def test_cluster_engine_parity(name, N):
+    """On-chip solvers on one thread-block cluster (cluster.cu; up to 16 CTAs with DSMEM
+    reductions, n <= 16384, ragged n included): Bi-CGSTAB and MGS GMRES bit-exact
+    against the oracle, with and without frame weights."""
+    s, val, b, _ = system(name, N, 2)
+    if s["n"] > 16384:
+        pytest.skip("beyond one cluster")
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    P = gsk.Plan(A, engine="cluster")
+    assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=600), oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 600))
+    for m in (1, 20, 30):
+        assert_same_solve(P.gmres(b, m=m, tol=1e-9, maxit=200),
+                          oracle.gmres(s["row_ptr"], s["col"], val, b, m, 1e-9, 200))
+    w = workloads.uniform(s["n"], 5, 6) + 1.5
+    Pw = gsk.Plan(A, engine="cluster", weights=w)
+    assert_same_solve(Pw.bicgstab(b, tol=1e-9, maxit=600),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 600, weights=w))
+    assert_same_solve(Pw.gmres(b, m=20, tol=1e-9, maxit=200),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 200, weights=w))

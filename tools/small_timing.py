@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_0812_2769_b200 as gsk  # noqa: E402
 import workloads  # noqa: E402
 
-CASES = [("C1", None, 20), ("C2", 40, 30), ("C2", 64, 30), ("C3", 16, 30), ("C5", 64, 50)]
+CASES = [("C1", None, 20), ("C2", 40, 30), ("C2", 64, 30), ("C3", 16, 30), ("C5", 64, 50), ("C5", 96, 30),
+         ("P1", None, 10)]
 
 
 def main(out):
@@ -22,7 +23,9 @@ def main(out):
         A, b, _ = gsk.gs_scale(A0, s["b"], 2)
         for solver in ("bicgstab", "gmres"):
             res = {}
-            for engine in ("small", "graph"):
+            for engine in ("small", "cluster", "graph"):
+                if engine == "small" and s["n"] > 4096:
+                    continue
                 P = gsk.Plan(A, engine=engine)
                 best = None
                 for _ in range(3):  # first call: graph capture / module load
@@ -36,7 +39,7 @@ def main(out):
                 P.close()
             row = {"config": name, "N": N, "n": s["n"], "solver": solver + (f"({m})" if solver == "gmres" else ""),
                    **{f"{k}_{e}": v for e, d in res.items() for k, v in d.items()},
-                   "speedup": res["graph"]["solve_ms"] / res["small"]["solve_ms"]}
+                   "speedup_cluster": res["graph"]["solve_ms"] / res["cluster"]["solve_ms"]}
             print(json.dumps(row), flush=True)
             rows.append(row)
     with open(out, "w") as f:
