@@ -79,9 +79,9 @@ typedef struct gsk_opts {
                            slower on B200 at C4: DESIGN.md §5) */
   int32_t engine;       /* how the solvers run (all engines give bit-identical results):
                            GSK_ENGINE_AUTO (default) = one launch for the whole solve on
-                           one CTA (n <= 2048) or on one thread-block cluster
-                           (n <= 16384; GMRES with MGS and m <= 40), where each is
-                           measured faster, else graph-replayed passes; GSK_ENGINE_GRAPH = always the
+                           one CTA (n <= 2048) or on one thread-block cluster (Bi-CGSTAB
+                           n <= 32768, GMRES with MGS and m <= 40 n <= 65536), where each
+                           is measured faster, else graph-replayed passes; GSK_ENGINE_GRAPH = always the
                            passes; GSK_ENGINE_COOP = cooperative multi-CTA Bi-CGSTAB for
                            n <= 2^19 (opt-in); GSK_ENGINE_SMALL = the one-CTA solver
                            whenever n <= GSK_SMALL_NMAX; GSK_ENGINE_CLUSTER = the cluster
@@ -89,7 +89,7 @@ typedef struct gsk_opts {
 } gsk_opts;
 
 enum { GSK_ENGINE_AUTO = 0, GSK_ENGINE_GRAPH = 1, GSK_ENGINE_COOP = 2, GSK_ENGINE_SMALL = 3,
-       GSK_ENGINE_CLUSTER = 4 /* on-chip solver on one thread-block cluster, n <= 16384 */ };
+       GSK_ENGINE_CLUSTER = 4 /* on-chip solver on one thread-block cluster, n <= 65536 */ };
 #define GSK_SMALL_NMAX 4096
 
 enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2 };

@@ -238,9 +238,10 @@ class Plan:
     def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
                  orth: str = "mgs", sell_index: str = "plain", engine: str = "auto"):
         """engine: "auto" (one launch per solve on one CTA for n <= 2048 or on one
-        thread-block cluster for n <= 16384, where measured faster; else graph passes),
-        "graph" (always the passes), "coop" (cooperative multi-CTA Bi-CGSTAB), "small"
-        (one CTA for n <= 4096) or "cluster" (one cluster for n <= 16384)."""
+        thread-block cluster up to 32768 / 65536 rows for Bi-CGSTAB / GMRES, where
+        measured faster; else graph passes), "graph" (always the passes), "coop"
+        (cooperative multi-CTA Bi-CGSTAB), "small" (one CTA, n <= 4096) or "cluster"
+        (one cluster, n <= 65536)."""
         lib = load()
         self.A = A
         self.weights = _dev_f64(weights, A.n)

@@ -116,7 +116,8 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
                      (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX);
   // one thread-block cluster (cluster.cu) above that, up to 16384 rows: 12-15 vs 25-27
   // us per iteration on the graph passes
-  const bool clus = (P->engine == GSK_ENGINE_CLUSTER || P->engine == GSK_ENGINE_AUTO) && !small && n <= 16384;
+  const bool clus = !small && ((P->engine == GSK_ENGINE_AUTO && n <= GSK_CLUSTER_AUTO_BICG) ||
+                               (P->engine == GSK_ENGINE_CLUSTER && n <= GSK_CLUSTER_NMAX));
   if (small || clus || P->engine == GSK_ENGINE_COOP) {
     cudaStream_t s = P->st;
     GSK_TRY(join_in(P, caller));

@@ -1,9 +1,9 @@
 // cluster.cu — on-chip solvers on one thread-block cluster: the
 // single-CTA solvers of small.cu spread over CS <= 16 CTAs of a cluster, for systems
-// of up to 16 x 1024 rows (the paper's Problem 1 at 128 x 128 is 16384 rows).
+// of up to 16 x 4096 rows (the paper's Problem 1 at 128 x 128 is 16384 rows).
 //
-// CTA c of the cluster owns the aligned row block [c B, (c+1) B) (B = 1024 / 512 / ...,
-// a power of two), one row per thread.  A pass: the rows (SpMV gathers read the
+// CTA c of the cluster owns the aligned row block [c B, (c+1) B) (B a power of two,
+// <= 4096), rows c B + 1024 k + t for thread t.  A pass: the rows (SpMV gathers read the
 // vectors from global memory through L2: they were written by other CTAs), a warp
 // butterfly per 32 rows and the CTA's tree over its warps (a canonical subtree, the
 // block being aligned), the CTA value parked in shared memory, ONE cluster barrier
@@ -25,12 +25,14 @@ namespace gsk {
 
 constexpr int CL_T = 1024;      // threads per CTA = max rows per CTA
 constexpr int CL_MAX = 16;      // CTAs per cluster (non-portable size)
-constexpr int CL_NMAX = CL_T * CL_MAX;
+constexpr int CL_NMAX = 4 * CL_T * CL_MAX;  // 65536 rows
 constexpr int CL_MMAX = 40;     // GMRES restart length with its arrays in shared memory
 
+constexpr int CL_RPT = 4;       // rows per thread at most (CTA blocks of <= 4096 rows)
+
 struct ClusterRed {
-  double wsum[MAXD][32];
-  double cpart[2][MAXD];  // this CTA's block value, double-buffered by reducing pass
+  double wsum[MAXD][CL_RPT * 32];  // warp sums of the CTA's block, in row order
+  double cpart[2][MAXD];           // this CTA's block value, double-buffered by reducing pass
 };
 
 template <class Op>
@@ -41,44 +43,54 @@ __device__ __forceinline__ void cluster_pass(const CsrView& A, int n, int r0, in
   constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
   cg::cluster_group cluster = cg::this_cluster();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int i = r0 + t;
-  const bool mine = t < B && i < n;
+  const int slabs = (B + CL_T - 1) / CL_T;
   const bool run = op.begin();  // the shared state copy: identical in every CTA
-  double cc[DD];
+  if (run) {
+#pragma unroll 1
+    for (int k = 0; k < slabs; ++k) {  // rows r0 + 1024 k + t (warp sums in row order)
+      const int i = r0 + k * CL_T + t;
+      double cc[DD];
 #pragma unroll
-  for (int d = 0; d < DD; ++d) cc[d] = 0.0;
-  if (run && mine) {
-    double y = 0.0;
-    if constexpr (Op::kSpmv) {  // AC-3 chain in CSR order
-      const int e = __ldg(A.rp + i + 1);
-      for (int q = __ldg(A.rp + i); q < e; ++q) y = __fma_rn(__ldg(A.v + q), op.gather(__ldg(A.ci + q)), y);
-    }
-    double v[NVA];
+      for (int d = 0; d < DD; ++d) cc[d] = 0.0;
+      if (k * CL_T + t < B && i < n) {
+        double y = 0.0;
+        if constexpr (Op::kSpmv) {  // AC-3 chain in CSR order
+          const int e = __ldg(A.rp + i + 1);
+          for (int q = __ldg(A.rp + i); q < e; ++q) y = __fma_rn(__ldg(A.v + q), op.gather(__ldg(A.ci + q)), y);
+        }
+        double v[NVA];
 #pragma unroll
-    for (int k = 0; k < Op::NV; ++k) {
-      const double* src = op.vin(k);
-      v[k] = src ? src[i] : 0.0;  // own rows: written by this thread only
+        for (int kk = 0; kk < Op::NV; ++kk) {
+          const double* src = op.vin(kk);
+          v[kk] = src ? src[i] : 0.0;  // own rows: written by this thread only
+        }
+        op.row(i, y, v, cc);
+      }
+      if constexpr (D > 0) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+          for (int d = 0; d < D; ++d) cc[d] = cc[d] + __shfl_xor_sync(0xffffffffu, cc[d], off);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int d = 0; d < D; ++d) R.wsum[d][k * 32 + warp] = cc[d];
+        }
+      }
     }
-    op.row(i, y, v, cc);
   }
   if constexpr (D > 0) {
-    if (run) {
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-        for (int d = 0; d < D; ++d) cc[d] = cc[d] + __shfl_xor_sync(0xffffffffu, cc[d], off);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int d = 0; d < D; ++d) R.wsum[d][warp] = cc[d];
-      }
-    }
     __syncthreads();
     if (run && warp == 0) {
+      // the block's tree over its B/32 warp sums: lane l joins sums 4l..4l+3 (an
+      // aligned subtree), then a butterfly over the lanes
       const int nw = B >= 32 ? B / 32 : 1;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        double u = lane < nw ? R.wsum[d][lane] : 0.0;
+        double a4[CL_RPT];
+#pragma unroll
+        for (int q = 0; q < CL_RPT; ++q) a4[q] = CL_RPT * lane + q < nw ? R.wsum[d][CL_RPT * lane + q] : 0.0;
+        double u = (a4[0] + a4[1]) + (a4[2] + a4[3]);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
         if (lane == 0) R.cpart[par][d] = u;
@@ -143,13 +155,13 @@ __global__ void __launch_bounds__(CL_T, 1) cluster_bicgstab(ClusterBicgArgs a) {
 }
 
 // Cluster geometry for n rows: CS CTAs (power of two, <= 16) of B rows (power of two,
-// <= 1024); 0 if n is too large.
+// <= 4096, one to four rows per thread); 0 if n is too large.
 static int cluster_geometry(int n, int* B) {
+  if (n > CL_NMAX) return 0;
   int cs = 1;
-  while (cs * CL_T < n) cs <<= 1;
-  if (cs > CL_MAX) return 0;
-  int b = CL_T;
-  while (b / 2 * cs >= n && b > 32) b >>= 1;
+  while (cs * CL_T < n && cs < CL_MAX) cs <<= 1;
+  int b = 32;
+  while (b * cs < n) b <<= 1;
   *B = b;
   return cs;
 }

@@ -130,8 +130,9 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   // rows and m <= 40 (2-2.2x faster than the graph passes there)
   const bool small = ((P->engine == GSK_ENGINE_AUTO && n <= 2048) || (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX)) &&
                      P->orth == 0;
-  const bool clus = (P->engine == GSK_ENGINE_CLUSTER || P->engine == GSK_ENGINE_AUTO) && !small && P->orth == 0 &&
-                    n <= 16384 && m <= 40;
+  const bool clus = !small && P->orth == 0 && m <= 40 &&
+                    ((P->engine == GSK_ENGINE_AUTO && n <= GSK_CLUSTER_AUTO_GMRES) ||
+                     (P->engine == GSK_ENGINE_CLUSTER && n <= GSK_CLUSTER_NMAX));
   if (!small && !clus && (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d ||
       P->gkey_orth != P->orth)) {
     for (auto& g : P->ggraph)

@@ -245,7 +245,12 @@ int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, doubl
 // whole solve; the caller has set x = x0 and zeroed/initialised the state.
 int small_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x);
 int small_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h);
-// On-chip solvers on one thread-block cluster (cluster.cu) for n <= 16384; *used = 0
+#define GSK_CLUSTER_NMAX 65536        // rows the cluster solvers take (16 CTAs x 4096)
+// where engine AUTO picks them (measured, profiles/r01_small_timing.json): Bi-CGSTAB
+// up to 32768 rows (19.9 vs 24.0 us/it; 28.3 vs 24.6 at 40000), GMRES up to 65536
+#define GSK_CLUSTER_AUTO_BICG 32768
+#define GSK_CLUSTER_AUTO_GMRES 65536
+// On-chip solvers on one thread-block cluster (cluster.cu) for n <= 65536; *used = 0
 // when the system does not fit (the caller then runs the graph path).
 int cluster_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);
 int cluster_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h, int* used);

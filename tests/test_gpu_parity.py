@@ -489,7 +489,8 @@ def test_solver_argument_errors():
                       oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-9, 300))
 
 
-CLUSTER = [("C1", None), ("C2", 50), ("C3", 16), ("C5", 96), ("P1", None), ("C4", 24)]
+CLUSTER = [("C1", None), ("C2", 50), ("C3", 16), ("C5", 96), ("P1", None), ("C4", 24), ("C3", 32), ("C2", 200),
+           ("P4conv", None)]
 
 
 @pytest.mark.parametrize("name,N", CLUSTER)
@@ -498,7 +499,7 @@ def test_cluster_engine_parity(name, N):
     reductions, n <= 16384, ragged n included): Bi-CGSTAB and MGS GMRES bit-exact
     against the oracle, with and without frame weights."""
     s, val, b, _ = system(name, N, 2)
-    if s["n"] > 16384:
+    if s["n"] > 65536:
         pytest.skip("beyond one cluster")
     A = gsk.CSR(s["row_ptr"], s["col"], val)
     P = gsk.Plan(A, engine="cluster")

@@ -12,7 +12,7 @@ import paper_0812_2769_b200 as gsk  # noqa: E402
 import workloads  # noqa: E402
 
 CASES = [("C1", None, 20), ("C2", 40, 30), ("C2", 64, 30), ("C3", 16, 30), ("C5", 64, 50), ("C5", 96, 30),
-         ("P1", None, 10)]
+         ("P1", None, 10), ("C3", 24, 30), ("C3", 32, 30), ("C2", 200, 30), ("P4conv", None, 10)]
 
 
 def main(out):
