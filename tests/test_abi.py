@@ -47,3 +47,18 @@ def test_library_is_sm100a():
 def test_no_cpu_fallback():
     with pytest.raises(RuntimeError):
         gsk.CSR([0, 1], [0], [1.0])
+
+
+def test_header_enums_match_binding():
+    """The binding's option tables equal the enum values include/gsk.h declares."""
+    text = open(os.path.join(ROOT, "include", "gsk.h")).read()
+    vals = {k: int(v) for k, v in re.findall(r"\b(GSK_[A-Z0-9_]+)\s*=\s*(-?\d+)", text)}
+    from paper_0812_2769_b200 import _gsk
+    assert _gsk.FMT == {"csr": vals["GSK_FMT_CSR"], "sell": vals["GSK_FMT_SELL"]}
+    assert _gsk.SCHEDULE == {"auto": vals["GSK_BICG_AUTO"], "fused": vals["GSK_BICG_FUSED"],
+                             "split": vals["GSK_BICG_SPLIT"]}
+    assert _gsk.ORTH == {"mgs": vals["GSK_ORTH_MGS"], "cgs2": vals["GSK_ORTH_CGS2"]}
+    assert _gsk.ENGINE == {"auto": vals["GSK_ENGINE_AUTO"], "graph": vals["GSK_ENGINE_GRAPH"],
+                           "coop": vals["GSK_ENGINE_COOP"], "small": vals["GSK_ENGINE_SMALL"],
+                           "cluster": vals["GSK_ENGINE_CLUSTER"]}
+    assert vals["GSK_OK"] == _gsk.GSK_OK == 0
