@@ -277,6 +277,7 @@ struct OpS1 {
   BicgState* st;
   __device__ bool begin() { return !st->done; }
   __device__ const double* vin(int) const { return rh; }
+  __device__ const double* gathered() const { return p; }  // the one vector gather() reads
   __device__ double gather(int c) const { return L::ld(p + c); }
   __device__ void row(int i, double y, const double (&x)[NV], double (&c)[1]) const {
     v[i] = y;
@@ -331,6 +332,7 @@ struct OpS3 {
   BicgState* st;
   __device__ bool begin() { return !st->done; }
   __device__ const double* vin(int) const { return s_; }
+  __device__ const double* gathered() const { return s_; }  // the one vector gather() reads
   __device__ double gather(int c) const { return L::ld(s_ + c); }
   __device__ void row(int i, double y, const double (&x)[NV], double (&c)[2]) const {
     t[i] = y;

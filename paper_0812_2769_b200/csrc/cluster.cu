@@ -3,8 +3,10 @@
 // of up to 16 x 4096 rows (the paper's Problem 1 at 128 x 128 is 16384 rows).
 //
 // CTA c of the cluster owns the aligned row block [c B, (c+1) B) (B a power of two,
-// <= 4096), rows c B + 1024 k + t for thread t.  A pass: the rows (SpMV gathers read the
-// vectors from global memory through L2: they were written by other CTAs), a warp
+// <= 4096), rows c B + 1024 k + t for thread t.  Bi-CGSTAB keeps its six vectors in the
+// CTAs' shared memory (each CTA its block; SpMV gathers of another CTA's rows go
+// through distributed shared memory), GMRES its basis in global memory (L2; gathers of
+// rows written by other CTAs bypass L1).  A pass: the rows, a warp
 // butterfly per 32 rows and the CTA's tree over its warps (a canonical subtree, the
 // block being aligned), the CTA value parked in shared memory, ONE cluster barrier
 // (hardware, release/acquire at cluster scope: vectors and CTA values visible), then
@@ -35,7 +37,16 @@ struct ClusterRed {
   double cpart[2][MAXD];           // this CTA's block value, double-buffered by reducing pass
 };
 
+template <class Op, class = void>
+struct Gathers : std::false_type {};
 template <class Op>
+struct Gathers<Op, std::void_t<decltype(std::declval<Op>().gathered())>> : std::true_type {};
+
+// DSM: the vectors live in the CTAs' shared memory (each CTA its own block, addressed
+// through a base pointer offset by -r0 so that operators index them by global row);
+// an operator's gathered vector is then read from the owning CTA's shared memory —
+// local, or through distributed shared memory for rows of another CTA.
+template <bool DSM = false, class Op>
 __device__ __forceinline__ void cluster_pass(const CsrView& A, int n, int r0, int B, Op op, ClusterRed& R,
                                              int& par) {
   constexpr int D = Op::D;
@@ -54,7 +65,19 @@ __device__ __forceinline__ void cluster_pass(const CsrView& A, int n, int r0, in
       for (int d = 0; d < DD; ++d) cc[d] = 0.0;
       if (k * CL_T + t < B && i < n) {
         double y = 0.0;
-        if constexpr (Op::kSpmv) {  // AC-3 chain in CSR order
+        if constexpr (Op::kSpmv && DSM && Gathers<Op>::value) {  // AC-3 chain, DSMEM gathers
+          const double* gb = op.gathered() + r0;  // this CTA's block of the gathered vector
+          const unsigned me = cluster.block_rank();
+          const int lgB = __ffs(B) - 1;
+          const int e = __ldg(A.rp + i + 1);
+          for (int q = __ldg(A.rp + i); q < e; ++q) {
+            const int c = __ldg(A.ci + q);
+            const unsigned owner = (unsigned)c >> lgB;
+            const int off = c - (int)(owner << lgB);
+            const double xc = owner == me ? gb[off] : cluster.map_shared_rank(gb, owner)[off];
+            y = __fma_rn(__ldg(A.v + q), xc, y);
+          }
+        } else if constexpr (Op::kSpmv) {  // AC-3 chain in CSR order
           const int e = __ldg(A.rp + i + 1);
           for (int q = __ldg(A.rp + i); q < e; ++q) y = __fma_rn(__ldg(A.v + q), op.gather(__ldg(A.ci + q)), y);
         }
@@ -118,23 +141,25 @@ __device__ __forceinline__ void cluster_pass(const CsrView& A, int n, int r0, in
   }
 }
 
-// ---- Bi-CGSTAB: split schedule, vectors in global memory (L2) ---------------------------
+// ---- Bi-CGSTAB: split schedule, vectors in the cluster's shared memory ---------------------
 struct ClusterBicgArgs {
   CsrView csr;
   int n, B;
   const double *b, *w;
-  double *x, *hist, *V;  // V: r, r^, p, -, v, -, t and s at V + 3n (the graph path's layout)
+  double *x, *hist;
   BicgState* st_out;
   double tol;
   int maxit;
 };
 
 __global__ void __launch_bounds__(CL_T, 1) cluster_bicgstab(ClusterBicgArgs a) {
+  extern __shared__ double vec[];  // this CTA's rows of r, r^, p, v, s, t (B each)
   __shared__ BicgState st;
   __shared__ ClusterRed R;
-  const int n = a.n, r0 = (int)cg::this_cluster().block_rank() * a.B;
-  const size_t nn = (size_t)n;
-  double *r = a.V, *rh = a.V + nn, *p = a.V + 2 * nn, *s = a.V + 3 * nn, *v = a.V + 4 * nn, *t = a.V + 6 * nn;
+  const int n = a.n, B = a.B, r0 = (int)cg::this_cluster().block_rank() * B;
+  // base pointers offset by -r0: operators index the vectors by global row
+  double *r = vec - r0, *rh = vec + B - r0, *p = vec + 2 * B - r0, *v = vec + 3 * B - r0, *s = vec + 4 * B - r0,
+         *t = vec + 5 * B - r0;
   if (threadIdx.x == 0) {
     st = BicgState{};
     st.tol = a.tol;
@@ -142,15 +167,15 @@ __global__ void __launch_bounds__(CL_T, 1) cluster_bicgstab(ClusterBicgArgs a) {
   }
   __syncthreads();
   int par = 0;
-  cluster_pass(a.csr, n, r0, a.B, OpInit<LdCG>{a.x, a.b, a.w, r, rh, p, v, a.hist, &st}, R, par);
+  cluster_pass<true>(a.csr, n, r0, B, OpInit<LdCG>{a.x, a.b, a.w, r, rh, p, v, a.hist, &st}, R, par);
   while (!(st.done && !st.halfstep)) {
-    cluster_pass(a.csr, n, r0, a.B, OpS0{r, v, p, &st, 0, 0}, R, par);
-    cluster_pass(a.csr, n, r0, a.B, OpS1<LdCG>{p, rh, v, &st}, R, par);
-    cluster_pass(a.csr, n, r0, a.B, OpS2{r, v, a.w, s, a.hist, &st, 0}, R, par);
-    cluster_pass(a.csr, n, r0, a.B, OpS3<LdCG>{s, t, &st}, R, par);
-    cluster_pass(a.csr, n, r0, a.B, OpS4{s, p, t, rh, a.w, a.x, r, a.hist, &st, 0, 0, 0}, R, par);
+    cluster_pass<true>(a.csr, n, r0, B, OpS0{r, v, p, &st, 0, 0}, R, par);
+    cluster_pass<true>(a.csr, n, r0, B, OpS1<LdPlain>{p, rh, v, &st}, R, par);
+    cluster_pass<true>(a.csr, n, r0, B, OpS2{r, v, a.w, s, a.hist, &st, 0}, R, par);
+    cluster_pass<true>(a.csr, n, r0, B, OpS3<LdPlain>{s, t, &st}, R, par);
+    cluster_pass<true>(a.csr, n, r0, B, OpS4{s, p, t, rh, a.w, a.x, r, a.hist, &st, 0, 0, 0}, R, par);
   }
-  cluster_pass(a.csr, n, r0, a.B, OpFinal<LdCG>{a.x, a.b, a.w, &st}, R, par);
+  cluster_pass<true>(a.csr, n, r0, B, OpFinal<LdCG>{a.x, a.b, a.w, &st}, R, par);
   if (cg::this_cluster().block_rank() == 0 && threadIdx.x == 0) *a.st_out = st;
 }
 
@@ -166,10 +191,11 @@ static int cluster_geometry(int n, int* B) {
   return cs;
 }
 
-static cudaError_t launch_cluster(const void* kern, int cs, void** args, cudaStream_t s) {
+static cudaError_t launch_cluster(const void* kern, int cs, void** args, cudaStream_t s, size_t smem = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs);
   cfg.blockDim = dim3(CL_T);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -190,11 +216,13 @@ int cluster_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, do
   static bool attr = false;
   if (!attr) {
     GSK_CUDA(cudaFuncSetAttribute(cluster_bicgstab, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    GSK_CUDA(cudaFuncSetAttribute(cluster_bicgstab, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(6 * sizeof(double) * CL_RPT * CL_T)));
     attr = true;
   }
-  ClusterBicgArgs a{P->csr, n, B, b, P->weights, x, P->hist_d, P->bvec, P->bstate, tol, maxit};
+  ClusterBicgArgs a{P->csr, n, B, b, P->weights, x, P->hist_d, P->bstate, tol, maxit};
   void* args[] = {&a};
-  GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_bicgstab), cs, args, P->st));
+  GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_bicgstab), cs, args, P->st, 6 * sizeof(double) * B));
   GSK_LAUNCHED(1);
   *used = 1;
   return GSK_OK;
