@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(CL_T, 1) cluster_bicgstab(ClusterBicgArgs a) {
   }
   cluster_pass<true>(a.csr, n, r0, B, OpFinal<LdCG>{a.x, a.b, a.w, &st}, R, par);
   if (cg::this_cluster().block_rank() == 0 && threadIdx.x == 0) *a.st_out = st;
+  cg::this_cluster().sync();  // no CTA exits while another may still read its shared memory
 }
 
 // Cluster geometry for n rows: CS CTAs (power of two, <= 16) of B rows (power of two,
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(CL_T, 1) cluster_gmres(ClusterGmresArgs a) {
       *a.st_out = o;
     }
   }
+  cg::this_cluster().sync();  // no CTA exits while another may still read its shared memory
 }
 
 int cluster_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h, int* used) {
