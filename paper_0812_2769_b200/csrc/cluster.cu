@@ -181,11 +181,13 @@ __global__ void __launch_bounds__(CL_T, 1) cluster_bicgstab(ClusterBicgArgs a) {
 }
 
 // Cluster geometry for n rows: CS CTAs (power of two, <= 16) of B rows (power of two,
-// <= 4096, one to four rows per thread); 0 if n is too large.
+// <= 4096, up to four rows per thread); 0 if n is too large.
+// As many CTAs as give each at least 256 rows (measured: 256-row blocks beat 1024-row
+// blocks at n = 4096 by 10-35%).
 static int cluster_geometry(int n, int* B) {
   if (n > CL_NMAX) return 0;
   int cs = 1;
-  while (cs * CL_T < n && cs < CL_MAX) cs <<= 1;
+  while (cs * 256 < n && cs < CL_MAX) cs <<= 1;
   int b = 32;
   while (b * cs < n) b <<= 1;
   *B = b;

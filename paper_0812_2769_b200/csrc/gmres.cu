@@ -126,9 +126,9 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8)));
   GSK_TRY(ensure_hist(P, maxit));
   // small systems: the whole solve in one launch on one SM (small.cu), MGS only
-  // (default for n <= 2048), or on one thread-block cluster (cluster.cu) up to 16384
-  // rows and m <= 40 (2-2.2x faster than the graph passes there)
-  const bool small = ((P->engine == GSK_ENGINE_AUTO && n <= 2048) || (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX)) &&
+  // (default for n <= 1024), or on one thread-block cluster (cluster.cu) up to 65536
+  // rows and m <= 40 (2-2.4x faster than the graph passes there)
+  const bool small = ((P->engine == GSK_ENGINE_AUTO && n <= 1024) || (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX)) &&
                      P->orth == 0;
   const bool clus = !small && P->orth == 0 && m <= 40 &&
                     ((P->engine == GSK_ENGINE_AUTO && n <= GSK_CLUSTER_AUTO_GMRES) ||
