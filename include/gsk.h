@@ -79,9 +79,10 @@ typedef struct gsk_opts {
                            slower on B200 at C4: DESIGN.md §5) */
   int32_t engine;       /* how the solvers run (all engines give bit-identical results):
                            GSK_ENGINE_AUTO (default) = one launch for the whole solve on
-                           one CTA (n <= 2048) or on one thread-block cluster (Bi-CGSTAB
-                           n <= 32768, GMRES with MGS and m <= 40 n <= 65536), where each
-                           is measured faster, else graph-replayed passes; GSK_ENGINE_GRAPH = always the
+                           one CTA (Bi-CGSTAB n <= 2048, MGS GMRES n <= 1024) or on one
+                           thread-block cluster (Bi-CGSTAB n <= 32768, MGS GMRES with
+                           m <= 40 n <= 65536), where each is measured faster, else
+                           graph-replayed passes; GSK_ENGINE_GRAPH = always the
                            passes; GSK_ENGINE_COOP = cooperative multi-CTA Bi-CGSTAB for
                            n <= 2^19 (opt-in); GSK_ENGINE_SMALL = the one-CTA solver
                            whenever n <= GSK_SMALL_NMAX; GSK_ENGINE_CLUSTER = the cluster
