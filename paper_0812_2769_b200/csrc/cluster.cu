@@ -41,6 +41,15 @@ template <class Op, class = void>
 struct Gathers : std::false_type {};
 template <class Op>
 struct Gathers<Op, std::void_t<decltype(std::declval<Op>().gathered())>> : std::true_type {};
+// gather(c) = gxform(gathered()[c]) for ops that transform the gathered value
+template <class Op, class = void>
+struct GXform {
+  __device__ static double apply(const Op&, double v) { return v; }
+};
+template <class Op>
+struct GXform<Op, std::void_t<decltype(std::declval<Op>().gxform(0.0))>> {
+  __device__ static double apply(const Op& op, double v) { return op.gxform(v); }
+};
 
 // DSM: the vectors live in the CTAs' shared memory (each CTA its own block, addressed
 // through a base pointer offset by -r0 so that operators index them by global row);
@@ -74,7 +83,7 @@ __device__ __forceinline__ void cluster_pass(const CsrView& A, int n, int r0, in
             const int c = __ldg(A.ci + q);
             const unsigned owner = (unsigned)c >> lgB;
             const int off = c - (int)(owner << lgB);
-            const double xc = owner == me ? gb[off] : cluster.map_shared_rank(gb, owner)[off];
+            const double xc = GXform<Op>::apply(op, owner == me ? gb[off] : cluster.map_shared_rank(gb, owner)[off]);
             y = __fma_rn(__ldg(A.v + q), xc, y);
           }
         } else if constexpr (Op::kSpmv) {  // AC-3 chain in CSR order
@@ -241,7 +250,9 @@ struct ClusterGmresArgs {
   GmresState* st_out;
 };
 
+template <bool SMEMW>
 __global__ void __launch_bounds__(CL_T, 1) cluster_gmres(ClusterGmresArgs a) {
+  extern __shared__ double wsm[];  // SMEMW: this CTA's rows of the m+1 basis vectors
   __shared__ GmresState st;
   __shared__ ClusterRed R;
   constexpr int M = CL_MMAX;
@@ -262,20 +273,23 @@ __global__ void __launch_bounds__(CL_T, 1) cluster_gmres(ClusterGmresArgs a) {
     st.c2 = st.c1 + M;
   }
   __syncthreads();
-  auto slot = [&](int j) { return a.W + (size_t)(j - 1) * n; };
+  // basis slot j: global (stride n) or this CTA's shared block (stride B, base -r0)
+  double* const W0 = SMEMW ? wsm - r0 : a.W;
+  const size_t ws = SMEMW ? (size_t)a.B : (size_t)n;
+  auto slot = [&](int j) { return W0 + (size_t)(j - 1) * ws; };
   int par = 0;
-  cluster_pass(a.csr, n, r0, a.B, OpGResid<LdCG>{a.x, a.b, a.w, a.W, a.hist, &st, 1}, R, par);
+  cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpGResid<LdCG>{a.x, a.b, a.w, slot(1), a.hist, &st, 1}, R, par);
   const long long maxc = (long long)st.maxit + 2;
   for (long long c = 0; c < maxc && !st.done; ++c) {
     for (int j = 1; j <= m && !st.done && !st.cycle_stop; ++j) {
-      cluster_pass(a.csr, n, r0, a.B, OpCgsS<LdCG>{slot(j), slot(j + 1), &st, j, 0}, R, par);
-      cluster_pass(a.csr, n, r0, a.B, OpH1{slot(j + 1), slot(1), &st, j, 0}, R, par);
+      cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpCgsS<LdCG>{slot(j), slot(j + 1), &st, j, 0}, R, par);
+      cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpH1{slot(j + 1), slot(1), &st, j, 0}, R, par);
       for (int i = 1; i < j; ++i)
-        cluster_pass(a.csr, n, r0, a.B, OpMgs{slot(i), slot(i + 1), slot(j + 1), &st, i, j, 0, 0, 0}, R, par);
-      cluster_pass(a.csr, n, r0, a.B, OpLast{slot(j), slot(j + 1), a.hist, &st, j, 0, 0}, R, par);
+        cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpMgs{slot(i), slot(i + 1), slot(j + 1), &st, i, j, 0, 0, 0}, R, par);
+      cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpLast{slot(j), slot(j + 1), a.hist, &st, j, 0, 0}, R, par);
     }
-    cluster_pass(a.csr, n, r0, a.B, OpXupd<LdPlain>{a.W, a.x, &st, (size_t)n, 0, nullptr, nullptr}, R, par);
-    cluster_pass(a.csr, n, r0, a.B, OpGResid<LdCG>{a.x, a.b, a.w, a.W, a.hist, &st, 0}, R, par);
+    cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpXupd<LdPlain>{W0, a.x, &st, ws, 0, nullptr, nullptr}, R, par);
+    cluster_pass<SMEMW>(a.csr, n, r0, a.B, OpGResid<LdCG>{a.x, a.b, a.w, slot(1), a.hist, &st, 0}, R, par);
   }
   if (cg::this_cluster().block_rank() == 0) {
     if (threadIdx.x == 0) {  // scalars only (the report reads no arrays)
@@ -300,14 +314,22 @@ int cluster_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState&
   int B = 0;
   const int cs = cluster_geometry(n, &B);
   if (!cs || h.m > CL_MMAX) return GSK_OK;
+  constexpr size_t kWsm = 196 * 1024;  // basis in shared memory when it fits
+  const size_t wbytes = sizeof(double) * (size_t)(h.m + 1) * B;
+  const bool smemw = wbytes <= kWsm;
   static bool attr = false;
   if (!attr) {
-    GSK_CUDA(cudaFuncSetAttribute(cluster_gmres, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    GSK_CUDA(cudaFuncSetAttribute(cluster_gmres<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    GSK_CUDA(cudaFuncSetAttribute(cluster_gmres<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    GSK_CUDA(cudaFuncSetAttribute(cluster_gmres<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsm));
     attr = true;
   }
   ClusterGmresArgs a{P->csr, n, B, b, P->weights, x, P->W, P->hist_d, h, P->gstate};
   void* args[] = {&a};
-  GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_gmres), cs, args, P->st));
+  if (smemw)
+    GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_gmres<true>), cs, args, P->st, wbytes));
+  else
+    GSK_CUDA(launch_cluster(reinterpret_cast<const void*>(cluster_gmres<false>), cs, args, P->st));
   GSK_LAUNCHED(1);
   *used = 1;
   return GSK_OK;

@@ -319,7 +319,9 @@ struct OpCgsS {  // S: w = A v_j (no reduction)
     return true;
   }
   __device__ const double* vin(int) const { return nullptr; }
-  __device__ double gather(int c) const { return L::ld(Wj + c) * invj; }
+  __device__ const double* gathered() const { return Wj; }  // gather(c) = gxform(Wj[c])
+  __device__ double gxform(double v) const { return v * invj; }
+  __device__ double gather(int c) const { return gxform(L::ld(Wj + c)); }
   __device__ void row(int i, double y, const double (&)[1], double (&)[1]) const { Wn[i] = y; }
 };
 
