@@ -359,7 +359,7 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args)
+        e2e = measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args, dist)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, its_c, dt, cores = oracle_sample(s, cfg, m)
@@ -484,7 +484,7 @@ def run_sharded(args, rank, world, local):
         dist.destroy_process_group()
 
 
-def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args):
+def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args, dist=None):
     """Every step: pinned host -> device copy of the system, GS(2), plan build (SELL),
     both solves, x read back; timed with CUDA events on the current stream."""
     pin = {k: torch.from_numpy(np.ascontiguousarray(s[k])).pin_memory() for k in ("row_ptr", "col", "val", "b")}
@@ -518,6 +518,10 @@ def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if dist:  # whole job: every rank's replica, slowest rank's time
+        ms, its = reduce_over_ranks(ms, its, dist, "cuda")
+        h2d *= dist.get_world_size()
+        d2h *= dist.get_world_size()
     return {"value": its / (ms / 1e3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
 
