@@ -9,13 +9,21 @@ device (a11).  At N=1 the workload is BASELINE.json configs[3] (C4: 256^3, 7-poi
 upwind, 5 slabs, SELL-C-32-256; the headline roofline config), generated with the
 seeded recipe of DESIGN.md §3 and resident in HBM before timing.
 
+The GMRES(30) leg runs a fixed budget of 300 iterations (--gmres-maxit).
+
 value  = solver iterations per second (Bi-CGSTAB + GMRES iterations of the step,
          summed over ranks, / max-over-ranks device time); unit "iters/s".
 e2e    = the same through the public API with the system copied from pinned host
-         memory every step (plan rebuilt) and x read back.
-roofline: the dominant kernel (Bi-CGSTAB fused pass v = A p) — algorithmic bytes
-         12 nnz + 4(n+1) + 6*8n per launch / its CUDA-event time.
+         memory every step (plan rebuilt) and x read back (summed over ranks).
+roofline: the dominant kernel (the split schedule's S1 pass v = A p, <r^,v>) —
+         algorithmic bytes 12 nnz + 4(n+1) + 3*8n per launch / its
+         CUDA-event time inside the captured graphs; traffic from the committed ncu
+         capture (profiles/r01_ncu_traffic.json).
+extra  = SpMV and GS(2) rooflines, per-pass probes and time_to_tol (time to 1e-8 of
+         Bi-CGSTAB without scaling, with GS(1), GS(2) and two-sided scaling).
 --impl reference: the CPU oracle (oracle/) on a bounded sample of the same work.
+--shards P: one system in P row blocks: emulated on one GPU, or one
+         shard per rank over NCCL under torchrun ("scaling": "strong").
 Multi-GPU: the north star is one GPU; --gpus N runs N independent replicas
 (weak scaling, no data-path collective).
 """
