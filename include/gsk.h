@@ -132,7 +132,9 @@ int gsk_dot(int64_t n, const double *a, const double *b, double *result, void *s
 
 /* Plans: keep the SELL build, workspace and captured CUDA graphs out of repeated
  * solves.  The plan keeps A's pointers (not a copy) for CSR; for SELL it copies the
- * values, so rescaling A after gsk_plan_create needs gsk_plan_refresh. */
+ * values, so rescaling A after gsk_plan_create needs gsk_plan_refresh.  A plan runs on
+ * its own stream (ordered after / before the caller's stream by events) and is used by
+ * one host thread at a time; distinct plans may be used concurrently. */
 int gsk_plan_create(const gsk_csr *A, const gsk_opts *opts, gsk_plan **plan, void *stream);
 int gsk_plan_refresh(gsk_plan *plan, void *stream);
 int gsk_plan_spmv(gsk_plan *plan, const double *x, double *y, void *stream);

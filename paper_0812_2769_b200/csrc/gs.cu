@@ -5,6 +5,7 @@
 // segment in ascending column order (AC-4: p=2 fma chain + sqrt, p=1 running sum of
 // |a|, p>=3 repeated products + pow), the segment is rescaled in shared memory and
 // written back coalesced.  Bytes: 16 nnz + 4(n+1) + 24 n (read a, write a, r/w b, d).
+#include <mutex>
 #include "internal.cuh"
 
 namespace gsk {
@@ -149,7 +150,9 @@ static int launch_gs(int grid, cudaStream_t s, int n, const int* rp, const doubl
 }
 
 // Per-process device word for the zero-row flag (avoids a stream-ordered allocation
-// per call; calls are serialised by the stream synchronisation they end with).
+// per call).  Calls hold g_flag_mu from the reset to the read-back, so concurrent
+// callers on different streams / host threads never share it.
+static std::mutex g_flag_mu;
 static int* zero_row_flag(cudaStream_t s, int* err) {
   static int* flag = nullptr;
   if (!flag && cudaMalloc(&flag, sizeof(int)) != cudaSuccess) {
@@ -180,6 +183,7 @@ extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double
     return GSK_E_INVALID;
   }
   cudaStream_t s = as_stream(stream);
+  std::lock_guard<std::mutex> lock(g_flag_mu);
   int ferr = 0;
   int* dbad = zero_row_flag(s, &ferr);
   if (ferr) {
@@ -232,6 +236,7 @@ extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* va
     return GSK_E_INVALID;
   }
   cudaStream_t s = as_stream(stream);
+  std::lock_guard<std::mutex> lock(g_flag_mu);
   int ferr = 0;
   int* dbad = zero_row_flag(s, &ferr);
   if (ferr) {
