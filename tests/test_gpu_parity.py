@@ -513,3 +513,29 @@ def test_cluster_engine_parity(name, N):
                       oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 600, weights=w))
     assert_same_solve(Pw.gmres(b, m=20, tol=1e-9, maxit=200),
                       oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 200, weights=w))
+
+
+def test_concurrent_plans_two_threads():
+    """Two plans driven from two host threads at once (each on its own stream, the GIL
+    released inside the C calls): both solves stay bit-exact."""
+    import threading
+    jobs = [("C2", 64, "graph"), ("C3", 20, "graph"), ("C4", 24, "auto"), ("P1", 64, "auto")]
+    res = {}
+
+    def work(name, N, engine):
+        s, val, b, _ = system(name, N, 2)
+        P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), engine=engine)
+        for _ in range(3):
+            g = P.bicgstab(b, tol=1e-9, maxit=400)
+            h = P.gmres(b, m=20, tol=1e-9, maxit=100)
+        torch.cuda.synchronize()
+        res[name] = (s, val, b, g, h)
+
+    threads = [threading.Thread(target=work, args=j) for j in jobs]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for name, (s, val, b, g, h) in res.items():
+        assert_same_solve(g, oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400))
+        assert_same_solve(h, oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 100))
