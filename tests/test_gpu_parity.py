@@ -539,3 +539,14 @@ def test_concurrent_plans_two_threads():
     for name, (s, val, b, g, h) in res.items():
         assert_same_solve(g, oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400))
         assert_same_solve(h, oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 100))
+
+
+@pytest.mark.parametrize("name,N", [("C4", 24), ("C3", 20), ("C2", 100)])
+def test_sell_dict_solvers(name, N):
+    """Solvers on SELL-D plans (uint8 column index into per-chunk deltas): the same bits."""
+    s, val, b, _ = system(name, N, 2)
+    P = gsk.Plan(gsk.CSR(s["row_ptr"], s["col"], val), fmt="sell", sell_index="dict", engine="graph")
+    assert P.sell_dict() is not None
+    assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=400), oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400))
+    assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=100),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100))
