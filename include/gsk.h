@@ -195,8 +195,9 @@ typedef struct gsk_shard_opts {
   int32_t count;     /* shards held by this process: P (all of them, one GPU) or 1
                         (one shard per process, one process per GPU) */
   int32_t pad_;
-  void *nccl_comm;   /* ncclComm_t over the P processes when count == 1 < P, else NULL
-                        (gsk_nccl_comm_create); not owned by the plan */
+  void *nccl_comm;   /* ncclComm_t over the P processes (count == 1: this process holds
+                        shard `first`), or NULL (count == P: all shards on this GPU);
+                        from gsk_nccl_comm_create, not owned by the plan */
 } gsk_shard_opts;
 
 /* Host-only layout helpers (no GPU needed).  Rows of shard r; GSK_E_INVALID if P is not

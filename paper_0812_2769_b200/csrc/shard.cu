@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(256) halo_kernel(HaloList L) {
 template <class Base>
 static int shard_halo(gsk_plan* P, Base base, cudaStream_t s) {
   ShardSet* S = P->shards;
-  if (S->P == 1) return GSK_OK;
-  if (S->count == S->P) {
+  if (!S->comm) {  // every shard on this GPU: device copies
+    if (S->P == 1) return GSK_OK;
     HaloList L{};
     int c = 0;
     for (int i = 0; i < S->count; ++i) {
@@ -229,7 +229,7 @@ static int shard_pass(gsk_plan* P, MakeOp mk, cudaStream_t s, cudaEvent_t pe0 = 
     }
   }
   if constexpr (Op::D > 0) {
-    if (S->count < S->P)
+    if (S->comm)
       GSK_NCCL(nccl()->allGather(S->gath + (size_t)S->first * MAXD, S->gath, MAXD, ncclDouble, S->comm, s));
     GSK_CUDA(launch_k(finish_global_kernel<Op>, 1, 32, 0, s, mk(0), (const double*)S->gath, S->P));
     GSK_LAUNCHED(1);
@@ -564,11 +564,13 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
   const int P = so->nshards;
   int64_t lo0, hi0;
   GSK_TRY(shard_rows(A->n, P, 0, &lo0, &hi0));
-  const bool local = so->count == P && so->first == 0;
-  const bool remote = so->count == 1 && P > 1 && so->first >= 0 && so->first < P && so->nccl_comm;
+  // one process holding every shard (no communicator), or one shard per process over
+  // NCCL (P = 1 with a communicator runs the NCCL code path on a single GPU)
+  const bool local = !so->nccl_comm && so->count == P && so->first == 0;
+  const bool remote = so->nccl_comm && so->count == 1 && so->first >= 0 && so->first < P;
   if (!local && !remote) {
-    set_error("gsk_plan_create_sharded: need count == nshards (all shards on this GPU) or count == 1 with an "
-              "NCCL communicator");
+    set_error("gsk_plan_create_sharded: need count == nshards without a communicator (all shards on this GPU) "
+              "or count == 1 with an NCCL communicator");
     return GSK_E_INVALID;
   }
   if (remote && !nccl()) {

@@ -550,3 +550,29 @@ def test_sell_dict_solvers(name, N):
     assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=400), oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400))
     assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=100),
                       oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100))
+
+
+def test_sharded_nccl_single_rank():
+    """The multi-process code path (halo send/recv groups, ncclAllGather of the shard
+    values, all inside the captured graphs) on a 1-rank NCCL communicator: bit-exact."""
+    import ctypes
+    lib = gsk.load()
+    buf = ctypes.create_string_buffer(128)
+    assert lib.gsk_nccl_unique_id(buf) == 0
+    h = ctypes.c_void_p()
+    assert lib.gsk_nccl_comm_create(ctypes.c_char_p(bytes(buf.raw)), 1, 0, ctypes.byref(h)) == 0
+
+    class Comm:
+        world, rank = 1, 0
+
+    Comm.h = h
+    s, val, b, _ = system("C3", 20, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    for fmt in ("csr", "sell"):
+        SP = gsk.ShardedPlan(A, fmt=fmt, comm=Comm)
+        assert_same_solve(SP.bicgstab(b, tol=1e-9, maxit=400),
+                          oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400))
+        assert_same_solve(SP.gmres(b, m=20, tol=1e-9, maxit=100),
+                          oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 100))
+        SP.close()
+    assert lib.gsk_nccl_comm_destroy(h) == 0
