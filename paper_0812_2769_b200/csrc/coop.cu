@@ -124,7 +124,7 @@ __device__ __forceinline__ void coop_pass(const CoopArgs& a, Op op, double* sy, 
     }
     if constexpr (D > 0) {
       __syncthreads();
-      if (warp == 0) cta_partial<D>(wp, a.wpc, a.part + par * MAXD * 256, 256);
+      if (warp == 0) cta_partial<D>(wp, a.wpc, a.part + par * MAXD * 256, 256, blockIdx.x);
     }
   }
   grid_barrier(a.bar, a.bar + 1);  // pass results (vectors, partials) visible grid-wide

@@ -274,7 +274,7 @@ __device__ __forceinline__ void warp_leaves_multi(double (&c)[RPT][D], double* w
 // final + 0.0 of AC-5 canonicalises a zero's sign.
 constexpr int WMAX = 16;  // windows per CTA (SpMV passes, GSK_WPC)
 template <int D>
-__device__ __forceinline__ void cta_partial(const double* wp, int nw, double* part, int stride) {
+__device__ __forceinline__ void cta_partial(const double* wp, int nw, double* part, int stride, int slot) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -285,7 +285,7 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
     }
 #pragma unroll
     for (int off = 1; off < WMAX; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
-    if (lane == 0) part[(size_t)d * stride + blockIdx.x] = u;
+    if (lane == 0) part[(size_t)d * stride + slot] = u;
   }
 }
 
@@ -293,16 +293,21 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 // FMT 1/2/3: SpMV pass over wpc windows (CSR, SELL, SELL with column dictionary).
 template <int FMT, int RPT, class Op>
 __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
-    pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride) {
+    pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride, int rev) {
   pdl_enter();
   if (!op.begin()) return;
+  // rev: CTAs take their row blocks in descending order (the tile's partial keeps its
+  // slot, so the reduction tree is unchanged).  Consecutive passes alternate the
+  // direction, so a pass starts on the rows whose vectors the previous pass touched
+  // last, which are still in L2.
+  const int bx = rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
   constexpr int D = Op::D;
   constexpr int DD = D > 0 ? D : 1;
   constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
   __shared__ PassSmem<FMT> sm;
   const int t = threadIdx.x, warp = t >> 5;
   if constexpr (FMT == 0) {
-    const int r0 = blockIdx.x * (TB * RPT);
+    const int r0 = bx * (TB * RPT);
     double v[RPT][NVA];
 #pragma unroll
     for (int w = 0; w < RPT; ++w) {
@@ -320,10 +325,10 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     if constexpr (D > 0) {
       warp_leaves_multi<RPT, D>(cc, sm.wp);
       __syncthreads();
-      if (warp == 0) cta_partial<D>(sm.wp, RPT, part, stride);
+      if (warp == 0) cta_partial<D>(sm.wp, RPT, part, stride, bx);
     }
   } else {
-    const int rb = blockIdx.x * wpc * TB;
+    const int rb = bx * wpc * TB;
     constexpr bool kPre = PassOcc<FMT, Op>::kPrefetch;
     constexpr bool kAsync = PassOcc<FMT, Op>::kAsync;
     // own-row operands of window w -> sm.vin[w & 1] (one commit group per window; each
@@ -369,7 +374,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     }
     if constexpr (D > 0) {
       __syncthreads();
-      if (warp == 0) cta_partial<D>(sm.wp, wpc, part, stride);
+      if (warp == 0) cta_partial<D>(sm.wp, wpc, part, stride, bx);
     }
   }
 }

@@ -135,6 +135,7 @@ struct gsk_plan {
   double probe_ms[NPROBE] = {};
   int64_t probe_n[NPROBE] = {};
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  unsigned pass_seq = 0;  // passes launched (captured): parity = CTA order of the next
   gsk::ShardSet* shards = nullptr;  // non-null: a row-block sharded plan (shard.cu)
 };
 
@@ -143,7 +144,8 @@ namespace gsk {
 // plan's format (CSR or SELL) or a pure vector pass.
 int num_sms();
 bool pdl_enabled();  // GSK_PDL=0 in the environment disables programmatic launches
-int spmv_wpc_max();  // windows per CTA of SpMV passes (8; GSK_WPC overrides, pow2 <= 16)
+int spmv_wpc_max();
+bool pass_alternate();  // alternate the CTA order of consecutive passes (GSK_ALT=0: off)  // windows per CTA of SpMV passes (8; GSK_WPC overrides, pow2 <= 16)
 
 // Kernel launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KArgs, typename... Args>
@@ -171,16 +173,17 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
   const int n = P->geo.n;
   const int sms = num_sms();
   int ntiles;
+  const int rev = pass_alternate() ? (P->pass_seq++ & 1) : 0;
   if (pe0) GSK_CUDA(cudaEventRecordWithFlags(pe0, s, cudaEventRecordExternal));
   if constexpr (!Op::kSpmv) {
     // RPT rows per thread when that still leaves >= 2 CTAs per SM, else 2
     constexpr int R = VecRpt<Op::NV>::value;
     if ((long long)n >= 2LL * TB * R * sms) {
       ntiles = (n + TB * R - 1) / (TB * R);
-      GSK_CUDA(launch_k(pass_kernel<0, R, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, R, op, P->part, P->pstride));
+      GSK_CUDA(launch_k(pass_kernel<0, R, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, R, op, P->part, P->pstride, rev));
     } else {
       ntiles = (n + TB * 2 - 1) / (TB * 2);
-      GSK_CUDA(launch_k(pass_kernel<0, 2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, 2, op, P->part, P->pstride));
+      GSK_CUDA(launch_k(pass_kernel<0, 2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, 2, op, P->part, P->pstride, rev));
     }
   } else {
     const int windows = (n + TB - 1) / TB;
@@ -188,11 +191,11 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
     if (P->fmt == GSK_FMT_SELL && P->sell.dict)
-      GSK_CUDA(launch_k(pass_kernel<3, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
+      GSK_CUDA(launch_k(pass_kernel<3, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     else if (P->fmt == GSK_FMT_SELL)
-      GSK_CUDA(launch_k(pass_kernel<2, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
+      GSK_CUDA(launch_k(pass_kernel<2, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     else
-      GSK_CUDA(launch_k(pass_kernel<1, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride));
+      GSK_CUDA(launch_k(pass_kernel<1, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
   }
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));

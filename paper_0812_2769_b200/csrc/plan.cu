@@ -47,6 +47,15 @@ int spmv_wpc_max() {
   return w;
 }
 
+bool pass_alternate() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("GSK_ALT");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
