@@ -222,13 +222,13 @@ struct OpP3 {
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int i, double, const double (&v)[NV], double (&c)[2]) const {
     if (half) {
-      x[i] = __fma_rn(alpha, v[1], v[0]);
+      st_cold(x + i, __fma_rn(alpha, v[1], v[0]));
       c[0] = 0.0;
       c[1] = 0.0;
       return;
     }
     const double s = __fma_rn(-alpha, v[2], v[3]);
-    x[i] = __fma_rn(omega, s, __fma_rn(alpha, v[1], v[0]));
+    st_cold(x + i, __fma_rn(omega, s, __fma_rn(alpha, v[1], v[0])));
     const double rr = __fma_rn(-omega, v[4], s);
     r[i] = rr;
     c[0] = v[5] * rr;
@@ -249,6 +249,7 @@ struct OpP3 {
 struct OpS0 {
   static constexpr int D = 0;
   static constexpr int NV = 3;
+  static constexpr unsigned kEvict = 0b101u;  // S1 reads p only: v, r evict-first
   static constexpr bool kSpmv = false;
   const double *r, *v;
   double* p;
@@ -271,6 +272,7 @@ template <class L = LdNC>
 struct OpS1 {
   static constexpr int D = 1;
   static constexpr int NV = 1;
+  static constexpr unsigned kEvict = 0b1u;  // S2 does not read r^
   static constexpr bool kSpmv = true;
   const double *p, *rh;
   double* v;
@@ -299,6 +301,7 @@ struct OpS1 {
 struct OpS2 {
   static constexpr int D = 1;
   static constexpr int NV = 3;
+  static constexpr unsigned kEvict = 0b111u;  // S3 reads only s
   static constexpr bool kSpmv = false;
   const double *r, *v, *w;
   double *s_, *hist;
@@ -347,6 +350,7 @@ struct OpS3 {
 struct OpS4 {
   static constexpr int D = 2;
   static constexpr int NV = 6;
+  static constexpr unsigned kEvict = 0b111101u;  // S0 reads r, p, v: only p kept
   static constexpr bool kSpmv = false;
   const double *s_, *p, *t, *rh, *w;
   double *x, *r, *hist;
@@ -367,13 +371,13 @@ struct OpS4 {
   __device__ double gather(int) const { return 0.0; }
   __device__ void row(int i, double, const double (&v)[NV], double (&c)[2]) const {
     if (half) {
-      x[i] = __fma_rn(alpha, v[1], v[0]);
+      st_cold(x + i, __fma_rn(alpha, v[1], v[0]));
       c[0] = 0.0;
       c[1] = 0.0;
       return;
     }
     const double s = v[2];
-    x[i] = __fma_rn(omega, s, __fma_rn(alpha, v[1], v[0]));
+    st_cold(x + i, __fma_rn(omega, s, __fma_rn(alpha, v[1], v[0])));
     const double rr = __fma_rn(-omega, v[3], s);
     r[i] = rr;
     c[0] = v[4] * rr;

@@ -75,6 +75,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Store of a result no pass reads soon (x in Bi-CGSTAB S4): evict-first in L2.
+__device__ __forceinline__ void st_cold(double* p, double v) {
+#ifndef GSK_NO_EVICT
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ldcs(const int* p) { return __ldcs(p); }
 

@@ -192,13 +192,32 @@ __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G
   return sy[threadIdx.x];
 }
 
+// Op::kEvict (optional): bit k set = own-row operand vin(k) is not read by the NEXT
+// pass, so the register-path load of it is evict-first (ld.global.cs) and
+// leaves L2 to the vectors the next pass reads (pass order).
+#ifndef GSK_NO_EVICT
+template <class Op, class = void>
+struct OpEvict {
+  static constexpr unsigned value = 0;
+};
+template <class Op>
+struct OpEvict<Op, std::void_t<decltype(Op::kEvict)>> {
+  static constexpr unsigned value = Op::kEvict;
+};
+#else
+template <class Op>
+struct OpEvict {
+  static constexpr unsigned value = 0;
+};
+#endif
+
 // Own-row operands of the Op for row i.
 template <class Op>
 __device__ __forceinline__ void load_vin(const Op& op, int i, double (&v)[Op::NV > 0 ? Op::NV : 1]) {
 #pragma unroll
   for (int k = 0; k < Op::NV; ++k) {
     const double* src = op.vin(k);
-    v[k] = src ? __ldg(src + i) : 0.0;
+    v[k] = src ? (((OpEvict<Op>::value >> k) & 1u) ? __ldcs(src + i) : __ldg(src + i)) : 0.0;
   }
 }
 

@@ -122,6 +122,7 @@ struct OpH1 {
 struct OpMgs {
   static constexpr int D = 1;
   static constexpr int NV = 3;
+  static constexpr unsigned kEvict = 0b001u;  // the next pass reads w and v_{i+1}, not v_i
   static constexpr bool kSpmv = false;
   const double *Wi, *Wi1;
   double* Wn;
@@ -237,6 +238,7 @@ static __device__ void arnoldi_finish(GmresState* S, double* hist, int j, double
 struct OpLast {
   static constexpr int D = 1;
   static constexpr int NV = 2;
+  static constexpr unsigned kEvict = 0b01u;  // S_{j+1} gathers w only
   static constexpr bool kSpmv = false;
   const double* Wj;
   double* Wn;
