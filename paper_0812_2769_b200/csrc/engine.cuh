@@ -635,14 +635,15 @@ struct MdotSmem {
 
 template <int FMT, class Op>
 __global__ void __launch_bounds__(TB, MDOT_MINB)
-    mdot_pass(CsrView csr, SellView sell, int n, int tpc, Op op, double* part, int stride) {
+    mdot_pass(CsrView csr, SellView sell, int n, int tpc, Op op, double* part, int stride, int rev) {
   pdl_enter();
   if (!op.begin()) return;
   __shared__ __align__(16) MdotSmem sm;
+  const int bx = rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;  // as pass_kernel
   const int J = op.nd;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int tl = 0; tl < tpc; ++tl) {
-    const int r0 = (blockIdx.x * tpc + tl) * MD_TILE;
+    const int r0 = (bx * tpc + tl) * MD_TILE;
     if (r0 >= n) {  // uniform: an all-padding tile
       for (int d = t; d < J; d += TB) sm.tp[tl * MDOT_MAX + d] = 0.0;
       continue;
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(TB, MDOT_MINB)
     double a[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) a[w] = w < tpc ? sm.tp[w * MDOT_MAX + d] : 0.0;
-    part[(size_t)d * stride + blockIdx.x] = tree8(a);
+    part[(size_t)d * stride + bx] = tree8(a);
   }
 }
 

@@ -226,13 +226,14 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
   int tpc = 8;  // tiles per CTA: as many as still leave >= 2 waves of CTAs
   while (tpc > 1 && (long long)tiles < (long long)tpc * MDOT_MINB * sms * 2) tpc >>= 1;
   const int ntiles = (tiles + tpc - 1) / tpc;
+  const int rev = pass_alternate() ? (P->pass_seq++ & 1) : 0;
   if (pe0) GSK_CUDA(cudaEventRecordWithFlags(pe0, s, cudaEventRecordExternal));
   if constexpr (!Op::kSpmv)
-    GSK_CUDA(launch_k(mdot_pass<0, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride));
+    GSK_CUDA(launch_k(mdot_pass<0, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride, rev));
   else if (P->fmt == GSK_FMT_SELL)
-    GSK_CUDA(launch_k(mdot_pass<2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride));
+    GSK_CUDA(launch_k(mdot_pass<2, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride, rev));
   else
-    GSK_CUDA(launch_k(mdot_pass<1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride));
+    GSK_CUDA(launch_k(mdot_pass<1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, tpc, op, P->mpart, P->pstride, rev));
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));
   GSK_CUDA(launch_k(mdot_finish<Op>, J, FIN_THREADS, 0, s, op, P->mpart, P->pstride, ntiles));

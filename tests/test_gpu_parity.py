@@ -576,3 +576,34 @@ def test_sharded_nccl_single_rank():
                           oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 100))
         SP.close()
     assert lib.gsk_nccl_comm_destroy(h) == 0
+
+
+def test_pass_order_does_not_change_results(tmp_path):
+    """Alternating CTA order of consecutive passes (pass order and L2) keeps
+    every partial in its slot: solves with GSK_ALT=0 (read once per process, hence the
+    subprocess) are bit-identical to the default alternating order."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import workloads, oracle, paper_0812_2769_b200 as gsk\n"
+        "s = workloads.generate('C3', N=32); vo, bo, _ = oracle.gs_scale(s['row_ptr'], s['val'], s['b'], 2)\n"
+        "P = gsk.Plan(gsk.CSR(s['row_ptr'], s['col'], vo), fmt='sell', engine='graph')\n"
+        "x1, h1, _ = P.bicgstab(bo, tol=1e-8, maxit=300)\n"
+        "x2, h2, _ = P.gmres(bo, m=30, tol=1e-8, maxit=120)\n"
+        "np.savez(%r, x1=x1.cpu().numpy(), h1=h1, x2=x2.cpu().numpy(), h2=h2)\n"
+    ) % (root, str(tmp_path / "alt.npz"))
+    for alt in ("0", "1"):
+        env = dict(os.environ, GSK_ALT=alt)
+        subprocess.run([sys.executable, "-c", code.replace("alt.npz", "alt%s.npz" % alt)], check=True,
+                       timeout=600, env=env)
+    a = np.load(tmp_path / "alt0.npz")
+    b = np.load(tmp_path / "alt1.npz")
+    for k in ("x1", "h1", "x2", "h2"):
+        assert np.array_equal(a[k], b[k]), k
+    s = workloads.generate("C3", N=32)
+    _, vo, bo, _ = system("C3", 32, 2)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 300)
+    assert np.array_equal(a["x1"], o[0])
