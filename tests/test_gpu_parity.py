@@ -607,3 +607,23 @@ def test_pass_order_does_not_change_results(tmp_path):
     _, vo, bo, _ = system("C3", 32, 2)
     o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 300)
     assert np.array_equal(a["x1"], o[0])
+
+
+def test_max_grid_512():
+    """Maximum-size case: C4's recipe at 512³ (134 M rows, 938 M nonzeros; int32 indices
+    hold up to 674³).  GS(2) and the first 3 Bi-CGSTAB iterations (SELL plan, the bench
+    launch configuration) bit-exact against the oracle.  tools/max_grid.py runs the same
+    up to 640³ (1.83 G nonzeros, 137 GB; profiles/r01_max_grid.jsonl)."""
+    free, total = torch.cuda.mem_get_info()
+    if total < 120 * 2**30:
+        pytest.skip("needs a 180 GB B200")
+    s = workloads.generate("C4", N=512)
+    A = gsk.CSR.from_system(s)
+    As, bs, _ = gsk.gs_scale(A, s["b"], 2)
+    vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    assert np.array_equal(cpu(As.val), vo) and np.array_equal(cpu(bs), bo)
+    del A
+    P = gsk.Plan(As, fmt="sell")
+    g = P.bicgstab(bs, tol=1e-8, maxit=3)
+    o = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 3)
+    assert_same_solve(g, o)
