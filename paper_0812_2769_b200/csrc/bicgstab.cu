@@ -13,10 +13,11 @@
 // p_old/v_old at neighbouring columns).  Recomputing p and s at the gather is the
 // same operation on the same operands as the stored value, so results are
 // bit-identical to the unfused algorithm (AC-6) while moving 2 B_A + 17 vectors
-// per iteration instead of 2 B_A + 19+.  Each pass ends in the canonical grid
-// reduction; the last CTA runs the scalar epilogue, so iterations run back to back
-// from a captured CUDA graph (poll iterations per replay) with one host check of
-// the `done` flag per replay.
+// per iteration instead of 2 B_A + 19.  The split schedule S0..S4 (below; the
+// default, measured faster on B200) keeps plain SpMV gathers.  Each reducing pass is
+// followed by a one-CTA finish kernel (canonical tree + scalar epilogue), so
+// iterations run back to back from a captured CUDA graph (K iterations per replay)
+// with one host check of the `done` flag per replay, NQ replays in flight.
 #include <cmath>
 #include <vector>
 #include "bicg_ops.cuh"
