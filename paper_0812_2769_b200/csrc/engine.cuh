@@ -61,6 +61,9 @@ struct PassSmem<2> {
 };
 template <>
 struct PassSmem<3> : PassSmem<2> {};
+struct PassSmemDirect {  // direct passes use no shared memory
+  double wp[1];
+};
 
 // Register budget per pass kind (CTAs per SM): SELL keeps 8 slots (col, val, x) in
 // flight per lane, vector passes RPT rows of NV operands; CSR is bounded by its
@@ -87,8 +90,18 @@ struct SellTuning<Op, std::void_t<decltype(Op::kSellMinBlocks)>> {
 #ifndef GSK_SELLD_DOT_MINB
 #define GSK_SELLD_DOT_MINB 4
 #endif
+#ifndef GSK_SELL_DIRECT
+#define GSK_SELL_DIRECT 1
+#endif
+constexpr bool SELL_DIRECT = GSK_SELL_DIRECT;
+
 template <int FMT, class Op>
 struct PassOcc {
+  // SELL passes without dot products run "direct": each lane finishes
+  // the row of its own SELL slot (operands, output) with no per-window barrier.
+  // (Measured with dots too, leaves parked by row in shared memory and reduced once
+  // per CTA: bit-exact, but S1 unchanged and S3 slower — 80 registers to not spill.)
+  static constexpr bool kDirect = SELL_DIRECT && FMT >= 2 && Op::D == 0;
   static constexpr int kMinBlocks = FMT == 1 ? 4
                                   : FMT == 3 ? (Op::D > 0 && SellTuning<Op>::minb == 4 ? GSK_SELLD_DOT_MINB
                                                                                        : SellTuning<Op>::minb)
@@ -123,14 +136,16 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
   return acc;
 }
 
-// SELL window core: lane l of warp w computes slot l of chunk r0/32 + w and scatters
-// the row's y to sy at its in-window offset (no barrier).
-template <bool DICT, class G>
-__device__ __forceinline__ void sell_window_store(const SellView& A, int r0, const G& g, double* sy) {
+// SELL window core: lane l of warp w computes slot l of chunk r0/32 + w and hands the
+// row's y with its in-window offset to sink(rl, y).
+template <bool DICT, class G, class S, class Pre>
+__device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, const G& g, const S& sink,
+                                                 const Pre& pre) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int c = (r0 >> 5) + warp;
   if (c < A.nchunks) {
     const int rl = A.roff[c * SELL_C + lane];
+    pre(rl);
     const int p0 = A.cptr[c], L = (A.cptr[c + 1] - p0) >> 5;
     const int base = p0 + lane;
     double acc = 0.0;
@@ -180,8 +195,14 @@ __device__ __forceinline__ void sell_window_store(const SellView& A, int r0, con
         if (col != A.pad) acc = __fma_rn(__ldcs(A.sval + base + k * SELL_C), g(col), acc);
       }
     }
-    sy[rl] = acc;
+    sink(rl, acc);
   }
+}
+
+// ... scattering y to sy at its in-window offset (no barrier).
+template <bool DICT, class G>
+__device__ __forceinline__ void sell_window_store(const SellView& A, int r0, const G& g, double* sy) {
+  sell_window_sink<DICT>(A, r0, g, [&](int rl, double y) { sy[rl] = y; }, [](int) {});
 }
 
 // y for row r0 + t of a SELL window (scatter through sy, one barrier).
@@ -323,9 +344,28 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
   constexpr int D = Op::D;
   constexpr int DD = D > 0 ? D : 1;
   constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
-  __shared__ PassSmem<FMT> sm;
+  constexpr bool kDirect = PassOcc<FMT, Op>::kDirect;
+  using Smem = std::conditional_t<kDirect, PassSmemDirect, PassSmem<FMT>>;
+  __shared__ __align__(16) Smem sm;
   const int t = threadIdx.x, warp = t >> 5;
-  if constexpr (FMT == 0) {
+  if constexpr (kDirect) {
+    const int rb = bx * wpc * TB;
+    for (int w = 0; w < wpc; ++w) {
+      const int r0 = rb + w * TB;
+      if (r0 >= n) break;  // uniform over the CTA
+      auto g = [&](int col) { return op.gather(col); };
+      double v[NVA];
+      sell_window_sink<FMT == 3>(
+          sell, r0, g,
+          [&](int rl, double y) {
+            double cc[1];
+            if (r0 + rl < n) op.row(r0 + rl, y, v, cc);
+          },
+          [&](int rl) {  // own-row operands in flight during the row's SpMV
+            if (r0 + rl < n) load_vin(op, r0 + rl, v);
+          });
+    }
+  } else if constexpr (FMT == 0) {
     const int r0 = bx * (TB * RPT);
     double v[RPT][NVA];
 #pragma unroll
