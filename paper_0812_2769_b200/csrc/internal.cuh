@@ -164,6 +164,18 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Shared-memory carveout of the SELL pass kernels: 25% of the SM's 228 KB (57 KB), the rest
+// of the unified L1/shared memory caches the x gather.  Measured at C4 (sweep 18-100%,
+// the driver's choice, and the smallest carveout that keeps full occupancy): S1 0.330 ->
+// 0.325 ms, S3 0.306 -> 0.302 ms although S1 then runs 3 instead of 4 CTAs per SM.
+// GSK_CARVEOUT=<percent> overrides it, GSK_CARVEOUT=-1 leaves the driver's choice.
+int smem_carveout();
+void set_pass_carveout(const void* kern);
+template <typename... KArgs>
+void pass_carveout(void (*kern)(KArgs...)) {
+  set_pass_carveout(reinterpret_cast<const void*>(kern));
+}
+
 // Launch one pass kernel: an SpMV pass in the plan's format (CSR or SELL) or a vector
 // pass; *ntiles_out receives its CTA count (= CTA partials per dot).  pe0/pe1: optional
 // probe events recorded around the kernel (graph capture: external event nodes).
@@ -190,12 +202,15 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     int wpc = spmv_wpc_max();  // windows per CTA: as many as keep >= 3 CTAs per SM busy
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
-    if (P->fmt == GSK_FMT_SELL && P->sell.dict)
+    if (P->fmt == GSK_FMT_SELL && P->sell.dict) {
+      pass_carveout(pass_kernel<3, 1, Op>);
       GSK_CUDA(launch_k(pass_kernel<3, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
-    else if (P->fmt == GSK_FMT_SELL)
+    } else if (P->fmt == GSK_FMT_SELL) {
+      pass_carveout(pass_kernel<2, 1, Op>);
       GSK_CUDA(launch_k(pass_kernel<2, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
-    else
+    } else {  // CSR passes keep the driver's carveout (their 43 KB stage needs it)
       GSK_CUDA(launch_k(pass_kernel<1, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
+    }
   }
   GSK_LAUNCHED(1);
   if (pe1) GSK_CUDA(cudaEventRecordWithFlags(pe1, s, cudaEventRecordExternal));

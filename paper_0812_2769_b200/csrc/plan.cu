@@ -2,6 +2,8 @@
 // gsk_spmv / gsk_plan_spmv (SPEC sparse-core spmv; AC-3), gsk_dot (AC-5),
 // gsk_plan_residual_norm, SELL copy-out, probes, diagnostics.
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 #include "internal.cuh"
@@ -54,6 +56,29 @@ bool pass_alternate() {
     on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
+}
+
+int smem_carveout() {
+  static int c = -3;
+  if (c == -3) {
+    const char* e = std::getenv("GSK_CARVEOUT");
+    c = e ? std::atoi(e) : 25;
+    if (c > 100) c = 100;
+    if (c < -1) c = -1;
+  }
+  return c;
+}
+
+void set_pass_carveout(const void* kern) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  const int pct = smem_carveout();
+  if (pct < 0) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(kern)) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaGetLastError();  // a refused hint is not an error of the pass
+  done[kern] = pct;
 }
 
 int num_sms() {
