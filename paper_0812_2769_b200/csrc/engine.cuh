@@ -61,6 +61,20 @@ struct PassSmem<2> {
 };
 template <>
 struct PassSmem<3> : PassSmem<2> {};
+// SELL passes sized to the Op: cp.async slots only for the operands it prefetches (the
+// 25% carveout then holds 4 CTAs of a one-operand pass instead of 3)
+template <int NVS>
+struct PassSmemSell {
+  double sy[2][TB];
+  double wp[16 * MAXD * 8];
+  double vin[2][NVS][TB];
+};
+template <>
+struct PassSmemSell<0> {
+  double sy[2][TB];
+  double wp[16 * MAXD * 8];
+  double vin[2][1][1];
+};
 struct PassSmemDirect {  // direct passes use no shared memory
   double wp[1];
 };
@@ -345,7 +359,9 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
   constexpr int DD = D > 0 ? D : 1;
   constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
   constexpr bool kDirect = PassOcc<FMT, Op>::kDirect;
-  using Smem = std::conditional_t<kDirect, PassSmemDirect, PassSmem<FMT>>;
+  using Smem = std::conditional_t<
+      kDirect, PassSmemDirect,
+      std::conditional_t<(FMT >= 2), PassSmemSell<(PassOcc<FMT, Op>::kAsync ? Op::NV : 0)>, PassSmem<FMT>>>;
   __shared__ __align__(16) Smem sm;
   const int t = threadIdx.x, warp = t >> 5;
   if constexpr (kDirect) {
