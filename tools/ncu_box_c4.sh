@@ -1,7 +1,7 @@
 # On the GPU box: ncu --set full of tools/prof_c4.py (C4, top kernels), summarised on
 # the box (the raw report is too large to bring back).  TAG names the round/version.
 set -e
-TAG=${TAG:-r01_c4_v10}
+TAG=${TAG:-r01_c4_v11}
 mkdir -p gpurun_out
 python tools/prof_c4.py > /dev/null
 ncu --set full --clock-control none -k "regex:pass_kernel|mdot_pass|gs_kernel" -c 60 -o /tmp/prof_$TAG -f python tools/prof_c4.py > gpurun_out/ncu_$TAG.log 2>&1
