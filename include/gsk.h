@@ -19,6 +19,11 @@
  *  - Arithmetic: IEEE binary64 under the arithmetic contract of DESIGN.md §4
  *    (explicit FMAs, canonical pairwise-tree reductions); results are
  *    deterministic and bit-identical run to run.
+ *  - Tuning environment (read once per process; none changes any result bit):
+ *    GSK_PDL=0 (no programmatic dependent launch), GSK_WPC=1|2|4|8|16 (256-row
+ *    windows per CTA of SpMV passes, default 8), GSK_ALT=0 (no alternating CTA
+ *    order of consecutive passes), GSK_CARVEOUT=<percent>|-1 (shared-memory
+ *    carveout of SELL passes, default 25; -1 = the driver's choice).
  */
 #ifndef GSK_H
 #define GSK_H
