@@ -4,7 +4,15 @@ The paper ran AZTEC (CGS2 GMRES, Pentium IV); our oracle follows DESIGN.md's
 readings (MGS, face-midpoint k, h^2 scaling, GS(2)-frame stopping B2).  Bands:
 GMRES is insensitive to rounding, so its counts must land within
 2% of the paper; Bi-CGSTAB's residual history is chaotic on these systems, so its
-counts get a 20% band; verdicts ("no conv.", "---", stagnation level) must match.
+counts get a 10% band (SURVEY §4.2 reproduced every one within 10% with textbook
+numpy solvers); verdicts ("no conv.", "---", stagnation level) must match.
+
+One entry keeps 20%: tbl1a unscaled Bi-CGSTAB at 1e-7 (paper 224, oracle 190).  That
+history falls in a staircase — 2.8e-7 at iteration 188, 5.8e-8 at 190, back up to
+2.5e-7 at 215, 1.8e-8 at 218 — so which step first crosses 1e-7 depends on the
+rounding of the whole run: changing only the dot-product summation order moves such
+counts by tens of iterations.  `test_tbl1a_staircase` pins that
+explanation.
 """
 import json
 import os
@@ -30,11 +38,12 @@ def scaled(name, N=None, param=None):
 
 
 def check(ours, paper, band):
-    for o, p in zip(ours, paper):
+    bands = band if isinstance(band, (list, tuple)) else [band] * len(paper)
+    for o, p, bd in zip(ours, paper, bands):
         if p is None:
             assert o is None, (ours, paper)
         else:
-            assert o is not None and abs(o - p) <= band * p, (ours, paper)
+            assert o is not None and abs(o - p) <= bd * p, (ours, paper)
 
 
 def test_tbl1_problem1_bicgstab():
@@ -44,7 +53,7 @@ def test_tbl1_problem1_bicgstab():
     _, h, rep = oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-10, 10000, weights=d)
     assert first_crossings(h) == [None, None, None] and rep["status"] != 0
     _, h, rep = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-10, 10000)
-    check(first_crossings(h), GOLD["tbl1"]["bicgstab_gs2"], 0.20)
+    check(first_crossings(h), GOLD["tbl1"]["bicgstab_gs2"], 0.10)
 
 
 @pytest.mark.slow
@@ -75,9 +84,22 @@ def test_tbl1a_continuous_problem1():
     _, h, _ = oracle.gmres(s["row_ptr"], s["col"], s["val"], s["b"], 10, 1e-10, 7000)
     check(first_crossings(h), g["gmres10_unscaled"], 0.02)
     _, h, _ = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-10, 10000)
-    check(first_crossings(h), g["bicgstab_gs2"], 0.20)
+    check(first_crossings(h), g["bicgstab_gs2"], 0.10)
     _, h, _ = oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-10, 10000, weights=d)
-    check(first_crossings(h), g["bicgstab_unscaled"], 0.20)
+    check(first_crossings(h), g["bicgstab_unscaled"], [0.10, 0.20, 0.10])
+
+
+def test_tbl1a_staircase():
+    """The one 20% band above: the unscaled continuous-Problem-1 Bi-CGSTAB history
+    (GS(2) frame) crosses 1e-7 in jumps, with a relapse above 1e-7 between the
+    oracle's crossing (190) and the paper's (224), so a rounding-level change of the
+    run moves the first crossing by a whole step of the staircase."""
+    s, vo, bo, d = scaled("P1cont")
+    _, h, _ = oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-10, 10000, weights=d)
+    k = first_crossings(h)[1]
+    assert h[k - 2] > 2.5e-7 and h[k] < 6e-8        # 4x down across 1e-7 in two steps
+    assert (h[k:224] > 1e-7).any()                  # a relapse above 1e-7 before 224
+    assert h[224] < 1e-7
 
 
 @pytest.mark.slow
@@ -91,6 +113,6 @@ def test_tbl4_problem4(D):
     _, h, rep = oracle.bicgstab(s["row_ptr"], s["col"], s["val"], s["b"], 1e-10, 1000, weights=d)
     assert first_crossings(h) == [None, None, None]
     _, h, rep = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-10, 1000)
-    check(first_crossings(h), g["bicgstab_gs2_" + key], 0.20)
+    check(first_crossings(h), g["bicgstab_gs2_" + key], 0.10)
     _, h, rep = oracle.gmres(s["row_ptr"], s["col"], vo, bo, 10, 1e-10, 400)
     check(first_crossings(h), g["gmres10_gs2_" + key], 0.02)
