@@ -11,6 +11,10 @@ bytes).  Resumable: runs already in the file are skipped.
 
     OMP_NUM_THREADS=6 python tools/oracle_full_runs.py [C1 C2 ...]
     OMP_NUM_THREADS=6 python tools/oracle_full_runs.py --paper   # -> paper_runs_oracle.json
+    OMP_NUM_THREADS=4 python tools/oracle_full_runs.py --keys C4/gs2/bicgstab,C4/gs2/gmres(30)
+
+Several processes may run at once (disjoint runs): each save re-reads the file and
+merges its own record in.
 """
 import hashlib
 import json
@@ -51,13 +55,26 @@ def record(run, x, h, rep, secs):
     }
 
 
-def main(names, which="configs"):
+def save(OUT, key, rec):
+    db = json.load(open(OUT)) if os.path.exists(OUT) else \
+        {"_doc": __doc__.split("\n\n")[0], "host": platform.processor() or platform.machine(), "runs": {}}
+    db["runs"][key] = rec
+    tmp = f"{OUT}.{os.getpid()}.tmp"
+    with open(tmp, "w") as f:
+        json.dump(db, f, indent=1, sort_keys=True)
+    os.replace(tmp, OUT)
+
+
+def main(names, which="configs", keys=None):
     OUT = GOLDEN[which]
     db = {"_doc": __doc__.split("\n\n")[0], "host": platform.processor() or platform.machine(), "runs": {}}
     if os.path.exists(OUT):
         db = json.load(open(OUT))
     matrix = full_runs.runs() if which == "configs" else full_runs.paper_runs()
     todo = [r for r in matrix if (not names or r["config"] in names) and r["key"] not in db["runs"]]
+    if keys:  # explicit runs, in the order given
+        by_key = {r["key"]: r for r in todo}
+        todo = [by_key[k] for k in keys if k in by_key]
     cache = {}
     for run in todo:
         cfg = (run["config"], run["param"])
@@ -82,15 +99,16 @@ def main(names, which="configs"):
         else:
             # frame weights only enter GMRES's reported true_relres_w (reading B2)
             x, h, rep = oracle.gmres(s["row_ptr"], s["col"], val, b, run["m"], run["tol"], run["maxit"], weights=w)
-        db["runs"][run["key"]] = record(run, x, h, rep, time.time() - t0)
-        print(json.dumps({k: db["runs"][run["key"]][k] for k in ("key", "status", "iterations", "oracle_seconds")}),
-              flush=True)
-        tmp = OUT + ".tmp"
-        with open(tmp, "w") as f:
-            json.dump(db, f, indent=1, sort_keys=True)
-        os.replace(tmp, OUT)
+        rec = record(run, x, h, rep, time.time() - t0)
+        print(json.dumps({k: rec[k] for k in ("key", "status", "iterations", "oracle_seconds")}), flush=True)
+        save(OUT, run["key"], rec)
 
 
 if __name__ == "__main__":
     args = sys.argv[1:]
-    main([a for a in args if a != "--paper"], "paper" if "--paper" in args else "configs")
+    keys = None
+    if "--keys" in args:
+        i = args.index("--keys")
+        keys = args[i + 1].split(",")
+        del args[i:i + 2]
+    main([a for a in args if a != "--paper"], "paper" if "--paper" in args else "configs", keys)
