@@ -1,4 +1,6 @@
-# Builds every native artefact in-tree (the .so files travel to the GPU box).
+# Builds every native artefact in-tree (the .so files travel to the GPU box).  Each
+# library is written to a temporary file and renamed, so processes that have the old
+# one mapped keep running.
 #   workloads/libgskgen.so          seeded input generator (shared input module)
 #   oracle/liboracle.so             CPU parity oracle (test infrastructure)
 #   paper_0812_2769_b200/libgsk.so  the product: sm_100a kernels behind the C-ABI
@@ -18,13 +20,13 @@ GENFLAGS := -O2 -ffp-contract=off -fopenmp -fPIC -shared -std=c++17
 all: workloads/libgskgen.so oracle/liboracle.so $(PKG)/libgsk.so
 
 workloads/libgskgen.so: workloads/gen.cpp
-	$(HOSTCXX) $(GENFLAGS) -o $@ $<
+	$(HOSTCXX) $(GENFLAGS) -o $@.tmp $< && mv -f $@.tmp $@
 
 oracle/liboracle.so: oracle/oracle.cpp
-	$(HOSTCXX) $(ORCFLAGS) -o $@ $<
+	$(HOSTCXX) $(ORCFLAGS) -o $@.tmp $< && mv -f $@.tmp $@
 
 $(PKG)/libgsk.so: $(CU_SRC) $(CU_HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRC) -lcudart
+	$(NVCC) $(NVFLAGS) -shared -o $@.tmp.so $(CU_SRC) -lcudart && mv -f $@.tmp.so $@
 
 clean:
 	rm -f workloads/libgskgen.so oracle/liboracle.so $(PKG)/libgsk.so

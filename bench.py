@@ -25,8 +25,12 @@ extra  = SpMV and GS(2) rooflines, per-pass probes and time_to_tol (time to 1e-8
 --impl reference: the CPU oracle (oracle/) on a bounded sample of the same work.
 --shards P: one system in P row blocks: emulated on one GPU, or one
          shard per rank over NCCL under torchrun ("scaling": "strong").
-Multi-GPU: the north star is one GPU; --gpus N runs N independent replicas
-(weak scaling, no data-path collective).
+Multi-GPU: under torchrun with N > 1 ranks the default step is the
+         row-block sharded solve of ONE C4 system, one shard per rank, halos and the
+         reduction partials over NCCL ("scaling": "strong"; the residual history is
+         bit-identical at every N, its SHA-256 is in extra.history).  --replicas runs N
+         independent single-GPU replicas instead (weak scaling, no data-path
+         collective).
 """
 from __future__ import annotations
 
@@ -73,6 +77,9 @@ def parse():
     ap.add_argument("--fmt", default="sell", choices=["csr", "sell"],
                     help="plan layout built on the device from the CSR input (SELL-C-32-256 is faster "
                          "on every config: DESIGN.md §7)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with N > 1 ranks: N independent single-GPU replicas (weak scaling) instead of the "
+                         "sharded solve of one system")
     ap.add_argument("--shards", type=int, default=0,
                     help="row-block sharded solve (DESIGN.md §8): with one process, P shards emulated on "
                          "one GPU (the cost of sharding); under torchrun, one shard per rank over NCCL "
@@ -226,7 +233,7 @@ def main():
         run_reference(args, rank, world)
         return
 
-    if args.shards:
+    if args.shards or (world > 1 and not args.replicas):
         run_sharded(args, rank, world, local)
         return
 
@@ -457,6 +464,17 @@ def run_sharded(args, rank, world, local):
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
+    # the residual histories (global, identical on every rank) of one more untimed
+    # step: bit-identical at every N, compared across SCALE lines
+    import hashlib
+    _, h1, q1 = SP.bicgstab(bl, tol=cfg.tol, maxit=cfg.maxit, x=x1)
+    _, h2, q2 = SP.gmres(bl, m=m, tol=cfg.tol, maxit=gmaxit, x=x2)
+    history = {"bicgstab_iterations": q1["iterations"], "gmres_iterations": q2["iterations"],
+               "bicgstab_sha256": hashlib.sha256(np.ascontiguousarray(h1, "<f8").tobytes()).hexdigest(),
+               "gmres_sha256": hashlib.sha256(np.ascontiguousarray(h2, "<f8").tobytes()).hexdigest()}
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist)
     # roofline: shard 0's v = A p pass (probe 0) against its own rows' bytes
     l0, h0 = gsk.shard_rows(s["n"], P, rank if world > 1 else 0)
     nnz0 = int(s["row_ptr"][h0] - s["row_ptr"][l0])
@@ -481,11 +499,14 @@ def run_sharded(args, rank, world, local):
             "config": {**config_desc(args, cfg, s), "parallelism": f"rows/{P}", "shards": P,
                        "placement": f"{world} GPUs, NCCL halos + all-gathers" if world > 1
                        else "all shards on one GPU (device-copy halos)"},
-            "roofline": roof, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk,
+            "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "comm": {"backend": "nccl" if world > 1 else "none (one process)", "nranks": world,
+                     "shards": P, "nranks_ok": (comm.world == world) if comm else world == 1},
             "extra": {"bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
                                    "solve_ms": r1["solve_ms"]},
                       "gmres": {"iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
-                                "solve_ms": r2["solve_ms"]}},
+                                "solve_ms": r2["solve_ms"]},
+                      "history": history},
         }
         print(json.dumps(line), flush=True)
     SP.close()
@@ -534,6 +555,56 @@ def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args, dist=None):
         ms, its = reduce_over_ranks(ms, its, dist, "cuda")
         h2d *= dist.get_world_size()
         d2h *= dist.get_world_size()
+    return {"value": its / (ms / 1e3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
+
+
+def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist):
+    """e2e of the sharded step: every step each rank copies the system from pinned host
+    memory (the sharded plan reads its rows and halo from the global arrays), scales
+    it, builds its shard plan, runs both solves and reads its rows of x back.  Whole-job
+    value: the one system's iterations / the slowest rank's time."""
+    pin = {k: torch.from_numpy(np.ascontiguousarray(s[k])).pin_memory() for k in ("row_ptr", "col", "val", "b")}
+    h2d = sum(t.numel() * t.element_size() for t in pin.values())
+    lo, hi = gsk.shard_rows(s["n"], P, comm.rank if comm else 0)
+    if not comm:
+        lo, hi = 0, s["n"]
+    xo1 = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+    xo2 = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+    d2h = 2 * (hi - lo) * 8
+
+    def step():
+        dev = {k: v.to("cuda", non_blocking=True) for k, v in pin.items()}
+        A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
+        As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
+        x1, _, r1 = SP.bicgstab(bs[lo:hi], tol=cfg.tol, maxit=cfg.maxit, hist=False)
+        x2, _, r2 = SP.gmres(bs[lo:hi], m=m, tol=cfg.tol, maxit=gmaxit, hist=False)
+        xo1.copy_(x1, non_blocking=True)
+        xo2.copy_(x2, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        SP.close()
+        return r1["iterations"] + r2["iterations"]
+
+    step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its = 0
+    k = max(1, min(args.steps, 2))
+    for _ in range(k):
+        its += step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:  # one system: iterations once, the slowest rank's time; bytes of every rank
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        h2d *= dist.get_world_size()
+        d2h = 2 * s["n"] * 8
     return {"value": its / (ms / 1e3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
 

@@ -175,10 +175,13 @@ void orc_unscale(int64_t n, const double* s, const double* y, double* x) {
 
 // ---- SELL-C-sigma layout (BASELINE.json configs[3]) -------------------------------
 // Windows of sigma consecutive rows; inside a window rows are stably sorted by
-// descending length (ties keep row order); chunks of C sorted rows; chunk_len =
-// longest row of the chunk; slot (k, lane) of chunk c at chunk_ptr[c] + k*C + lane,
-// holding the row's k-th CSR entry (CSR order kept) or col -1 / val 0 as padding;
-// roff[c*C + lane] = in-window offset of the row (uint8, sigma <= 256).
+// descending length (ties keep row order) — unless the rows in their natural order
+// need no more padded slots than sorted (reading L1: the sort only exists to
+// cut padding), in which case the window keeps the natural order; chunks of C rows;
+// chunk_len = longest row of the chunk; slot (k, lane) of chunk c at
+// chunk_ptr[c] + k*C + lane, holding the row's k-th CSR entry (CSR order kept) or
+// col -1 / val 0 as padding; roff[c*C + lane] = in-window offset of the row (uint8,
+// sigma <= 256).
 int64_t orc_sell_size(int64_t n, const int32_t* rp, int C, int sigma) {
   int64_t nch = (n + C - 1) / C, tot = 0;
   for (int64_t w = 0; w * sigma < n; ++w) {
@@ -200,15 +203,29 @@ int orc_sell_build(int64_t n, const int32_t* rp, const int32_t* ci, const double
   chunk_ptr[0] = 0;
   for (int64_t w = 0; w * sigma < n; ++w) {
     int64_t r0 = w * sigma, r1 = std::min<int64_t>(n, r0 + sigma), cnt = r1 - r0;
-    std::vector<int32_t> order(cnt);
+    std::vector<int32_t> order(cnt), sorted(cnt);
     std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    std::iota(sorted.begin(), sorted.end(), 0);
+    std::stable_sort(sorted.begin(), sorted.end(), [&](int32_t a, int32_t b) {
       return (rp[r0 + a + 1] - rp[r0 + a]) > (rp[r0 + b + 1] - rp[r0 + b]);
     });
+    auto slots = [&](const std::vector<int32_t>& ord) {  // padded slots of the window / C
+      int64_t tot = 0;
+      for (int64_t s0 = 0; s0 < cnt; s0 += C) {
+        int32_t L = 0;
+        for (int64_t s = s0; s < std::min<int64_t>(cnt, s0 + C); ++s)
+          L = std::max(L, rp[r0 + ord[s] + 1] - rp[r0 + ord[s]]);
+        tot += L;
+      }
+      return tot;
+    };
+    if (slots(order) > slots(sorted)) order = sorted;
     int64_t c0 = r0 / C, c1 = (r1 + C - 1) / C;
     for (int64_t c = c0; c < c1; ++c) {
-      int64_t s0 = c * C - r0;  // first sorted position of the chunk in this window
-      int32_t L = rp[r0 + order[s0] + 1] - rp[r0 + order[s0]];
+      int64_t s0 = c * C - r0;  // first position of the chunk in this window
+      int32_t L = 0;
+      for (int64_t s = s0; s < std::min<int64_t>(cnt, s0 + C); ++s)
+        L = std::max(L, rp[r0 + order[s] + 1] - rp[r0 + order[s]]);
       chunk_len[c] = L;
       chunk_ptr[c + 1] = chunk_ptr[c] + L * C;
       for (int lane = 0; lane < C; ++lane) {

@@ -139,6 +139,21 @@ def _dev_f64(t, n=None):
     return t
 
 
+def _out_f64(t, n, name, avoid=()):
+    """A caller-supplied OUTPUT buffer: the kernels write n doubles through its raw
+    pointer, so it must be a contiguous CUDA float64 tensor of exactly n entries and
+    must not overlap an input."""
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.dtype != torch.float64:
+        raise TypeError(f"{name}: expected a CUDA float64 tensor")
+    if not t.is_contiguous() or t.numel() != n:
+        raise ValueError(f"{name}: expected a contiguous tensor of {n} entries, got shape {tuple(t.shape)}")
+    a0, a1 = t.data_ptr(), t.data_ptr() + 8 * n
+    for u in avoid:
+        if u is not None and u.numel() and a0 < u.data_ptr() + u.numel() * u.element_size() and u.data_ptr() < a1:
+            raise ValueError(f"{name} overlaps an input of the same call")
+    return t
+
+
 def _dev_i32(t):
     if not isinstance(t, torch.Tensor):
         t = torch.as_tensor(np.ascontiguousarray(t, dtype=np.int32))
@@ -175,6 +190,10 @@ def gs_scale(A: CSR, b=None, p: int = 2, inplace: bool = False, out=None):
     b = _dev_f64(b, A.n)
     if out is not None:
         vout, bout, d = out
+        _out_f64(vout, A.val.numel(), "out[0] (values)")
+        if bout is not None:
+            _out_f64(bout, A.n, "out[1] (b)")
+        _out_f64(d, A.n, "out[2] (d)")
     else:
         vout = A.val if inplace else torch.empty_like(A.val)
         bout = None if b is None else (b if inplace else torch.empty_like(b))
@@ -270,7 +289,7 @@ class Plan:
 
     def spmv(self, x, y=None):
         x = _dev_f64(x, self.nloc)
-        y = torch.empty_like(x) if y is None else y
+        y = torch.empty_like(x) if y is None else _out_f64(y, self.nloc, "y", avoid=(x,))
         _check(load().gsk_plan_spmv(self.h, _ptr(x), _ptr(y), _stream()))
         return y
 
@@ -325,7 +344,8 @@ class Plan:
         lib = load()
         b = _dev_f64(b, self.nloc)
         x0 = _dev_f64(x0, self.nloc)
-        x = torch.empty(self.nloc, dtype=torch.float64, device="cuda") if x is None else x
+        x = torch.empty(self.nloc, dtype=torch.float64, device="cuda") if x is None else \
+            _out_f64(x, self.nloc, "x", avoid=(b,))
         H = np.empty(maxit + 1, np.float64) if hist else None
         rep = Report()
         hp = None if H is None else H.ctypes.data_as(ctypes.c_void_p)

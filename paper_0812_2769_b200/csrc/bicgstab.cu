@@ -128,17 +128,23 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
     } else {
       GSK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     }
-    int used = 1;
+    int used = 1, rc;
     if (small)
-      GSK_TRY(small_bicgstab_run(P, b, tol, maxit, x));
+      rc = small_bicgstab_run(P, b, tol, maxit, x);
     else if (clus)
-      GSK_TRY(cluster_bicgstab_run(P, b, tol, maxit, x, &used));
+      rc = cluster_bicgstab_run(P, b, tol, maxit, x, &used);
     else
-      GSK_TRY(coop_bicgstab_run(P, b, tol, maxit, x, &used));
+      rc = coop_bicgstab_run(P, b, tol, maxit, x, &used);
+    if (rc != GSK_OK) {  // e.g. a cluster that cannot be scheduled (MIG, partitioned GPU)
+      if (P->engine != GSK_ENGINE_AUTO) return rc;
+      cudaGetLastError();  // AUTO: the graph passes below instead
+      used = 0;
+    }
     if (used) {
       GSK_CUDA(cudaEventRecord(P->t1, s));
       return bicgstab_report(P, hist, rep, caller);
     }
+    GSK_CUDA(cudaStreamSynchronize(s));  // nothing pending on the plan stream before the capture
   }
   const int K = batch_size(P);
   if (!P->bgraph[0] || P->bkey_b != b || P->bkey_x != x || P->bK != K || P->bkey_h != P->hist_d) {

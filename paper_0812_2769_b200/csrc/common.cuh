@@ -36,6 +36,10 @@ struct SellView {
   const int* __restrict__ dict;      // [ndict]
   int pad;  // column value of padding slots: -1, or INT_MIN in a shard plan, whose
             // remapped columns may be negative (left halo)
+  // windows kept in natural row order (sell.cu): wid[w] = 1 when lane l of warp k of
+  // window w holds row 32 k + l; all_nat = every window is (null / 0: use roff)
+  const uint8_t* __restrict__ wid;  // [nwindows]
+  int all_nat;
 };
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the

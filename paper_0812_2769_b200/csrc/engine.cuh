@@ -151,14 +151,15 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
 }
 
 // SELL window core: lane l of warp w computes slot l of chunk r0/32 + w and hands the
-// row's y with its in-window offset to sink(rl, y).
-template <bool DICT, class G, class S, class Pre>
+// row's y with its in-window offset to sink(rl, y).  NAT: the window keeps its natural
+// row order (sell.cu), so the slot's row is r0 + t and roff is not read.
+template <bool DICT, bool NAT = false, class G, class S, class Pre>
 __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, const G& g, const S& sink,
                                                  const Pre& pre) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int c = (r0 >> 5) + warp;
   if (c < A.nchunks) {
-    const int rl = A.roff[c * SELL_C + lane];
+    const int rl = NAT ? (t & (TB - 1)) : A.roff[c * SELL_C + lane];
     pre(rl);
     const int p0 = A.cptr[c], L = (A.cptr[c + 1] - p0) >> 5;
     const int base = p0 + lane;
@@ -225,6 +226,26 @@ __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G
   sell_window_store<DICT>(A, r0, g, sy);
   __syncthreads();
   return sy[threadIdx.x];
+}
+
+// ... of a natural-order window: thread t computes row r0 + t itself (no scatter, no
+// barrier; 0 beyond the last chunk).
+template <bool DICT, class G>
+__device__ __forceinline__ double sell_window_nat(const SellView& A, int r0, const G& g) {
+  double y = 0.0;
+  sell_window_sink<DICT, true>(A, r0, g, [&](int, double v) { y = v; }, [](int) {});
+  return y;
+}
+
+// Bit w set: window w of this CTA keeps its natural row order.  Every lane of every
+// warp gets the same mask (lane w of each warp reads window w's flag).
+__device__ __forceinline__ unsigned sell_nat_mask(const SellView& A, int bx, int wpc, int n) {
+  if (A.all_nat) return 0xffffffffu;
+  if (!A.wid) return 0u;
+  const int lane = threadIdx.x & 31;
+  const long long wi = (long long)bx * wpc + lane;
+  const bool f = lane < wpc && wi * TB < n && A.wid[wi];
+  return __ballot_sync(0xffffffffu, f);
 }
 
 // Op::kEvict (optional): bit k set = own-row operand vin(k) is not read by the NEXT
@@ -366,20 +387,21 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
   const int t = threadIdx.x, warp = t >> 5;
   if constexpr (kDirect) {
     const int rb = bx * wpc * TB;
+    const unsigned nat = sell_nat_mask(sell, bx, wpc, n);
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       if (r0 >= n) break;  // uniform over the CTA
       auto g = [&](int col) { return op.gather(col); };
       double v[NVA];
-      sell_window_sink<FMT == 3>(
-          sell, r0, g,
-          [&](int rl, double y) {
-            double cc[1];
-            if (r0 + rl < n) op.row(r0 + rl, y, v, cc);
-          },
-          [&](int rl) {  // own-row operands in flight during the row's SpMV
-            if (r0 + rl < n) load_vin(op, r0 + rl, v);
-          });
+      auto sink = [&](int rl, double y) {
+        double cc[1];
+        if (r0 + rl < n) op.row(r0 + rl, y, v, cc);
+      };
+      auto pre = [&](int rl) {  // own-row operands in flight during the row's SpMV
+        if (r0 + rl < n) load_vin(op, r0 + rl, v);
+      };
+      if ((nat >> w) & 1u) sell_window_sink<FMT == 3, true>(sell, r0, g, sink, pre);
+      else sell_window_sink<FMT == 3>(sell, r0, g, sink, pre);
     }
   } else if constexpr (FMT == 0) {
     const int r0 = bx * (TB * RPT);
@@ -422,6 +444,11 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       }
     };
     issue(0);
+    // natural-order windows (sell.cu) need neither the scatter nor its barrier; the
+    // others alternate the two scatter buffers (ks counts them: a buffer is rewritten
+    // only after the barrier of the scatter window in between)
+    const unsigned nat = FMT >= 2 ? sell_nat_mask(sell, bx, wpc, n) : 0u;
+    int ks = 0;
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       double cc[DD];
@@ -434,8 +461,14 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
         double v[NVA];
         if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
-        if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
-        else y = sell_window<FMT == 3>(sell, r0, g, sm.sy[w & 1]);
+        if constexpr (FMT == 1) {
+          y = csr_window(csr, r0, g, sm.st[w & 1]);
+        } else if ((nat >> w) & 1u) {
+          y = sell_window_nat<FMT == 3>(sell, r0, g);
+        } else {
+          y = sell_window<FMT == 3>(sell, r0, g, sm.sy[ks & 1]);
+          ++ks;
+        }
         if constexpr (kAsync) {
           cp_async_wait<1>();  // all groups but window w+1's are complete
 #pragma unroll

@@ -133,8 +133,11 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   const bool clus = !small && P->orth == 0 && m <= 40 &&
                     ((P->engine == GSK_ENGINE_AUTO && n <= GSK_CLUSTER_AUTO_GMRES) ||
                      (P->engine == GSK_ENGINE_CLUSTER && n <= GSK_CLUSTER_NMAX));
-  if (!small && !clus && (!P->ggraph[0] || P->gkey_b != b || P->gkey_x != x || P->gkey_m != m || P->gkey_h != P->hist_d ||
-      P->gkey_orth != P->orth)) {
+  // the graph passes' captured cycles (for these b, x, m, history and orthogonalisation)
+  auto ensure_graphs = [&]() -> int {
+    if (P->ggraph[0] && P->gkey_b == b && P->gkey_x == x && P->gkey_m == m && P->gkey_h == P->hist_d &&
+        P->gkey_orth == P->orth)
+      return GSK_OK;
     for (auto& g : P->ggraph)
       if (g) {
         cudaGraphExecDestroy(g);
@@ -146,7 +149,9 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
     P->gkey_m = m;
     P->gkey_h = P->hist_d;
     P->gkey_orth = P->orth;
-  }
+    return GSK_OK;
+  };
+  if (!small && !clus) GSK_TRY(ensure_graphs());
   cudaStream_t s = P->st;
   GSK_TRY(join_in(P, caller));
   GSK_CUDA(cudaEventRecord(P->t0, s));
@@ -171,11 +176,22 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8), s));
   GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   int cused = 0;
-  if (clus) GSK_TRY(cluster_gmres_run(P, b, x, h, &cused));
+  if (clus) {
+    const int rc = cluster_gmres_run(P, b, x, h, &cused);
+    if (rc != GSK_OK) {  // e.g. a cluster that cannot be scheduled (MIG, partitioned GPU)
+      if (P->engine != GSK_ENGINE_AUTO) return rc;
+      cudaGetLastError();  // AUTO: the graph passes below instead
+      cused = 0;
+    }
+  }
   if (small) {
     GSK_TRY(small_gmres_run(P, b, x, h));
   } else if (cused) {
   } else {
+    if (clus) {  // the cluster engine declined: capture now (nothing pending on the plan stream)
+      GSK_CUDA(cudaStreamSynchronize(s));
+      GSK_TRY(ensure_graphs());
+    }
     OpGResid<> init{x, b, P->weights, P->W, P->hist_d, P->gstate, 1};
     if (run_pass(P, init, s) < 0) return GSK_E_CUDA;
     const long long maxc = (long long)maxit + 2;

@@ -85,6 +85,7 @@ struct gsk_plan {
   int* scol = nullptr;
   double* sval = nullptr;
   uint8_t* roff = nullptr;
+  uint8_t* wid = nullptr;   // [nwindows] natural-order windows (sell.cu)
   int64_t nchunks = 0, nslots = 0;
   uint8_t* sidx = nullptr;  // column-index dictionary (SELL-D); null = plain int32 columns
   int* dptr = nullptr;

@@ -384,7 +384,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
-  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->part, P->scratch,
+  void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->wid, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
                   P->cpart};
   for (void* b : bufs)

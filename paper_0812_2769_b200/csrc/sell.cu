@@ -1,19 +1,27 @@
 // sell.cu — CSR -> SELL-C-sigma (C = 32, sigma = 256) on the device (BASELINE.json
-// configs[3]).  Integer work, bit-exact with the oracle's layout:
-//   1. per sigma-window: stable rank of rows by descending length (ties by row id);
-//      roff[sorted slot] = in-window row offset; chunk_len = longest row of a chunk;
-//   2. chunk_ptr = exclusive scan of 32 * chunk_len (one CTA);
+// configs[3]; DESIGN.md §5/§6).  Integer work, bit-exact with the oracle's layout:
+//   1. per sigma-window: stable rank of rows by descending length (ties by row id) —
+//      unless the window's rows in natural order need no more padded slots than
+//      sorted (reading L1: the sort exists to cut padding), in which
+//      case they keep their natural order and the window is marked "natural" (wid);
+//      roff[slot] = in-window row offset; chunk_len = longest row of a chunk;
+//   2. chunk_ptr = exclusive scan of 32 * chunk_len (3 launches, 64-bit; a layout of
+//      2^31 slots or more is rejected);
 //   3. fill: slot (k, lane) of chunk c at chunk_ptr[c] + 32 k + lane, CSR order kept,
 //      padding col = -1, val = 0 (predicated off in the SpMV, AC-3).
+// In a natural window lane l of warp w holds row 32 w + l, so a pass finishes its rows
+// in row order without the shared-memory scatter and its barrier (engine.cuh).
 #include <climits>
+#include <vector>
 #include "internal.cuh"
 
 namespace gsk {
 
 __global__ void __launch_bounds__(TB) sell_rank_kernel(int n, int nchunks, const int* __restrict__ rp,
-                                                       uint8_t* roff, int* clen) {
+                                                       uint8_t* roff, int* clen, uint8_t* wid) {
   __shared__ int len[TB];
   __shared__ int slen[TB];
+  __shared__ int cmax[2][TB / SELL_C];
   const int w = blockIdx.x, t = threadIdx.x, r = w * TB + t;
   len[t] = r < n ? rp[r + 1] - rp[r] : 0;
   __syncthreads();
@@ -24,12 +32,26 @@ __global__ void __launch_bounds__(TB) sell_rank_kernel(int n, int nchunks, const
     rank += (lj > li) || (lj == li && j < t);
   }
   slen[rank] = li;
-  const int c = w * (TB / SELL_C) + (rank >> 5);
-  if (c < nchunks) roff[(size_t)w * TB + rank] = (uint8_t)t;
+  // longest row of each chunk in natural order (rows beyond n have length 0)
+  const int nat = __reduce_max_sync(0xffffffffu, li);
+  if ((t & 31) == 0) cmax[0][t >> 5] = nat;
   __syncthreads();
+  if ((t & 31) == 0) cmax[1][t >> 5] = slen[t];  // sorted: the chunk's first row
+  __syncthreads();
+  int snat = 0, ssrt = 0;  // padded slots / 32 of the window, natural vs sorted
+#pragma unroll
+  for (int k = 0; k < TB / SELL_C; ++k) {
+    snat += cmax[0][k];
+    ssrt += cmax[1][k];
+  }
+  const bool natural = snat <= ssrt;
+  const int slot = natural ? t : rank;
+  const int c = w * (TB / SELL_C) + (slot >> 5);
+  if (c < nchunks) roff[(size_t)w * TB + slot] = (uint8_t)t;
+  if (t == 0) wid[w] = natural ? 1 : 0;
   if ((t & 31) == 0) {
     const int cc = w * (TB / SELL_C) + (t >> 5);
-    if (cc < nchunks) clen[cc] = slen[t];
+    if (cc < nchunks) clen[cc] = cmax[natural ? 0 : 1][t >> 5];
   }
 }
 
@@ -80,6 +102,7 @@ __global__ void __launch_bounds__(SCAN_T) sell_scan_offsets(int nblocks, long lo
     if (i < nblocks) bsum[i] = carry + ex;
     carry += tot;
   }
+  if (threadIdx.x == 0) bsum[nblocks] = carry;  // the grand total (checked on the host)
 }
 
 __global__ void __launch_bounds__(SCAN_T) sell_scan_final(int nchunks, const int* __restrict__ clen,
@@ -105,15 +128,25 @@ __global__ void __launch_bounds__(SCAN_T) sell_scan_final(int nchunks, const int
   }
 }
 
-static int sell_scan(int nchunks, const int* clen, int* cptr, int mult, cudaStream_t s) {
+// *total (nullable) receives the 64-bit sum; cptr is int32, so a sum of 2^31 or more
+// is GSK_E_INVALID (the wrapped offsets are never used).
+static int sell_scan(int nchunks, const int* clen, int* cptr, int mult, cudaStream_t s, long long* total) {
   const int nb = (nchunks + SCAN_B - 1) / SCAN_B;
   long long* bsum = nullptr;
-  GSK_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (nb > 0 ? nb : 1), s));
+  GSK_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (nb + 1), s));
   sell_scan_sums<<<nb, SCAN_T, 0, s>>>(nchunks, clen, bsum, mult);
   sell_scan_offsets<<<1, SCAN_T, 0, s>>>(nb, bsum);
   sell_scan_final<<<nb, SCAN_T, 0, s>>>(nchunks, clen, bsum, cptr, mult);
   GSK_LAUNCHED(3);
+  long long tot = 0;
+  GSK_CUDA(cudaMemcpyAsync(&tot, bsum + nb, sizeof tot, cudaMemcpyDeviceToHost, s));
   GSK_CUDA(cudaFreeAsync(bsum, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  if (total) *total = tot;
+  if (tot > INT_MAX) {
+    set_error("SELL layout: %lld slots do not fit int32 offsets (limit 2^31 - 1)", tot);
+    return GSK_E_INVALID;
+  }
   return GSK_OK;
 }
 
@@ -147,19 +180,27 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&P->clen, sizeof(int) * P->nchunks));
   GSK_CUDA(cudaMalloc(&P->cptr, sizeof(int) * (P->nchunks + 1)));
   GSK_CUDA(cudaMalloc(&P->roff, (size_t)P->nchunks * SELL_C));
-  sell_rank_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->roff, P->clen);
+  GSK_CUDA(cudaMalloc(&P->wid, (size_t)nwin));
+  sell_rank_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->roff, P->clen, P->wid);
   GSK_LAUNCHED(1);
-  GSK_TRY(sell_scan((int)P->nchunks, P->clen, P->cptr, SELL_C, s));
-  int tot = 0;
-  GSK_CUDA(cudaMemcpyAsync(&tot, P->cptr + P->nchunks, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GSK_CUDA(cudaStreamSynchronize(s));
+  long long tot = 0;
+  GSK_TRY(sell_scan((int)P->nchunks, P->clen, P->cptr, SELL_C, s, &tot));
   P->nslots = tot;
+  // every window natural? (then the passes need no per-window flag)
+  int all_nat = 1;
+  {
+    std::vector<uint8_t> h(nwin);
+    GSK_CUDA(cudaMemcpyAsync(h.data(), P->wid, nwin, cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaStreamSynchronize(s));
+    for (uint8_t f : h) all_nat &= f;
+  }
   GSK_CUDA(cudaMalloc(&P->scol, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
   GSK_CUDA(cudaMalloc(&P->sval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
                                        P->cptr, P->roff, P->scol, P->sval, false, P->sell_pad);
   GSK_LAUNCHED(1);
-  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr, P->sell_pad};
+  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr,
+                     P->sell_pad, P->wid, all_nat};
   return GSK_OK;
 }
 
@@ -239,7 +280,7 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
     P->dptr = nullptr;
     return GSK_OK;
   }
-  GSK_TRY(sell_scan(nch, ucount, P->dptr, 1, s));
+  GSK_TRY(sell_scan(nch, ucount, P->dptr, 1, s, nullptr));
   int tot = 0;
   GSK_CUDA(cudaMemcpyAsync(&tot, P->dptr + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
   GSK_CUDA(cudaStreamSynchronize(s));

@@ -225,7 +225,7 @@ def test_sell_round_trip(C, sigma):
         L = S["chunk_len"][c]
         assert S["chunk_ptr"][c + 1] - S["chunk_ptr"][c] == L * C
         w0 = (c * C) // sigma * sigma
-        prev = None
+        lmax = 0
         for lane in range(C):
             row = w0 + S["roff"][c * C + lane]
             if row >= n:
@@ -234,19 +234,62 @@ def test_sell_round_trip(C, sigma):
             seen[row] = True
             ln = rp[row + 1] - rp[row]
             assert ln <= L
-            if lane == 0:
-                assert ln == L
+            lmax = max(lmax, ln)
             slots = S["chunk_ptr"][c] + np.arange(L) * C + lane
             assert np.array_equal(S["scol"][slots[:ln]], col[rp[row]:rp[row + 1]])
             assert np.array_equal(S["sval"][slots[:ln]], val[rp[row]:rp[row + 1]])
             assert np.all(S["scol"][slots[ln:]] == -1) and np.all(S["sval"][slots[ln:]] == 0)
+        assert lmax == L  # chunk_len = the chunk's longest row
     assert seen.all()
     # within a window the sorted order is by descending length, ties by row id
+    _check_window_order(S, rp, n, C, sigma)
+
+
+def _chunk_slots(lens, C):
+    return sum(max(lens[s:s + C]) for s in range(0, len(lens), C))
+
+
+def _check_window_order(S, rp, n, C, sigma):
+    """Per window: the rows in natural order when that needs no more padded slots than
+    sorting them by descending length (ties by row id), else sorted (reading L1); either
+    way the window's slot count is the sorted (minimal) one."""
+    nch = (n + C - 1) // C
+    roff = np.asarray(S["roff"], np.int64)
+    naturals = 0
     for w0 in range(0, n, sigma):
-        rows = [w0 + S["roff"][s] for s in range(w0, min(w0 + sigma, nch * C))
-                if w0 + S["roff"][s] < n]
-        key = [(-(rp[r + 1] - rp[r]), r) for r in rows]
-        assert key == sorted(key)
+        rows = [w0 + int(roff[s]) for s in range(w0, min(w0 + sigma, nch * C)) if w0 + roff[s] < n]
+        lens = [int(rp[r + 1] - rp[r]) for r in range(w0, min(n, w0 + sigma))]
+        srt = sorted(lens, reverse=True)
+        if _chunk_slots(lens, C) <= _chunk_slots(srt, C):
+            assert rows == list(range(w0, min(n, w0 + sigma)))
+            naturals += 1
+        else:
+            key = [(-(rp[r + 1] - rp[r]), r) for r in rows]
+            assert key == sorted(key)
+        c0, c1 = w0 // C, (min(n, w0 + sigma) + C - 1) // C
+        assert sum(S["chunk_len"][c0:c1]) == _chunk_slots(srt, C)
+    return naturals
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "P4"])
+def test_sell_stencil_windows_natural(name):
+    """On the stencil systems sorting a window cannot save slots (its short boundary rows
+    share a chunk with full rows either way), so every window keeps its natural order —
+    and a window with a chunk of short rows is still sorted (constructed case)."""
+    s = workloads.generate(name)
+    S = oracle.sell_build(s["row_ptr"], s["col"], s["val"])
+    nwin = (s["n"] + 255) // 256
+    assert _check_window_order(S, s["row_ptr"], s["n"], 32, 256) == nwin
+    lens = np.full(512, 7)
+    lens[:32] = 3  # window 0: natural 3 + 7*7 = 52 slots / 32, sorted 7*7 + 3 = 52: natural
+    lens[40] = 1
+    lens[256:256 + 16] = 2
+    lens[256 + 40:256 + 56] = 2  # window 1: natural 8*7 = 56, sorted 7*7 + 2 = 51: sorted
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.arange(l) for l in lens]).astype(np.int32)
+    S = oracle.sell_build(rp, col, np.ones(rp[-1]))
+    assert _check_window_order(S, rp, 512, 32, 256) == 1
+    assert list(S["roff"][256:256 + 32]) != list(range(32))
 
 
 # ---------------------------------------------------------------- solvers
