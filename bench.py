@@ -28,9 +28,10 @@ extra  = SpMV and GS(2) rooflines, per-pass probes and time_to_tol (time to 1e-8
 Multi-GPU: under torchrun with N > 1 ranks the default step is the
          row-block sharded solve of ONE C4 system, one shard per rank, halos and the
          reduction partials over NCCL ("scaling": "strong"; the residual history is
-         bit-identical at every N, its SHA-256 is in extra.history).  --replicas runs N
-         independent single-GPU replicas instead (weak scaling, no data-path
-         collective).
+         bit-identical at every N, its SHA-256 is in extra.history).  --weak: weak
+         scaling instead — C4's 256^3 block stacked N times in z (C4w), one block per
+         rank, each rank generating and holding only its own rows.  --replicas runs N
+         independent single-GPU replicas (no data-path collective).
 """
 from __future__ import annotations
 
@@ -80,6 +81,9 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="with N > 1 ranks: N independent single-GPU replicas (weak scaling) instead of the "
                          "sharded solve of one system")
+    ap.add_argument("--weak", action="store_true",
+                    help="with N > 1 ranks: weak scaling — C4's 256^3 block stacked N times in z (C4w), one "
+                         "block per rank, each rank generating and holding only its own rows")
     ap.add_argument("--shards", type=int, default=0,
                     help="row-block sharded solve (DESIGN.md §8): with one process, P shards emulated on "
                          "one GPU (the cost of sharding); under torchrun, one shard per rank over NCCL "
@@ -214,8 +218,14 @@ def reduce_over_ranks(ms, its, dist, device):
 
 
 def config_desc(args, cfg, s):
-    return {"workload": f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", "n": int(s["n"]),
-            "nnz": int(s["nnz"]), "grid": f"{cfg.N if args.N is None else args.N}^{3 if cfg.cfg in (3, 4) else 2}",
+    N = cfg.N if args.N is None else args.N
+    if cfg.name == "C4w":
+        G = int(s["n"]) // N ** 3
+        wl, grid = (f"C4w: BASELINE.json configs[3] stacked {G}x in z (one 256^3 block of C4's layered "
+                    f"medium per GPU; weak scaling, DESIGN.md §8)", f"{N}x{N}x{N * G}")
+    else:
+        wl, grid = f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", f"{N}^{3 if cfg.cfg in (3, 4) else 2}"
+    return {"workload": wl, "n": int(s["n"]), "nnz": int(s["nnz"]), "grid": grid,
             "format": ("SELL-C-32-256" if getattr(args, "fmt", "sell") == "sell" else "CSR")
             + " (built on the device from the CSR input)", "scaling": "GS(2)",
             "solvers": ["Bi-CGSTAB to tol (maxit %d)" % cfg.maxit,
@@ -420,16 +430,31 @@ def run_sharded(args, rank, world, local):
     P = world if world > 1 else args.shards
     cfg = workloads.CONFIGS[args.config]
     m, gmaxit = 30, args.gmres_maxit
-    s = workloads.generate(args.config, N=args.N)
+    weak = args.weak and world > 1
+    fmt = args.fmt
+    comm = gsk.NcclComm() if world > 1 else None
+    if weak:
+        # C4w: one 256^3 block of C4's layered medium per rank, stacked in z; each rank
+        # generates and holds only its own rows (gsk_shard_opts.local_input)
+        cfg = workloads.STACKED
+        n_glob, nnz_glob = workloads.dims(cfg.cfg, args.N or cfg.N, world)
+        lo, hi = gsk.shard_rows(n_glob, world, rank)
+        s = workloads.generate_rows("C4w", lo, hi, N=args.N, param=world)
+        s_desc = {"n": n_glob, "nnz": nnz_glob}
+    else:
+        s = workloads.generate(args.config, N=args.N)
+        s_desc = s
     A0 = gsk.CSR.from_system(s)
     b0 = torch.tensor(s["b"], device="cuda")
     vbuf, bbuf, dbuf = torch.empty_like(A0.val), torch.empty_like(b0), torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
-    fmt = args.fmt
-    comm = gsk.NcclComm() if world > 1 else None
-    SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
-    lo, hi = SP.rows
-    bl = bbuf[lo:hi]
+    if weak:
+        SP = gsk.ShardedPlan(As, fmt=fmt, comm=comm, n_global=n_glob)
+        bl = bbuf
+    else:
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
+        lo, hi = SP.rows
+        bl = bbuf[lo:hi]
     x1 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
     x2 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
 
@@ -474,10 +499,15 @@ def run_sharded(args, rank, world, local):
                "gmres_sha256": hashlib.sha256(np.ascontiguousarray(h2, "<f8").tobytes()).hexdigest()}
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist)
-    # roofline: shard 0's v = A p pass (probe 0) against its own rows' bytes
-    l0, h0 = gsk.shard_rows(s["n"], P, rank if world > 1 else 0)
-    nnz0 = int(s["row_ptr"][h0] - s["row_ptr"][l0])
+        e2e = measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist,
+                                  n_global=n_glob if weak else None)
+    # roofline: this rank's (or emulated shard 0's) v = A p pass (probe 0) against its
+    # own rows' bytes
+    if weak:
+        l0, h0, nnz0 = lo, hi, int(s["nnz"])
+    else:
+        l0, h0 = gsk.shard_rows(s["n"], P, rank if world > 1 else 0)
+        nnz0 = int(s["row_ptr"][h0] - s["row_ptr"][l0])
     tot, cnt = SP.probe(0)
     t0, c0 = probes0[0]
     p_ms = (tot * cnt - t0 * c0) / (cnt - c0) if cnt > c0 else None
@@ -494,11 +524,13 @@ def run_sharded(args, rank, world, local):
         line = {
             "metric": METRIC, "value": its / (ms / 1e3), "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "none (emulated shards on one GPU)",
+            "scaling": "weak" if weak else ("strong" if world > 1 else "none (emulated shards on one GPU)"),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**config_desc(args, cfg, s), "parallelism": f"rows/{P}", "shards": P,
-                       "placement": f"{world} GPUs, NCCL halos + all-gathers" if world > 1
-                       else "all shards on one GPU (device-copy halos)"},
+            "config": {**config_desc(args, cfg, s_desc), "parallelism": f"rows/{P}", "shards": P,
+                       "placement": (f"{world} GPUs, NCCL halos + all-gathers" if world > 1
+                                     else "all shards on one GPU (device-copy halos)")
+                       + ("; each rank generates and holds only its own 256^3 block (local input)"
+                          if weak else "")},
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "comm": {"backend": "nccl" if world > 1 else "none (one process)", "nranks": world,
                      "shards": P, "nranks_ok": (comm.world == world) if comm else world == 1},
@@ -559,15 +591,19 @@ def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args, dist=None):
             "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
 
 
-def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist):
+def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist, n_global=None):
     """e2e of the sharded step: every step each rank copies the system from pinned host
-    memory (the sharded plan reads its rows and halo from the global arrays), scales
-    it, builds its shard plan, runs both solves and reads its rows of x back.  Whole-job
-    value: the one system's iterations / the slowest rank's time."""
+    memory (the sharded plan reads its rows and halo from the global arrays; with
+    n_global, the rank's own rows only), scales it, builds its shard plan, runs both
+    solves and reads its rows of x back.  Whole-job value: the one system's iterations
+    / the slowest rank's time."""
     pin = {k: torch.from_numpy(np.ascontiguousarray(s[k])).pin_memory() for k in ("row_ptr", "col", "val", "b")}
     h2d = sum(t.numel() * t.element_size() for t in pin.values())
-    lo, hi = gsk.shard_rows(s["n"], P, comm.rank if comm else 0)
-    if not comm:
+    if n_global is not None:
+        lo, hi = 0, s["hi"] - s["lo"]
+    elif comm:
+        lo, hi = gsk.shard_rows(s["n"], P, comm.rank)
+    else:
         lo, hi = 0, s["n"]
     xo1 = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
     xo2 = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
@@ -577,7 +613,7 @@ def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist)
         dev = {k: v.to("cuda", non_blocking=True) for k, v in pin.items()}
         A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
         As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
-        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, n_global=n_global)
         x1, _, r1 = SP.bicgstab(bs[lo:hi], tol=cfg.tol, maxit=cfg.maxit, hist=False)
         x2, _, r2 = SP.gmres(bs[lo:hi], m=m, tol=cfg.tol, maxit=gmaxit, hist=False)
         xo1.copy_(x1, non_blocking=True)
@@ -603,8 +639,13 @@ def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist)
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
-        h2d *= dist.get_world_size()
-        d2h = 2 * s["n"] * 8
+        if n_global is None:
+            h2d *= dist.get_world_size()
+            d2h = 2 * s["n"] * 8
+        else:  # each rank copied its own rows
+            t = torch.tensor([float(h2d), float(d2h)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t)
+            h2d, d2h = int(t[0].item()), int(t[1].item())
     return {"value": its / (ms / 1e3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
 

@@ -71,6 +71,11 @@ typedef struct gsk_report {
  * weights: NULL, or DEVICE [n] w_i > 0.  When set, Bi-CGSTAB's stopping test and
  * history use ||w o r|| / ||w o r0|| — the paper measures the relative residual on
  * the GS(2)-scaled system, i.e. w = d_GS(2) / d_applied.
+ * GMRES does NOT stop in the weighted frame: its per-step residual is the
+ * least-squares estimate |g_{j+1}|, which exists only in the solved frame (the
+ * weighted norm of r_j = V_{j+1} Q^T e_{j+1} g_{j+1} would cost a pass over the basis
+ * per step), so GMRES stops and records history in the solved frame and the weights
+ * enter only the reported true_relres_w (reading B2).
  * poll: iterations per device-resident batch between host checks (0 = auto). */
 typedef struct gsk_opts {
   int32_t format;
@@ -199,7 +204,13 @@ typedef struct gsk_shard_opts {
   int32_t first;     /* first shard held by this process */
   int32_t count;     /* shards held by this process: P (all of them, one GPU) or 1
                         (one shard per process, one process per GPU) */
-  int32_t pad_;
+  int32_t local_input; /* 0: A is the GLOBAL matrix (every process passes all of it).
+                        1 (count == 1 with a communicator only): A holds only this
+                        process's rows [lo, hi) of shard `first` — A->n is still the
+                        GLOBAL row count, A->row_ptr has hi - lo + 1 entries (any
+                        base), A->col_idx global columns, A->nnz the local count — so no
+                        process ever holds the whole system (weak scaling); the halo
+                        widths are all-gathered over the communicator. */
   void *nccl_comm;   /* ncclComm_t over the P processes (count == 1: this process holds
                         shard `first`), or NULL (count == P: all shards on this GPU);
                         from gsk_nccl_comm_create, not owned by the plan */
@@ -215,7 +226,7 @@ int gsk_shard_halo_host(int64_t n, const int32_t *row_ptr, const int32_t *col, i
                         int32_t *hl, int32_t *hr);
 
 /* Plan over this process's shards of the GLOBAL matrix A (device, global columns;
- * every process passes the whole matrix).  Each shard gets its own CSR (rebased row
+ * every process passes the whole matrix, or with sh->local_input only its own rows).  Each shard gets its own CSR (rebased row
  * pointers, columns relative to its first row) and, for GSK_FMT_SELL, its own SELL
  * layout; values are read from A->values (gsk_plan_refresh after rescaling).  Solves
  * on the plan (gsk_bicgstab_solve_plan, gsk_gmres_solve_plan) take b, x0, x and the

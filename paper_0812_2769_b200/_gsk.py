@@ -57,7 +57,7 @@ class Opts(ctypes.Structure):
 
 class ShardOpts(ctypes.Structure):
     _fields_ = [("nshards", ctypes.c_int32), ("first", ctypes.c_int32), ("count", ctypes.c_int32),
-                ("pad_", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p)]
+                ("local_input", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p)]
 
 
 class GskError(RuntimeError):
@@ -364,7 +364,9 @@ class Plan:
         return self._solve("bicgstab", b, x0, tol, maxit, x=x, hist=hist)
 
     def gmres(self, b, x0=None, m=30, tol=1e-8, maxit=10000, x=None, hist=True):
-        """Restarted GMRES(m) on the plan's system; returns (x, hist, report)."""
+        """Restarted GMRES(m) on the plan's system; returns (x, hist, report).  GMRES stops
+        on its least-squares estimate in the SOLVED frame; the plan's frame weights only
+        enter report["true_relres_w"] (gsk.h, reading B2)."""
         return self._solve("gmres", b, x0, tol, maxit, m=m, x=x, hist=hist)
 
 
@@ -413,25 +415,34 @@ class ShardedPlan(Plan):
     """Row-block sharded plan: `shards` row blocks of the GLOBAL matrix A.
     On one GPU (comm=None) this process holds all shards; with an NcclComm each rank
     holds shard `comm.rank` of `comm.world`.  Solves take and return this process's
-    rows; the history is global.  Bit-identical to the unsharded solvers."""
+    rows; the history is global.  Bit-identical to the unsharded solvers.
+
+    ``n_global`` (with a comm only): A holds just this rank's rows [lo, hi) with global
+    column indices (gsk_shard_opts.local_input), so no rank holds the whole system."""
 
     def __init__(self, A: CSR, shards: int = 2, fmt: str = "csr", weights=None, poll: int = 0,
-                 comm: "NcclComm" = None):
+                 comm: "NcclComm" = None, n_global: int = None):
         lib = load()
         self.A = A
         if comm is None:
+            if n_global is not None:
+                raise ValueError("n_global (local input) needs an NcclComm: one shard per rank")
             first, count, ch = 0, int(shards), None
         else:
             shards, first, count, ch = comm.world, comm.rank, 1, comm.h
-        lo, _ = shard_rows(A.n, shards, first)
-        _, hi = shard_rows(A.n, shards, first + count - 1)
+        ng = A.n if n_global is None else int(n_global)
+        lo, _ = shard_rows(ng, shards, first)
+        _, hi = shard_rows(ng, shards, first + count - 1)
+        if n_global is not None and hi - lo != A.n:
+            raise ValueError(f"local input: A has {A.n} rows, shard {first} of {ng} rows owns {hi - lo}")
         self.rows = (lo, hi)
         self.nloc = hi - lo
         self.weights = _dev_f64(weights, self.nloc)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
                     SCHEDULE["split"], ORTH["mgs"], 0, ENGINE["graph"])
-        so = ShardOpts(int(shards), int(first), int(count), 0, ch)
+        so = ShardOpts(int(shards), int(first), int(count), int(n_global is not None), ch)
         self._csr = A.struct()
+        self._csr.n = ng
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create_sharded(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(so),
                                            ctypes.byref(h), _stream()))

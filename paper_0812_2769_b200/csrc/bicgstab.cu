@@ -191,6 +191,7 @@ using namespace gsk;
 
 extern "C" int gsk_bicgstab_solve_plan(gsk_plan* plan, const double* b, const double* x0, double tol,
                                        int maxit, double* x, double* hist, gsk_report* rep, void* stream) {
+  NvtxRange nv("gsk:bicgstab");
   if (!plan) {
     set_error("gsk_bicgstab_solve_plan: plan is NULL");
     return GSK_E_INVALID;

@@ -225,12 +225,12 @@ int cluster_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, do
   int B = 0;
   const int cs = cluster_geometry(n, &B);
   if (!cs) return GSK_OK;
-  static bool attr = false;
-  if (!attr) {
+  static const char attr_key = 0;  // function attributes are per device
+  if (!device_attr_done(&attr_key)) {
     GSK_CUDA(cudaFuncSetAttribute(cluster_bicgstab, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     GSK_CUDA(cudaFuncSetAttribute(cluster_bicgstab, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(6 * sizeof(double) * CL_RPT * CL_T)));
-    attr = true;
+    device_attr_mark(&attr_key);
   }
   ClusterBicgArgs a{P->csr, n, B, b, P->weights, x, P->hist_d, P->bstate, tol, maxit};
   void* args[] = {&a};
@@ -317,12 +317,12 @@ int cluster_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState&
   constexpr size_t kWsm = 196 * 1024;  // basis in shared memory when it fits
   const size_t wbytes = sizeof(double) * (size_t)(h.m + 1) * B;
   const bool smemw = wbytes <= kWsm;
-  static bool attr = false;
-  if (!attr) {
+  static const char attr_key = 0;  // function attributes are per device
+  if (!device_attr_done(&attr_key)) {
     GSK_CUDA(cudaFuncSetAttribute(cluster_gmres<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     GSK_CUDA(cudaFuncSetAttribute(cluster_gmres<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     GSK_CUDA(cudaFuncSetAttribute(cluster_gmres<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsm));
-    attr = true;
+    device_attr_mark(&attr_key);
   }
   ClusterGmresArgs a{P->csr, n, B, b, P->weights, x, P->W, P->hist_d, h, P->gstate};
   void* args[] = {&a};

@@ -208,6 +208,7 @@ using namespace gsk;
 
 extern "C" int gsk_gmres_solve_plan(gsk_plan* plan, const double* b, const double* x0, int m, double tol,
                                     int maxit, double* x, double* hist, gsk_report* rep, void* stream) {
+  NvtxRange nv("gsk:gmres");
   if (!plan) {
     set_error("gsk_gmres_solve_plan: plan is NULL");
     return GSK_E_INVALID;

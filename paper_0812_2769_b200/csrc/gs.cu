@@ -149,18 +149,24 @@ static int launch_gs(int grid, cudaStream_t s, int n, const int* rp, const doubl
   return GSK_OK;
 }
 
-// Per-process device word for the zero-row flag (avoids a stream-ordered allocation
-// per call).  Calls hold g_flag_mu from the reset to the read-back, so concurrent
-// callers on different streams / host threads never share it.
-static std::mutex g_flag_mu;
-static int* zero_row_flag(cudaStream_t s, int* err) {
-  static int* flag = nullptr;
-  if (!flag && cudaMalloc(&flag, sizeof(int)) != cudaSuccess) {
+// One device word per GPU for the zero-row flag (avoids a stream-ordered allocation per
+// call).  Calls hold that device's mutex from the reset to the read-back, so concurrent
+// callers on different streams / host threads never share a flag; calls on different
+// devices do not wait for each other.
+constexpr int kMaxDevices = 64;
+static std::mutex g_flag_mu[kMaxDevices];
+static int current_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+static int* zero_row_flag(int dev, int* err) {
+  static int* flag[kMaxDevices] = {};
+  if (dev < 0 || dev >= kMaxDevices || (!flag[dev] && cudaMalloc(&flag[dev], sizeof(int)) != cudaSuccess)) {
     *err = 1;
     return nullptr;
   }
-  (void)s;
-  return flag;
+  return flag[dev];
 }
 
 }  // namespace gsk
@@ -169,6 +175,7 @@ using namespace gsk;
 
 extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double* values_out,
                                 double* b_out, double* s_out, int32_t* bad_row, void* stream) {
+  NvtxRange nv("gsk:gs_scale_sym");
   if (!A || A->n < 1 || A->nnz < 0 || !A->row_ptr || !s_out ||
       (A->nnz > 0 && (!A->values || !values_out || !A->col_idx))) {
     set_error("gsk_gs_scale_sym: invalid arguments");
@@ -183,9 +190,14 @@ extern "C" int gsk_gs_scale_sym(const gsk_csr* A, const double* b, int p, double
     return GSK_E_INVALID;
   }
   cudaStream_t s = as_stream(stream);
-  std::lock_guard<std::mutex> lock(g_flag_mu);
+  const int dev = current_dev();
+  if (dev < 0 || dev >= kMaxDevices) {
+    set_error("gs: device ordinal %d out of range", dev);
+    return GSK_E_INVALID;
+  }
+  std::lock_guard<std::mutex> lock(g_flag_mu[dev]);
   int ferr = 0;
-  int* dbad = zero_row_flag(s, &ferr);
+  int* dbad = zero_row_flag(dev, &ferr);
   if (ferr) {
     set_error("gs: cannot allocate the zero-row flag");
     return GSK_E_NOMEM;
@@ -223,6 +235,7 @@ extern "C" int gsk_gs_unscale(int64_t n, const double* s_in, const double* y, do
 
 extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* values_out,
                             double* b_out, double* d_out, int32_t* bad_row, void* stream) {
+  NvtxRange nv("gsk:gs_scale");
   if (!A || A->n < 1 || A->nnz < 0 || !A->row_ptr || (A->nnz > 0 && (!A->values || !values_out))) {
     set_error("gsk_gs_scale: invalid matrix");
     return GSK_E_INVALID;
@@ -236,9 +249,14 @@ extern "C" int gsk_gs_scale(const gsk_csr* A, const double* b, int p, double* va
     return GSK_E_INVALID;
   }
   cudaStream_t s = as_stream(stream);
-  std::lock_guard<std::mutex> lock(g_flag_mu);
+  const int dev = current_dev();
+  if (dev < 0 || dev >= kMaxDevices) {
+    set_error("gs: device ordinal %d out of range", dev);
+    return GSK_E_INVALID;
+  }
+  std::lock_guard<std::mutex> lock(g_flag_mu[dev]);
   int ferr = 0;
-  int* dbad = zero_row_flag(s, &ferr);
+  int* dbad = zero_row_flag(dev, &ferr);
   if (ferr) {
     set_error("gs: cannot allocate the zero-row flag");
     return GSK_E_NOMEM;

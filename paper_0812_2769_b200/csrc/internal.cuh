@@ -6,11 +6,22 @@
 #include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
+#include <nvtx3/nvToolsExt.h>
 #include "common.cuh"
 #include "engine.cuh"
 #include "gsk.h"
 
 namespace gsk {
+
+// NVTX range over one library call (header-only NVTX3: no cost unless a profiler
+// injects itself), so nsys / ncu timelines show the solver phases by name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 void set_error(const char* fmt, ...);
 extern std::atomic<int64_t> g_launches;
@@ -172,6 +183,9 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // GSK_CARVEOUT=<percent> overrides it, GSK_CARVEOUT=-1 leaves the driver's choice.
 int smem_carveout();
 void set_pass_carveout(const void* kern);
+// per-device "function attributes already set" registry (keyed by any pointer)
+bool device_attr_done(const void* key);
+void device_attr_mark(const void* key);
 template <typename... KArgs>
 void pass_carveout(void (*kern)(KArgs...)) {
   set_pass_carveout(reinterpret_cast<const void*>(kern));

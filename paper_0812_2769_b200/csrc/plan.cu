@@ -3,6 +3,7 @@
 // gsk_plan_residual_norm, SELL copy-out, probes, diagnostics.
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <unordered_map>
 #include <string>
 #include <vector>
@@ -69,27 +70,43 @@ int smem_carveout() {
   return c;
 }
 
+// Function attributes are per device: (device, key) pairs already configured.
+static std::mutex g_attr_mu;
+static std::set<std::pair<int, const void*>> g_attr_done;
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+bool device_attr_done(const void* key) {
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  return g_attr_done.count({current_device(), key}) > 0;
+}
+void device_attr_mark(const void* key) {
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  g_attr_done.insert({current_device(), key});
+}
+
 void set_pass_carveout(const void* kern) {
-  static std::mutex mu;
-  static std::unordered_map<const void*, int> done;
   const int pct = smem_carveout();
-  if (pct < 0) return;
-  std::lock_guard<std::mutex> lock(mu);
-  if (done.count(kern)) return;
+  if (pct < 0 || device_attr_done(kern)) return;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaGetLastError();  // a refused hint is not an error of the pass
-  done[kern] = pct;
+  device_attr_mark(kern);
 }
 
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
+  static std::mutex mu;
+  static std::unordered_map<int, int> sms;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (v <= 0) v = 148;
+  sms[dev] = v;
+  return v;
 }
 
 // Reduction scratch: CTA partials of one pass ([MAXD][pstride], pstride >= CTAs).
@@ -232,6 +249,7 @@ int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels
 
 int run_batches(gsk_plan* P, cudaGraphExec_t* graphs, long long maxb, long long kernels, const int* done_dev,
                 const int* kinds, int nkinds) {
+  NvtxRange nv("gsk:graph_batches");
   constexpr int NQ = gsk_plan::NQ;
   cudaStream_t s = P->st;
   // batches in flight: 3 for large systems (a late host check never idles the GPU);
@@ -302,6 +320,7 @@ int gsk_plan_create(const gsk_csr* A, const gsk_opts* opts, gsk_plan** plan, voi
 
 namespace gsk {
 int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_plan** plan, cudaStream_t stream) {
+  NvtxRange nv("gsk:plan_create");
   GSK_TRY(check_csr(A, "gsk_plan_create"));
   if (!plan) {
     set_error("gsk_plan_create: plan is NULL");
@@ -365,6 +384,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
 extern "C" {
 
 int gsk_plan_refresh(gsk_plan* P, void* stream) {
+  NvtxRange nv("gsk:plan_refresh");
   if (!P) return GSK_E_INVALID;
   if (P->shards) return shard_refresh(P, as_stream(stream));
   if (P->fmt != GSK_FMT_SELL) return GSK_OK;

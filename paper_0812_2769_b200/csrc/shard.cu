@@ -557,6 +557,7 @@ int gsk_nccl_comm_destroy(void* comm) {
 
 int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_shard_opts* so, gsk_plan** plan,
                             void* stream) {
+  NvtxRange nv("gsk:plan_create_sharded");
   if (!A || !so || !plan || A->n < 1 || !A->row_ptr || (A->nnz > 0 && (!A->col_idx || !A->values))) {
     set_error("gsk_plan_create_sharded: invalid arguments");
     return GSK_E_INVALID;
@@ -571,6 +572,11 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
   if (!local && !remote) {
     set_error("gsk_plan_create_sharded: need count == nshards without a communicator (all shards on this GPU) "
               "or count == 1 with an NCCL communicator");
+    return GSK_E_INVALID;
+  }
+  const bool linput = so->local_input != 0;
+  if (linput && !remote) {
+    set_error("gsk_plan_create_sharded: local_input needs count == 1 and an NCCL communicator");
     return GSK_E_INVALID;
   }
   if (remote && !nccl()) {
@@ -605,15 +611,22 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
     return fail(GSK_E_NOMEM);
   }
   if (cudaMemsetAsync(S->gath, 0, sizeof(double) * P * MAXD, s) != cudaSuccess) return fail(GSK_E_CUDA);
-  // layout and halo widths of every shard (every process computes all of them)
-  std::vector<int> rph(2);
-  for (int r = 0; r < P; ++r) {
-    shard_rows(A->n, P, r, &S->lo[r], &S->hi[r]);
-    int k01[2];
-    if (cudaMemcpyAsync(&k01[0], A->row_ptr + S->lo[r], sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(&k01[1], A->row_ptr + S->hi[r], sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+  // entries [k0, k1) of shard r in A's arrays (local input: this process's rows only)
+  auto entry_range = [&](int r, int* k01) -> int {
+    const int64_t a = linput ? 0 : S->lo[r], b = linput ? S->hi[r] - S->lo[r] : S->hi[r];
+    if (cudaMemcpyAsync(&k01[0], A->row_ptr + a, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(&k01[1], A->row_ptr + b, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
-      return fail(GSK_E_CUDA);
+      return GSK_E_CUDA;
+    return GSK_OK;
+  };
+  for (int r = 0; r < P; ++r) shard_rows(A->n, P, r, &S->lo[r], &S->hi[r]);
+  // halo widths of every shard: from the global matrix (every process computes all of
+  // them), or — local input — each process its own, all-gathered
+  for (int r = 0; r < P; ++r) {
+    if (linput && r != so->first) continue;
+    int k01[2];
+    if (entry_range(r, k01) != GSK_OK) return fail(GSK_E_CUDA);
     const int init[2] = {INT_MAX, INT_MIN};
     int mm[2] = {INT_MAX, INT_MIN};
     if (k01[1] > k01[0]) {
@@ -625,6 +638,27 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
     }
     S->hl[r] = mm[0] < S->lo[r] ? (int)(S->lo[r] - mm[0]) : 0;
     S->hr[r] = mm[1] > S->hi[r] - 1 ? (int)(mm[1] - (S->hi[r] - 1)) : 0;
+  }
+  if (linput && P > 1) {  // every process's (hl, hr), all-gathered
+    int* hh = nullptr;
+    if (cudaMalloc(&hh, sizeof(int) * 2 * P) != cudaSuccess) return fail(GSK_E_NOMEM);
+    const int mine[2] = {S->hl[so->first], S->hr[so->first]};
+    std::vector<int> all(2 * P);
+    int rc = GSK_OK;
+    if (cudaMemcpyAsync(hh + 2 * so->first, mine, sizeof mine, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = GSK_E_CUDA;
+    if (rc == GSK_OK && nccl()->allGather(hh + 2 * so->first, hh, 2, ncclInt32, S->comm, s) != ncclSuccess) {
+      set_error("gsk_plan_create_sharded: ncclAllGather of the halo widths failed");
+      rc = GSK_E_CUDA;
+    }
+    if (rc == GSK_OK && (cudaMemcpyAsync(all.data(), hh, sizeof(int) * 2 * P, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                         cudaStreamSynchronize(s) != cudaSuccess))
+      rc = GSK_E_CUDA;
+    cudaFree(hh);
+    if (rc != GSK_OK) return fail(rc);
+    for (int r = 0; r < P; ++r) {
+      S->hl[r] = all[2 * r];
+      S->hr[r] = all[2 * r + 1];
+    }
   }
   for (int r = 0; r < P; ++r) {
     if ((r > 0 && S->hl[r] > S->hi[r - 1] - S->lo[r - 1]) || (r + 1 < P && S->hr[r] > S->hi[r + 1] - S->lo[r + 1]) ||
@@ -649,17 +683,14 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
     d.hr = S->hr[r];
     d.pitch = (size_t)d.hl + d.n + d.hr;
     int k01[2];
-    if (cudaMemcpyAsync(&k01[0], A->row_ptr + d.lo, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(&k01[1], A->row_ptr + d.hi, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-      return fail(GSK_E_CUDA);
+    if (entry_range(r, k01) != GSK_OK) return fail(GSK_E_CUDA);
     const int64_t nnz = k01[1] - k01[0];
     if (cudaMalloc(&d.rp, sizeof(int) * (d.n + 1)) != cudaSuccess ||
         cudaMalloc(&d.ci, sizeof(int) * (nnz > 0 ? nnz : 1)) != cudaSuccess) {
       set_error("gsk_plan_create_sharded: allocation failed");
       return fail(GSK_E_NOMEM);
     }
-    shard_rp_kernel<<<(d.n + 256) / 256, 256, 0, s>>>(A->row_ptr, d.lo, d.n, d.rp);
+    shard_rp_kernel<<<(d.n + 256) / 256, 256, 0, s>>>(A->row_ptr, linput ? 0 : d.lo, d.n, d.rp);
     if (nnz > 0) shard_ci_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(A->col_idx, k01[0], nnz, (int)d.lo, d.ci);
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) {
       set_error("gsk_plan_create_sharded: shard CSR kernels failed");

@@ -140,11 +140,11 @@ __global__ void __launch_bounds__(SMALL_T, 1) small_bicgstab(SmallBicgArgs a) {
 
 int small_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x) {
   const int n = P->A.n;
-  static bool attr = false;
-  if (!attr) {
+  static const char attr_key = 0;  // function attributes are per device
+  if (!device_attr_done(&attr_key)) {
     GSK_CUDA(cudaFuncSetAttribute(small_bicgstab, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(6 * sizeof(double) * GSK_SMALL_NMAX)));
-    attr = true;
+    device_attr_mark(&attr_key);
   }
   SmallBicgArgs a{P->csr, n, b, P->weights, x, P->hist_d, P->bstate, tol, maxit};
   small_bicgstab<<<1, SMALL_T, 6 * sizeof(double) * (size_t)n, P->st>>>(a);

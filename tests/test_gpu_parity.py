@@ -67,6 +67,37 @@ CASES = [("C1", None), ("C2", 100), ("C2", 128), ("C3", 20), ("C4", 24), ("C5", 
 
 
 # ---------------------------------------------------------------- GS(p)
+@pytest.mark.parametrize("p", [1, 2])
+def test_gs_zero_rows_outputs(p):
+    """Zero rows (PAPER.md:207-208 assumes none; reading G5): GSK_E_ZERO_ROW names the
+    smallest one, and the GPU's outputs are fixed as gsk.h states — d_i = 0, the row's
+    values and b_i stay zero, every other row is scaled exactly as the oracle scales it
+    (GS is row-local: the oracle is run with the zero rows given a placeholder value)."""
+    s = workloads.generate("C1")
+    rp, val, b = s["row_ptr"], s["val"].copy(), s["b"].copy()
+    zero = [700, 3, 517]
+    for r in zero:
+        val[rp[r]:rp[r + 1]] = 0.0
+    A = gsk.CSR(rp, s["col"], val)
+    vout = torch.full((val.size,), 7.0, dtype=torch.float64, device="cuda")
+    bout = torch.full((s["n"],), 7.0, dtype=torch.float64, device="cuda")
+    dout = torch.full((s["n"],), 7.0, dtype=torch.float64, device="cuda")
+    with pytest.raises(gsk.GskError) as e:
+        gsk.gs_scale(A, b, p, out=(vout, bout, dout))
+    assert e.value.code == -2 and e.value.bad_row == 3  # GSK_E_ZERO_ROW
+    ph = val.copy()
+    for r in zero:
+        ph[rp[r]:rp[r + 1]] = 1.0
+    vo, bo, do = oracle.gs_scale(rp, ph, b, p)
+    vg, bg, dg = cpu(vout), cpu(bout), cpu(dout)
+    zmask = np.zeros(s["n"], bool)
+    zmask[zero] = True
+    emask = np.repeat(zmask, np.diff(rp))
+    assert np.array_equal(vg[~emask], vo[~emask]) and np.array_equal(bg[~zmask], bo[~zmask])
+    assert np.array_equal(dg[~zmask], do[~zmask])
+    assert np.all(vg[emask] == 0.0) and np.all(bg[zmask] == 0.0) and np.all(dg[zmask] == 0.0)
+
+
 @pytest.mark.parametrize("name,N", CASES + [("C4", None), ("C5", None)])
 @pytest.mark.parametrize("p", [1, 2, 3])
 def test_gs_scale_parity(name, N, p):
@@ -638,6 +669,37 @@ def test_sharded_nccl_single_rank():
                           oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400))
         assert_same_solve(SP.gmres(b, m=20, tol=1e-9, maxit=100),
                           oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 100))
+        SP.close()
+    assert lib.gsk_nccl_comm_destroy(h) == 0
+
+
+def test_sharded_local_input_single_rank():
+    """gsk_shard_opts.local_input (each rank passes only its own rows, global columns;
+    DESIGN.md §8 weak scaling) on a 1-rank NCCL communicator: the rows come from
+    workloads.generate_rows, and the solve is bit-identical to the oracle on the whole
+    system — here the stacked-slab workload C4w at reduced size."""
+    import ctypes
+    lib = gsk.load()
+    buf = ctypes.create_string_buffer(128)
+    assert lib.gsk_nccl_unique_id(buf) == 0
+    h = ctypes.c_void_p()
+    assert lib.gsk_nccl_comm_create(ctypes.c_char_p(bytes(buf.raw)), 1, 0, ctypes.byref(h)) == 0
+
+    class Comm:
+        world, rank = 1, 0
+
+    Comm.h = h
+    s = workloads.generate("C4w", N=16, param=2)
+    loc = workloads.generate_rows("C4w", 0, s["n"], N=16, param=2)
+    vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    A = gsk.CSR(loc["row_ptr"], loc["col"], loc["val"])
+    As, bs, _ = gsk.gs_scale(A, loc["b"], 2)
+    for fmt in ("csr", "sell"):
+        SP = gsk.ShardedPlan(As, fmt=fmt, comm=Comm, n_global=s["n"])
+        assert_same_solve(SP.bicgstab(bs, tol=1e-9, maxit=300),
+                          oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-9, 300))
+        assert_same_solve(SP.gmres(bs, m=30, tol=1e-9, maxit=90),
+                          oracle.gmres(s["row_ptr"], s["col"], vo, bo, 30, 1e-9, 90))
         SP.close()
     assert lib.gsk_nccl_comm_destroy(h) == 0
 

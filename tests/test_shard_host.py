@@ -149,3 +149,65 @@ def test_sharded_spmv_and_dot_gloo():
             ys, d = res[rank][name]
             assert np.array_equal(ys, y)
             assert d == oracle.dot(x, y)
+
+
+def _worker_local(rank, world, port, q):
+    """Local input (gsk_shard_opts.local_input; DESIGN.md §8 weak scaling): each rank
+    generates ONLY its rows of the stacked workload C4w (G = world), computes its own
+    halo widths from them, all-gathers the (hl, hr) pairs — what the library does over
+    NCCL at plan creation — and runs the halo-exchanged SpMV on its rows."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    N = 12
+    n, _ = workloads.dims(24, N, world)
+    lo, hi = gsk.shard_rows(n, world, rank)
+    loc = workloads.generate_rows("C4w", lo, hi, N=N, param=world)
+    hl = max(0, lo - int(loc["col"].min()))
+    hr = max(0, int(loc["col"].max()) - (hi - 1))
+    hh = [torch.empty(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(hh, torch.tensor([hl, hr], dtype=torch.int64))
+    nb = [tuple(int(v) for v in t) for t in hh]
+    x = workloads.uniform(n, 11, 12)
+    own = torch.tensor(x[lo:hi])
+    ext = torch.zeros(hl + (hi - lo) + hr, dtype=torch.float64)
+    ext[hl:hl + hi - lo] = own
+    reqs = []
+    if rank > 0:
+        reqs.append(dist.isend(own[:nb[rank - 1][1]].contiguous(), rank - 1))
+        left = torch.empty(hl, dtype=torch.float64)
+        reqs.append(dist.irecv(left, rank - 1))
+    if rank + 1 < world:
+        reqs.append(dist.isend(own[hi - lo - nb[rank + 1][0]:].contiguous(), rank + 1))
+        right = torch.empty(hr, dtype=torch.float64)
+        reqs.append(dist.irecv(right, rank + 1))
+    for rq in reqs:
+        rq.wait()
+    if rank > 0:
+        ext[:hl] = left
+    if rank + 1 < world:
+        ext[hl + hi - lo:] = right
+    y = oracle.spmv(loc["row_ptr"], loc["col"] - lo + hl, loc["val"], ext.numpy())
+    q.put((rank, (nb, lo, hi, y, loc["b"])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_local_input_layout_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29750 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker_local, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s = workloads.generate("C4w", N=12, param=2)  # the whole system, for comparison
+    x = workloads.uniform(s["n"], 11, 12)
+    y = oracle.spmv(s["row_ptr"], s["col"], s["val"], x)
+    for rank in (0, 1):
+        nb, lo, hi, yl, bl = res[rank]
+        assert nb == [gsk.shard_halo(s["row_ptr"], s["col"], 2, r) for r in range(2)]
+        assert np.array_equal(yl, y[lo:hi]) and np.array_equal(bl, s["b"][lo:hi])

@@ -177,3 +177,31 @@ def test_paper_tbl1b_eigenvalues():
     assert abs(lmin - g["lmin"]) / g["lmin"] < 0.005
     # "all real in (0, 8000)"; closed form 1000(4-2cos(pi h)-2cos(pi h))
     assert imag < 1e-6 * lmax
+
+
+@pytest.mark.parametrize("N", [6, 10])
+def test_stacked_slabs(N):
+    """C4w (weak scaling): G = 1 is C4 exactly; G copies have the closed-form
+    nnz 7 N^2 Nz - 4 N Nz - 2 N^2 (Nz = G N); row blocks from generate_rows (what each
+    rank builds) concatenate to the whole system; a block's k field repeats C4's."""
+    c4 = workloads.generate("C4", N=N)
+    w1 = workloads.generate("C4w", N=N, param=1)
+    for k in ("row_ptr", "col", "val", "b", "xstar"):
+        assert np.array_equal(c4[k], w1[k])
+    G = 3
+    s = workloads.generate("C4w", N=N, param=G)
+    Nz = G * N
+    assert s["n"] == N * N * Nz and s["nnz"] == 7 * N * N * Nz - 4 * N * Nz - 2 * N * N
+    cuts = [0, 7, s["n"] // 3, s["n"] // 3 + 1, s["n"]]
+    parts = [workloads.generate_rows("C4w", a, b, N=N, param=G) for a, b in zip(cuts, cuts[1:])]
+    off = np.cumsum([0] + [p["nnz"] for p in parts])
+    rp = np.concatenate([[0]] + [p["row_ptr"][1:] + o for p, o in zip(parts, off)])
+    assert np.array_equal(rp, s["row_ptr"])
+    for k in ("col", "val", "b", "xstar"):
+        assert np.array_equal(np.concatenate([p[k] for p in parts]), s[k])
+    # the middle block's interior rows (planes 1..N-2) equal C4's
+    NN = N * N
+    b1 = workloads.generate_rows("C4w", N * NN + NN, 2 * N * NN - NN, N=N, param=G)
+    ref = slice(c4["row_ptr"][NN], c4["row_ptr"][N * NN - NN])
+    assert np.array_equal(b1["val"], c4["val"][ref])
+    assert np.array_equal(b1["col"] - N * NN, c4["col"][ref])

@@ -38,6 +38,11 @@ def _lib():
         lib.gen_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
                                     ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
         lib.gen_uniform.restype = None
+        lib.gen_dims_stacked.argtypes = [ctypes.c_int, ctypes.c_int, i64p, i64p]
+        lib.gen_dims_stacked.restype = ctypes.c_int
+        lib.gen_fill_rows.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                                      ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 5
+        lib.gen_fill_rows.restype = ctypes.c_int
         _LIB = lib
     return _LIB
 
@@ -77,16 +82,23 @@ PAPER = {
 }
 
 
-def dims(cfg: int, N: int):
+# Weak-scaling variant of C4: G copies of C4's layered medium stacked
+# in z, 256 x 256 x 256G nodes, G = param (one 256^3 block per GPU); G = 1 is C4.
+STACKED = Config("C4w", 24, 256, 4, 1e-8, 10000, 30, ("none", 2), (1e-8,), param=1.0, sell=True)
+
+
+def dims(cfg: int, N: int, param: float = 0.0):
     n = ctypes.c_int64()
     nnz = ctypes.c_int64()
-    if _lib().gen_dims(cfg, N, ctypes.byref(n), ctypes.byref(nnz)) != 0:
+    rc = (_lib().gen_dims_stacked(N, int(param) if param >= 1 else 1, ctypes.byref(n), ctypes.byref(nnz))
+          if cfg == 24 else _lib().gen_dims(cfg, N, ctypes.byref(n), ctypes.byref(nnz)))
+    if rc != 0:
         raise ValueError(f"unknown generator cfg {cfg} / N {N}")
     return n.value, nnz.value
 
 
 def generate_raw(cfg: int, N: int, seed: int = 0, param: float = 0.0) -> dict:
-    n, nnz = dims(cfg, N)
+    n, nnz = dims(cfg, N, param)
     out = {
         "row_ptr": np.empty(n + 1, np.int32), "col": np.empty(nnz, np.int32),
         "val": np.empty(nnz, np.float64), "xstar": np.empty(n, np.float64),
@@ -108,11 +120,39 @@ def generate(name: str, N: int | None = None, seed: int | None = None, param: fl
         c = CONFIGS.get(name) or PAPER[name]
         return generate_raw(c.cfg, N or c.N, c.seed if seed is None else seed,
                             c.param if param is None else param)
+    if name == "C4w":
+        c = STACKED
+        return generate_raw(c.cfg, N or c.N, c.seed if seed is None else seed, c.param if param is None else param)
     if name == "lap2d":
         return generate_raw(20, N or 16, 0)
     if name == "lap3d":
         return generate_raw(21, N or 8, 0)
     raise KeyError(name)
+
+
+def generate_rows(name: str, lo: int, hi: int, N: int | None = None, param: float | None = None) -> dict:
+    """Rows [lo, hi) of config ``name`` (global column indices; row_ptr starts at 0), with
+    x* and b = A x* on those rows — one rank's block of a row-block sharded solve,
+    without generating the rest (not for C5, whose permutation is global).  Row for
+    row identical to ``generate``.  ``n`` is the global row count."""
+    c = STACKED if name == "C4w" else CONFIGS[name]
+    N = N or c.N
+    param = c.param if param is None else param
+    n, _ = dims(c.cfg, N, param)
+    # exact nnz of the block from the row lengths' closed form is config-specific;
+    # bound it by 7 (3D) / 5 (2D) entries per row and trim
+    cap = (7 if c.cfg in (3, 4, 24) else 5) * (hi - lo)
+    out = {"row_ptr": np.empty(hi - lo + 1, np.int32), "col": np.empty(cap, np.int32),
+           "val": np.empty(cap, np.float64), "xstar": np.empty(hi - lo, np.float64),
+           "b": np.empty(hi - lo, np.float64)}
+    rc = _lib().gen_fill_rows(c.cfg, N, c.seed, param, lo, hi,
+                              *(out[k].ctypes.data for k in ("row_ptr", "col", "val", "xstar", "b")))
+    if rc != 0:
+        raise ValueError(f"gen_fill_rows failed for {name} rows [{lo}, {hi})")
+    nnz = int(out["row_ptr"][-1])
+    out["col"], out["val"] = out["col"][:nnz].copy(), out["val"][:nnz].copy()
+    out.update(n=n, nnz=nnz, lo=lo, hi=hi)
+    return out
 
 
 def uniform(n: int, seed: int, stream: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:

@@ -55,6 +55,7 @@ enum Scheme { CENTRED = 0, UPWIND = 1, CONSERVATIVE = 2 };
 struct Problem {
   int dim = 2;
   int N = 0;
+  int Nz = 0;  // planes in z (3D); N except for the stacked-slab variant (cfg 24)
   Scheme scheme = CENTRED;
   // k at a face midpoint given by doubled-lattice coords (mx, my, mz); a point
   // has coordinate m / (2(N+1)).  Used when node_k is empty.
@@ -69,7 +70,7 @@ struct Problem {
 
 inline int64_t nrows(const Problem& P) {
   int64_t N = P.N;
-  return P.dim == 2 ? N * N : N * N * N;
+  return P.dim == 2 ? N * N : N * N * P.Nz;
 }
 
 // number of structural neighbours of node (I,J,K) inside the grid
@@ -77,7 +78,7 @@ inline int row_len(const Problem& P, int64_t I, int64_t J, int64_t K) {
   int N = P.N;
   int c = 1;
   c += (I > 0) + (I < N - 1) + (J > 0) + (J < N - 1);
-  if (P.dim == 3) c += (K > 0) + (K < N - 1);
+  if (P.dim == 3) c += (K > 0) + (K < P.Nz - 1);
   return c;
 }
 
@@ -156,7 +157,7 @@ int assemble_row(const Problem& P, int64_t I, int64_t J, int64_t K,
   put(true, r, off[3]);
   put(I < N - 1, r + 1, off[4]);
   put(J < N - 1, r + N, off[5]);
-  if (P.dim == 3) put(K < N - 1, r + NN, off[6]);
+  if (P.dim == 3) put(K < P.Nz - 1, r + NN, off[6]);
   return cnt;
 }
 
@@ -167,6 +168,7 @@ int assemble_row(const Problem& P, int64_t I, int64_t J, int64_t K,
 // convection; closed-form eigenvectors).
 bool make_problem(int cfg, int N, uint64_t seed, double param, Problem& P) {
   P.N = N;
+  P.Nz = N;
   switch (cfg) {
     case 1: {  // C1: 2D, k=1e4 strictly inside (1/4,3/4)^2, b=(10,10), centred
       P.dim = 2; P.scheme = CENTRED;
@@ -236,6 +238,22 @@ bool make_problem(int cfg, int N, uint64_t seed, double param, Problem& P) {
         return kvv[s];
       };
       P.vel = [](double, double, double, double* v) { v[0] = 30; v[1] = 0; v[2] = -30; };
+      return true;
+    }
+    case 24: {  // C4 stacked: G = param copies of C4's layered medium in z (weak scaling,
+      // DESIGN.md §8).  N x N x (G N) nodes, the same h, velocity and slab cuts; a face
+      // takes the slab of its block's local doubled coordinate (the face between two
+      // blocks is the upper block's bottom face; the top face of the last block keeps
+      // C4's top slab), so G = 1 is exactly C4.
+      const int G = param >= 1 ? (int)param : 1;
+      if (!make_problem(4, N, seed, 0.0, P)) return false;
+      P.Nz = N * G;
+      auto k4 = P.kface;
+      const int64_t twoN = 2 * (int64_t)N;
+      P.kface = [k4, twoN, G](int64_t mx, int64_t my, int64_t mz) {
+        const int64_t g = std::min<int64_t>(G - 1, (mz - 1) / twoN);
+        return k4(mx, my, mz - g * twoN);
+      };
       return true;
     }
     case 5: {  // C5: 2D centred, log-uniform k via Gaussian-copula field (M13)
@@ -326,6 +344,15 @@ bool make_problem(int cfg, int N, uint64_t seed, double param, Problem& P) {
 
 extern "C" {
 
+// Sizes of the stacked-slab system (cfg 24): N x N x (G N) nodes.
+int gen_dims_stacked(int N, int G, int64_t* n, int64_t* nnz) {
+  if (N < 2 || G < 1) return -1;
+  const int64_t NN = (int64_t)N * N, Nz = (int64_t)N * G;
+  *n = NN * Nz;
+  *nnz = 7 * NN * Nz - 4 * (int64_t)N * Nz - 2 * NN;
+  return 0;
+}
+
 // Sizes of the system for (cfg, N).  Returns 0, or -1 for an unknown cfg.
 int gen_dims(int cfg, int N, int64_t* n, int64_t* nnz) {
   Problem P;
@@ -409,6 +436,42 @@ int gen_fill(int cfg, int N, uint64_t seed, double param, int32_t* row_ptr, int3
     double acc = 0.0;
     for (int32_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) acc = std::fma(val[q], xstar[col[q]], acc);
     b[r] = acc;
+  }
+  return 0;
+}
+
+// Rows [lo, hi) of the system (global column indices, row_ptr[0] = 0), x* and b = A x*
+// on those rows — what one rank of a row-block sharded solve needs,
+// without building the rest.  Any config but C5 (whose permutation is global) and
+// the paper's P-workloads (b from boundary data).  Row for row identical to gen_fill.
+int gen_fill_rows(int cfg, int N, uint64_t seed, double param, int64_t lo, int64_t hi, int32_t* row_ptr,
+                  int32_t* col, double* val, double* xstar, double* b) {
+  if (cfg == 5 || cfg == 11 || cfg == 12 || cfg == 14 || cfg == 15) return -1;
+  Problem P;
+  if (!make_problem(cfg, N, seed, param, P)) return -1;
+  const int64_t n = nrows(P);
+  if (lo < 0 || hi > n || lo > hi) return -1;
+  const int64_t NN = (int64_t)N * N, m = hi - lo;
+  row_ptr[0] = 0;
+  for (int64_t q = 0; q < m; ++q) {
+    const int64_t r = lo + q;
+    int64_t I = r % N, J = (r / N) % N, K = P.dim == 3 ? r / NN : 0;
+    row_ptr[q + 1] = row_ptr[q] + row_len(P, I, J, K);
+  }
+  #pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < m; ++q) {
+    const int64_t r = lo + q;
+    int64_t I = r % N, J = (r / N) % N, K = P.dim == 3 ? r / NN : 0;
+    double bc = 0.0;
+    assemble_row(P, I, J, K, col + row_ptr[q], val + row_ptr[q], &bc);
+  }
+  #pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < m; ++q) {
+    xstar[q] = 2.0 * u01(seed, 1, lo + q) - 1.0;
+    double acc = 0.0;
+    for (int32_t k = row_ptr[q]; k < row_ptr[q + 1]; ++k)
+      acc = std::fma(val[k], 2.0 * u01(seed, 1, col[k]) - 1.0, acc);
+    b[q] = acc;
   }
   return 0;
 }
