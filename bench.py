@@ -18,7 +18,7 @@ e2e    = the same through the public API with the system copied from pinned host
 roofline: the dominant kernel (the split schedule's S1 pass v = A p, <r^,v>) —
          algorithmic bytes 12 nnz + 4(n+1) + 3*8n per launch / its
          CUDA-event time inside the captured graphs; traffic from the committed ncu
-         capture (profiles/r01_ncu_traffic.json).
+         capture (profiles/r02_ncu_traffic.json).
 extra  = SpMV and GS(2) rooflines, per-pass probes and time_to_tol (time to 1e-8 of
          Bi-CGSTAB and of GMRES(30) without scaling, with GS(1), GS(2) and two-sided
          scaling).
@@ -192,9 +192,9 @@ def run_reference(args, rank, world):
 
 def ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
-    capture (profiles/r01_ncu_traffic.json), or None."""
+    capture (profiles/r02_ncu_traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
             k = json.load(f)["kernels"].get(kernel)
         return k["bytes_per_launch"] if k else None
     except (OSError, ValueError, KeyError):

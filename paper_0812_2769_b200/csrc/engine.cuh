@@ -237,16 +237,6 @@ __device__ __forceinline__ double sell_window_nat(const SellView& A, int r0, con
   return y;
 }
 
-// Bit w set: window w of this CTA keeps its natural row order.  Every lane of every
-// warp gets the same mask (lane w of each warp reads window w's flag).
-__device__ __forceinline__ unsigned sell_nat_mask(const SellView& A, int bx, int wpc, int n) {
-  if (A.all_nat) return 0xffffffffu;
-  if (!A.wid) return 0u;
-  const int lane = threadIdx.x & 31;
-  const long long wi = (long long)bx * wpc + lane;
-  const bool f = lane < wpc && wi * TB < n && A.wid[wi];
-  return __ballot_sync(0xffffffffu, f);
-}
 
 // Op::kEvict (optional): bit k set = own-row operand vin(k) is not read by the NEXT
 // pass, so the register-path load of it is evict-first (ld.global.cs) and
@@ -366,7 +356,10 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 
 // FMT 0: vector pass, RPT windows (rows r0 + 256 w + t) per CTA, all loads in flight.
 // FMT 1/2/3: SpMV pass over wpc windows (CSR, SELL, SELL with column dictionary).
-template <int FMT, int RPT, class Op>
+// NAT (SELL only): every window of the plan keeps its natural row order (sell.cu), so
+// thread t computes row r0 + t itself — no roff, no scatter, no per-window barrier.
+// A compile-time choice: one code path per kernel keeps the 64-register budget.
+template <int FMT, int RPT, class Op, bool NAT = false>
 __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride, int rev) {
   pdl_enter();
@@ -387,7 +380,6 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
   const int t = threadIdx.x, warp = t >> 5;
   if constexpr (kDirect) {
     const int rb = bx * wpc * TB;
-    const unsigned nat = sell_nat_mask(sell, bx, wpc, n);
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       if (r0 >= n) break;  // uniform over the CTA
@@ -400,8 +392,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       auto pre = [&](int rl) {  // own-row operands in flight during the row's SpMV
         if (r0 + rl < n) load_vin(op, r0 + rl, v);
       };
-      if ((nat >> w) & 1u) sell_window_sink<FMT == 3, true>(sell, r0, g, sink, pre);
-      else sell_window_sink<FMT == 3>(sell, r0, g, sink, pre);
+      sell_window_sink<FMT == 3, NAT>(sell, r0, g, sink, pre);
     }
   } else if constexpr (FMT == 0) {
     const int r0 = bx * (TB * RPT);
@@ -444,11 +435,6 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       }
     };
     issue(0);
-    // natural-order windows (sell.cu) need neither the scatter nor its barrier; the
-    // others alternate the two scatter buffers (ks counts them: a buffer is rewritten
-    // only after the barrier of the scatter window in between)
-    const unsigned nat = FMT >= 2 ? sell_nat_mask(sell, bx, wpc, n) : 0u;
-    int ks = 0;
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       double cc[DD];
@@ -461,14 +447,9 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
         double v[NVA];
         if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
-        if constexpr (FMT == 1) {
-          y = csr_window(csr, r0, g, sm.st[w & 1]);
-        } else if ((nat >> w) & 1u) {
-          y = sell_window_nat<FMT == 3>(sell, r0, g);
-        } else {
-          y = sell_window<FMT == 3>(sell, r0, g, sm.sy[ks & 1]);
-          ++ks;
-        }
+        if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
+        else if constexpr (NAT) y = sell_window_nat<FMT == 3>(sell, r0, g);
+        else y = sell_window<FMT == 3>(sell, r0, g, sm.sy[w & 1]);
         if constexpr (kAsync) {
           cp_async_wait<1>();  // all groups but window w+1's are complete
 #pragma unroll

@@ -15,6 +15,7 @@
 // cycle-ending step return at once (device flag), so the host checks once per cycle.
 #include <cmath>
 #include <vector>
+#include <cstring>
 #include "gmres_ops.cuh"
 
 namespace gsk {
@@ -39,11 +40,24 @@ static int capture_cycle(gsk_plan* P, const double* b, double* x, int m, int cop
     if (rc >= 0) rc = j == 2 ? run_mdot(P, bp, j, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_mdot(P, bp, j, s);
     if (rc >= 0) rc = run_mdot(P, c, 1, s);
   }
+  // GSK_ARNOLDI=fused: S_j and h_1j in one SpMV pass with a dot (OpArnoldi; the same
+  // leaves and tree as OpCgsS + OpH1, so the same bits) — an experiment for
+  // natural-order SELL plans, whose dot passes need no per-window barrier
+  static const bool fused_env = [] {
+    const char* e = std::getenv("GSK_ARNOLDI");
+    return e && std::strcmp(e, "fused") == 0;
+  }();
+  const bool fused = fused_env && P->fmt == GSK_FMT_SELL && P->sell.all_nat;
   for (int j = 1; j <= m && rc >= 0 && P->orth == 0; ++j) {
-    // S_j as a plain SpMV pass (w = A v_j) + the h_1j dot pass (OpH1)
-    OpCgsS<> a{slot(j), slot(j + 1), st, j, 0};
-    rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
-    if (rc >= 0) rc = run_pass(P, OpH1{slot(j + 1), slot(1), st, j, 0}, s);
+    if (fused) {
+      OpArnoldi<> a{slot(j), slot(1), slot(j + 1), st, j, 0, 0};
+      rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
+    } else {
+      // S_j as a plain SpMV pass (w = A v_j) + the h_1j dot pass (OpH1)
+      OpCgsS<> a{slot(j), slot(j + 1), st, j, 0};
+      rc = j == 1 ? run_pass(P, a, s, P->pev[3][copy][0], P->pev[3][copy][1]) : run_pass(P, a, s);
+      if (rc >= 0) rc = run_pass(P, OpH1{slot(j + 1), slot(1), st, j, 0}, s);
+    }
     for (int i = 1; i < j && rc >= 0; ++i) {
       OpMgs mg{slot(i), slot(i + 1), slot(j + 1), st, i, j, 0, 0, 0};
       rc = (j == 2 && i == 1) ? run_pass(P, mg, s, P->pev[2][copy][0], P->pev[2][copy][1]) : run_pass(P, mg, s);

@@ -217,12 +217,16 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     int wpc = spmv_wpc_max();  // windows per CTA: as many as keep >= 3 CTAs per SM busy
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
+    // natural-order SELL plans (every window unsorted, sell.cu) run the NAT kernels
+    const bool nat = P->sell.all_nat != 0;
     if (P->fmt == GSK_FMT_SELL && P->sell.dict) {
-      pass_carveout(pass_kernel<3, 1, Op>);
-      GSK_CUDA(launch_k(pass_kernel<3, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
+      auto k = nat ? pass_kernel<3, 1, Op, true> : pass_kernel<3, 1, Op, false>;
+      pass_carveout(k);
+      GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     } else if (P->fmt == GSK_FMT_SELL) {
-      pass_carveout(pass_kernel<2, 1, Op>);
-      GSK_CUDA(launch_k(pass_kernel<2, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
+      auto k = nat ? pass_kernel<2, 1, Op, true> : pass_kernel<2, 1, Op, false>;
+      pass_carveout(k);
+      GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     } else {  // CSR passes keep the driver's carveout (their 43 KB stage needs it)
       GSK_CUDA(launch_k(pass_kernel<1, 1, Op>, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     }

@@ -1,7 +1,10 @@
 // plan.cu — plan lifecycle and the non-solver entry points of the C-ABI:
 // gsk_spmv / gsk_plan_spmv (SPEC sparse-core spmv; AC-3), gsk_dot (AC-5),
 // gsk_plan_residual_norm, SELL copy-out, probes, diagnostics.
+#include <csignal>
 #include <cstring>
+#include <execinfo.h>
+#include <unistd.h>
 #include <mutex>
 #include <set>
 #include <unordered_map>
@@ -10,6 +13,35 @@
 #include "internal.cuh"
 
 namespace gsk {
+
+// Debug aid (GSK_SEGV_TRACE=1): on SIGSEGV print the native backtrace to stderr, then
+// hand the signal to the previous handler (Python's faulthandler prints its stacks).
+static struct sigaction g_prev_segv;
+static void segv_trace(int sig, siginfo_t* info, void* ctx) {
+  void* frames[64];
+  const int k = backtrace(frames, 64);
+  const char msg[] = "gsk: SIGSEGV, native backtrace:\n";
+  (void)!write(2, msg, sizeof msg - 1);
+  backtrace_symbols_fd(frames, k, 2);
+  sigaction(SIGSEGV, &g_prev_segv, nullptr);
+  if (g_prev_segv.sa_flags & SA_SIGINFO) {
+    if (g_prev_segv.sa_sigaction) g_prev_segv.sa_sigaction(sig, info, ctx);
+  } else if (g_prev_segv.sa_handler != SIG_DFL && g_prev_segv.sa_handler != SIG_IGN) {
+    g_prev_segv.sa_handler(sig);
+  }
+  raise(sig);
+}
+static int install_segv_trace() {
+  const char* e = std::getenv("GSK_SEGV_TRACE");
+  if (!e || e[0] != '1') return 0;
+  struct sigaction sa {};
+  sa.sa_sigaction = segv_trace;
+  sa.sa_flags = SA_SIGINFO;
+  sigemptyset(&sa.sa_mask);
+  sigaction(SIGSEGV, &sa, &g_prev_segv);
+  return 1;
+}
+static const int g_segv_installed = install_segv_trace();
 
 static thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
