@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
     ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
                     help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
+    ap.add_argument("--sell-index", default="plain", choices=["plain", "dict", "uniform"],
+                    help="SELL column indices: int32 per slot (plain), the SELL-D per-chunk delta dictionary, "
+                         "or SELL-U chunk-uniform deltas (DESIGN.md §5)")
     ap.add_argument("--fmt", default="sell", choices=["csr", "sell"],
                     help="plan layout built on the device from the CSR input (SELL-C-32-256 is faster "
                          "on every config: DESIGN.md §7)")
@@ -267,7 +270,7 @@ def main():
     dbuf = torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
     fmt = args.fmt
-    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth)
+    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth, sell_index=args.sell_index)
     x1 = torch.empty(n, dtype=torch.float64, device="cuda")
     x2 = torch.empty(n, dtype=torch.float64, device="cuda")
 

@@ -86,7 +86,11 @@ typedef struct gsk_opts {
   int32_t sell_index;   /* SELL column indices: 0 = plain int32 (default), 1 = uint8
                            index into a per-chunk dictionary of col - row deltas when
                            every chunk has <= 32 of them (25% fewer matrix bytes, but
-                           slower on B200 at C4: DESIGN.md §5) */
+                           slower on B200 at C4: DESIGN.md §5), 2 = chunk-uniform
+                           offsets (SELL-U): slot k of a chunk holds each row's entry at
+                           delta udel[k] (ascending, <= 8 per chunk; lane masks mark
+                           padding), 8 bytes of column data per 32 slots; falls back to
+                           plain columns when some chunk has more deltas */
   int32_t engine;       /* how the solvers run (all engines give bit-identical results):
                            GSK_ENGINE_AUTO (default) = one launch for the whole solve on
                            one CTA (Bi-CGSTAB n <= 2048, MGS GMRES n <= 1024) or on one
@@ -158,6 +162,12 @@ int gsk_plan_sell_copy(gsk_plan *plan, int32_t *chunk_ptr, int32_t *chunk_len,
  * padding).  *ndict = -1 when the plan uses plain int32 columns.  Outputs nullable. */
 int gsk_plan_sell_dict(gsk_plan *plan, int64_t *ndict, int32_t *dict_ptr, int32_t *dict,
                        uint8_t *sidx, void *stream);
+/* SELL-U arrays of a plan built with sell_index = 2 (tests): *nuslots = slot count, or
+ * -1 if the layout was inapplicable; uptr [nchunks+1], udel / umask [nchunks * 8] (the
+ * chunk's ascending deltas col - row and, per delta, the lanes whose row has it; unused
+ * entries 0), uval [nuslots] (device, nullable). */
+int gsk_plan_sell_uniform(gsk_plan *plan, int64_t *nuslots, int32_t *uptr, int32_t *udel, uint32_t *umask,
+                          double *uval, void *stream);
 void gsk_plan_destroy(gsk_plan *plan);
 
 /* Bi-CGSTAB (van der Vorst 1992) on A x = b.

@@ -60,6 +60,8 @@ def _lib():
         lib.orc_sell_dict_size.restype = i64
         lib.orc_sell_dict.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, vp]
         lib.orc_sell_dict.restype = i32
+        lib.orc_sell_uniform.argtypes = [i64, i32, i32, i32] + [vp] * 8
+        lib.orc_sell_uniform.restype = i64
         lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, vp, d, i32, vp, vp,
                                      ctypes.POINTER(Report)]
         lib.orc_bicgstab.restype = i32
@@ -187,6 +189,24 @@ def sell_dict(n, S, C=32, sigma=256):
     if rc != 0:
         return None
     out["dict"] = out["dict"][:tot]
+    return out
+
+
+def sell_uniform(row_ptr, col, val, S, C=32, sigma=256, maxu=8):
+    """SELL-U encoding (chunk-uniform column deltas) of a SELL layout S (sell_build):
+    uptr, udel, umask, uval — or None if some chunk has more than maxu deltas."""
+    row_ptr, col, val = _i32(row_ptr), _i32(col), _f64(val)
+    ro = np.ascontiguousarray(S["roff"], np.uint8)
+    n = row_ptr.size - 1
+    nch = (n + C - 1) // C
+    tot = _lib().orc_sell_uniform(n, C, sigma, maxu, _p(ro), _p(row_ptr), _p(col), _p(val), None, None, None, None)
+    if tot < 0:
+        return None
+    out = {"uptr": np.zeros(nch + 1, np.int32), "udel": np.zeros(nch * maxu, np.int32),
+           "umask": np.zeros(nch * maxu, np.uint32), "uval": np.zeros(max(tot, 1), np.float64)}
+    _lib().orc_sell_uniform(n, C, sigma, maxu, _p(ro), _p(row_ptr), _p(col), _p(val),
+                            *(_p(out[k]) for k in ("uptr", "udel", "umask", "uval")))
+    out["uval"] = out["uval"][:tot]
     return out
 
 

@@ -306,6 +306,53 @@ int orc_sell_dict(int64_t n, int C, int sigma, const int32_t* chunk_ptr, const i
   return 0;
 }
 
+// ---- SELL-U: chunk-uniform column offsets (storage format of the GPU path)
+// For chunk c of a SELL layout (rows given by roff): U_c = the ascending distinct deltas
+// col - row over the chunk's rows (at most maxu; else the encoding is inapplicable and
+// -1 is returned); slot k of lane l (at uptr[c] + k*C + lane) holds row l's entry at
+// column row + U_c[k], or 0.0 with bit l of umask[c*maxu + k] clear.  Sizes: return
+// the slot total (call with null outputs first), uptr [nch+1], udel/umask [nch*maxu].
+int64_t orc_sell_uniform(int64_t n, int C, int sigma, int maxu, const uint8_t* roff, const int32_t* rp,
+                         const int32_t* ci, const double* v, int32_t* uptr, int32_t* udel, uint32_t* umask,
+                         double* uval) {
+  const int64_t nch = (n + C - 1) / C;
+  int64_t tot = 0;
+  if (uptr) uptr[0] = 0;
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t w0 = (c * C) / sigma * sigma;
+    std::vector<int64_t> U;  // ascending distinct deltas of the chunk
+    for (int lane = 0; lane < C; ++lane) {
+      const int64_t row = w0 + roff[c * C + lane];
+      if (row >= n) continue;
+      for (int32_t q = rp[row]; q < rp[row + 1]; ++q) U.push_back((int64_t)ci[q] - row);
+    }
+    std::sort(U.begin(), U.end());
+    U.erase(std::unique(U.begin(), U.end()), U.end());
+    if ((int64_t)U.size() > maxu) return -1;
+    if (uptr) {
+      uptr[c + 1] = (int32_t)(uptr[c] + (int64_t)U.size() * C);
+      for (int k = 0; k < maxu; ++k) {
+        udel[c * maxu + k] = k < (int)U.size() ? (int32_t)U[k] : 0;
+        umask[c * maxu + k] = 0u;
+      }
+      for (int lane = 0; lane < C; ++lane) {
+        const int64_t row = w0 + roff[c * C + lane];
+        for (size_t k = 0; k < U.size(); ++k) {
+          double a = 0.0;
+          bool has = false;
+          if (row < n)
+            for (int32_t q = rp[row]; q < rp[row + 1]; ++q)
+              if ((int64_t)ci[q] - row == U[k]) { a = v[q]; has = true; }
+          uval[uptr[c] + (int64_t)k * C + lane] = a;
+          if (has) umask[c * maxu + k] |= 1u << lane;
+        }
+      }
+    }
+    tot += (int64_t)U.size() * C;
+  }
+  return tot;
+}
+
 // ---- Bi-CGSTAB (van der Vorst 1992, cited PAPER.md:102) ----------------------------
 // DESIGN.md §4 algorithm B, arithmetic AC-6; stopping PAPER.md:302-307 (reading B1/B2:
 // strict <, frame weights w optional); breakdown exact-zero tests (PAPER.md:315-321,

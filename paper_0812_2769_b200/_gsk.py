@@ -24,7 +24,7 @@ ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
 SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
-           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_destroy",
+           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_sell_uniform", "gsk_plan_destroy",
            "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
            "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
            "gsk_shard_rows", "gsk_shard_halo_host", "gsk_plan_create_sharded", "gsk_nccl_unique_id",
@@ -91,6 +91,7 @@ def load(path: str = LIB_PATH):
     lib.gsk_plan_sell_info.argtypes = [vp, P(i64), P(i64)]
     lib.gsk_plan_sell_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     lib.gsk_plan_sell_dict.argtypes = [vp, P(i64), vp, vp, vp, vp]
+    lib.gsk_plan_sell_uniform.argtypes = [vp, P(i64), vp, vp, vp, vp, vp]
     lib.gsk_plan_destroy.argtypes = [vp]
     lib.gsk_plan_destroy.restype = None
     lib.gsk_bicgstab_solve.argtypes = [P(CsrStruct), vp, vp, d, i32, vp, vp, P(Report), vp]
@@ -265,7 +266,7 @@ class Plan:
         self.A = A
         self.weights = _dev_f64(weights, A.n)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE[schedule], ORTH[orth], {"plain": 0, "dict": 1}[sell_index], ENGINE[engine])
+                    SCHEDULE[schedule], ORTH[orth], {"plain": 0, "dict": 1, "uniform": 2}[sell_index], ENGINE[engine])
         self._csr = A.struct()
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))
@@ -333,6 +334,26 @@ class Plan:
         res = {k: v.cpu().numpy() for k, v in out.items()}
         res["dict"] = res["dict"][:nd.value]
         res["sidx"] = res["sidx"][:nsl.value]
+        return res
+
+    def sell_uniform(self):
+        """The plan's SELL-U arrays (chunk-uniform column deltas; None when not built)."""
+        lib = load()
+        nu = ctypes.c_int64()
+        _check(lib.gsk_plan_sell_uniform(self.h, ctypes.byref(nu), None, None, None, None, _stream()))
+        if nu.value < 0:
+            return None
+        nch, nsl = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.gsk_plan_sell_info(self.h, ctypes.byref(nch), ctypes.byref(nsl)))
+        out = {"uptr": torch.empty(nch.value + 1, dtype=torch.int32, device="cuda"),
+               "udel": torch.empty(nch.value * 8, dtype=torch.int32, device="cuda"),
+               "umask": torch.empty(nch.value * 8, dtype=torch.int32, device="cuda"),
+               "uval": torch.empty(max(nu.value, 1), dtype=torch.float64, device="cuda")}
+        _check(lib.gsk_plan_sell_uniform(self.h, ctypes.byref(nu), *(_ptr(out[k]) for k in
+                                                                    ("uptr", "udel", "umask", "uval")), _stream()))
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res["umask"] = res["umask"].view(np.uint32)
+        res["uval"] = res["uval"][:nu.value]
         return res
 
     def probe(self, kind: int):
@@ -421,7 +442,7 @@ class ShardedPlan(Plan):
     column indices (gsk_shard_opts.local_input), so no rank holds the whole system."""
 
     def __init__(self, A: CSR, shards: int = 2, fmt: str = "csr", weights=None, poll: int = 0,
-                 comm: "NcclComm" = None, n_global: int = None):
+                 comm: "NcclComm" = None, n_global: int = None, sell_index: str = "plain"):
         lib = load()
         self.A = A
         if comm is None:
@@ -439,7 +460,8 @@ class ShardedPlan(Plan):
         self.nloc = hi - lo
         self.weights = _dev_f64(weights, self.nloc)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE["split"], ORTH["mgs"], 0, ENGINE["graph"])
+                    SCHEDULE["split"], ORTH["mgs"], {"plain": 0, "dict": 1, "uniform": 2}[sell_index],
+                    ENGINE["graph"])
         so = ShardOpts(int(shards), int(first), int(count), int(n_global is not None), ch)
         self._csr = A.struct()
         self._csr.n = ng

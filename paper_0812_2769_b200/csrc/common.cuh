@@ -12,6 +12,7 @@ namespace gsk {
 constexpr int TB = 256;         // threads per CTA = rows per sub-tile = SELL sigma
 constexpr int SELL_C = 32;      // SELL chunk height (one warp)
 constexpr int SELL_SIGMA = 256; // SELL sorting window
+constexpr int SELLU_MAXL = 8;   // SELL-U: distinct column deltas per chunk (at most)
 constexpr int CSR_CAP = 1792;   // entries of a 256-row CSR window staged in smem (7 per row)
 constexpr int MAXD = 3;         // max dot products fused into one pass
 
@@ -40,6 +41,13 @@ struct SellView {
   // window w holds row 32 k + l; all_nat = every window is (null / 0: use roff)
   const uint8_t* __restrict__ wid;  // [nwindows]
   int all_nat;
+  // optional chunk-uniform column offsets (SELL-U, sell.cu; null: not built): per chunk
+  // SELLU_MAXL deltas col - row and lane masks, slot offsets and values of that layout
+  const int* __restrict__ uptr;        // [nchunks+1]
+  const int* __restrict__ udel;        // [nchunks * SELLU_MAXL]
+  const unsigned* __restrict__ umask;  // [nchunks * SELLU_MAXL]
+  const double* __restrict__ uval;     // [nuslots]
+  int l2pf;  // > 0: a pass prefetches the matrix data of the window l2pf ahead into L2
 };
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the
@@ -74,6 +82,15 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* g) {
 __device__ __forceinline__ void cp_async4(int* smem, const int* g) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
+}
+// TMA bulk prefetch of [p, p + bytes) into L2 (cp.async.bulk.prefetch.L2): one thread,
+// no registers, nothing to wait for.  The range is shrunk to 16-byte boundaries inside
+// it (the start of every array here is 256-byte aligned).
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~uintptr_t(15);
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>

@@ -108,7 +108,7 @@ __device__ __forceinline__ void coop_pass(const CoopArgs& a, Op op, double* sy, 
           if (i < a.n)
             for (int k = a.csr.rp[i]; k < a.csr.rp[i + 1]; ++k) y = __fma_rn(a.csr.v[k], op.gather(a.csr.ci[k]), y);
         } else if constexpr (FMT == 2) {
-          y = sell_window<false>(a.sell, r0, [&](int col) { return op.gather(col); }, sy + (w & 1) * TB);
+          y = sell_window<0>(a.sell, r0, [&](int col) { return op.gather(col); }, sy + (w & 1) * TB);
         }
         if (i < a.n) {
           double v[NVA];

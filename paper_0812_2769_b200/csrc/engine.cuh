@@ -109,6 +109,12 @@ struct SellTuning<Op, std::void_t<decltype(Op::kSellMinBlocks)>> {
 #endif
 constexpr bool SELL_DIRECT = GSK_SELL_DIRECT;
 
+// column-index encoding of a SELL pass format: FMT 2 int32, 3 SELL-D, 4 SELL-U
+template <int FMT>
+struct SellIdx {
+  static constexpr int value = FMT == 3 ? 1 : FMT == 4 ? 2 : 0;
+};
+
 template <int FMT, class Op>
 struct PassOcc {
   // SELL passes without dot products run "direct": each lane finishes
@@ -119,7 +125,7 @@ struct PassOcc {
   static constexpr int kMinBlocks = FMT == 1 ? 4
                                   : FMT == 3 ? (Op::D > 0 && SellTuning<Op>::minb == 4 ? GSK_SELLD_DOT_MINB
                                                                                        : SellTuning<Op>::minb)
-                                  : FMT == 2 ? SellTuning<Op>::minb : 3;
+                                  : (FMT == 2 || FMT == 4) ? SellTuning<Op>::minb : 3;
   static constexpr bool kPrefetch = FMT == 1 || (FMT >= 2 && SellTuning<Op>::minb < 4);
   // otherwise (SELL at 4 CTAs/SM, no registers to spare) up to ASYNC_NV own-row
   // operands of window w+1 are copied into shared memory with cp.async during window w
@@ -153,14 +159,47 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
 // SELL window core: lane l of warp w computes slot l of chunk r0/32 + w and hands the
 // row's y with its in-window offset to sink(rl, y).  NAT: the window keeps its natural
 // row order (sell.cu), so the slot's row is r0 + t and roff is not read.
-template <bool DICT, bool NAT = false, class G, class S, class Pre>
+// IDX: 0 int32 column per slot, 1 SELL-D (uint8 index into the chunk's delta
+// dictionary), 2 SELL-U (chunk-uniform deltas: slot k of every lane at delta udel[k],
+// lane masks mark padding; no per-slot column data at all).
+template <int IDX, bool NAT = false, class G, class S, class Pre>
 __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, const G& g, const S& sink,
                                                  const Pre& pre) {
+  constexpr bool DICT = IDX == 1;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int c = (r0 >> 5) + warp;
   if (c < A.nchunks) {
     const int rl = NAT ? (t & (TB - 1)) : A.roff[c * SELL_C + lane];
     pre(rl);
+    if constexpr (IDX == 2) {
+      const int p0 = A.uptr[c], L = (A.uptr[c + 1] - p0) >> 5;  // <= SELLU_MAXL
+      // lane k < L holds delta k and its lane mask (two 32-byte loads per chunk)
+      const int dv = lane < SELLU_MAXL ? __ldg(A.udel + (size_t)c * SELLU_MAXL + lane) : 0;
+      const unsigned mv = lane < SELLU_MAXL ? __ldg(A.umask + (size_t)c * SELLU_MAXL + lane) : 0u;
+      const int row = r0 + rl;
+      const double* vb = A.uval + p0 + lane;
+      double vals[SELLU_MAXL], xs[SELLU_MAXL];
+      unsigned ok = 0u;
+#pragma unroll
+      for (int k = 0; k < SELLU_MAXL; ++k)  // the slot values first (one streaming stream)
+        if (k < L) vals[k] = __ldcs(vb + k * SELL_C);
+#pragma unroll
+      for (int k = 0; k < SELLU_MAXL; ++k)
+        if (k < L) {
+          const int d = __shfl_sync(0xffffffffu, dv, k);
+          const unsigned m = __shfl_sync(0xffffffffu, mv, k);
+          if ((m >> lane) & 1u) {
+            ok |= 1u << k;
+            xs[k] = g(row + d);
+          }
+        }
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < SELLU_MAXL; ++k)
+        if (k < L && ((ok >> k) & 1u)) acc = __fma_rn(vals[k], xs[k], acc);
+      sink(rl, acc);
+      return;
+    }
     const int p0 = A.cptr[c], L = (A.cptr[c + 1] - p0) >> 5;
     const int base = p0 + lane;
     double acc = 0.0;
@@ -214,26 +253,47 @@ __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, cons
   }
 }
 
+// L2 prefetch (TMA bulk, thread 0 of the CTA) of the matrix data of the window starting
+// at row r0: the slot values and the column data of its chunks in the pass's encoding.
+// It gives the window's streaming loads an L2 latency instead of a DRAM one without
+// holding registers.
+template <int IDX>
+__device__ __forceinline__ void sell_prefetch_window(const SellView& A, int r0) {
+  const int c0 = r0 >> 5;
+  if (c0 >= A.nchunks) return;
+  const int c1 = min(c0 + TB / SELL_C, A.nchunks);
+  const int* ptr = IDX == 2 ? A.uptr : A.cptr;
+  const int s0 = ptr[c0], s1 = ptr[c1];
+  const double* vals = IDX == 2 ? A.uval : A.sval;
+  prefetch_l2(vals + s0, sizeof(double) * (size_t)(s1 - s0));
+  if constexpr (IDX == 0) prefetch_l2(A.scol + s0, sizeof(int) * (size_t)(s1 - s0));
+  if constexpr (IDX == 1) prefetch_l2(A.sidx + s0, (size_t)(s1 - s0));
+  if constexpr (IDX == 2) {
+    prefetch_l2(A.udel + (size_t)c0 * SELLU_MAXL, sizeof(int) * SELLU_MAXL * (size_t)(c1 - c0));
+    prefetch_l2(A.umask + (size_t)c0 * SELLU_MAXL, sizeof(unsigned) * SELLU_MAXL * (size_t)(c1 - c0));
+  }
+}
+
 // ... scattering y to sy at its in-window offset (no barrier).
-template <bool DICT, class G>
+template <int IDX, class G>
 __device__ __forceinline__ void sell_window_store(const SellView& A, int r0, const G& g, double* sy) {
-  sell_window_sink<DICT>(A, r0, g, [&](int rl, double y) { sy[rl] = y; }, [](int) {});
+  sell_window_sink<IDX>(A, r0, g, [&](int rl, double y) { sy[rl] = y; }, [](int) {});
 }
 
 // y for row r0 + t of a SELL window (scatter through sy, one barrier).
-template <bool DICT, class G>
+template <int IDX, class G>
 __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G& g, double* sy) {
-  sell_window_store<DICT>(A, r0, g, sy);
+  sell_window_store<IDX>(A, r0, g, sy);
   __syncthreads();
   return sy[threadIdx.x];
 }
 
 // ... of a natural-order window: thread t computes row r0 + t itself (no scatter, no
 // barrier; 0 beyond the last chunk).
-template <bool DICT, class G>
+template <int IDX, class G>
 __device__ __forceinline__ double sell_window_nat(const SellView& A, int r0, const G& g) {
   double y = 0.0;
-  sell_window_sink<DICT, true>(A, r0, g, [&](int, double v) { y = v; }, [](int) {});
+  sell_window_sink<IDX, true>(A, r0, g, [&](int, double v) { y = v; }, [](int) {});
   return y;
 }
 
@@ -380,9 +440,13 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
   const int t = threadIdx.x, warp = t >> 5;
   if constexpr (kDirect) {
     const int rb = bx * wpc * TB;
+    if (sell.l2pf && threadIdx.x == 0)
+      for (int q = 1; q <= sell.l2pf && q < wpc; ++q) sell_prefetch_window<SellIdx<FMT>::value>(sell, rb + q * TB);
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       if (r0 >= n) break;  // uniform over the CTA
+      if (sell.l2pf && threadIdx.x == 0 && w + sell.l2pf + 1 < wpc)
+        sell_prefetch_window<SellIdx<FMT>::value>(sell, r0 + (sell.l2pf + 1) * TB);
       auto g = [&](int col) { return op.gather(col); };
       double v[NVA];
       auto sink = [&](int rl, double y) {
@@ -392,7 +456,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       auto pre = [&](int rl) {  // own-row operands in flight during the row's SpMV
         if (r0 + rl < n) load_vin(op, r0 + rl, v);
       };
-      sell_window_sink<FMT == 3, NAT>(sell, r0, g, sink, pre);
+      sell_window_sink<SellIdx<FMT>::value, NAT>(sell, r0, g, sink, pre);
     }
   } else if constexpr (FMT == 0) {
     const int r0 = bx * (TB * RPT);
@@ -435,8 +499,16 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       }
     };
     issue(0);
+    if constexpr (FMT >= 2) {
+      if (sell.l2pf && threadIdx.x == 0)
+        for (int q = 1; q <= sell.l2pf && q < wpc; ++q) sell_prefetch_window<SellIdx<FMT>::value>(sell, rb + q * TB);
+    }
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
+      if constexpr (FMT >= 2) {
+        if (sell.l2pf && threadIdx.x == 0 && w + sell.l2pf + 1 < wpc && r0 < n)
+          sell_prefetch_window<SellIdx<FMT>::value>(sell, r0 + (sell.l2pf + 1) * TB);
+      }
       double cc[DD];
 #pragma unroll
       for (int d = 0; d < DD; ++d) cc[d] = 0.0;
@@ -448,8 +520,8 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
         if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
         if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
-        else if constexpr (NAT) y = sell_window_nat<FMT == 3>(sell, r0, g);
-        else y = sell_window<FMT == 3>(sell, r0, g, sm.sy[w & 1]);
+        else if constexpr (NAT) y = sell_window_nat<SellIdx<FMT>::value>(sell, r0, g);
+        else y = sell_window<SellIdx<FMT>::value>(sell, r0, g, sm.sy[w & 1]);
         if constexpr (kAsync) {
           cp_async_wait<1>();  // all groups but window w+1's are complete
 #pragma unroll
@@ -727,7 +799,7 @@ __global__ void __launch_bounds__(TB, MDOT_MINB)
       auto g = [&](int col) { return op.gather(col); };
       if constexpr (FMT == 2) {
         for (int w = 0; w < MD_R; ++w)
-          if (r0 + w * TB < n) sell_window_store<false>(sell, r0 + w * TB, g, sm.sy + w * TB);
+          if (r0 + w * TB < n) sell_window_store<0>(sell, r0 + w * TB, g, sm.sy + w * TB);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < 8; ++k) y[k] = sm.sy[MD_R * t + k];

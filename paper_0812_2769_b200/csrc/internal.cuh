@@ -102,7 +102,12 @@ struct gsk_plan {
   int* dptr = nullptr;
   int* dict = nullptr;
   int64_t ndict = 0;
-  int sell_index = 0;       // 0 auto (dictionary when applicable), 1 plain
+  int* uptr = nullptr;      // SELL-U (sell_index 2): slot offsets, deltas, masks, values
+  int* udel = nullptr;
+  unsigned* umask = nullptr;
+  double* uval = nullptr;
+  int64_t nuslots = 0;
+  int sell_index = 0;       // 0 plain int32 columns, 1 dictionary (SELL-D), 2 uniform (SELL-U)
   int sell_pad = -1;        // padding column value (INT_MIN in shard plans)
   // reduction scratch
   double* part = nullptr;      // [MAXD][pstride] CTA partials of the current pass
@@ -219,7 +224,11 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     ntiles = (windows + wpc - 1) / wpc;
     // natural-order SELL plans (every window unsorted, sell.cu) run the NAT kernels
     const bool nat = P->sell.all_nat != 0;
-    if (P->fmt == GSK_FMT_SELL && P->sell.dict) {
+    if (P->fmt == GSK_FMT_SELL && P->sell.uptr) {
+      auto k = nat ? pass_kernel<4, 1, Op, true> : pass_kernel<4, 1, Op, false>;
+      pass_carveout(k);
+      GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
+    } else if (P->fmt == GSK_FMT_SELL && P->sell.dict) {
       auto k = nat ? pass_kernel<3, 1, Op, true> : pass_kernel<3, 1, Op, false>;
       pass_carveout(k);
       GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
@@ -278,6 +287,7 @@ int run_mdot(gsk_plan* P, const Op& op, int J, cudaStream_t s, cudaEvent_t pe0 =
 int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
 int sell_dict_build(gsk_plan* P, cudaStream_t s);
+int sellu_build(gsk_plan* P, cudaStream_t s);
 int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);
 // On-chip single-CTA solvers (small.cu) for n <= GSK_SMALL_NMAX: one launch runs the
 // whole solve; the caller has set x = x0 and zeroed/initialised the state.

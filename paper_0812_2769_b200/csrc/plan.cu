@@ -390,7 +390,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
     set_error("gsk_plan_create: unknown engine %d", opts->engine);
     return GSK_E_INVALID;
   }
-  if (P->sell_index != 0 && P->sell_index != 1) {
+  if (P->sell_index < 0 || P->sell_index > 2) {
     delete P;
     set_error("gsk_plan_create: unknown sell_index %d", opts->sell_index);
     return GSK_E_INVALID;
@@ -401,6 +401,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
     rc = join_in(P, s);
     if (rc == GSK_OK) rc = sell_build(P, P->st);
     if (rc == GSK_OK && P->sell_index == 1) rc = sell_dict_build(P, P->st);
+    if (rc == GSK_OK && P->sell_index == 2) rc = sellu_build(P, P->st);
     if (rc == GSK_OK) rc = join_out(P, s);
     if (rc == GSK_OK && cudaStreamSynchronize(P->st) != cudaSuccess) rc = GSK_E_CUDA;
   }
@@ -438,7 +439,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->wid, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
-                  P->cpart};
+                  P->cpart, P->uptr, P->udel, P->umask, P->uval};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (P->h_flag) cudaFreeHost(P->h_flag);
@@ -574,6 +575,27 @@ int gsk_plan_sell_dict(gsk_plan* P, int64_t* ndict, int32_t* dict_ptr, int32_t* 
   if (dict_ptr) GSK_CUDA(cudaMemcpyAsync(dict_ptr, P->dptr, sizeof(int) * (P->nchunks + 1), cudaMemcpyDeviceToDevice, s));
   if (dict) GSK_CUDA(cudaMemcpyAsync(dict, P->dict, sizeof(int) * P->ndict, cudaMemcpyDeviceToDevice, s));
   if (sidx) GSK_CUDA(cudaMemcpyAsync(sidx, P->sidx, P->nslots, cudaMemcpyDeviceToDevice, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
+
+int gsk_plan_sell_uniform(gsk_plan* P, int64_t* nuslots, int32_t* uptr, int32_t* udel, uint32_t* umask,
+                          double* uval, void* stream) {
+  if (!P || P->shards || P->fmt != GSK_FMT_SELL) {
+    set_error("gsk_plan_sell_uniform: plan is not an unsharded SELL plan");
+    return GSK_E_INVALID;
+  }
+  if (!P->uptr) {
+    if (nuslots) *nuslots = -1;
+    return GSK_OK;
+  }
+  if (nuslots) *nuslots = P->nuslots;
+  cudaStream_t s = as_stream(stream);
+  const size_t nch = (size_t)P->nchunks;
+  if (uptr) GSK_CUDA(cudaMemcpyAsync(uptr, P->uptr, sizeof(int) * (nch + 1), cudaMemcpyDeviceToDevice, s));
+  if (udel) GSK_CUDA(cudaMemcpyAsync(udel, P->udel, sizeof(int) * nch * SELLU_MAXL, cudaMemcpyDeviceToDevice, s));
+  if (umask) GSK_CUDA(cudaMemcpyAsync(umask, P->umask, sizeof(unsigned) * nch * SELLU_MAXL, cudaMemcpyDeviceToDevice, s));
+  if (uval) GSK_CUDA(cudaMemcpyAsync(uval, P->uval, sizeof(double) * P->nuslots, cudaMemcpyDeviceToDevice, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   return GSK_OK;
 }

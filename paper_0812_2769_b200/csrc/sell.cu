@@ -201,6 +201,13 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   GSK_LAUNCHED(1);
   P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr,
                      P->sell_pad, P->wid, all_nat};
+  // GSK_L2PF: windows of L2 prefetch lead in the SELL passes (default 1: measured at
+  // C4 SpMV 0.274 -> 0.266 ms, S3 0.283 -> 0.275 ms; 2 was slower, 0 disables)
+  static const int l2pf = [] {
+    const char* e = std::getenv("GSK_L2PF");
+    return e ? std::atoi(e) : 1;
+  }();
+  P->sell.l2pf = l2pf;
   return GSK_OK;
 }
 
@@ -298,12 +305,148 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
   return GSK_OK;
 }
 
+int sellu_fill_values(gsk_plan* P, cudaStream_t s);
+
 int sell_fill_values(gsk_plan* P, cudaStream_t s) {
+  if (P->uval) GSK_TRY(sellu_fill_values(P, s));
   const int n = P->A.n;
   const int nwin = (n + TB - 1) / TB;
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
                                        P->cptr, P->roff, P->scol, P->sval, true, P->sell_pad);
   GSK_LAUNCHED(1);
+  return GSK_OK;
+}
+
+}  // namespace gsk
+
+namespace gsk {
+
+// ---- chunk-uniform column offsets ("SELL-U") ---------------------------
+// A chunk is stored with one slot per distinct delta col - row of its rows (ascending,
+// <= SELLU_MAXL): slot k of lane l holds row l's entry at column row + udel[c][k], or
+// padding (bit l of umask[c][k] clear).  The deltas and masks are per chunk, so the
+// column index costs 8 bytes per 32 slots instead of 4 bytes per slot, and the gather
+// addresses need no per-slot load.  Each row's entries stay in ascending column order
+// (ascending deltas), so the SpMV chain is AC-3's.  On the stencil systems a chunk has
+// exactly as many deltas as its longest row: the same slots as SELL-C-sigma.
+__global__ void __launch_bounds__(TB) sellu_meta_kernel(int n, int nchunks, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci, const uint8_t* __restrict__ roff,
+                                                        int* ucnt, int* udel, unsigned* umask, int* fail) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (TB / 32) + (threadIdx.x >> 5);
+  if (c >= nchunks) return;
+  const long long row = (long long)(c * SELL_C) / SELL_SIGMA * SELL_SIGMA + roff[c * SELL_C + lane];
+  const bool real = row < n;
+  const int a = real ? rp[row] : 0, e = real ? rp[row + 1] : 0;
+  long long last = LLONG_MIN;
+  int U = 0, dv = 0;
+  unsigned mv = 0u;
+  for (;;) {
+    long long mine = LLONG_MAX;
+    for (int q = a; q < e; ++q) {
+      const long long d = (long long)ci[q] - row;
+      if (d > last && d < mine) mine = d;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const long long o = __shfl_xor_sync(0xffffffffu, mine, off);
+      mine = o < mine ? o : mine;
+    }
+    if (mine == LLONG_MAX) break;
+    bool has = false;
+    for (int q = a; q < e; ++q) has |= ((long long)ci[q] - row == mine);
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (lane == U) {
+      dv = (int)mine;
+      mv = m;
+    }
+    ++U;
+    last = mine;
+    if (U > SELLU_MAXL) break;
+  }
+  if (lane == 0) {
+    ucnt[c] = U;
+    if (U > SELLU_MAXL) atomicExch(fail, 1);
+  }
+  if (lane < SELLU_MAXL) {
+    udel[(size_t)c * SELLU_MAXL + lane] = lane < U ? dv : 0;
+    umask[(size_t)c * SELLU_MAXL + lane] = lane < U ? mv : 0u;
+  }
+}
+
+// values of a SELL-U layout (at plan creation and after every rescaling): the row's
+// entries (ascending columns) merged with the chunk's ascending deltas
+__global__ void __launch_bounds__(TB) sellu_fill_kernel(int n, int nchunks, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci, const double* __restrict__ v,
+                                                        const uint8_t* __restrict__ roff, const int* __restrict__ uptr,
+                                                        const int* __restrict__ udel, double* uval) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (TB / 32) + (threadIdx.x >> 5);
+  if (c >= nchunks) return;
+  const long long row = (long long)(c * SELL_C) / SELL_SIGMA * SELL_SIGMA + roff[c * SELL_C + lane];
+  const bool real = row < n;
+  int q = real ? rp[row] : 0;
+  const int e = real ? rp[row + 1] : 0;
+  const int p0 = uptr[c], U = (uptr[c + 1] - p0) / SELL_C;
+  for (int k = 0; k < U; ++k) {
+    const long long d = udel[(size_t)c * SELLU_MAXL + k];
+    double val = 0.0;
+    if (q < e && (long long)ci[q] - row == d) val = v[q++];
+    uval[(size_t)p0 + (size_t)k * SELL_C + lane] = val;
+  }
+}
+
+int sellu_fill_values(gsk_plan* P, cudaStream_t s) {
+  const int nch = (int)P->nchunks;
+  const int grid = (nch + TB / 32 - 1) / (TB / 32);
+  sellu_fill_kernel<<<grid, TB, 0, s>>>(P->A.n, nch, P->A.row_ptr, P->A.col_idx, P->A.values, P->roff, P->uptr,
+                                        P->udel, P->uval);
+  GSK_LAUNCHED(1);
+  return GSK_OK;
+}
+
+int sellu_build(gsk_plan* P, cudaStream_t s) {
+  const int nch = (int)P->nchunks;
+  const int grid = (nch + TB / 32 - 1) / (TB / 32);
+  int* ucnt = nullptr;
+  int* fail = nullptr;
+  GSK_CUDA(cudaMalloc(&ucnt, sizeof(int) * (nch + 1)));
+  GSK_CUDA(cudaMalloc(&fail, sizeof(int)));
+  GSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
+  GSK_CUDA(cudaMalloc(&P->udel, sizeof(int) * (size_t)nch * SELLU_MAXL));
+  GSK_CUDA(cudaMalloc(&P->umask, sizeof(unsigned) * (size_t)nch * SELLU_MAXL));
+  sellu_meta_kernel<<<grid, TB, 0, s>>>(P->A.n, nch, P->A.row_ptr, P->A.col_idx, P->roff, ucnt, P->udel, P->umask,
+                                        fail);
+  GSK_LAUNCHED(1);
+  int hfail = 0;
+  GSK_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  long long tot = 0;
+  int rc = GSK_OK;
+  if (!hfail) {
+    GSK_CUDA(cudaMalloc(&P->uptr, sizeof(int) * (nch + 1)));
+    rc = sell_scan(nch, ucnt, P->uptr, SELL_C, s, &tot);
+  }
+  cudaFree(ucnt);
+  cudaFree(fail);
+  // inapplicable (a chunk with more than SELLU_MAXL deltas, or int32 offsets would
+  // overflow): the plan keeps plain int32 columns
+  if (hfail || rc != GSK_OK) {
+    for (void* b : {(void*)P->udel, (void*)P->umask, (void*)P->uptr})
+      if (b) cudaFree(b);
+    P->udel = nullptr;
+    P->umask = nullptr;
+    P->uptr = nullptr;
+    return GSK_OK;
+  }
+  P->nuslots = tot;
+  GSK_CUDA(cudaMalloc(&P->uval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_TRY(sellu_fill_values(P, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  P->sell.uptr = P->uptr;
+  P->sell.udel = P->udel;
+  P->sell.umask = P->umask;
+  P->sell.uval = P->uval;
   return GSK_OK;
 }
 

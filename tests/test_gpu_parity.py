@@ -647,6 +647,56 @@ def test_sell_dict_solvers(name, N):
                       oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100))
 
 
+@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 100), ("C3", 20), ("C4", 24), ("C4", None), ("C5", 64),
+                                    ("P4", 12)])
+def test_sell_uniform_parity(name, N):
+    """SELL-U (chunk-uniform column deltas) built on the device == the oracle's encoding
+    (integer arrays and values bit-exact; also after a value refresh); the permuted C5
+    system keeps plain int32 columns on both sides."""
+    s = workloads.generate(name, N=N)
+    A = gsk.CSR.from_system(s)
+    P = gsk.Plan(A, fmt="sell", sell_index="uniform")
+    g = P.sell_uniform()
+    o = oracle.sell_uniform(s["row_ptr"], s["col"], s["val"], oracle.sell_build(s["row_ptr"], s["col"], s["val"]))
+    if o is None:
+        assert g is None
+        return
+    for k in ("uptr", "udel", "umask", "uval"):
+        assert np.array_equal(g[k], o[k]), k
+    vo, _, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)  # refresh after rescaling in place
+    A.val.copy_(torch.tensor(vo, device="cuda"))
+    P.refresh()
+    o2 = oracle.sell_uniform(s["row_ptr"], s["col"], vo, oracle.sell_build(s["row_ptr"], s["col"], vo))
+    assert np.array_equal(P.sell_uniform()["uval"], o2["uval"])
+    x = workloads.uniform(s["n"], 9, 9)
+    assert np.array_equal(cpu(P.spmv(x)), oracle.spmv(s["row_ptr"], s["col"], vo, x))
+
+
+@pytest.mark.parametrize("name,N", [("C4", 24), ("C3", 20), ("C2", 100), ("P1", 64)])
+def test_sell_uniform_solvers(name, N):
+    """Solvers on SELL-U plans (no per-slot column data): the same bits as the oracle —
+    split and fused Bi-CGSTAB, MGS and CGS2 GMRES, with frame weights, and sharded."""
+    s, val, b, _ = system(name, N, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    ob = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400)
+    og = oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100)
+    for schedule in ("split", "fused"):
+        P = gsk.Plan(A, fmt="sell", sell_index="uniform", engine="graph", schedule=schedule)
+        assert P.sell_uniform() is not None
+        assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=400), ob)
+        assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=100), og)
+    P = gsk.Plan(A, fmt="sell", sell_index="uniform", engine="graph", orth="cgs2")
+    assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=100),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100, orth="cgs2"))
+    w = workloads.uniform(s["n"], 5, 6) + 1.5
+    Pw = gsk.Plan(A, fmt="sell", sell_index="uniform", engine="graph", weights=w)
+    assert_same_solve(Pw.bicgstab(b, tol=1e-9, maxit=400),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400, weights=w))
+    SP = gsk.ShardedPlan(A, shards=2, fmt="sell", sell_index="uniform")
+    assert_same_solve(SP.bicgstab(b, tol=1e-9, maxit=400), ob)
+    assert_same_solve(SP.gmres(b, m=30, tol=1e-9, maxit=100), og)
+
+
 def test_sharded_nccl_single_rank():
     """The multi-process code path (halo send/recv groups, ncclAllGather of the shard
     values, all inside the captured graphs) on a 1-rank NCCL communicator: bit-exact."""

@@ -501,3 +501,81 @@ def test_verdict_branches_hand_derived(case):
         assert np.allclose(x, xw, rtol=1e-14, atol=1e-300), (x, xw)
     if e["status"] == 3:
         assert not np.isfinite(rep["relres"])
+
+
+# ---------------------------------------------------------------- SELL-U
+def _decode_uniform(U, S, rp, n, C=32, sigma=256, maxu=8):
+    """Rows rebuilt from a SELL-U encoding: {row: [(col, val), ...]} in slot order."""
+    rows = {}
+    nch = (n + C - 1) // C
+    roff = np.asarray(S["roff"], np.int64)
+    for c in range(nch):
+        w0 = (c * C) // sigma * sigma
+        L = (U["uptr"][c + 1] - U["uptr"][c]) // C
+        for lane in range(C):
+            row = w0 + int(roff[c * C + lane])
+            if row >= n:
+                continue
+            ent = []
+            for k in range(L):
+                v = U["uval"][U["uptr"][c] + k * C + lane]
+                if (int(U["umask"][c * maxu + k]) >> lane) & 1:
+                    ent.append((row + int(U["udel"][c * maxu + k]), v))
+                else:
+                    assert v == 0.0
+            rows[row] = ent
+    return rows
+
+
+@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 64), ("C3", 16), ("C4", 20), ("P4", 12), ("lap3d", 16)])
+def test_sell_uniform_round_trip(name, N):
+    """SELL-U (chunk-uniform column deltas): decoding every masked slot gives
+    back each row's CSR entries in ascending column order (so the SpMV chain is AC-3's),
+    deltas ascend, unused entries are zero, and on the stencil systems a chunk has exactly
+    as many deltas as its longest row — the same slot count as SELL-C-sigma."""
+    s = workloads.generate(name, N=N)
+    S = oracle.sell_build(s["row_ptr"], s["col"], s["val"])
+    U = oracle.sell_uniform(s["row_ptr"], s["col"], s["val"], S)
+    assert U is not None
+    rows = _decode_uniform(U, S, s["row_ptr"], s["n"])
+    rp = s["row_ptr"]
+    for r in range(s["n"]):
+        ent = rows[r]
+        assert [c for c, _ in ent] == list(s["col"][rp[r]:rp[r + 1]])
+        assert np.array_equal([v for _, v in ent], s["val"][rp[r]:rp[r + 1]])
+    nch = (s["n"] + 31) // 32
+    for c in range(nch):
+        L = (U["uptr"][c + 1] - U["uptr"][c]) // 32
+        d = U["udel"][c * 8:c * 8 + L]
+        assert np.all(np.diff(d) > 0) and np.all(U["udel"][c * 8 + L:c * 8 + 8] == 0)
+        assert np.all(U["umask"][c * 8 + L:c * 8 + 8] == 0) and np.all(U["umask"][c * 8:c * 8 + L] != 0)
+    # a chunk holds at least its longest row's slots; where a window keeps its natural
+    # order (every window of the full-size stencil configs) exactly that many, so the
+    # layout has SELL-C-sigma's slot count; sorted boundary windows of these small grids
+    # mix rows missing different neighbours (a few % more slots)
+    L = np.diff(U["uptr"]) // 32
+    assert np.all(L >= S["chunk_len"])
+    nat = _check_window_order(S, rp, s["n"], 32, 256) == (s["n"] + 255) // 256
+    assert (U["uptr"][-1] == S["chunk_ptr"][-1]) if nat else (U["uptr"][-1] <= 1.05 * S["chunk_ptr"][-1])
+
+
+def test_sell_uniform_inapplicable_and_constructed():
+    """A chunk with more than 8 distinct deltas (the permuted C5 system) makes SELL-U
+    inapplicable; a hand-built 2-chunk system pins the encoding exactly."""
+    s = workloads.generate("C5", N=64)
+    S = oracle.sell_build(s["row_ptr"], s["col"], s["val"])
+    assert oracle.sell_uniform(s["row_ptr"], s["col"], s["val"], S) is None
+    # 40 rows: row r has entries at r-1 (r>0), r, r+3 (r+3<40); values 10r + k
+    cols, vals, rp = [], [], [0]
+    for r in range(40):
+        cc = [c for c in (r - 1, r, r + 3) if 0 <= c < 40]
+        cols += cc
+        vals += [10.0 * r + k for k in range(len(cc))]
+        rp.append(len(cols))
+    S = oracle.sell_build(np.array(rp), np.array(cols), np.array(vals))
+    U = oracle.sell_uniform(np.array(rp), np.array(cols), np.array(vals), S)
+    assert list(U["uptr"]) == [0, 96, 192] and list(U["udel"][:3]) == [-1, 0, 3] and list(U["udel"][8:11]) == [-1, 0, 3]
+    assert U["umask"][0] == 0xFFFFFFFE and U["umask"][1] == 0xFFFFFFFF and U["umask"][2] == 0xFFFFFFFF
+    assert U["umask"][8] == 0xFF and U["umask"][9] == 0xFF and U["umask"][10] == 0x1F  # rows 32..39; r+3 < 40 for r <= 36
+    assert U["uval"][0] == 0.0 and U["uval"][32] == 0.0 and U["uval"][64] == 1.0  # row 0: (0 -> 0.0), (3 -> 1.0)
+    assert U["uval"][1] == 10.0 and U["uval"][33] == 11.0 and U["uval"][65] == 12.0
