@@ -63,15 +63,16 @@ template <>
 struct PassSmem<3> : PassSmem<2> {};
 // SELL passes sized to the Op: cp.async slots only for the operands it prefetches (the
 // 25% carveout then holds 4 CTAs of a one-operand pass instead of 3)
-template <int NVS>
+// (natural-order kernels never scatter: no sy buffer, 4 KB less per CTA)
+template <int NVS, bool NAT = false>
 struct PassSmemSell {
-  double sy[2][TB];
+  double sy[2][NAT ? 1 : TB];
   double wp[16 * MAXD * 8];
   double vin[2][NVS][TB];
 };
-template <>
-struct PassSmemSell<0> {
-  double sy[2][TB];
+template <bool NAT>
+struct PassSmemSell<0, NAT> {
+  double sy[2][NAT ? 1 : TB];
   double wp[16 * MAXD * 8];
   double vin[2][1][1];
 };
@@ -115,7 +116,10 @@ struct SellIdx {
   static constexpr int value = FMT == 3 ? 1 : FMT == 4 ? 2 : 0;
 };
 
-template <int FMT, class Op>
+#ifndef GSK_SHORT_MINB
+#define GSK_SHORT_MINB 5
+#endif
+template <int FMT, class Op, int MAXL = 8>
 struct PassOcc {
   // SELL passes without dot products run "direct": each lane finishes
   // the row of its own SELL slot (operands, output) with no per-window barrier.
@@ -125,7 +129,9 @@ struct PassOcc {
   static constexpr int kMinBlocks = FMT == 1 ? 4
                                   : FMT == 3 ? (Op::D > 0 && SellTuning<Op>::minb == 4 ? GSK_SELLD_DOT_MINB
                                                                                        : SellTuning<Op>::minb)
-                                  : (FMT == 2 || FMT == 4) ? SellTuning<Op>::minb : 3;
+                                  : (FMT == 2 || FMT == 4)
+                                      ? (MAXL <= 5 && SellTuning<Op>::minb == 4 ? GSK_SHORT_MINB : SellTuning<Op>::minb)
+                                      : 3;
   static constexpr bool kPrefetch = FMT == 1 || (FMT >= 2 && SellTuning<Op>::minb < 4);
   // otherwise (SELL at 4 CTAs/SM, no registers to spare) up to ASYNC_NV own-row
   // operands of window w+1 are copied into shared memory with cp.async during window w
@@ -162,7 +168,7 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
 // IDX: 0 int32 column per slot, 1 SELL-D (uint8 index into the chunk's delta
 // dictionary), 2 SELL-U (chunk-uniform deltas: slot k of every lane at delta udel[k],
 // lane masks mark padding; no per-slot column data at all).
-template <int IDX, bool NAT = false, class G, class S, class Pre>
+template <int IDX, bool NAT = false, int MAXL = 8, class G, class S, class Pre>
 __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, const G& g, const S& sink,
                                                  const Pre& pre) {
   constexpr bool DICT = IDX == 1;
@@ -228,20 +234,20 @@ __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, cons
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         if (k < L && cols[k] != A.pad) acc = __fma_rn(vals[k], xs[k], acc);
-    } else if (L <= 8) {
-      int cols[8];
-      double vals[8], xs[8];
+    } else if (L <= MAXL) {  // MAXL: the slot arrays kept in registers (8; 5 for 2-D plans)
+      int cols[MAXL];
+      double vals[MAXL], xs[MAXL];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < MAXL; ++k)
         if (k < L) {
           cols[k] = __ldcs(A.scol + base + k * SELL_C);
           vals[k] = __ldcs(A.sval + base + k * SELL_C);
         }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < MAXL; ++k)
         if (k < L && cols[k] != A.pad) xs[k] = g(cols[k]);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < MAXL; ++k)
         if (k < L && cols[k] != A.pad) acc = __fma_rn(vals[k], xs[k], acc);
     } else {
       for (int k = 0; k < L; ++k) {  // long chunks: plain int32 columns (kept in every plan)
@@ -290,10 +296,10 @@ __device__ __forceinline__ double sell_window(const SellView& A, int r0, const G
 
 // ... of a natural-order window: thread t computes row r0 + t itself (no scatter, no
 // barrier; 0 beyond the last chunk).
-template <int IDX, class G>
+template <int IDX, int MAXL = 8, class G>
 __device__ __forceinline__ double sell_window_nat(const SellView& A, int r0, const G& g) {
   double y = 0.0;
-  sell_window_sink<IDX, true>(A, r0, g, [&](int, double v) { y = v; }, [](int) {});
+  sell_window_sink<IDX, true, MAXL>(A, r0, g, [&](int, double v) { y = v; }, [](int) {});
   return y;
 }
 
@@ -419,8 +425,10 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 // NAT (SELL only): every window of the plan keeps its natural row order (sell.cu), so
 // thread t computes row r0 + t itself — no roff, no scatter, no per-window barrier.
 // A compile-time choice: one code path per kernel keeps the 64-register budget.
-template <int FMT, int RPT, class Op, bool NAT = false>
-__global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
+// MAXL (plain SELL): slots per lane kept in registers; 5 for plans whose chunks are all
+// at most 5 long (the 2-D 5-point systems), which frees registers for more CTAs per SM.
+template <int FMT, int RPT, class Op, bool NAT = false, int MAXL = 8>
+__global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
     pass_kernel(CsrView csr, SellView sell, int n, int wpc, Op op, double* part, int stride, int rev) {
   pdl_enter();
   if (!op.begin()) return;
@@ -435,17 +443,17 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
   constexpr bool kDirect = PassOcc<FMT, Op>::kDirect;
   using Smem = std::conditional_t<
       kDirect, PassSmemDirect,
-      std::conditional_t<(FMT >= 2), PassSmemSell<(PassOcc<FMT, Op>::kAsync ? Op::NV : 0)>, PassSmem<FMT>>>;
+      std::conditional_t<(FMT >= 2), PassSmemSell<(PassOcc<FMT, Op>::kAsync ? Op::NV : 0), NAT>, PassSmem<FMT>>>;
   __shared__ __align__(16) Smem sm;
   const int t = threadIdx.x, warp = t >> 5;
   if constexpr (kDirect) {
     const int rb = bx * wpc * TB;
-    if (sell.l2pf && threadIdx.x == 0)
+    if (sell.l2pf && wpc >= 4 && threadIdx.x == 0)
       for (int q = 1; q <= sell.l2pf && q < wpc; ++q) sell_prefetch_window<SellIdx<FMT>::value>(sell, rb + q * TB);
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       if (r0 >= n) break;  // uniform over the CTA
-      if (sell.l2pf && threadIdx.x == 0 && w + sell.l2pf + 1 < wpc)
+      if (sell.l2pf && wpc >= 4 && threadIdx.x == 0 && w + sell.l2pf + 1 < wpc)
         sell_prefetch_window<SellIdx<FMT>::value>(sell, r0 + (sell.l2pf + 1) * TB);
       auto g = [&](int col) { return op.gather(col); };
       double v[NVA];
@@ -456,7 +464,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
       auto pre = [&](int rl) {  // own-row operands in flight during the row's SpMV
         if (r0 + rl < n) load_vin(op, r0 + rl, v);
       };
-      sell_window_sink<SellIdx<FMT>::value, NAT>(sell, r0, g, sink, pre);
+      sell_window_sink<SellIdx<FMT>::value, NAT, MAXL>(sell, r0, g, sink, pre);
     }
   } else if constexpr (FMT == 0) {
     const int r0 = bx * (TB * RPT);
@@ -500,13 +508,13 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
     };
     issue(0);
     if constexpr (FMT >= 2) {
-      if (sell.l2pf && threadIdx.x == 0)
+      if (sell.l2pf && wpc >= 4 && threadIdx.x == 0)
         for (int q = 1; q <= sell.l2pf && q < wpc; ++q) sell_prefetch_window<SellIdx<FMT>::value>(sell, rb + q * TB);
     }
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       if constexpr (FMT >= 2) {
-        if (sell.l2pf && threadIdx.x == 0 && w + sell.l2pf + 1 < wpc && r0 < n)
+        if (sell.l2pf && wpc >= 4 && threadIdx.x == 0 && w + sell.l2pf + 1 < wpc && r0 < n)
           sell_prefetch_window<SellIdx<FMT>::value>(sell, r0 + (sell.l2pf + 1) * TB);
       }
       double cc[DD];
@@ -520,7 +528,7 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op>::kMinBlocks)
         if (kPre && i < n) load_vin(op, i, v);  // own-row operands in flight during the SpMV
         double y;
         if constexpr (FMT == 1) y = csr_window(csr, r0, g, sm.st[w & 1]);
-        else if constexpr (NAT) y = sell_window_nat<SellIdx<FMT>::value>(sell, r0, g);
+        else if constexpr (NAT) y = sell_window_nat<SellIdx<FMT>::value, MAXL>(sell, r0, g);
         else y = sell_window<SellIdx<FMT>::value>(sell, r0, g, sm.sy[w & 1]);
         if constexpr (kAsync) {
           cp_async_wait<1>();  // all groups but window w+1's are complete

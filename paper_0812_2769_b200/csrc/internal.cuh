@@ -107,6 +107,7 @@ struct gsk_plan {
   unsigned* umask = nullptr;
   double* uval = nullptr;
   int64_t nuslots = 0;
+  int sell_maxlen = 0;      // longest SELL chunk (slots per lane)
   int sell_index = 0;       // 0 plain int32 columns, 1 dictionary (SELL-D), 2 uniform (SELL-U)
   int sell_pad = -1;        // padding column value (INT_MIN in shard plans)
   // reduction scratch
@@ -188,6 +189,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // GSK_CARVEOUT=<percent> overrides it, GSK_CARVEOUT=-1 leaves the driver's choice.
 int smem_carveout();
 void set_pass_carveout(const void* kern);
+bool short_slots_enabled();  // GSK_SHORT=0 disables the <= 5-slot kernels
 // per-device "function attributes already set" registry (keyed by any pointer)
 bool device_attr_done(const void* key);
 void device_attr_mark(const void* key);
@@ -233,7 +235,10 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
       pass_carveout(k);
       GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     } else if (P->fmt == GSK_FMT_SELL) {
-      auto k = nat ? pass_kernel<2, 1, Op, true> : pass_kernel<2, 1, Op, false>;
+      // natural plans with chunks of <= 5 slots (2-D 5-point) run the short-slot kernels
+      auto k = !nat ? pass_kernel<2, 1, Op, false>
+                    : (P->sell_maxlen <= 5 && short_slots_enabled()) ? pass_kernel<2, 1, Op, true, 5>
+                                                                       : pass_kernel<2, 1, Op, true>;
       pass_carveout(k);
       GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     } else {  // CSR passes keep the driver's carveout (their 43 KB stage needs it)

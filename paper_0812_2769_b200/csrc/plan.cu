@@ -91,6 +91,15 @@ bool pass_alternate() {
   return on == 1;
 }
 
+bool short_slots_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("GSK_SHORT");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int smem_carveout() {
   static int c = -3;
   if (c == -3) {

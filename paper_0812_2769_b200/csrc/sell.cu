@@ -11,6 +11,7 @@
 //      padding col = -1, val = 0 (predicated off in the SpMV, AC-3).
 // In a natural window lane l of warp w holds row 32 w + l, so a pass finishes its rows
 // in row order without the shared-memory scatter and its barrier (engine.cuh).
+#include <algorithm>
 #include <climits>
 #include <vector>
 #include "internal.cuh"
@@ -186,14 +187,19 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   long long tot = 0;
   GSK_TRY(sell_scan((int)P->nchunks, P->clen, P->cptr, SELL_C, s, &tot));
   P->nslots = tot;
-  // every window natural? (then the passes need no per-window flag)
-  int all_nat = 1;
+  // every window natural? (then the passes run the NAT kernels) and the longest chunk
+  // (<= 5: the short-slot kernels)
+  int all_nat = 1, maxlen = 0;
   {
     std::vector<uint8_t> h(nwin);
+    std::vector<int> cl(P->nchunks);
     GSK_CUDA(cudaMemcpyAsync(h.data(), P->wid, nwin, cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaMemcpyAsync(cl.data(), P->clen, sizeof(int) * P->nchunks, cudaMemcpyDeviceToHost, s));
     GSK_CUDA(cudaStreamSynchronize(s));
     for (uint8_t f : h) all_nat &= f;
+    for (int v : cl) maxlen = std::max(maxlen, v);
   }
+  P->sell_maxlen = maxlen;
   GSK_CUDA(cudaMalloc(&P->scol, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
   GSK_CUDA(cudaMalloc(&P->sval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
@@ -202,7 +208,8 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr,
                      P->sell_pad, P->wid, all_nat};
   // GSK_L2PF: windows of L2 prefetch lead in the SELL passes (default 1: measured at
-  // C4 SpMV 0.274 -> 0.266 ms, S3 0.283 -> 0.275 ms; 2 was slower, 0 disables)
+  // C4 SpMV 0.274 -> 0.266 ms, S3 0.283 -> 0.275 ms; 2 was slower, 0 disables).  Passes
+  // with fewer than 4 windows per CTA skip it (C3, 2 windows: 5% slower with it).
   static const int l2pf = [] {
     const char* e = std::getenv("GSK_L2PF");
     return e ? std::atoi(e) : 1;
