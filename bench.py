@@ -87,6 +87,9 @@ def parse():
     ap.add_argument("--weak", action="store_true",
                     help="with N > 1 ranks: weak scaling — C4's 256^3 block stacked N times in z (C4w), one "
                          "block per rank, each rank generating and holding only its own rows")
+    ap.add_argument("--peer", action="store_true",
+                    help="sharded modes: reductions by device-initiated peer stores over CUDA IPC / NVLink "
+                         "(gsk_shard_opts.peer_reduce) instead of ncclAllGather")
     ap.add_argument("--shards", type=int, default=0,
                     help="row-block sharded solve (DESIGN.md §8): with one process, P shards emulated on "
                          "one GPU (the cost of sharding); under torchrun, one shard per rank over NCCL "
@@ -452,10 +455,10 @@ def run_sharded(args, rank, world, local):
     vbuf, bbuf, dbuf = torch.empty_like(A0.val), torch.empty_like(b0), torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
     if weak:
-        SP = gsk.ShardedPlan(As, fmt=fmt, comm=comm, n_global=n_glob)
+        SP = gsk.ShardedPlan(As, fmt=fmt, comm=comm, n_global=n_glob, peer_reduce=args.peer)
         bl = bbuf
     else:
-        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm)
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, peer_reduce=args.peer)
         lo, hi = SP.rows
         bl = bbuf[lo:hi]
     x1 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
@@ -536,6 +539,8 @@ def run_sharded(args, rank, world, local):
                           if weak else "")},
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "comm": {"backend": "nccl" if world > 1 else "none (one process)", "nranks": world,
+                     "reductions": "device-initiated peer stores + epoch flags (CUDA IPC)" if args.peer
+                     else ("ncclAllGather" if world > 1 else "in place"),
                      "shards": P, "nranks_ok": (comm.world == world) if comm else world == 1},
             "extra": {"bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
                                    "solve_ms": r1["solve_ms"]},
@@ -616,7 +621,7 @@ def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist,
         dev = {k: v.to("cuda", non_blocking=True) for k, v in pin.items()}
         A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
         As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
-        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, n_global=n_global)
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, n_global=n_global, peer_reduce=args.peer)
         x1, _, r1 = SP.bicgstab(bs[lo:hi], tol=cfg.tol, maxit=cfg.maxit, hist=False)
         x2, _, r2 = SP.gmres(bs[lo:hi], m=m, tol=cfg.tol, maxit=gmaxit, hist=False)
         xo1.copy_(x1, non_blocking=True)

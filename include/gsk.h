@@ -224,6 +224,15 @@ typedef struct gsk_shard_opts {
   void *nccl_comm;   /* ncclComm_t over the P processes (count == 1: this process holds
                         shard `first`), or NULL (count == P: all shards on this GPU);
                         from gsk_nccl_comm_create, not owned by the plan */
+  int32_t peer_reduce; /* 0: the P shard values of every reduction are all-gathered with
+                        ncclAllGather (host-enqueued).  1: device-initiated instead —
+                        each shard's finish kernel stores its values straight into every
+                        process's gather buffer (CUDA IPC mappings over NVLink, set up
+                        at plan creation by all-gathering the handles over the
+                        communicator) and releases a per-shard epoch flag; the global
+                        finish acquires the P flags and reduces.  Double-buffered by
+                        epoch parity.  Same tree, same bits. */
+  int32_t pad_;
 } gsk_shard_opts;
 
 /* Host-only layout helpers (no GPU needed).  Rows of shard r; GSK_E_INVALID if P is not

@@ -57,7 +57,8 @@ class Opts(ctypes.Structure):
 
 class ShardOpts(ctypes.Structure):
     _fields_ = [("nshards", ctypes.c_int32), ("first", ctypes.c_int32), ("count", ctypes.c_int32),
-                ("local_input", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p)]
+                ("local_input", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
+                ("peer_reduce", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class GskError(RuntimeError):
@@ -439,10 +440,13 @@ class ShardedPlan(Plan):
     rows; the history is global.  Bit-identical to the unsharded solvers.
 
     ``n_global`` (with a comm only): A holds just this rank's rows [lo, hi) with global
-    column indices (gsk_shard_opts.local_input), so no rank holds the whole system."""
+    column indices (gsk_shard_opts.local_input), so no rank holds the whole system.
+    ``peer_reduce``: the reductions' shard values travel by device-initiated peer
+    stores + epoch flags instead of ncclAllGather (gsk_shard_opts.peer_reduce)."""
 
     def __init__(self, A: CSR, shards: int = 2, fmt: str = "csr", weights=None, poll: int = 0,
-                 comm: "NcclComm" = None, n_global: int = None, sell_index: str = "plain"):
+                 comm: "NcclComm" = None, n_global: int = None, sell_index: str = "plain",
+                 peer_reduce: bool = False):
         lib = load()
         self.A = A
         if comm is None:
@@ -462,7 +466,7 @@ class ShardedPlan(Plan):
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
                     SCHEDULE["split"], ORTH["mgs"], {"plain": 0, "dict": 1, "uniform": 2}[sell_index],
                     ENGINE["graph"])
-        so = ShardOpts(int(shards), int(first), int(count), int(n_global is not None), ch)
+        so = ShardOpts(int(shards), int(first), int(count), int(n_global is not None), ch, int(peer_reduce), 0)
         self._csr = A.struct()
         self._csr.n = ng
         h = ctypes.c_void_p()

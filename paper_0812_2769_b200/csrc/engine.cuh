@@ -720,6 +720,73 @@ __global__ void __launch_bounds__(32) finish_global_kernel(Op op, const double* 
   op.finish(s, lane);
 }
 
+// Device-initiated shard reductions (shard.cu, gsk_shard_opts.peer_reduce).  Every
+// process owns one buffer, [2][P][MAXD] doubles (epoch parity, shard, dot), then P
+// uint64 epoch flags, then P uint64 epoch counters (its own shards'), and holds
+// pointers to every process's buffer (CUDA IPC mappings; its own for local shards).
+__device__ __forceinline__ unsigned long long* peer_flags(double* buf, int P) {
+  return reinterpret_cast<unsigned long long*>(buf + 2 * (size_t)P * MAXD);
+}
+// ... each shard's finish stores its subtree values into every buffer's slot for this
+// epoch's parity, then releases its flag (system scope) with the epoch number ...
+template <class Op>
+__global__ void __launch_bounds__(FIN_THREADS) finish_peer_local_kernel(Op op, const double* part, int stride,
+                                                                        int ntiles, double* const* peers, int P,
+                                                                        int me, unsigned long long* ep) {
+  pdl_enter();
+  if (!op.begin()) return;
+  double s[Op::D];
+  fin_tree<Op::D>(part, stride, ntiles, s);
+  if (threadIdx.x == 0) {
+    const unsigned long long e = *ep + 1;
+    *ep = e;
+    const int par = (int)(e & 1ull);
+    for (int q = 0; q < P; ++q) {
+      volatile double* g = peers[q] + ((size_t)par * P + me) * MAXD;
+#pragma unroll
+      for (int d = 0; d < Op::D; ++d) g[d] = s[d];
+    }
+    __threadfence_system();
+    for (int q = 0; q < P; ++q) {
+      unsigned long long* f = peer_flags(peers[q], P) + me;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+    }
+  }
+}
+// ... and one warp acquires the P flags of the epoch (lane q spins on flag q), reads the
+// P values, joins them with the top of the canonical tree (+ 0.0) and runs the epilogue.
+// Epochs advance identically on every process (the same reductions in the same order),
+// and a value slot is rewritten two epochs later, after its reader has passed.
+template <class Op>
+__global__ void __launch_bounds__(32) finish_peer_global_kernel(Op op, double* own, int P,
+                                                                const unsigned long long* ep) {
+  pdl_enter();
+  if (!op.begin()) return;
+  const int lane = threadIdx.x;
+  const unsigned long long e = *ep;
+  const int par = (int)(e & 1ull);
+  if (lane < P) {
+    const unsigned long long* f = peer_flags(own, P) + lane;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= e) break;
+      __nanosleep(32);
+    }
+  }
+  __syncwarp();
+  const volatile double* g = own + ((size_t)par * P + (lane < P ? lane : 0)) * MAXD;
+  double s[Op::D];
+#pragma unroll
+  for (int d = 0; d < Op::D; ++d) {
+    double u = lane < P ? g[d] : 0.0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) u = u + __shfl_xor_sync(0xffffffffu, u, off);
+    s[d] = u + 0.0;
+  }
+  op.finish(s, lane);
+}
+
 // ---------------------------------------------------------------------------------
 // Multi-dot passes (GMRES with double classical Gram-Schmidt): J
 // dot products per row, J known at launch (<= MDOT_MAX).  A CTA owns tpc tiles of

@@ -115,6 +115,12 @@ struct ShardSet {
   double* gath = nullptr;        // [P][MAXD] shard values of the current reduction
   int* mm = nullptr;             // halo scan scratch
   int64_t rows0 = 0;             // first row held by this process
+  // device-initiated reductions (peer_reduce): this process's buffer (values, flags,
+  // epoch counters; engine.cuh), the P buffer pointers on the device, the IPC mappings
+  bool peer = false;
+  double* pbuf = nullptr;
+  double** dpeers = nullptr;
+  std::vector<void*> opened;
 };
 
 void shard_destroy(ShardSet* S) {
@@ -126,6 +132,9 @@ void shard_destroy(ShardSet* S) {
   }
   if (S->gath) cudaFree(S->gath);
   if (S->mm) cudaFree(S->mm);
+  for (void* p : S->opened) cudaIpcCloseMemHandle(p);
+  if (S->dpeers) cudaFree(S->dpeers);
+  if (S->pbuf) cudaFree(S->pbuf);
   delete S;
 }
 
@@ -223,15 +232,25 @@ static int shard_pass(gsk_plan* P, MakeOp mk, cudaStream_t s, cudaEvent_t pe0 = 
     int nt = 0;
     GSK_TRY(launch_pass(Q, op, s, &nt, i == 0 ? pe0 : nullptr, i == 0 ? pe1 : nullptr));
     if constexpr (Op::D > 0) {
-      GSK_CUDA(launch_k(finish_local_kernel<Op>, 1, FIN_THREADS, 0, s, op, (const double*)Q->part, Q->pstride, nt,
-                        S->gath + (size_t)(S->first + i) * MAXD));
+      if (S->peer)  // values stored into every process's buffer + a released epoch flag
+        GSK_CUDA(launch_k(finish_peer_local_kernel<Op>, 1, FIN_THREADS, 0, s, op, (const double*)Q->part,
+                          Q->pstride, nt, (double* const*)S->dpeers, S->P, S->first + i,
+                          peer_flags(S->pbuf, S->P) + S->P + (S->first + i)));
+      else
+        GSK_CUDA(launch_k(finish_local_kernel<Op>, 1, FIN_THREADS, 0, s, op, (const double*)Q->part, Q->pstride,
+                          nt, S->gath + (size_t)(S->first + i) * MAXD));
       GSK_LAUNCHED(1);
     }
   }
   if constexpr (Op::D > 0) {
-    if (S->comm)
-      GSK_NCCL(nccl()->allGather(S->gath + (size_t)S->first * MAXD, S->gath, MAXD, ncclDouble, S->comm, s));
-    GSK_CUDA(launch_k(finish_global_kernel<Op>, 1, 32, 0, s, mk(0), (const double*)S->gath, S->P));
+    if (S->peer) {
+      GSK_CUDA(launch_k(finish_peer_global_kernel<Op>, 1, 32, 0, s, mk(0), S->pbuf, S->P,
+                        (const unsigned long long*)(peer_flags(S->pbuf, S->P) + S->P + S->first)));
+    } else {
+      if (S->comm)
+        GSK_NCCL(nccl()->allGather(S->gath + (size_t)S->first * MAXD, S->gath, MAXD, ncclDouble, S->comm, s));
+      GSK_CUDA(launch_k(finish_global_kernel<Op>, 1, 32, 0, s, mk(0), (const double*)S->gath, S->P));
+    }
     GSK_LAUNCHED(1);
   }
   return GSK_OK;
@@ -669,6 +688,51 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
     }
   }
   S->rows0 = S->lo[S->first];
+  if (so->peer_reduce) {  // device-initiated reductions: buffers, IPC mappings
+    S->peer = true;
+    const size_t bytes = sizeof(double) * 2 * (size_t)P * MAXD + 2 * sizeof(unsigned long long) * (size_t)P;
+    if (cudaMalloc(&S->pbuf, bytes) != cudaSuccess || cudaMalloc(&S->dpeers, sizeof(double*) * P) != cudaSuccess) {
+      set_error("gsk_plan_create_sharded: allocation of the peer-reduction buffers failed");
+      return fail(GSK_E_NOMEM);
+    }
+    if (cudaMemsetAsync(S->pbuf, 0, bytes, s) != cudaSuccess) return fail(GSK_E_CUDA);
+    std::vector<double*> ptrs(P, S->pbuf);  // one process: every shard's buffer is this one
+    if (remote && P > 1) {
+      cudaIpcMemHandle_t mine;
+      if (cudaIpcGetMemHandle(&mine, S->pbuf) != cudaSuccess) {
+        set_error("gsk_plan_create_sharded: cudaIpcGetMemHandle failed");
+        return fail(GSK_E_CUDA);
+      }
+      char* dh = nullptr;
+      const size_t hb = sizeof(cudaIpcMemHandle_t);
+      std::vector<cudaIpcMemHandle_t> all(P);
+      int rc = cudaMalloc(&dh, hb * P) == cudaSuccess ? GSK_OK : GSK_E_NOMEM;
+      if (rc == GSK_OK && cudaMemcpyAsync(dh + hb * so->first, &mine, hb, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        rc = GSK_E_CUDA;
+      if (rc == GSK_OK && nccl()->allGather(dh + hb * so->first, dh, hb, ncclChar, S->comm, s) != ncclSuccess) {
+        set_error("gsk_plan_create_sharded: ncclAllGather of the IPC handles failed");
+        rc = GSK_E_CUDA;
+      }
+      if (rc == GSK_OK && (cudaMemcpyAsync(all.data(), dh, hb * P, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                           cudaStreamSynchronize(s) != cudaSuccess))
+        rc = GSK_E_CUDA;
+      if (dh) cudaFree(dh);
+      if (rc != GSK_OK) return fail(rc);
+      for (int q = 0; q < P; ++q) {
+        if (q == so->first) continue;
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          set_error("gsk_plan_create_sharded: cudaIpcOpenMemHandle of rank %d's buffer failed", q);
+          return fail(GSK_E_CUDA);
+        }
+        S->opened.push_back(p);
+        ptrs[q] = static_cast<double*>(p);
+      }
+    }
+    if (cudaMemcpyAsync(S->dpeers, ptrs.data(), sizeof(double*) * P, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return fail(GSK_E_CUDA);
+  }
   // this process's shards: local CSR arrays and sub-plans
   S->sh.resize(S->count);
   gsk_opts so2 = opts ? *opts : gsk_opts{};

@@ -62,3 +62,30 @@ def test_header_enums_match_binding():
                            "coop": vals["GSK_ENGINE_COOP"], "small": vals["GSK_ENGINE_SMALL"],
                            "cluster": vals["GSK_ENGINE_CLUSTER"]}
     assert vals["GSK_OK"] == _gsk.GSK_OK == 0
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """Every struct the binding passes through the C-ABI has the header's size and field
+    offsets (a C program compiled against include/gsk.h prints them)."""
+    import ctypes
+    from paper_0812_2769_b200 import _gsk
+    structs = {"gsk_csr": _gsk.CsrStruct, "gsk_report": _gsk.Report, "gsk_opts": _gsk.Opts,
+               "gsk_shard_opts": _gsk.ShardOpts}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gsk.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        c, f, v = ln.split()
+        got[(c, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)

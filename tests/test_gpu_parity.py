@@ -723,6 +723,25 @@ def test_sharded_nccl_single_rank():
     assert lib.gsk_nccl_comm_destroy(h) == 0
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("fmt", ["csr", "sell"])
+def test_sharded_peer_reduce(P, fmt):
+    """gsk_shard_opts.peer_reduce on one GPU (all shards in this process): every shard's
+    finish stores its values into the gather buffer and releases its epoch flag, the
+    global finish acquires the flags (already set: same stream) and reduces — the
+    protocol of the multi-process path without the IPC mappings.  Bit-exact, over many
+    epochs (both parities) and several solves on one plan."""
+    s, val, b, _ = system("C3", 24, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    SP = gsk.ShardedPlan(A, shards=P, fmt=fmt, peer_reduce=True)
+    ob = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400)
+    og = oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100)
+    for _ in range(2):
+        assert_same_solve(SP.bicgstab(b, tol=1e-9, maxit=400), ob)
+        assert_same_solve(SP.gmres(b, m=30, tol=1e-9, maxit=100), og)
+    SP.close()
+
+
 def test_sharded_local_input_single_rank():
     """gsk_shard_opts.local_input (each rank passes only its own rows, global columns;
     DESIGN.md §8 weak scaling) on a 1-rank NCCL communicator: the rows come from
@@ -744,8 +763,8 @@ def test_sharded_local_input_single_rank():
     vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
     A = gsk.CSR(loc["row_ptr"], loc["col"], loc["val"])
     As, bs, _ = gsk.gs_scale(A, loc["b"], 2)
-    for fmt in ("csr", "sell"):
-        SP = gsk.ShardedPlan(As, fmt=fmt, comm=Comm, n_global=s["n"])
+    for fmt, peer in (("csr", False), ("sell", False), ("sell", True)):
+        SP = gsk.ShardedPlan(As, fmt=fmt, comm=Comm, n_global=s["n"], peer_reduce=peer)
         assert_same_solve(SP.bicgstab(bs, tol=1e-9, maxit=300),
                           oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-9, 300))
         assert_same_solve(SP.gmres(bs, m=30, tol=1e-9, maxit=90),

@@ -1,7 +1,7 @@
 """One rank of a row-block sharded solve across processes, for
 tests/test_multi_gpu.py under torchrun (one GPU per rank, NCCL):
 
-    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/shard_rank.py --N 16 [--local]
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/shard_rank.py --N 16 [--local] [--peer]
 
 Every rank builds its shard plan — from the global system, or with --local from only
 its own rows (workloads.generate_rows of the stacked-slab workload C4w, G = world:
@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--N", type=int, default=16)
     ap.add_argument("--local", action="store_true")
     ap.add_argument("--fmt", default="sell")
+    ap.add_argument("--peer", action="store_true", help="device-initiated reductions (peer_reduce)")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -41,12 +42,12 @@ def main():
         loc = workloads.generate_rows("C4w", lo, hi, N=a.N, param=world)
         A = gsk.CSR(loc["row_ptr"], loc["col"], loc["val"])
         As, bs, _ = gsk.gs_scale(A, loc["b"], 2)
-        SP = gsk.ShardedPlan(As, fmt=a.fmt, comm=comm, n_global=s["n"])
+        SP = gsk.ShardedPlan(As, fmt=a.fmt, comm=comm, n_global=s["n"], peer_reduce=a.peer)
     else:
         A = gsk.CSR.from_system(s)
         As, bs, _ = gsk.gs_scale(A, s["b"], 2)
         bs = bs[lo:hi]
-        SP = gsk.ShardedPlan(As, fmt=a.fmt, comm=comm)
+        SP = gsk.ShardedPlan(As, fmt=a.fmt, comm=comm, peer_reduce=a.peer)
     x1, h1, r1 = SP.bicgstab(bs, tol=1e-9, maxit=400)
     x2, h2, r2 = SP.gmres(bs, m=30, tol=1e-9, maxit=120)
     xs1 = [torch.empty(gsk.shard_rows(s["n"], world, r)[1] - gsk.shard_rows(s["n"], world, r)[0],
@@ -64,7 +65,7 @@ def main():
         g2 = torch.cat(xs2).cpu().numpy()
         ok = (np.array_equal(h1, ho1) and np.array_equal(g1, xo1) and r1["status"] == ro1["status"]
               and np.array_equal(h2, ho2) and np.array_equal(g2, xo2) and r2["status"] == ro2["status"])
-        print(json.dumps({"world": world, "local_input": a.local, "n": s["n"], "bicgstab_its": r1["iterations"],
+        print(json.dumps({"world": world, "local_input": a.local, "peer_reduce": a.peer, "n": s["n"], "bicgstab_its": r1["iterations"],
                           "gmres_its": r2["iterations"], "equal": bool(ok)}), flush=True)
     SP.close()
     comm.close()
