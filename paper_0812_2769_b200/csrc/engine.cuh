@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(32) finish_global_kernel(Op op, const double* 
 // process owns one buffer, [2][P][MAXD] doubles (epoch parity, shard, dot), then P
 // uint64 epoch flags, then P uint64 epoch counters (its own shards'), and holds
 // pointers to every process's buffer (CUDA IPC mappings; its own for local shards).
-__device__ __forceinline__ unsigned long long* peer_flags(double* buf, int P) {
+__host__ __device__ __forceinline__ unsigned long long* peer_flags(double* buf, int P) {
   return reinterpret_cast<unsigned long long*>(buf + 2 * (size_t)P * MAXD);
 }
 // ... each shard's finish stores its subtree values into every buffer's slot for this

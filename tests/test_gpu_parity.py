@@ -731,7 +731,7 @@ def test_sharded_peer_reduce(P, fmt):
     global finish acquires the flags (already set: same stream) and reduces — the
     protocol of the multi-process path without the IPC mappings.  Bit-exact, over many
     epochs (both parities) and several solves on one plan."""
-    s, val, b, _ = system("C3", 24, 2)
+    s, val, b, _ = system("C3", 32, 2)  # 32768 rows: 8 shards of 4096, halos of one plane
     A = gsk.CSR(s["row_ptr"], s["col"], val)
     SP = gsk.ShardedPlan(A, shards=P, fmt=fmt, peer_reduce=True)
     ob = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400)
