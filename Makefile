@@ -25,10 +25,18 @@ workloads/libgskgen.so: workloads/gen.cpp
 oracle/liboracle.so: oracle/oracle.cpp
 	$(HOSTCXX) $(ORCFLAGS) -o $@.tmp $< && mv -f $@.tmp $@
 
-$(PKG)/libgsk.so: $(CU_SRC) $(CU_HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@.tmp.so $(CU_SRC) -lcudart && mv -f $@.tmp.so $@
+# one object per translation unit (make -j compiles them in parallel), then one link
+CU_OBJ := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(CU_SRC))
+
+build/obj/%.o: $(PKG)/csrc/%.cu $(CU_HDR)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(PKG)/libgsk.so: $(CU_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@.tmp.so $(CU_OBJ) -lcudart && mv -f $@.tmp.so $@
 
 clean:
 	rm -f workloads/libgskgen.so oracle/liboracle.so $(PKG)/libgsk.so
+	rm -rf build/obj
 
 .PHONY: all clean
