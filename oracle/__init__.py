@@ -60,6 +60,8 @@ def _lib():
         lib.orc_sell_dict_size.restype = i64
         lib.orc_sell_dict.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, vp]
         lib.orc_sell_dict.restype = i32
+        lib.orc_set_fault.argtypes = [i32, i32]
+        lib.orc_set_fault.restype = None
         lib.orc_sell_uniform.argtypes = [i64, i32, i32, i32] + [vp] * 8
         lib.orc_sell_uniform.restype = i64
         lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, vp, d, i32, vp, vp,
@@ -208,6 +210,16 @@ def sell_uniform(row_ptr, col, val, S, C=32, sigma=256, maxu=8):
                             *(_p(out[k]) for k in ("uptr", "udel", "umask", "uval")))
     out["uval"] = out["uval"][:tot]
     return out
+
+
+FAULTS = {"none": 0, "rho0": 1, "omega0": 2, "nan": 3}
+
+
+def set_fault(kind="none", iteration=0):
+    """Test-only fault hook of Bi-CGSTAB (the GPU's GSK_FAULT mirrors it):
+    "rho0" / "omega0" force rho = 0 at the end of / omega = 0 in the given iteration,
+    "nan" writes NaN into r_0 in its update.  set_fault() clears it."""
+    _lib().orc_set_fault(FAULTS[kind], int(iteration))
 
 
 def bicgstab(row_ptr, col, val, b, tol, maxit, x0=None, weights=None):

@@ -84,7 +84,7 @@ static std::vector<double>& leaves(int64_t n) {
 double orc_dot(int64_t n, const double* a, const double* b) {
   std::vector<double>& q = leaves(n);
   double* qp = q.data();
-  #pragma omp parallel for schedule(static)
+  #pragma omp parallel for schedule(static) if (n > 65536)
   for (int64_t i = 0; i < n; ++i) qp[i] = a[i] * b[i];
   return tree_sum(q, n);
 }
@@ -93,7 +93,7 @@ double orc_dot(int64_t n, const double* a, const double* b) {
 double orc_wnorm2(int64_t n, const double* a, const double* w) {
   std::vector<double>& q = leaves(n);
   double* qp = q.data();
-  #pragma omp parallel for schedule(static)
+  #pragma omp parallel for schedule(static) if (n > 65536)
   for (int64_t i = 0; i < n; ++i) {
     double u = w ? w[i] * a[i] : a[i];
     qp[i] = u * u;
@@ -104,7 +104,7 @@ double orc_wnorm2(int64_t n, const double* a, const double* w) {
 // ---- SpMV, AC-3 (SPEC sparse-core spmv; y = A x) -----------------------------------
 void orc_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
               const double* x, double* y) {
-  #pragma omp parallel for schedule(static)
+  #pragma omp parallel for schedule(static) if (n > 65536)
   for (int64_t i = 0; i < n; ++i) {
     double acc = 0.0;
     for (int32_t k = rp[i]; k < rp[i + 1]; ++k) acc = std::fma(v[k], x[ci[k]], acc);
@@ -358,6 +358,16 @@ int64_t orc_sell_uniform(int64_t n, int C, int sigma, int maxu, const uint8_t* r
 // strict <, frame weights w optional); breakdown exact-zero tests (PAPER.md:315-321,
 // reading B5); ||s|| half-step exit (B4); iterations = completed iterations (B6).
 // hist[maxit+1] (nullable).  x0 nullable (= 0).  Returns 0 or -1 (bad args).
+// Test-only fault hook, mirrored by the GPU's GSK_FAULT: kind 1 forces
+// rho = 0 at the end of iteration g_fault_it, 2 forces omega = 0 in it, 3 writes NaN into
+// r_0 in its update — so the breakdown and divergence verdicts can be reached on any
+// system, identically on both sides.  Not part of the method.
+static int g_fault_kind = 0, g_fault_it = 0;
+void orc_set_fault(int kind, int it) {
+  g_fault_kind = kind;
+  g_fault_it = it;
+}
+
 int orc_bicgstab(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
                  const double* b, const double* x0, const double* w, double tol, int maxit,
                  double* x, double* hist, orc_report* rep) {
@@ -397,10 +407,12 @@ int orc_bicgstab(int64_t n, const int32_t* rp, const int32_t* ci, const double* 
       if (tt == 0.0) { status = 2; bd = i; break; }
       double ts = orc_dot(n, t.data(), s.data());
       omega = ts / tt;
+      if (g_fault_kind == 2 && i == g_fault_it) omega = 0.0;
       for (int64_t k = 0; k < n; ++k) {
         x[k] = std::fma(omega, s[k], std::fma(alpha, p[k], x[k]));
         r[k] = std::fma(-omega, t[k], s[k]);
       }
+      if (g_fault_kind == 3 && i == g_fault_it) r[0] = std::nan("");
       rho_prev = rho;
       double rn = std::sqrt(orc_wnorm2(n, r.data(), w)) / n0;
       H.push_back(rn); iters = i;
@@ -409,6 +421,7 @@ int orc_bicgstab(int64_t n, const int32_t* rp, const int32_t* ci, const double* 
       if (omega == 0.0) { status = 2; bd = i; break; }
       if (i == maxit) { status = 1; break; }
       rho = orc_dot(n, rh.data(), r.data());
+      if (g_fault_kind == 1 && i == g_fault_it) rho = 0.0;
     }
   }
   // final true residual (one extra SpMV), PAPER.md:672-677 / SPEC true_relres

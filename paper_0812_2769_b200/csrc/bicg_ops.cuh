@@ -124,7 +124,7 @@ __device__ __forceinline__ void set_omega(BicgState* st, double ts, double tt) {
     st->done = 1;
     return;
   }
-  st->omega = ts / tt;
+  st->omega = (st->fault_kind == GSK_FAULT_OMEGA0 && st->fault_it == st->iter) ? 0.0 : ts / tt;
 }
 
 template <class L = LdNC>
@@ -186,7 +186,7 @@ __device__ __forceinline__ void update_finish(BicgState* st, double* hist, int h
     st->status = GSK_MAXIT;
     st->done = 1;
   } else {
-    const double rho = s[0];
+    const double rho = (st->fault_kind == GSK_FAULT_RHO0 && st->fault_it == i) ? 0.0 : s[0];
     st->rho = rho;
     if (rho == 0.0) {
       st->status = GSK_BREAKDOWN;
@@ -207,12 +207,13 @@ struct OpP3 {
   double *x, *r, *hist;
   BicgState* st;
   double alpha, omega;
-  int half;
+  int half, nan0;
   __device__ bool begin() {
     half = st->halfstep;
     if (st->done && !half) return false;
     alpha = st->alpha;
     omega = st->omega;
+    nan0 = st->fault_kind == GSK_FAULT_NAN && st->fault_it == st->iter;
     return true;
   }
   __device__ const double* vin(int k) const {
@@ -229,7 +230,7 @@ struct OpP3 {
     }
     const double s = __fma_rn(-alpha, v[2], v[3]);
     st_cold(x + i, __fma_rn(omega, s, __fma_rn(alpha, v[1], v[0])));
-    const double rr = __fma_rn(-omega, v[4], s);
+    const double rr = (nan0 && i == 0) ? __longlong_as_double(0x7ff8000000000000ll) : __fma_rn(-omega, v[4], s);
     r[i] = rr;
     c[0] = v[5] * rr;
     const double u = w ? v[6] * rr : rr;
@@ -356,12 +357,13 @@ struct OpS4 {
   double *x, *r, *hist;
   BicgState* st;
   double alpha, omega;
-  int half;
+  int half, nan0;
   __device__ bool begin() {
     half = st->halfstep;
     if (st->done && !half) return false;
     alpha = st->alpha;
     omega = st->omega;
+    nan0 = st->fault_kind == GSK_FAULT_NAN && st->fault_it == st->iter;
     return true;
   }
   __device__ const double* vin(int k) const {
@@ -378,7 +380,7 @@ struct OpS4 {
     }
     const double s = v[2];
     st_cold(x + i, __fma_rn(omega, s, __fma_rn(alpha, v[1], v[0])));
-    const double rr = __fma_rn(-omega, v[3], s);
+    const double rr = (nan0 && i == 0) ? __longlong_as_double(0x7ff8000000000000ll) : __fma_rn(-omega, v[3], s);
     r[i] = rr;
     c[0] = v[4] * rr;
     const double u = w ? v[5] * rr : rr;

@@ -170,6 +170,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   BicgState h{};
   h.tol = tol;
   h.maxit = maxit;
+  read_fault(&h.fault_kind, &h.fault_it);  // test-only hook (graph passes, unsharded)
   GSK_CUDA(cudaMemcpyAsync(P->bstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   double* V = P->bvec;
   OpInit<> init{x, b, P->weights, V, V + (size_t)n, V + 2 * (size_t)n, V + 4 * (size_t)n, P->hist_d, P->bstate};

@@ -58,11 +58,17 @@ struct Geometry {
 Geometry make_geometry(int n);
 
 // Device-resident Bi-CGSTAB state (scalars + control flags), DESIGN.md §5.
+// fault_kind / fault_it: the test-only fault hook (GSK_FAULT=<kind>:<iteration>, read at
+// solve start on unsharded plans; the oracle's orc_set_fault mirrors it): 1 forces
+// rho = 0 at the end of that iteration, 2 forces omega = 0 in it, 3 writes NaN into r_0
+// in its update (exercises the verdict paths identically on both sides).
 struct BicgState {
   double rho, rho_prev, alpha, omega, beta, n0, n0u, tol;
   double true_rel, true_rel_w;
   int iter, maxit, done, status, halfstep, bd, hist_len, pad;
+  int fault_kind, fault_it;
 };
+enum { GSK_FAULT_NONE = 0, GSK_FAULT_RHO0 = 1, GSK_FAULT_OMEGA0 = 2, GSK_FAULT_NAN = 3 };
 
 // Device-resident GMRES(m) state; arrays H[(m+1)*m] (row-major), cs[m], sn[m],
 // g[m+1], y[m], inv[m+2] (inv[j] = 1/||w_j||, basis slot j is stored unnormalised).
@@ -190,6 +196,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 int smem_carveout();
 void set_pass_carveout(const void* kern);
 bool short_slots_enabled();  // GSK_SHORT=0 disables the <= 5-slot kernels
+void read_fault(int* kind, int* it);  // GSK_FAULT test hook (BicgState)
 // per-device "function attributes already set" registry (keyed by any pointer)
 bool device_attr_done(const void* key);
 void device_attr_mark(const void* key);

@@ -91,6 +91,19 @@ bool pass_alternate() {
   return on == 1;
 }
 
+// Test-only fault hook: GSK_FAULT=<rho0|omega0|nan>:<iteration> (BicgState).
+void read_fault(int* kind, int* it) {
+  *kind = GSK_FAULT_NONE;
+  *it = 0;
+  const char* e = std::getenv("GSK_FAULT");
+  if (!e) return;
+  const char* c = std::strchr(e, ':');
+  if (!c) return;
+  const std::string k(e, c - e);
+  *kind = k == "rho0" ? GSK_FAULT_RHO0 : k == "omega0" ? GSK_FAULT_OMEGA0 : k == "nan" ? GSK_FAULT_NAN : GSK_FAULT_NONE;
+  *it = std::atoi(c + 1);
+}
+
 bool short_slots_enabled() {
   static int on = -1;
   if (on < 0) {

@@ -647,6 +647,26 @@ def test_sell_dict_solvers(name, N):
                       oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 100))
 
 
+@pytest.mark.parametrize("kind,k", [("rho0", 7), ("omega0", 7), ("nan", 7), ("nan", 1)])
+@pytest.mark.parametrize("fmt,schedule", [("csr", "split"), ("sell", "split"), ("sell", "fused")])
+def test_fault_hook_parity(kind, k, fmt, schedule, monkeypatch):
+    """The test-only fault hook on both sides — GSK_FAULT on the GPU,
+    oracle.set_fault on the host — reaches the breakdown and divergence verdicts on a
+    system that has none, with identical iterates, history and verdict."""
+    s, val, b, _ = system("C3", 20, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    P = gsk.Plan(A, fmt=fmt, schedule=schedule, engine="graph")
+    monkeypatch.setenv("GSK_FAULT", f"{kind}:{k}")
+    try:
+        oracle.set_fault(kind, k)
+        o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 400)
+    finally:
+        oracle.set_fault()
+    g = P.bicgstab(b, tol=1e-9, maxit=400)
+    assert o[2]["status"] == (3 if kind == "nan" else 2)
+    assert_same_solve(g, o)
+
+
 @pytest.mark.parametrize("name,N", [("C1", None), ("C2", 100), ("C3", 20), ("C4", 24), ("C4", None), ("C5", 64),
                                     ("P4", 12)])
 def test_sell_uniform_parity(name, N):

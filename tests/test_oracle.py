@@ -579,3 +579,28 @@ def test_sell_uniform_inapplicable_and_constructed():
     assert U["umask"][8] == 0xFF and U["umask"][9] == 0xFF and U["umask"][10] == 0x1F  # rows 32..39; r+3 < 40 for r <= 36
     assert U["uval"][0] == 0.0 and U["uval"][32] == 0.0 and U["uval"][64] == 1.0  # row 0: (0 -> 0.0), (3 -> 1.0)
     assert U["uval"][1] == 10.0 and U["uval"][33] == 11.0 and U["uval"][65] == 12.0
+
+
+@pytest.mark.parametrize("kind,k", [("rho0", 10), ("omega0", 10), ("nan", 10), ("rho0", 1), ("nan", 90)])
+def test_fault_hook_verdicts(kind, k):
+    """Test-only fault hook (the GPU mirrors it with GSK_FAULT): forcing rho = 0
+    at the end of iteration k gives BREAKDOWN at k + 1, omega = 0 in iteration k gives
+    BREAKDOWN at k (after the x, r update, reading B5), NaN in r_0 gives DIVERGED at k; the
+    history before the fault is the un-faulted run's, and clearing the hook restores it."""
+    s = workloads.generate("C1")
+    vo, bo, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    x0, h0, r0 = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 2000)
+    try:
+        oracle.set_fault(kind, k)
+        x, h, rep = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 2000)
+    finally:
+        oracle.set_fault()
+    want = {"rho0": (2, k, k + 1), "omega0": (2, k, k), "nan": (3, k, 0)}[kind]
+    assert (rep["status"], rep["iterations"], rep["breakdown_at"]) == want
+    assert np.array_equal(h[:k], h0[:k])
+    if kind == "rho0":
+        assert np.array_equal(h, h0[:k + 1])
+    if kind == "nan":
+        assert np.isnan(h[k])
+    x2, h2, _ = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 2000)
+    assert np.array_equal(h2, h0) and np.array_equal(x2, x0)
