@@ -207,14 +207,15 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   GSK_LAUNCHED(1);
   P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr,
                      P->sell_pad, P->wid, all_nat};
-  // GSK_L2PF: windows of L2 prefetch lead in the SELL passes (default 1: measured at
-  // C4 SpMV 0.274 -> 0.266 ms, S3 0.283 -> 0.275 ms; 2 was slower, 0 disables).  Passes
-  // with fewer than 4 windows per CTA skip it (C3, 2 windows: 5% slower with it).
-  static const int l2pf = [] {
+  // L2 prefetch lead in windows (engine.cuh): 1 when the slot data is far larger than
+  // L2 (C4: SpMV 0.274 -> 0.266 ms, S3 0.283 -> 0.275 ms), else 0 — with a matrix of
+  // 1.5-2x L2 (C3, C5) it cost 3-6% (profiles/r02_experiments); passes with fewer than
+  // 4 windows per CTA skip it too.  GSK_L2PF overrides (2 was slower at C4).
+  static const int l2pf_env = [] {
     const char* e = std::getenv("GSK_L2PF");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : -1;
   }();
-  P->sell.l2pf = l2pf;
+  P->sell.l2pf = l2pf_env >= 0 ? l2pf_env : (12.0 * (double)tot > 512e6 ? 1 : 0);
   return GSK_OK;
 }
 
