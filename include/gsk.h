@@ -225,13 +225,17 @@ typedef struct gsk_shard_opts {
                         shard `first`), or NULL (count == P: all shards on this GPU);
                         from gsk_nccl_comm_create, not owned by the plan */
   int32_t peer_reduce; /* 0: the P shard values of every reduction are all-gathered with
-                        ncclAllGather (host-enqueued).  1: device-initiated instead —
-                        each shard's finish kernel stores its values straight into every
-                        process's gather buffer (CUDA IPC mappings over NVLink, set up
-                        at plan creation by all-gathering the handles over the
-                        communicator) and releases a per-shard epoch flag; the global
-                        finish acquires the P flags and reduces.  Double-buffered by
-                        epoch parity.  Same tree, same bits. */
+                        ncclAllGather and halos move by ncclSend/ncclRecv (host-enqueued
+                        collectives).  1: device-initiated instead, over CUDA IPC
+                        mappings of every process's buffer (NVLink; the handles are
+                        all-gathered over the communicator at plan creation): each
+                        shard's finish kernel stores its values into every process's
+                        gather buffer and releases a per-shard epoch flag, the global
+                        finish acquires the P flags and reduces; a halo exchange pushes
+                        each shard's boundary rows into its neighbours' mailboxes and
+                        releases their flags, then pulls its own mailbox into the
+                        vector's margins.  Double-buffered by epoch parity.  Same tree,
+                        same bits. */
   int32_t pad_;
 } gsk_shard_opts;
 

@@ -121,7 +121,87 @@ struct ShardSet {
   double* pbuf = nullptr;
   double** dpeers = nullptr;
   std::vector<void*> opened;
+  // device-initiated halos (peer mode): each shard's mailbox as seen from this process
+  // (its own, or a neighbour's through the IPC mapping of that process's buffer)
+  std::vector<char*> box;
+  double* ebuf = nullptr;       // emulation (all shards here): the mailboxes
 };
+
+// Halo mailbox of shard q (peer mode): [2][hl_q] doubles received from
+// the left neighbour, [2][hr_q] from the right (by epoch parity), then four uint64 —
+// the epochs released by the left / right neighbour, this shard's halo epoch, and its
+// push ticket counter.
+static size_t box_bytes(int hl, int hr) { return ((16 * ((size_t)hl + hr) + 32) + 255) & ~size_t(255); }
+static size_t red_bytes(int P) {
+  return ((sizeof(double) * 2 * (size_t)P * MAXD + 2 * sizeof(unsigned long long) * (size_t)P) + 255) & ~size_t(255);
+}
+
+struct BoxView {
+  double* left;   // [2][hl]
+  double* right;  // [2][hr]
+  unsigned long long* flags;  // [0] from left, [1] from right, [2] halo epoch, [3] ticket
+  int hl, hr;
+};
+static BoxView box_view(char* b, int hl, int hr) {
+  BoxView v{};
+  if (!b) return v;
+  v.left = reinterpret_cast<double*>(b);
+  v.right = v.left + 2 * (size_t)hl;
+  v.flags = reinterpret_cast<unsigned long long*>(v.right + 2 * (size_t)hr);
+  v.hl = hl;
+  v.hr = hr;
+  return v;
+}
+
+// push: shard r's boundary rows into its neighbours' mailboxes (peer stores over
+// NVLink); the last CTA (a ticket per launch) releases the neighbours' flags with the
+// new epoch and records it in r's own mailbox
+__global__ void __launch_bounds__(256) halo_push_kernel(const double* v, int n, BoxView me, BoxView lnb, int to_left,
+                                                        BoxView rnb, int to_right) {
+  pdl_enter();
+  const unsigned long long e = me.flags[2] + 1;
+  const int par = (int)(e & 1ull);
+  const int tot = to_left + to_right;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    if (i < to_left) lnb.right[(size_t)par * lnb.hr + i] = v[i];
+    else rnb.left[(size_t)par * rnb.hl + (i - to_left)] = v[n - to_right + (i - to_left)];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long t = atomicAdd(me.flags + 3, 1ull);
+    if (t == e * gridDim.x - 1) {  // every CTA's stores are fenced: release them
+      __threadfence_system();
+      if (to_left) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(lnb.flags + 1), "l"(e) : "memory");
+      if (to_right) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(rnb.flags + 0), "l"(e) : "memory");
+      me.flags[2] = e;
+    }
+  }
+}
+
+// pull: wait for the neighbours' epoch, copy the mailboxes into the vector's margins
+__global__ void __launch_bounds__(256) halo_pull_kernel(double* v, int n, BoxView me) {
+  pdl_enter();
+  const unsigned long long e = me.flags[2];
+  const int par = (int)(e & 1ull);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      if ((k == 0 && !me.hl) || (k == 1 && !me.hr)) continue;
+      for (;;) {
+        unsigned long long f;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(me.flags + k) : "memory");
+        if (f >= e) break;
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  const int tot = me.hl + me.hr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    if (i < me.hl) v[i - me.hl] = __ldcv(me.left + (size_t)par * me.hl + i);
+    else v[n + (i - me.hl)] = __ldcv(me.right + (size_t)par * me.hr + (i - me.hl));
+  }
+}
 
 void shard_destroy(ShardSet* S) {
   if (!S) return;
@@ -135,6 +215,7 @@ void shard_destroy(ShardSet* S) {
   for (void* p : S->opened) cudaIpcCloseMemHandle(p);
   if (S->dpeers) cudaFree(S->dpeers);
   if (S->pbuf) cudaFree(S->pbuf);
+  if (S->ebuf) cudaFree(S->ebuf);
   delete S;
 }
 
@@ -186,6 +267,26 @@ __global__ void __launch_bounds__(256) halo_kernel(HaloList L) {
 template <class Base>
 static int shard_halo(gsk_plan* P, Base base, cudaStream_t s) {
   ShardSet* S = P->shards;
+  if (S->peer && S->P > 1) {  // device-initiated: pushes into the neighbours' mailboxes, then pulls
+    constexpr int kHaloCtas = 16;
+    for (int i = 0; i < S->count; ++i) {
+      const int r = S->first + i;
+      const Shard& d = S->sh[i];
+      const BoxView me = box_view(S->box[r], S->hl[r], S->hr[r]);
+      const BoxView l = r > 0 ? box_view(S->box[r - 1], S->hl[r - 1], S->hr[r - 1]) : BoxView{};
+      const BoxView rr = r + 1 < S->P ? box_view(S->box[r + 1], S->hl[r + 1], S->hr[r + 1]) : BoxView{};
+      GSK_CUDA(launch_k(halo_push_kernel, kHaloCtas, 256, 0, s, (const double*)base(i), d.n, me, l,
+                        r > 0 ? S->hr[r - 1] : 0, rr, r + 1 < S->P ? S->hl[r + 1] : 0));
+      GSK_LAUNCHED(1);
+    }
+    for (int i = 0; i < S->count; ++i) {
+      const int r = S->first + i;
+      GSK_CUDA(launch_k(halo_pull_kernel, kHaloCtas, 256, 0, s, base(i), S->sh[i].n,
+                        box_view(S->box[r], S->hl[r], S->hr[r])));
+      GSK_LAUNCHED(1);
+    }
+    return GSK_OK;
+  }
   if (!S->comm) {  // every shard on this GPU: device copies
     if (S->P == 1) return GSK_OK;
     HaloList L{};
@@ -688,14 +789,26 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
     }
   }
   S->rows0 = S->lo[S->first];
-  if (so->peer_reduce) {  // device-initiated reductions: buffers, IPC mappings
+  if (so->peer_reduce) {  // device-initiated reductions and halos: buffers, IPC mappings
     S->peer = true;
-    const size_t bytes = sizeof(double) * 2 * (size_t)P * MAXD + 2 * sizeof(unsigned long long) * (size_t)P;
+    // reduction area, then (one shard per process) this shard's halo mailbox
+    const size_t rb = red_bytes(P);
+    const size_t bytes = rb + (remote ? box_bytes(S->hl[so->first], S->hr[so->first]) : 0);
     if (cudaMalloc(&S->pbuf, bytes) != cudaSuccess || cudaMalloc(&S->dpeers, sizeof(double*) * P) != cudaSuccess) {
       set_error("gsk_plan_create_sharded: allocation of the peer-reduction buffers failed");
       return fail(GSK_E_NOMEM);
     }
     if (cudaMemsetAsync(S->pbuf, 0, bytes, s) != cudaSuccess) return fail(GSK_E_CUDA);
+    S->box.assign(P, nullptr);
+    if (remote) {
+      S->box[so->first] = reinterpret_cast<char*>(S->pbuf) + rb;
+    } else {  // all shards here: one mailbox each
+      std::vector<size_t> off(P + 1, 0);
+      for (int q = 0; q < P; ++q) off[q + 1] = off[q] + box_bytes(S->hl[q], S->hr[q]);
+      if (cudaMalloc(&S->ebuf, off[P]) != cudaSuccess) return fail(GSK_E_NOMEM);
+      if (cudaMemsetAsync(S->ebuf, 0, off[P], s) != cudaSuccess) return fail(GSK_E_CUDA);
+      for (int q = 0; q < P; ++q) S->box[q] = reinterpret_cast<char*>(S->ebuf) + off[q];
+    }
     std::vector<double*> ptrs(P, S->pbuf);  // one process: every shard's buffer is this one
     if (remote && P > 1) {
       cudaIpcMemHandle_t mine;
@@ -727,6 +840,7 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
         }
         S->opened.push_back(p);
         ptrs[q] = static_cast<double*>(p);
+        if (q == so->first - 1 || q == so->first + 1) S->box[q] = static_cast<char*>(p) + rb;  // neighbours' mailboxes
       }
     }
     if (cudaMemcpyAsync(S->dpeers, ptrs.data(), sizeof(double*) * P, cudaMemcpyHostToDevice, s) != cudaSuccess ||
