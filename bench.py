@@ -197,14 +197,18 @@ def run_reference(args, rank, world):
 
 
 def ncu_traffic(kernel):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
-    capture (profiles/r02_ncu_traffic.json), or None."""
+    """DRAM bytes (read + write) per launch of `kernel` (a short name or its prefix before
+    the engine's variant arguments, e.g. pass_kernel<2,1,OpS1) from the committed ncu
+    --set full capture (profiles/r02_ncu_traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
-            k = json.load(f)["kernels"].get(kernel)
-        return k["bytes_per_launch"] if k else None
+            ks = json.load(f)["kernels"]
     except (OSError, ValueError, KeyError):
         return None
+    for name, k in ks.items():
+        if name == kernel or name.startswith(kernel.rstrip(">") + ","):
+            return k["bytes_per_launch"]
+    return None
 
 
 def plan_schedule(args):
