@@ -53,3 +53,12 @@ def test_reference_arm_line():
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "iters/s"
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_roofline_traffic_from_committed_ncu():
+    """The bench line's roofline `traffic` comes from the committed ncu capture: the
+    dominant kernel (split Bi-CGSTAB S1) has a DRAM byte count within 10% of its
+    algorithmic bytes (no wasted re-reads)."""
+    t = bench.ncu_traffic("pass_kernel<2,1,OpS1>")
+    alg = bench.byte_model(16777216, 117047296)["bicg_s1"]
+    assert t is not None and 0.9 * alg < t < 1.1 * alg
