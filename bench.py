@@ -72,7 +72,7 @@ def parse():
     ap.add_argument("--no-time-to-tol", action="store_true",
                     help="skip the time-to-tolerance runs (Bi-CGSTAB and GMRES(30): none / GS(1) / GS(2) / "
                          "two-sided, ~40 s at C4)")
-    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split", "split4"])
     ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
                     help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
     ap.add_argument("--sell-index", default="plain", choices=["plain", "dict", "uniform"],
@@ -153,6 +153,8 @@ def byte_model(n, nnz):
             "bicg_p1": BA + 48 * n, "bicg_p2": BA + 24 * n,
             # split schedule: S1 v = A p (p gather, r^, v), S3 t = A s (s gather, t)
             "bicg_s1": BA + 24 * n, "bicg_s3": BA + 16 * n,
+            # four-pass schedule: S1q gathers q, r (p = r + beta q), reads r^, writes p, v
+            "bicg_s1q": BA + 40 * n,
             "bicg_iter": 2 * BA + 17 * 8 * n, "bicg_iter_split": 2 * BA + 19 * 8 * n,
             # GMRES S_j: w = A v_j as a plain SpMV pass (its h_1j dot is a separate pass)
             "gmres_mgs": 32 * n, "gmres_arnoldi": BA + 16 * n}
@@ -213,7 +215,7 @@ def ncu_traffic(kernel):
 
 def plan_schedule(args):
     """Bi-CGSTAB schedule the plan runs (auto = split)."""
-    return "fused" if args.schedule == "fused" else "split"
+    return args.schedule if args.schedule in ("fused", "split4") else "split"
 
 
 def reduce_over_ranks(ms, its, dist, device):
@@ -330,14 +332,18 @@ def main():
     hbm, src = peaks()
     p1_ms = probes[0]
     roof = None
-    split = plan_schedule(args) == "split"
+    sched = plan_schedule(args)
+    split = sched == "split"
     if p1_ms:
-        key = "bicg_s1" if split else "bicg_p1"
+        key, kname, kshort = {
+            "split": ("bicg_s1", "pass_kernel<SELL, OpS1> (v = A p, <r^,v>)", "pass_kernel<2,1,OpS1>"),
+            "split4": ("bicg_s1q", "pass_kernel<SELL, OpS1q> (p = r + beta q at the gather, v = A p, <r^,v>)",
+                       "pass_kernel<2,1,OpS1q>"),
+            "fused": ("bicg_p1", "pass_kernel<SELL, OpP1> (p update at the gather, v = A p, <r^,v>)",
+                      "pass_kernel<2,1,OpP1>")}[sched]
         ach = bm[key] / (p1_ms / 1e3) / 1e9
-        kname = ("pass_kernel<SELL, OpS1> (v = A p, <r^,v>)" if split
-                 else "pass_kernel<SELL, OpP1> (p update at the gather, v = A p, <r^,v>)")
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": ncu_traffic("pass_kernel<2,1,OpS1>" if split else "pass_kernel<2,1,OpP1>"),
+                "traffic": ncu_traffic(kshort),
                 "kernel": kname, "bytes_per_launch": bm[key], "ms_per_launch": p1_ms,
                 "peak_source": src, "frac_of_8TBps": ach / 8000.0}
 
@@ -373,7 +379,7 @@ def main():
         "bicgstab": {"iterations": r1["iterations"], "status": gsk.STATUS[r1["status"]],
                      "relres": r1["relres"], "true_relres": r1["true_relres"], "solve_ms": r1["solve_ms"],
                      "iters_per_s": r1["iterations"] / (r1["solve_ms"] / 1e3) if r1["solve_ms"] else None,
-                     "gbps_model": bm["bicg_iter_split" if split else "bicg_iter"] * r1["iterations"]
+                     "gbps_model": bm["bicg_iter" if sched == "fused" else "bicg_iter_split"] * r1["iterations"]
                      / (r1["solve_ms"] / 1e3) / 1e9 if r1["solve_ms"] else None,
                      "gbps_17vector_model": bm["bicg_iter"] * r1["iterations"] / (r1["solve_ms"] / 1e3) / 1e9
                      if r1["solve_ms"] else None, "schedule": plan_schedule(args)},
@@ -388,9 +394,10 @@ def main():
                 "frac_of_8TBps": gs_gbps / 8000.0},
         "probe_ms": {"bicg_v_pass": probes[0], "bicg_t_pass": probes[1], "gmres_mgs": probes[2],
                      "gmres_arnoldi_spmv": probes[3]},
-        "probe_gbps": {"bicg_v_pass": bm["bicg_s1" if split else "bicg_p1"] / (probes[0] / 1e3) / 1e9
+        "probe_gbps": {"bicg_v_pass": bm[{"split": "bicg_s1", "split4": "bicg_s1q", "fused": "bicg_p1"}[sched]]
+                       / (probes[0] / 1e3) / 1e9
                        if probes[0] else None,
-                       "bicg_t_pass": bm["bicg_s3" if split else "bicg_p2"] / (probes[1] / 1e3) / 1e9
+                       "bicg_t_pass": bm["bicg_p2" if sched == "fused" else "bicg_s3"] / (probes[1] / 1e3) / 1e9
                        if probes[1] else None,
                        "gmres_mgs": bm["gmres_mgs"] / (probes[2] / 1e3) / 1e9 if probes[2] else None,
                        "gmres_arnoldi_spmv": bm["gmres_arnoldi"] / (probes[3] / 1e3) / 1e9

@@ -66,7 +66,9 @@ typedef struct gsk_report {
 /* Plan options.  format: GSK_FMT_CSR or GSK_FMT_SELL (SELL-C-sigma, C = 32,
  * sigma = 256, built on the device from the CSR at plan creation).
  * bicg_schedule: 0 = auto, 1 = fused 3-pass iteration (p and s recomputed at the
- * SpMV gather), 2 = split 5-pass iteration (plain SpMV gathers); both give
+ * SpMV gather), 2 = split 5-pass iteration (plain SpMV gathers), 3 = four-pass
+ * iteration (the p update folded into the neighbouring passes: q = p - omega v stored
+ * by the update pass, p = r + beta q formed at the SpMV gather); all give
  * bit-identical results.
  * weights: NULL, or DEVICE [n] w_i > 0.  When set, Bi-CGSTAB's stopping test and
  * history use ||w o r|| / ||w o r0|| — the paper measures the relative residual on

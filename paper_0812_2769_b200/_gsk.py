@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GSK_LIB") or os.path.join(_HERE, "libgsk.so")  # GSK_
 GSK_OK, GSK_E_INVALID, GSK_E_ZERO_ROW, GSK_E_CUDA, GSK_E_NOMEM = 0, -1, -2, -3, -4
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "DIVERGED"}
 FMT = {"csr": 0, "sell": 1}
-SCHEDULE = {"auto": 0, "fused": 1, "split": 2}
+SCHEDULE = {"auto": 0, "fused": 1, "split": 2, "split4": 3}
 ENGINE = {"auto": 0, "graph": 1, "coop": 2, "small": 3, "cluster": 4}
 ORTH = {"mgs": 0, "cgs2": 1}
 

@@ -299,6 +299,46 @@ struct OpS1 {
   }
 };
 
+// ---- four-pass schedule (bicg_schedule 3): S0 folded into its neighbours ------------
+// S4q = S4 + q = p - omega v stored over p (own rows, in place); S1q gathers q and r and
+// forms p = r + beta q at every gathered column (the same two FMAs as S0, in the same
+// order: AC-6), writes p for its own rows into the other p buffer, then v = A p and
+// <r^, v>.  Same bytes per iteration as the split schedule, one kernel fewer, a second
+// gather stream in the SpMV pass.
+template <class L = LdNC>
+struct OpS1q {
+  static constexpr int D = 1;
+  static constexpr int NV = 3;
+  static constexpr bool kSpmv = true;
+  const double *q, *r, *rh;
+  double *p, *v;
+  BicgState* st;
+  double beta;
+  __device__ bool begin() {
+    if (st->done) return false;
+    beta = st->beta;
+    return true;
+  }
+  __device__ const double* vin(int k) const { return k == 0 ? rh : k == 1 ? q : r; }
+  __device__ double gather(int c) const { return __fma_rn(beta, L::ld(q + c), L::ld(r + c)); }
+  __device__ void row(int i, double y, const double (&x)[NV], double (&c)[1]) const {
+    p[i] = __fma_rn(beta, x[1], x[2]);
+    v[i] = y;
+    c[0] = x[0] * y;
+  }
+  __device__ void finish(const double (&s)[1], int lane) const {
+    if (lane) return;
+    const double sigma = s[0];
+    if (sigma == 0.0) {
+      st->status = GSK_BREAKDOWN;
+      st->bd = st->iter;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / sigma;
+  }
+};
+
 struct OpS2 {
   static constexpr int D = 1;
   static constexpr int NV = 3;
@@ -385,6 +425,50 @@ struct OpS4 {
     c[0] = v[4] * rr;
     const double u = w ? v[5] * rr : rr;
     c[1] = u * u;
+  }
+  __device__ void finish(const double (&s)[2], int lane) const {
+    if (lane == 0) update_finish(st, hist, half, alpha, omega, s);
+  }
+};
+
+// S4 of the four-pass schedule: also q = p - omega v over p (the next S1q's gather)
+struct OpS4q {
+  static constexpr int D = 2;
+  static constexpr int NV = 7;
+  static constexpr bool kSpmv = false;
+  const double *s_, *t, *rh, *w, *v;
+  double *p, *x, *r, *hist;
+  BicgState* st;
+  double alpha, omega;
+  int half, nan0;
+  __device__ bool begin() {
+    half = st->halfstep;
+    if (st->done && !half) return false;
+    alpha = st->alpha;
+    omega = st->omega;
+    nan0 = st->fault_kind == GSK_FAULT_NAN && st->fault_it == st->iter;
+    return true;
+  }
+  __device__ const double* vin(int k) const {
+    return k == 0 ? x : k == 1 ? p : k == 2 ? (half ? nullptr : s_) : k == 3 ? (half ? nullptr : t)
+         : k == 4 ? (half ? nullptr : rh) : k == 5 ? (half ? nullptr : w) : (half ? nullptr : v);
+  }
+  __device__ double gather(int) const { return 0.0; }
+  __device__ void row(int i, double, const double (&u)[NV], double (&c)[2]) const {
+    if (half) {
+      st_cold(x + i, __fma_rn(alpha, u[1], u[0]));
+      c[0] = 0.0;
+      c[1] = 0.0;
+      return;
+    }
+    const double s = u[2];
+    st_cold(x + i, __fma_rn(omega, s, __fma_rn(alpha, u[1], u[0])));
+    const double rr = (nan0 && i == 0) ? __longlong_as_double(0x7ff8000000000000ll) : __fma_rn(-omega, u[3], s);
+    r[i] = rr;
+    p[i] = __fma_rn(-omega, u[6], u[1]);  // q for the next S1q (p is not read again)
+    c[0] = u[4] * rr;
+    const double uw = w ? u[5] * rr : rr;
+    c[1] = uw * uw;
   }
   __device__ void finish(const double (&s)[2], int lane) const {
     if (lane == 0) update_finish(st, hist, half, alpha, omega, s);

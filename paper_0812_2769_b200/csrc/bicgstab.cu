@@ -53,6 +53,17 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
       rc = run_pass(P, p1, s, ev(0, 0, k), ev(0, 1, k));
       if (rc >= 0) rc = run_pass(P, p2, s, ev(1, 0, k), ev(1, 1, k));
       if (rc >= 0) rc = run_pass(P, p3, s);
+    } else if (P->bmode == 3) {  // four-pass schedule: q / p alternate between pa and vb
+      double *qs = (k & 1) ? vb : pa, *pd = (k & 1) ? pa : vb;
+      double *v = va, *sv = pb;
+      OpS1q<> s1{qs, r, rh, pd, v, P->bstate, 0.0};
+      OpS2 s2{r, v, w, sv, P->hist_d, P->bstate, 0};
+      OpS3<> s3{sv, t, P->bstate};
+      OpS4q s4{sv, t, rh, w, v, pd, x, r, P->hist_d, P->bstate, 0, 0, 0, 0};
+      rc = run_pass(P, s1, s, ev(0, 0, k), ev(0, 1, k));
+      if (rc >= 0) rc = run_pass(P, s2, s);
+      if (rc >= 0) rc = run_pass(P, s3, s, ev(1, 0, k), ev(1, 1, k));
+      if (rc >= 0) rc = run_pass(P, s4, s);
     } else {  // split 5-pass schedule: p = pa, v = va, s = pb
       double *p = pa, *v = va, *sv = pb;
       OpS0 s0{r, v, p, P->bstate, 0, 0};
@@ -153,7 +164,7 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_bicg(P, x, K, c, &P->bgraph[c]));
+    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_retry([&] { return capture_bicg(P, x, K, c, &P->bgraph[c]); }));
     P->bkey_b = b;
     P->bkey_x = x;
     P->bK = K;

@@ -157,7 +157,7 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_cycle(P, b, x, m, c, &P->ggraph[c]));
+    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_retry([&] { return capture_cycle(P, b, x, m, c, &P->ggraph[c]); }));
     P->gkey_b = b;
     P->gkey_x = x;
     P->gkey_m = m;

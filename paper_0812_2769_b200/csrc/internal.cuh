@@ -327,6 +327,20 @@ int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).
 int end_capture(cudaStream_t s, int rc, cudaGraphExec_t* out, long long* kernels, const char* what);
+
+// A stream capture fails if another host thread makes a device-wide call meanwhile
+// (e.g. cudaDeviceSynchronize invalidates every capture in progress on the device), so
+// a failed capture is retried a few times before its error is returned.
+template <class F>
+int capture_retry(F&& capture) {
+  int rc = GSK_OK;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    rc = capture();
+    if (rc == GSK_OK) return rc;
+    cudaGetLastError();  // the invalidation is not sticky; clear it before the next attempt
+  }
+  return rc;
+}
 int join_in(gsk_plan* P, cudaStream_t caller);
 // Replay graphs[b % NQ] for batch b until the device flag *done_dev is set (checked on
 // the host one batch behind, NQ batches in flight) or maxb batches ran; accumulates

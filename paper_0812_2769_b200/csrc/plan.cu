@@ -392,7 +392,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
   P->poll = opts ? opts->poll : 0;
   P->weights = opts ? opts->weights : nullptr;
   const int sched = opts ? opts->bicg_schedule : GSK_BICG_AUTO;
-  if (sched < 0 || sched > 2) {
+  if (sched < 0 || sched > 3) {
     delete P;
     set_error("gsk_plan_create: unknown bicg_schedule %d", sched);
     return GSK_E_INVALID;

@@ -422,7 +422,7 @@ int shard_bicgstab_run(gsk_plan* P, const double* b, const double* x0, double to
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(shard_capture_bicg(P, K, c, &P->bgraph[c]));
+    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_retry([&] { return shard_capture_bicg(P, K, c, &P->bgraph[c]); }));
     P->bkey_b = b;
     P->bK = K;
     P->bkey_h = P->hist_d;
@@ -526,7 +526,7 @@ int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doubl
         cudaGraphExecDestroy(g);
         g = nullptr;
       }
-    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(shard_capture_cycle(P, b, m, c, &P->ggraph[c]));
+    for (int c = 0; c < gsk_plan::NQ; ++c) GSK_TRY(capture_retry([&] { return shard_capture_cycle(P, b, m, c, &P->ggraph[c]); }));
     P->gkey_b = b;
     P->gkey_m = m;
     P->gkey_h = P->hist_d;
