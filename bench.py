@@ -213,9 +213,14 @@ def ncu_traffic(kernel):
     return None
 
 
-def plan_schedule(args):
-    """Bi-CGSTAB schedule the plan runs (auto = split)."""
-    return args.schedule if args.schedule in ("fused", "split4") else "split"
+def plan_schedule(args, n=None, nnz=None):
+    """Bi-CGSTAB schedule the plan runs (auto: four-pass when the matrix and eight
+    vectors fit in 64 MB, else split)."""
+    if args.schedule != "auto":
+        return args.schedule
+    if n is not None and 12 * nnz + 4 * n + 64 * n <= 64e6:
+        return "split4"
+    return "split"
 
 
 def reduce_over_ranks(ms, its, dist, device):
@@ -332,8 +337,7 @@ def main():
     hbm, src = peaks()
     p1_ms = probes[0]
     roof = None
-    sched = plan_schedule(args)
-    split = sched == "split"
+    sched = plan_schedule(args, n, nnz)
     if p1_ms:
         key, kname, kshort = {
             "split": ("bicg_s1", "pass_kernel<SELL, OpS1> (v = A p, <r^,v>)", "pass_kernel<2,1,OpS1>"),
@@ -382,7 +386,7 @@ def main():
                      "gbps_model": bm["bicg_iter" if sched == "fused" else "bicg_iter_split"] * r1["iterations"]
                      / (r1["solve_ms"] / 1e3) / 1e9 if r1["solve_ms"] else None,
                      "gbps_17vector_model": bm["bicg_iter"] * r1["iterations"] / (r1["solve_ms"] / 1e3) / 1e9
-                     if r1["solve_ms"] else None, "schedule": plan_schedule(args)},
+                     if r1["solve_ms"] else None, "schedule": sched},
         "gmres": {"m": m, "orth": args.orth, "iterations": r2["iterations"], "status": gsk.STATUS[r2["status"]],
                   "relres": r2["relres"], "true_relres": r2["true_relres"], "solve_ms": r2["solve_ms"],
                   "iters_per_s": r2["iterations"] / (r2["solve_ms"] / 1e3) if r2["solve_ms"] else None},

@@ -69,7 +69,8 @@ typedef struct gsk_report {
  * SpMV gather), 2 = split 5-pass iteration (plain SpMV gathers), 3 = four-pass
  * iteration (the p update folded into the neighbouring passes: q = p - omega v stored
  * by the update pass, p = r + beta q formed at the SpMV gather); all give
- * bit-identical results.
+ * bit-identical results.  Auto: four-pass when the matrix and eight
+ * vectors fit in 64 MB (L2-resident, launch-bound: C2 +6%), else split.
  * weights: NULL, or DEVICE [n] w_i > 0.  When set, Bi-CGSTAB's stopping test and
  * history use ||w o r|| / ||w o r0|| — the paper measures the relative residual on
  * the GS(2)-scaled system, i.e. w = d_GS(2) / d_applied.
@@ -109,7 +110,7 @@ enum { GSK_ENGINE_AUTO = 0, GSK_ENGINE_GRAPH = 1, GSK_ENGINE_COOP = 2, GSK_ENGIN
        GSK_ENGINE_CLUSTER = 4 /* on-chip solver on one thread-block cluster, n <= 65536 */ };
 #define GSK_SMALL_NMAX 4096
 
-enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2 };
+enum { GSK_BICG_AUTO = 0, GSK_BICG_FUSED = 1, GSK_BICG_SPLIT = 2, GSK_BICG_SPLIT4 = 3 };
 /* gmres_orth: GSK_ORTH_MGS (modified Gram-Schmidt, j+1 passes per Arnoldi step; the
  * north star's choice) or GSK_ORTH_CGS2 (double classical Gram-Schmidt as in AZTEC,
  * three passes per step, H(:,j) = h + h'; m <= 64). */

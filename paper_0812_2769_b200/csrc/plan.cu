@@ -397,7 +397,11 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
     set_error("gsk_plan_create: unknown bicg_schedule %d", sched);
     return GSK_E_INVALID;
   }
-  P->bmode = sched == GSK_BICG_AUTO ? GSK_BICG_SPLIT : sched;
+  // auto: the four-pass schedule (one kernel fewer, a second gather stream) where the
+  // iteration is L2-resident and launch-bound (C2: 37.4k vs 35.2k it/s), else split
+  // (C3 / C4 / C5: the extra gathers cost 7-23%; profiles/r02_experiments)
+  const double ws = 12.0 * (double)A->nnz + 4.0 * (double)A->n + 64.0 * (double)A->n;
+  P->bmode = sched == GSK_BICG_AUTO ? (ws <= 64e6 ? GSK_BICG_SPLIT4 : GSK_BICG_SPLIT) : sched;
   const int orth = opts ? opts->gmres_orth : GSK_ORTH_MGS;
   if (orth != GSK_ORTH_MGS && orth != GSK_ORTH_CGS2) {
     delete P;

@@ -56,7 +56,7 @@ def test_header_enums_match_binding():
     from paper_0812_2769_b200 import _gsk
     assert _gsk.FMT == {"csr": vals["GSK_FMT_CSR"], "sell": vals["GSK_FMT_SELL"]}
     assert _gsk.SCHEDULE == {"auto": vals["GSK_BICG_AUTO"], "fused": vals["GSK_BICG_FUSED"],
-                             "split": vals["GSK_BICG_SPLIT"]}
+                             "split": vals["GSK_BICG_SPLIT"], "split4": vals["GSK_BICG_SPLIT4"]}
     assert _gsk.ORTH == {"mgs": vals["GSK_ORTH_MGS"], "cgs2": vals["GSK_ORTH_CGS2"]}
     assert _gsk.ENGINE == {"auto": vals["GSK_ENGINE_AUTO"], "graph": vals["GSK_ENGINE_GRAPH"],
                            "coop": vals["GSK_ENGINE_COOP"], "small": vals["GSK_ENGINE_SMALL"],
