@@ -98,10 +98,12 @@ typedef struct gsk_opts {
                            GSK_ENGINE_AUTO (default) = one launch for the whole solve on
                            one CTA (Bi-CGSTAB n <= 2048, MGS GMRES n <= 1024) or on one
                            thread-block cluster (Bi-CGSTAB n <= 32768, MGS GMRES with
-                           m <= 40 n <= 65536), where each is measured faster, else
+                           m <= 40 n <= 65536) or on a persistent cooperative grid
+                           (Bi-CGSTAB n <= 81920), where each is measured faster, else
                            graph-replayed passes; GSK_ENGINE_GRAPH = always the
-                           passes; GSK_ENGINE_COOP = cooperative multi-CTA Bi-CGSTAB for
-                           n <= 2^19 (opt-in); GSK_ENGINE_SMALL = the one-CTA solver
+                           passes; GSK_ENGINE_COOP = the cooperative Bi-CGSTAB whenever
+                           its grid fits (<= 16 windows of 256 rows per co-resident CTA,
+                           plain-column SELL or CSR; else the passes); GSK_ENGINE_SMALL = the one-CTA solver
                            whenever n <= GSK_SMALL_NMAX; GSK_ENGINE_CLUSTER = the cluster
                            solver whenever it fits. */
 } gsk_opts;

@@ -259,9 +259,10 @@ class Plan:
     def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
                  orth: str = "mgs", sell_index: str = "plain", engine: str = "auto"):
         """engine: "auto" (one launch per solve on one CTA up to 2048 / 1024 rows or on
-        one thread-block cluster up to 32768 / 65536 rows for Bi-CGSTAB / GMRES, where
-        measured faster; else graph passes), "graph" (always the passes), "coop"
-        (cooperative multi-CTA Bi-CGSTAB), "small" (one CTA, n <= 4096) or "cluster"
+        one thread-block cluster up to 32768 / 65536 rows for Bi-CGSTAB / GMRES, or a
+        persistent cooperative grid up to 81920 rows for Bi-CGSTAB, where measured
+        faster; else graph passes), "graph" (always the passes), "coop" (persistent
+        cooperative multi-CTA Bi-CGSTAB whenever its grid fits), "small" (one CTA, n <= 4096) or "cluster"
         (one cluster, n <= 65536)."""
         lib = load()
         self.A = A

@@ -122,15 +122,20 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   GSK_TRY(ensure_hist(P, maxit));
   // small systems: one launch runs the whole iteration loop — on one SM with the
   // vectors in shared memory (small.cu; by default for n <= 2048, where
-  // it is measured faster: 6.7 vs 31 us per iteration at n = 1024), or on a
-  // cooperative grid (coop.cu, opt-in).  Same operators, bit-identical results.
+  // it is measured faster: 6.7 vs 31 us per iteration at n = 1024), on one cluster or
+  // on a cooperative grid.  Same operators, bit-identical results.
   const bool small = (P->engine == GSK_ENGINE_AUTO && n <= 2048) ||
                      (P->engine == GSK_ENGINE_SMALL && n <= GSK_SMALL_NMAX);
   // one thread-block cluster (cluster.cu) above that, up to 16384 rows: 12-15 vs 25-27
   // us per iteration on the graph passes
   const bool clus = !small && ((P->engine == GSK_ENGINE_AUTO && n <= GSK_CLUSTER_AUTO_BICG) ||
                                (P->engine == GSK_ENGINE_CLUSTER && n <= GSK_CLUSTER_NMAX));
-  if (small || clus || P->engine == GSK_ENGINE_COOP) {
+  // a persistent cooperative grid (coop.cu) above that, up to 81920 rows: 20.7-24.1 vs
+  // 22.9-26.9 us per iteration on the graph passes (profiles/r02v_coop.json); even at
+  // ~90000 rows, slower beyond
+  const bool coop = !small && !clus && ((P->engine == GSK_ENGINE_AUTO && n <= GSK_COOP_AUTO_BICG) ||
+                                        P->engine == GSK_ENGINE_COOP);
+  if (small || clus || coop) {
     cudaStream_t s = P->st;
     GSK_TRY(join_in(P, caller));
     GSK_CUDA(cudaEventRecord(P->t0, s));

@@ -310,6 +310,7 @@ int small_gmres_run(gsk_plan* P, const double* b, double* x, const GmresState& h
 // up to 32768 rows (19.9 vs 24.0 us/it; 28.3 vs 24.6 at 40000), GMRES up to 65536
 #define GSK_CLUSTER_AUTO_BICG 32768
 #define GSK_CLUSTER_AUTO_GMRES 65536
+#define GSK_COOP_AUTO_BICG 81920  // the cooperative Bi-CGSTAB above the cluster range
 // On-chip solvers on one thread-block cluster (cluster.cu) for n <= 65536; *used = 0
 // when the system does not fit (the caller then runs the graph path).
 int cluster_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);

@@ -610,6 +610,31 @@ def test_cluster_engine_parity(name, N):
                       oracle.gmres(s["row_ptr"], s["col"], val, b, 20, 1e-9, 200, weights=w))
 
 
+COOP = [("C2", 128, None), ("C2", 264, None), ("C2", 200, "7"), ("C5", 200, None), ("C3", 32, "5"),
+        ("C2", 264, "1"), ("C4", 24, None)]
+
+
+@pytest.mark.parametrize("name,N,gcap", COOP)
+@pytest.mark.parametrize("fmt", ["csr", "sell"])
+def test_coop_engine_parity(name, N, gcap, fmt, monkeypatch):
+    """Persistent cooperative Bi-CGSTAB (coop.cu: per-CTA epoch flags, every CTA
+    reducing the CTA partials itself): bit-exact against the oracle over grids of one
+    CTA, of G > 256 CTAs (two partials per finish thread) and of capped grids with
+    several windows per CTA (GSK_COOP_G), natural / sorted SELL windows and CSR, with
+    and without frame weights."""
+    if gcap:
+        monkeypatch.setenv("GSK_COOP_G", gcap)
+    s, val, b, _ = system(name, N, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    P = gsk.Plan(A, fmt=fmt, engine="coop")
+    assert_same_solve(P.bicgstab(b, tol=1e-10, maxit=400),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-10, 400))
+    w = workloads.uniform(s["n"], 5, 6) + 1.5
+    Pw = gsk.Plan(A, fmt=fmt, engine="coop", weights=w)
+    assert_same_solve(Pw.bicgstab(b, tol=1e-10, maxit=300),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-10, 300, weights=w))
+
+
 def test_concurrent_plans_two_threads():
     """Two plans driven from two host threads at once (each on its own stream, the GIL
     released inside the C calls): both solves stay bit-exact."""
