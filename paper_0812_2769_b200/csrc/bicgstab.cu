@@ -117,8 +117,8 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   }
   if (P->shards) return shard_bicgstab_run(P, b, x0, tol, maxit, x, hist, rep, caller);
   const int n = P->A.n;
-  if (!P->bvec) GSK_CUDA(cudaMalloc(&P->bvec, sizeof(double) * 7 * (size_t)n));
-  if (!P->bstate) GSK_CUDA(cudaMalloc(&P->bstate, sizeof(BicgState)));
+  if (!P->bvec) GSK_CUDA(pool_alloc((void**)&P->bvec, sizeof(double) * 7 * (size_t)n));
+  if (!P->bstate) GSK_CUDA(pool_alloc((void**)&P->bstate, sizeof(BicgState)));
   GSK_TRY(ensure_hist(P, maxit));
   // small systems: one launch runs the whole iteration loop — on one SM with the
   // vectors in shared memory (small.cu; by default for n <= 2048, where

@@ -308,7 +308,7 @@ int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, doubl
   const int lpt = G <= 256 ? 1 : G <= 512 ? 2 : 4;
   // [2][MAXD][COOP_GMAX] partials, [2][MAXD] results, then COOP_GMAX flags + the broadcast word
   const size_t pdoubles = 2 * MAXD * COOP_GMAX + 2 * MAXD;
-  if (!P->cpart) GSK_CUDA(cudaMalloc(&P->cpart, sizeof(double) * pdoubles + sizeof(unsigned) * (COOP_GMAX + 32)));
+  if (!P->cpart) GSK_CUDA(pool_alloc((void**)&P->cpart, sizeof(double) * pdoubles + sizeof(unsigned) * (COOP_GMAX + 32)));
   unsigned* flags = reinterpret_cast<unsigned*>(P->cpart + pdoubles);
   GSK_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned) * (COOP_GMAX + 32), P->st));
   double* V = P->bvec;

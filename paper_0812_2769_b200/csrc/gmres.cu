@@ -115,9 +115,12 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   if (P->shards) return shard_gmres_run(P, b, x0, m, tol, maxit, x, hist, rep, caller);
   const size_t n = (size_t)P->A.n;
   if (P->Wm < m) {
-    if (P->W) GSK_CUDA(cudaFree(P->W));
+    if (P->W) {
+      GSK_CUDA(cudaStreamSynchronize(P->st));  // no queued pass still reads it
+      pool_release(P->W);
+    }
     P->W = nullptr;
-    cudaError_t e = cudaMalloc(&P->W, sizeof(double) * (size_t)(m + 1) * n);
+    cudaError_t e = pool_alloc((void**)&P->W, sizeof(double) * (size_t)(m + 1) * n);
     if (e != cudaSuccess) {
       set_error("gmres: cannot allocate the (m+1) x n basis: %s", cudaGetErrorString(e));
       P->Wm = 0;
@@ -135,9 +138,9 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
     return GSK_E_INVALID;
   }
   if (P->orth == 1 && !P->mpart)
-    GSK_CUDA(cudaMalloc(&P->mpart, sizeof(double) * MDOT_MAX * (size_t)P->pstride));
-  if (!P->gstate) GSK_CUDA(cudaMalloc(&P->gstate, sizeof(GmresState)));
-  if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8)));
+    GSK_CUDA(pool_alloc((void**)&P->mpart, sizeof(double) * MDOT_MAX * (size_t)P->pstride));
+  if (!P->gstate) GSK_CUDA(pool_alloc((void**)&P->gstate, sizeof(GmresState)));
+  if (!P->garr) GSK_CUDA(pool_alloc((void**)&P->garr, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8)));
   GSK_TRY(ensure_hist(P, maxit));
   // small systems: the whole solve in one launch on one SM (small.cu), MGS only
   // (default for n <= 1024), or on one thread-block cluster (cluster.cu) up to 65536

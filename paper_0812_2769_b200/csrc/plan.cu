@@ -5,6 +5,7 @@
 #include <cstring>
 #include <execinfo.h>
 #include <unistd.h>
+#include <map>
 #include <mutex>
 #include <set>
 #include <unordered_map>
@@ -141,6 +142,83 @@ void device_attr_mark(const void* key) {
   g_attr_done.insert({current_device(), key});
 }
 
+// Workspace cache: device blocks released by a plan (after its stream
+// drained) stay mapped, keyed by (device, size class), and serve the next plan that asks
+// for the same class, so plans built and destroyed in a loop (bench.py's e2e step: SELL
+// arrays, 7 Bi-CGSTAB vectors, the 31-vector GMRES basis — ~7 GB at C4) cost no
+// cudaMalloc / cudaFree; a cudaFree of a GB-sized block synchronises the device and
+// unmaps it (10-270 ms per plan at C4, profiles/r02_e2e_breakdown.txt).  Size classes:
+// powers of two below 2 MB, multiples of 2 MB above.  The cache holds at most
+// GSK_POOL_MB (default 32768) per device; GSK_POOL_MB=0 disables it; a failed
+// cudaMalloc first returns the device's cached blocks and retries.
+static std::mutex g_pool_mu;
+static std::multimap<std::pair<int, size_t>, void*> g_pool_free;
+static std::unordered_map<void*, std::pair<int, size_t>> g_pool_live;
+static std::unordered_map<int, size_t> g_pool_bytes;  // cached (free) bytes per device
+static size_t pool_cap() {
+  static const size_t cap = [] {
+    const char* e = std::getenv("GSK_POOL_MB");
+    return (size_t)(e ? std::atoll(e) : 32768LL) << 20;
+  }();
+  return cap;
+}
+static size_t pool_class(size_t bytes) {
+  if (bytes == 0) bytes = 1;
+  if (bytes >= (2u << 20)) return (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
+  size_t c = 256;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+static void pool_trim_locked(int dev) {
+  for (auto it = g_pool_free.begin(); it != g_pool_free.end();) {
+    if (it->first.first == dev) {
+      cudaFree(it->second);
+      it = g_pool_free.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  g_pool_bytes[dev] = 0;
+}
+cudaError_t pool_alloc(void** p, size_t bytes) {
+  const int dev = current_device();
+  const size_t cls = pool_class(bytes);
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  auto it = g_pool_free.find({dev, cls});
+  if (it != g_pool_free.end()) {
+    *p = it->second;
+    g_pool_free.erase(it);
+    g_pool_bytes[dev] -= cls;
+    g_pool_live[*p] = {dev, cls};
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc(p, cls);
+  if (e == cudaErrorMemoryAllocation && g_pool_bytes[dev] > 0) {
+    cudaGetLastError();
+    pool_trim_locked(dev);
+    e = cudaMalloc(p, cls);
+  }
+  if (e == cudaSuccess) g_pool_live[*p] = {dev, cls};
+  return e;
+}
+void pool_release(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  auto it = g_pool_live.find(p);
+  if (it == g_pool_live.end()) {  // not a pool block
+    cudaFree(p);
+    return;
+  }
+  const auto key = it->second;
+  g_pool_live.erase(it);
+  if (g_pool_bytes[key.first] + key.second > pool_cap()) {
+    cudaFree(p);
+    return;
+  }
+  g_pool_free.insert({key, p});
+  g_pool_bytes[key.first] += key.second;
+}
+
 void set_pass_carveout(const void* kern) {
   const int pct = smem_carveout();
   if (pct < 0 || device_attr_done(kern)) return;
@@ -170,7 +248,7 @@ int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
   if (async)
     GSK_CUDA(cudaMallocAsync(&P->part, bytes, s));
   else
-    GSK_CUDA(cudaMalloc(&P->part, bytes));
+    GSK_CUDA(pool_alloc((void**)&P->part, bytes));
   return GSK_OK;
 }
 
@@ -228,7 +306,7 @@ struct OpResNorm {
 static int plan_alloc_common(gsk_plan* P) {
   P->geo = make_geometry(P->A.n);
   GSK_TRY(alloc_reduction(P, nullptr, false));
-  GSK_CUDA(cudaMalloc(&P->scratch, sizeof(double) * 8));
+  GSK_CUDA(pool_alloc((void**)&P->scratch, sizeof(double) * 8));
   GSK_CUDA(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
   GSK_CUDA(cudaMallocHost(&P->h_flag, sizeof(int) * 16));
   for (int q = 0; q < 16; ++q) P->h_flag[q] = 0;
@@ -349,9 +427,12 @@ int run_batches(gsk_plan* P, cudaGraphExec_t* graphs, long long maxb, long long 
 
 int ensure_hist(gsk_plan* P, int maxit) {
   if (P->hist_cap >= maxit + 1) return GSK_OK;
-  if (P->hist_d) GSK_CUDA(cudaFree(P->hist_d));
+  if (P->hist_d) {
+    GSK_CUDA(cudaStreamSynchronize(P->st));  // no queued pass still writes it
+    pool_release(P->hist_d);
+  }
   P->hist_d = nullptr;
-  GSK_CUDA(cudaMalloc(&P->hist_d, sizeof(double) * (size_t)(maxit + 1)));
+  GSK_CUDA(pool_alloc((void**)&P->hist_d, sizeof(double) * (size_t)(maxit + 1)));
   P->hist_cap = maxit + 1;
   return GSK_OK;
 }
@@ -466,8 +547,7 @@ void gsk_plan_destroy(gsk_plan* P) {
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->wid, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
                   P->cpart, P->uptr, P->udel, P->umask, P->uval};
-  for (void* b : bufs)
-    if (b) cudaFree(b);
+  for (void* b : bufs) pool_release(b);  // the plan stream drained above
   if (P->h_flag) cudaFreeHost(P->h_flag);
   for (auto& k : P->pev)
     for (auto& e : k) {

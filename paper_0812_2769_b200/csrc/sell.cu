@@ -178,10 +178,10 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   const int n = P->A.n;
   const int nwin = (n + TB - 1) / TB;
   P->nchunks = (n + SELL_C - 1) / SELL_C;
-  GSK_CUDA(cudaMalloc(&P->clen, sizeof(int) * P->nchunks));
-  GSK_CUDA(cudaMalloc(&P->cptr, sizeof(int) * (P->nchunks + 1)));
-  GSK_CUDA(cudaMalloc(&P->roff, (size_t)P->nchunks * SELL_C));
-  GSK_CUDA(cudaMalloc(&P->wid, (size_t)nwin));
+  GSK_CUDA(pool_alloc((void**)&P->clen, sizeof(int) * P->nchunks));
+  GSK_CUDA(pool_alloc((void**)&P->cptr, sizeof(int) * (P->nchunks + 1)));
+  GSK_CUDA(pool_alloc((void**)&P->roff, (size_t)P->nchunks * SELL_C));
+  GSK_CUDA(pool_alloc((void**)&P->wid, (size_t)nwin));
   sell_rank_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->roff, P->clen, P->wid);
   GSK_LAUNCHED(1);
   long long tot = 0;
@@ -200,8 +200,8 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
     for (int v : cl) maxlen = std::max(maxlen, v);
   }
   P->sell_maxlen = maxlen;
-  GSK_CUDA(cudaMalloc(&P->scol, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
-  GSK_CUDA(cudaMalloc(&P->sval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_CUDA(pool_alloc((void**)&P->scol, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_CUDA(pool_alloc((void**)&P->sval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
                                        P->cptr, P->roff, P->scol, P->sval, false, P->sell_pad);
   GSK_LAUNCHED(1);
@@ -282,7 +282,7 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&ucount, sizeof(int) * (nch + 1)));
   GSK_CUDA(cudaMalloc(&fail, sizeof(int)));
   GSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
-  GSK_CUDA(cudaMalloc(&P->dptr, sizeof(int) * (nch + 1)));
+  GSK_CUDA(pool_alloc((void**)&P->dptr, sizeof(int) * (nch + 1)));
   sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, nullptr, nullptr, nullptr, fail, 0, P->sell_pad);
   GSK_LAUNCHED(1);
   int hfail = 0;
@@ -291,7 +291,7 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
   if (hfail) {  // some chunk has > 32 distinct deltas: keep plain int32 columns
     cudaFree(ucount);
     cudaFree(fail);
-    cudaFree(P->dptr);
+    pool_release(P->dptr);  // the stream was synchronised above
     P->dptr = nullptr;
     return GSK_OK;
   }
@@ -300,8 +300,8 @@ int sell_dict_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMemcpyAsync(&tot, P->dptr + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   P->ndict = tot;
-  GSK_CUDA(cudaMalloc(&P->dict, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
-  GSK_CUDA(cudaMalloc(&P->sidx, (size_t)(P->nslots > 0 ? P->nslots : 1)));
+  GSK_CUDA(pool_alloc((void**)&P->dict, sizeof(int) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_CUDA(pool_alloc((void**)&P->sidx, (size_t)(P->nslots > 0 ? P->nslots : 1)));
   sell_dict_kernel<<<grid, TB, 0, s>>>(nch, P->cptr, P->scol, P->roff, ucount, P->dptr, P->dict, P->sidx, fail, 1, P->sell_pad);
   GSK_LAUNCHED(1);
   GSK_CUDA(cudaStreamSynchronize(s));
@@ -421,8 +421,8 @@ int sellu_build(gsk_plan* P, cudaStream_t s) {
   GSK_CUDA(cudaMalloc(&ucnt, sizeof(int) * (nch + 1)));
   GSK_CUDA(cudaMalloc(&fail, sizeof(int)));
   GSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s));
-  GSK_CUDA(cudaMalloc(&P->udel, sizeof(int) * (size_t)nch * SELLU_MAXL));
-  GSK_CUDA(cudaMalloc(&P->umask, sizeof(unsigned) * (size_t)nch * SELLU_MAXL));
+  GSK_CUDA(pool_alloc((void**)&P->udel, sizeof(int) * (size_t)nch * SELLU_MAXL));
+  GSK_CUDA(pool_alloc((void**)&P->umask, sizeof(unsigned) * (size_t)nch * SELLU_MAXL));
   sellu_meta_kernel<<<grid, TB, 0, s>>>(P->A.n, nch, P->A.row_ptr, P->A.col_idx, P->roff, ucnt, P->udel, P->umask,
                                         fail);
   GSK_LAUNCHED(1);
@@ -432,7 +432,7 @@ int sellu_build(gsk_plan* P, cudaStream_t s) {
   long long tot = 0;
   int rc = GSK_OK;
   if (!hfail) {
-    GSK_CUDA(cudaMalloc(&P->uptr, sizeof(int) * (nch + 1)));
+    GSK_CUDA(pool_alloc((void**)&P->uptr, sizeof(int) * (nch + 1)));
     rc = sell_scan(nch, ucnt, P->uptr, SELL_C, s, &tot);
   }
   cudaFree(ucnt);
@@ -441,14 +441,14 @@ int sellu_build(gsk_plan* P, cudaStream_t s) {
   // overflow): the plan keeps plain int32 columns
   if (hfail || rc != GSK_OK) {
     for (void* b : {(void*)P->udel, (void*)P->umask, (void*)P->uptr})
-      if (b) cudaFree(b);
+      pool_release(b);  // cudaFree(ucnt) above synchronised the device
     P->udel = nullptr;
     P->umask = nullptr;
     P->uptr = nullptr;
     return GSK_OK;
   }
   P->nuslots = tot;
-  GSK_CUDA(cudaMalloc(&P->uval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
+  GSK_CUDA(pool_alloc((void**)&P->uval, sizeof(double) * (size_t)(tot > 0 ? tot : 1)));
   GSK_TRY(sellu_fill_values(P, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   P->sell.uptr = P->uptr;
