@@ -64,6 +64,8 @@ def _lib():
         lib.orc_set_fault.restype = None
         lib.orc_sell_uniform.argtypes = [i64, i32, i32, i32] + [vp] * 8
         lib.orc_sell_uniform.restype = i64
+        lib.orc_row_classes.argtypes = [i64, vp, vp, vp, i32, i32, vp, vp, vp, vp]
+        lib.orc_row_classes.restype = i64
         lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, vp, d, i32, vp, vp,
                                      ctypes.POINTER(Report)]
         lib.orc_bicgstab.restype = i32
@@ -210,6 +212,25 @@ def sell_uniform(row_ptr, col, val, S, C=32, sigma=256, maxu=8):
                             *(_p(out[k]) for k in ("uptr", "udel", "umask", "uval")))
     out["uval"] = out["uval"][:tot]
     return out
+
+
+def row_classes(row_ptr, col, val, maxlen=8, maxcls=4096):
+    """Row-class dictionary of a CSR matrix (oracle.cpp, "RCD"): rows with the same
+    length, deltas col - row and bit-identical values share a class, numbered by first
+    occurrence.  Returns {"cls" uint16 [n], "len" int32 [K], "delta" int32 [K, maxlen],
+    "val" float64 [K, maxlen]} or None when a row is longer than maxlen or there are more
+    than maxcls classes."""
+    row_ptr, col, val = _i32(row_ptr), _i32(col), _f64(val)
+    n = row_ptr.size - 1
+    cls = np.zeros(n, np.uint16)
+    dlen = np.zeros(maxcls, np.int32)
+    ddel = np.zeros((maxcls, maxlen), np.int32)
+    dval = np.zeros((maxcls, maxlen), np.float64)
+    k = _lib().orc_row_classes(n, _p(row_ptr), _p(col), _p(val), maxlen, maxcls,
+                               _p(cls), _p(dlen), _p(ddel), _p(dval))
+    if k < 0:
+        return None
+    return {"cls": cls, "len": dlen[:k].copy(), "delta": ddel[:k].copy(), "val": dval[:k].copy()}
 
 
 FAULTS = {"none": 0, "rho0": 1, "omega0": 2, "nan": 3}

@@ -353,6 +353,52 @@ int64_t orc_sell_uniform(int64_t n, int C, int sigma, int maxu, const uint8_t* r
   return tot;
 }
 
+// ---- Row-class dictionary (storage format of the GPU path; DESIGN.md §5 "RCD") ----------
+// The paper's test problems have piecewise-constant coefficients (PAPER.md:269-294,
+// 328-347, 878-895): whole regions of the grid share one stencil row, before and after
+// GS(p).  Two rows are of the same class when they have the same length, the same
+// deltas col - row and bit-identical values, entry by entry in CSR order.  Classes are
+// numbered by first occurrence in ascending row order; class k's entry holds its length,
+// deltas and values (unused places 0).  Inapplicable (-1) when some row has more than
+// maxlen entries or there are more than maxcls classes.  Outputs (nullable to only
+// count): cls [n], dlen [maxcls], ddel / dval [maxcls * maxlen].  Returns the class count.
+int64_t orc_row_classes(int64_t n, const int32_t* rp, const int32_t* ci, const double* v, int maxlen,
+                        int maxcls, uint16_t* cls, int32_t* dlen, int32_t* ddel, double* dval) {
+  std::vector<int64_t> rep;  // first row of every class, in order of appearance
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t a = rp[i], len = rp[i + 1] - a;
+    if (len > maxlen) return -1;
+    int64_t k = 0;
+    for (; k < (int64_t)rep.size(); ++k) {  // plain linear search over the classes so far
+      const int64_t r = rep[k];
+      if (rp[r + 1] - rp[r] != len) continue;
+      bool same = true;
+      for (int32_t q = 0; q < len && same; ++q) {
+        same = ((int64_t)ci[a + q] - i == (int64_t)ci[rp[r] + q] - r) &&
+               std::memcmp(&v[a + q], &v[rp[r] + q], sizeof(double)) == 0;
+      }
+      if (same) break;
+    }
+    if (k == (int64_t)rep.size()) {
+      if ((int64_t)rep.size() == maxcls) return -1;
+      rep.push_back(i);
+    }
+    if (cls) cls[i] = (uint16_t)k;
+  }
+  if (dlen) {
+    for (int64_t k = 0; k < (int64_t)rep.size(); ++k) {
+      const int64_t r = rep[k];
+      const int32_t len = rp[r + 1] - rp[r];
+      dlen[k] = len;
+      for (int q = 0; q < maxlen; ++q) {
+        ddel[k * maxlen + q] = q < len ? (int32_t)((int64_t)ci[rp[r] + q] - r) : 0;
+        dval[k * maxlen + q] = q < len ? v[rp[r] + q] : 0.0;
+      }
+    }
+  }
+  return (int64_t)rep.size();
+}
+
 // ---- Bi-CGSTAB (van der Vorst 1992, cited PAPER.md:102) ----------------------------
 // DESIGN.md §4 algorithm B, arithmetic AC-6; stopping PAPER.md:302-307 (reading B1/B2:
 // strict <, frame weights w optional); breakdown exact-zero tests (PAPER.md:315-321,

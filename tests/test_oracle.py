@@ -604,3 +604,82 @@ def test_fault_hook_verdicts(kind, k):
         assert np.isnan(h[k])
     x2, h2, _ = oracle.bicgstab(s["row_ptr"], s["col"], vo, bo, 1e-8, 2000)
     assert np.array_equal(h2, h0) and np.array_equal(x2, x0)
+
+
+def _decode_classes(R, n):
+    """CSR arrays decoded from a row-class dictionary."""
+    rp, cols, vals = [0], [], []
+    for r in range(n):
+        k = int(R["cls"][r])
+        L = int(R["len"][k])
+        cols += [r + int(d) for d in R["delta"][k, :L]]
+        vals += list(R["val"][k, :L])
+        rp.append(len(cols))
+    return np.array(rp), np.array(cols), np.array(vals)
+
+
+@pytest.mark.parametrize("name,N,p,ncls", [("C1", None, 2, 14), ("C3", 16, 2, None), ("C4", 20, 0, None),
+                                           ("C4", 64, 2, 99), ("P4", 12, 1, None), ("lap3d", 8, 0, 27)])
+def test_row_classes_round_trip(name, N, p, ncls):
+    """Row-class dictionary (oracle.cpp "RCD"; the paper's piecewise-constant problems,
+    PAPER.md:269-294): lossless — decoding cls + dictionary gives back every row's columns
+    and bit-identical values in CSR order; classes are numbered by first occurrence; the
+    class count is what the geometry fixes (a Laplacian on a box: 3^3 boundary types; C1:
+    pinned by an independent np.unique over (len, deltas, value bits))."""
+    s = workloads.generate(name, N=N)
+    val = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], p)[0] if p else s["val"]
+    R = oracle.row_classes(s["row_ptr"], s["col"], val)
+    assert R is not None
+    rp, cols, vals = _decode_classes(R, s["n"])
+    assert np.array_equal(rp, s["row_ptr"]) and np.array_equal(cols, s["col"])
+    assert np.array_equal(vals.view(np.uint64), np.ascontiguousarray(val).view(np.uint64))
+    # first-occurrence numbering: the first row of class k has no smaller class after it
+    first = np.full(len(R["len"]), s["n"])
+    np.minimum.at(first, R["cls"], np.arange(s["n"]))
+    assert np.all(np.diff(first) > 0) and first[0] == 0
+    # unused dictionary places are zero
+    for k, L in enumerate(R["len"]):
+        assert np.all(R["delta"][k, L:] == 0) and np.all(R["val"][k, L:] == 0.0)
+    # independent count of the distinct rows
+    ln = np.diff(s["row_ptr"])
+    K = 8
+    key = np.zeros((s["n"], 1 + 2 * K), np.uint64)
+    rows = np.repeat(np.arange(s["n"]), ln)
+    pos = np.arange(len(s["col"])) - np.repeat(s["row_ptr"][:-1], ln)
+    key[:, 0] = ln
+    key[rows, 1 + pos] = (s["col"] - rows).astype(np.int64).view(np.uint64)
+    key[rows, 1 + K + pos] = np.ascontiguousarray(val).view(np.uint64)
+    assert len(np.unique(key, axis=0)) == len(R["len"])
+    if ncls is not None:
+        assert len(R["len"]) == ncls
+
+
+def test_row_classes_constructed_and_inapplicable():
+    """A hand-built system pins the encoding entry by entry; -0.0 and +0.0 are different
+    values (bit patterns, not ==); a row longer than maxlen, or more classes than maxcls
+    (C2: the velocity depends on the node), make the format inapplicable."""
+    # 6 rows: entries (r-1: -1.0), (r: d_r), (r+1: -1.0) inside [0, 6); d = 2,2,2,3,2,2
+    d = [2.0, 2.0, 2.0, 3.0, 2.0, 2.0]
+    rp, cols, vals = [0], [], []
+    for r in range(6):
+        for c, v in ((r - 1, -1.0), (r, d[r]), (r + 1, -1.0)):
+            if 0 <= c < 6:
+                cols.append(c)
+                vals.append(v)
+        rp.append(len(cols))
+    R = oracle.row_classes(np.array(rp), np.array(cols), np.array(vals), maxlen=4)
+    # classes by first occurrence: 0 = first row (no left), 1 = interior d=2, 2 = d=3, 3 = last row
+    assert list(R["cls"]) == [0, 1, 1, 2, 1, 3]
+    assert list(R["len"]) == [2, 3, 3, 2]
+    assert R["delta"].tolist() == [[0, 1, 0, 0], [-1, 0, 1, 0], [-1, 0, 1, 0], [-1, 0, 0, 0]]
+    assert R["val"].tolist() == [[2.0, -1.0, 0, 0], [-1.0, 2.0, -1.0, 0], [-1.0, 3.0, -1.0, 0], [-1.0, 2.0, 0, 0]]
+    # signed zero: row 4's diagonal -0.0 vs row 1's would-be +0.0 are distinct classes
+    v2 = np.array(vals)
+    v2[rp[1] + 1] = 0.0
+    v2[rp[2] + 1] = -0.0
+    R2 = oracle.row_classes(np.array(rp), np.array(cols), v2, maxlen=4)
+    assert R2["cls"][1] != R2["cls"][2]
+    assert oracle.row_classes(np.array(rp), np.array(cols), np.array(vals), maxlen=2) is None
+    assert oracle.row_classes(np.array(rp), np.array(cols), np.array(vals), maxlen=4, maxcls=3) is None
+    s = workloads.generate("C2", N=96)
+    assert oracle.row_classes(s["row_ptr"], s["col"], s["val"]) is None
