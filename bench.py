@@ -75,9 +75,13 @@ def parse():
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "split", "split4"])
     ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
                     help="GMRES orthogonalisation (MGS: north star; CGS2: the paper's AZTEC)")
-    ap.add_argument("--sell-index", default="plain", choices=["plain", "dict", "uniform"],
-                    help="SELL column indices: int32 per slot (plain), the SELL-D per-chunk delta dictionary, "
-                         "or SELL-U chunk-uniform deltas (DESIGN.md §5)")
+    ap.add_argument("--sell-index", default="classes", choices=["plain", "dict", "uniform", "classes"],
+                    help="SELL plan encoding: the row-class dictionary (classes, the default: a 2-byte class id per "
+                         "row instead of slot data where the rows repeat, else plain), int32 columns per slot "
+                         "(plain), the SELL-D per-chunk delta dictionary, or SELL-U chunk-uniform deltas "
+                         "(DESIGN.md §5); all bit-identical")
+    ap.add_argument("--no-plain-compare", action="store_true",
+                    help="skip the extra.sell_plain comparison run (one step on plain SELL-C-32-256 slots)")
     ap.add_argument("--fmt", default="sell", choices=["csr", "sell"],
                     help="plan layout built on the device from the CSR input (SELL-C-32-256 is faster "
                          "on every config: DESIGN.md §7)")
@@ -145,9 +149,11 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def byte_model(n, nnz):
-    """Algorithmic bytes per launch; B_A = 12 nnz + 4(n+1)."""
-    BA = 12 * nnz + 4 * (n + 1)
+def byte_model(n, nnz, rcd=False):
+    """Algorithmic bytes per launch; B_A = 12 nnz + 4(n+1),
+    or 2 n with the row-class dictionary (a uint16 class id per row; the class lines
+    stay in L1)."""
+    BA = 2 * n if rcd else 12 * nnz + 4 * (n + 1)
     return {"spmv": BA + 16 * n, "gs": 16 * nnz + 4 * (n + 1) + 24 * n,
             # fused schedule: P1 gathers r, p, v and writes p, v (+ r^ own row); P2 r, v -> t
             "bicg_p1": BA + 48 * n, "bicg_p2": BA + 24 * n,
@@ -155,6 +161,7 @@ def byte_model(n, nnz):
             "bicg_s1": BA + 24 * n, "bicg_s3": BA + 16 * n,
             # four-pass schedule: S1q gathers q, r (p = r + beta q), reads r^, writes p, v
             "bicg_s1q": BA + 40 * n,
+            "bicg_s4": 56 * n, "bicg_p3": 64 * n,
             "bicg_iter": 2 * BA + 17 * 8 * n, "bicg_iter_split": 2 * BA + 19 * 8 * n,
             # GMRES S_j: w = A v_j as a plain SpMV pass (its h_1j dot is a separate pass)
             "gmres_mgs": 32 * n, "gmres_arnoldi": BA + 16 * n}
@@ -234,7 +241,7 @@ def reduce_over_ranks(ms, its, dist, device):
     return float(tmax[0]), float(t[1])
 
 
-def config_desc(args, cfg, s):
+def config_desc(args, cfg, s, ncls=None):
     N = cfg.N if args.N is None else args.N
     if cfg.name == "C4w":
         G = int(s["n"]) // N ** 3
@@ -244,11 +251,17 @@ def config_desc(args, cfg, s):
         wl, grid = f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", f"{N}^{3 if cfg.cfg in (3, 4) else 2}"
     return {"workload": wl, "n": int(s["n"]), "nnz": int(s["nnz"]), "grid": grid,
             "format": ("SELL-C-32-256" if getattr(args, "fmt", "sell") == "sell" else "CSR")
-            + " (built on the device from the CSR input)", "scaling": "GS(2)",
+            + " (built on the device from the CSR input)"
+            + (f"; passes read the plan's row-class dictionary ({ncls} classes: a uint16 class id per row + "
+               "128-byte class lines instead of the slot data; lossless, bit-identical results; DESIGN.md §5)"
+               if ncls else ""), "scaling": "GS(2)",
             "solvers": ["Bi-CGSTAB to tol (maxit %d)" % cfg.maxit,
                         "GMRES(30) for %d iterations (or to tol)" % args.gmres_maxit],
             "tol": cfg.tol, "seed": cfg.seed,
-            "l2": "inputs larger than L2 (matrix %.2f GB > 126 MB)" % ((12 * s["nnz"] + 4 * s["n"]) / 1e9)}
+            "l2": ("inputs larger than L2 (8 solver vectors of %.0f MB + %.0f MB of class ids per Bi-CGSTAB "
+                   "iteration, a %.2f GB GMRES basis > 126 MB)" % (8 * s["n"] / 1e6, 2 * s["n"] / 1e6,
+                                                                   31 * 8 * s["n"] / 1e9)) if ncls else
+                  "inputs larger than L2 (matrix %.2f GB > 126 MB)" % ((12 * s["nnz"] + 4 * s["n"]) / 1e9)}
 
 
 def main():
@@ -284,7 +297,8 @@ def main():
     dbuf = torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
     fmt = args.fmt
-    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth, sell_index=args.sell_index)
+    sidx = args.sell_index if fmt == "sell" else "plain"
+    plan = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth, sell_index=sidx)
     x1 = torch.empty(n, dtype=torch.float64, device="cuda")
     x2 = torch.empty(n, dtype=torch.float64, device="cuda")
 
@@ -297,9 +311,7 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    for k in range(4):
-        plan_probe_reset = plan.probe(k)  # noqa: F841 (probes accumulate; deltas below)
-    probes0 = [plan.probe(k) for k in range(4)]
+    probes0 = [plan.probe(k) for k in range(5)]
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -326,30 +338,64 @@ def main():
         ms, its = reduce_over_ranks(ms, its, dist, "cuda")
     value = its / (ms / 1e3)
 
-    # dominant kernel: per-launch time from the CUDA-event probes inside the timed steps
+    # dominant kernel: per-launch times from the CUDA-event probes inside the timed steps;
+    # the roofline object reports the probed kernel with the largest share of the step
+    NP = 5
     probes = []
-    for k in range(4):
+    for k in range(NP):
         tot, cnt = plan.probe(k)
         t0, c0 = probes0[k]
         dc = cnt - c0
         probes.append(((tot * cnt - t0 * c0) / dc) if dc > 0 else None)
-    bm = byte_model(n, nnz)
+    try:
+        ncls = plan.num_classes() if fmt == "sell" else -1
+    except Exception:
+        ncls = -1
+    rcd = ncls > 0
+    bm = byte_model(n, nnz, rcd)
     hbm, src = peaks()
-    p1_ms = probes[0]
-    roof = None
     sched = plan_schedule(args, n, nnz)
-    if p1_ms:
-        key, kname, kshort = {
-            "split": ("bicg_s1", "pass_kernel<SELL, OpS1> (v = A p, <r^,v>)", "pass_kernel<2,1,OpS1>"),
-            "split4": ("bicg_s1q", "pass_kernel<SELL, OpS1q> (p = r + beta q at the gather, v = A p, <r^,v>)",
-                       "pass_kernel<2,1,OpS1q>"),
-            "fused": ("bicg_p1", "pass_kernel<SELL, OpP1> (p update at the gather, v = A p, <r^,v>)",
-                      "pass_kernel<2,1,OpP1>")}[sched]
-        ach = bm[key] / (p1_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": ncu_traffic(kshort),
-                "kernel": kname, "bytes_per_launch": bm[key], "ms_per_launch": p1_ms,
-                "peak_source": src, "frac_of_8TBps": ach / 8000.0}
+    F = 5 if rcd else (2 if fmt == "sell" else 1)
+    r1l, r2l = reps[-1]
+    its_b, its_g = r1l["iterations"], r2l["iterations"]
+    # MGS projection passes of a GMRES(m) run of its_g steps: step j of a cycle has j - 1
+    full, rest = divmod(its_g, m)
+    n_mgs = full * (m * (m - 1) // 2) + rest * (rest - 1) // 2
+    vkey, vname, vshort = {
+        "split": ("bicg_s1", f"pass_kernel<{F},1,OpS1> (v = A p, <r^,v>)", f"pass_kernel<{F},1,OpS1>"),
+        "split4": ("bicg_s1q", f"pass_kernel<{F},1,OpS1q> (p = r + beta q at the gather, v = A p, <r^,v>)",
+                   f"pass_kernel<{F},1,OpS1q>"),
+        "fused": ("bicg_p1", f"pass_kernel<{F},1,OpP1> (p update at the gather, v = A p, <r^,v>)",
+                  f"pass_kernel<{F},1,OpP1>")}[sched]
+    ukey, uname, ushort = {
+        "split": ("bicg_s4", "pass_kernel<0,4,OpS4> (x, r update, 3 dots)", "pass_kernel<0,4,OpS4>"),
+        "split4": ("bicg_s4", "pass_kernel<0,4,OpS4q> (x, r, q update, 3 dots)", "pass_kernel<0,4,OpS4q>"),
+        "fused": ("bicg_p3", "pass_kernel<0,4,OpP3> (x, r update, 3 dots)", "pass_kernel<0,4,OpP3>")}[sched]
+    cands = [
+        (vkey, vname, vshort, probes[0], its_b),
+        ("bicg_p2" if sched == "fused" else "bicg_s3",
+         f"pass_kernel<{F},1,{'OpP2' if sched == 'fused' else 'OpS3'}> (t = A s, <t,s>, <t,t>)",
+         f"pass_kernel<{F},1,{'OpP2' if sched == 'fused' else 'OpS3'}>", probes[1], its_b),
+        (ukey, uname, ushort, probes[4], its_b),
+        ("gmres_arnoldi", f"pass_kernel<{F},1,OpCgsS> (GMRES w = A v_j)", f"pass_kernel<{F},1,OpCgsS>", probes[3], its_g),
+    ]
+    if args.orth == "mgs":
+        cands.append(("gmres_mgs", "pass_kernel<0,4,OpMgs> (GMRES MGS: w -= h v_i, <w,v_{i+1}>)",
+                      "pass_kernel<0,8,OpMgs>", probes[2], n_mgs))
+    step_ms_last = step_ms[-1]
+    roofs = []
+    for key, kname, kshort, p_ms, count in cands:
+        if not p_ms:
+            continue
+        ach = bm[key] / (p_ms / 1e3) / 1e9
+        roofs.append({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                      "traffic": ncu_traffic(kshort), "kernel": kname, "bytes_per_launch": bm[key],
+                      "ms_per_launch": p_ms, "launches_per_step": count,
+                      "share_of_step": p_ms * count / step_ms_last, "peak_source": src,
+                      "frac_of_8TBps": ach / 8000.0})
+    roofs.sort(key=lambda r: -r["share_of_step"])
+    roof = roofs[0] if roofs else None
+    p1_ms = probes[0]
 
     # SpMV standalone roofline (same plan, 50 back-to-back launches)
     x = torch.tensor(workloads.uniform(n, 9, 9), device="cuda")
@@ -397,7 +443,10 @@ def main():
         "gs2": {"ms": gs_ms, "gbps": gs_gbps, "bytes": bm["gs"], "frac_of_hbm": gs_gbps / hbm,
                 "frac_of_8TBps": gs_gbps / 8000.0},
         "probe_ms": {"bicg_v_pass": probes[0], "bicg_t_pass": probes[1], "gmres_mgs": probes[2],
-                     "gmres_arnoldi_spmv": probes[3]},
+                     "gmres_arnoldi_spmv": probes[3], "bicg_update_pass": probes[4]},
+        "roofline_all": roofs,
+        "encoding": {"sell_index": args.sell_index, "row_classes": ncls if rcd else None,
+                     "matrix_bytes_per_spmv": bm["spmv"] - 16 * n},
         "probe_gbps": {"bicg_v_pass": bm[{"split": "bicg_s1", "split4": "bicg_s1q", "fused": "bicg_p1"}[sched]]
                        / (probes[0] / 1e3) / 1e9
                        if probes[0] else None,
@@ -408,6 +457,23 @@ def main():
                        if probes[3] else None},
     }
 
+    if rcd and not args.no_plain_compare:
+        # the same two solves on the plain SELL-C-32-256 slots (one warm-up, one timed)
+        pp = gsk.Plan(As, fmt=fmt, schedule=args.schedule, orth=args.orth, sell_index="plain")
+        for _ in range(2):
+            _, _, q1 = pp.bicgstab(bbuf, tol=cfg.tol, maxit=cfg.maxit, x=x1, hist=False)
+            _, _, q2 = pp.gmres(bbuf, m=m, tol=cfg.tol, maxit=gmaxit, x=x2, hist=False)
+        bmp = byte_model(n, nnz, False)
+        pv = pp.probe(0)[0]
+        extra["sell_plain"] = {
+            "iters_per_s": (q1["iterations"] + q2["iterations"]) / ((q1["solve_ms"] + q2["solve_ms"]) / 1e3),
+            "bicgstab_iters_per_s": q1["iterations"] / (q1["solve_ms"] / 1e3),
+            "gmres_iters_per_s": q2["iterations"] / (q2["solve_ms"] / 1e3),
+            "bicgstab_iterations": q1["iterations"], "gmres_iterations": q2["iterations"],
+            "bicg_v_pass_ms": pv, "bicg_v_pass_gbps": bmp[vkey] / (pv / 1e3) / 1e9 if pv else None,
+            "bicg_v_pass_frac_of_hbm": bmp[vkey] / (pv / 1e3) / 1e9 / hbm if pv else None,
+            "same_iterations": q1["iterations"] == r1["iterations"] and q2["iterations"] == r2["iterations"]}
+        pp.close()
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args, dist)
@@ -417,7 +483,7 @@ def main():
         cpu = {"value": v, "unit": "iters/s", "cores": cores, "kind": "oracle",
                "sample": f"GS(2) + 8 Bi-CGSTAB its + 8 GMRES(30) steps of {cfg.name} ({dt:.1f} s)"}
     if not args.no_time_to_tol and rank == 0:
-        extra["time_to_tol"] = time_to_tol(gsk, torch, s, cfg, fmt)
+        extra["time_to_tol"] = time_to_tol(gsk, torch, s, cfg, fmt, sidx=sidx)
 
     if rank == 0:
         line = {
@@ -425,7 +491,7 @@ def main():
             "unit": "iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_desc(args, cfg, s),
+            "config": config_desc(args, cfg, s, ncls if rcd else None),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "extra": extra,
         }
@@ -469,11 +535,12 @@ def run_sharded(args, rank, world, local):
     b0 = torch.tensor(s["b"], device="cuda")
     vbuf, bbuf, dbuf = torch.empty_like(A0.val), torch.empty_like(b0), torch.empty_like(b0)
     As, bs, _ = gsk.gs_scale(A0, b0, 2, out=(vbuf, bbuf, dbuf))
+    sidx = args.sell_index if fmt == "sell" else "plain"
     if weak:
-        SP = gsk.ShardedPlan(As, fmt=fmt, comm=comm, n_global=n_glob, peer_reduce=args.peer)
+        SP = gsk.ShardedPlan(As, fmt=fmt, comm=comm, n_global=n_glob, peer_reduce=args.peer, sell_index=sidx)
         bl = bbuf
     else:
-        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, peer_reduce=args.peer)
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, peer_reduce=args.peer, sell_index=sidx)
         lo, hi = SP.rows
         bl = bbuf[lo:hi]
     x1 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
@@ -532,7 +599,11 @@ def run_sharded(args, rank, world, local):
     tot, cnt = SP.probe(0)
     t0, c0 = probes0[0]
     p_ms = (tot * cnt - t0 * c0) / (cnt - c0) if cnt > c0 else None
-    bm = byte_model(h0 - l0, nnz0)
+    try:
+        ncls = SP.num_classes() if fmt == "sell" else -1
+    except Exception:
+        ncls = -1
+    bm = byte_model(h0 - l0, nnz0, ncls > 0)
     hbm, src = peaks()
     roof = None
     if p_ms:
@@ -547,7 +618,8 @@ def run_sharded(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if weak else ("strong" if world > 1 else "none (emulated shards on one GPU)"),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**config_desc(args, cfg, s_desc), "parallelism": f"rows/{P}", "shards": P,
+            "config": {**config_desc(args, cfg, s_desc, ncls if ncls > 0 else None), "parallelism": f"rows/{P}",
+                       "shards": P,
                        "placement": (f"{world} GPUs, NCCL halos + all-gathers" if world > 1
                                      else "all shards on one GPU (device-copy halos)")
                        + ("; each rank generates and holds only its own 256^3 block (local input)"
@@ -586,7 +658,7 @@ def measure_e2e(gsk, torch, s, cfg, m, gmaxit, fmt, args, dist=None):
         dev = {k: v.to("cuda", non_blocking=True) for k, v in pin.items()}
         A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
         As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
-        P = gsk.Plan(As, fmt=fmt)
+        P = gsk.Plan(As, fmt=fmt, sell_index=args.sell_index if fmt == "sell" else "plain")
         x1, _, r1 = P.bicgstab(bs, tol=cfg.tol, maxit=cfg.maxit, hist=False)
         x2, _, r2 = P.gmres(bs, m=m, tol=cfg.tol, maxit=gmaxit, hist=False)
         xo1.copy_(x1, non_blocking=True)
@@ -636,7 +708,8 @@ def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist,
         dev = {k: v.to("cuda", non_blocking=True) for k, v in pin.items()}
         A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
         As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
-        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, n_global=n_global, peer_reduce=args.peer)
+        SP = gsk.ShardedPlan(As, shards=P, fmt=fmt, comm=comm, n_global=n_global, peer_reduce=args.peer,
+                             sell_index=args.sell_index if fmt == "sell" else "plain")
         x1, _, r1 = SP.bicgstab(bs[lo:hi], tol=cfg.tol, maxit=cfg.maxit, hist=False)
         x2, _, r2 = SP.gmres(bs[lo:hi], m=m, tol=cfg.tol, maxit=gmaxit, hist=False)
         xo1.copy_(x1, non_blocking=True)
@@ -673,7 +746,7 @@ def measure_e2e_sharded(gsk, torch, s, cfg, m, gmaxit, fmt, args, P, comm, dist,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms / k, "steps": k}
 
 
-def time_to_tol(gsk, torch, s, cfg, fmt, m=30):
+def time_to_tol(gsk, torch, s, cfg, fmt, m=30, sidx="plain"):
     """Time to cfg.tol with and without GS (north-star metric; the paper times both
     solvers): Bi-CGSTAB and GMRES(m) from the device-resident
     unscaled system — scaling + plan (SELL build) + solve, CUDA events — for no
@@ -681,11 +754,11 @@ def time_to_tol(gsk, torch, s, cfg, fmt, m=30):
     frame for every variant; GMRES stops on its least-squares
     estimate in the solved frame (reading B2) and reports the GS(2)-frame true
     residual."""
-    return {"bicgstab": _time_to_tol(gsk, torch, s, cfg, fmt, None),
-            f"gmres({m})": _time_to_tol(gsk, torch, s, cfg, fmt, m)}
+    return {"bicgstab": _time_to_tol(gsk, torch, s, cfg, fmt, None, sidx),
+            f"gmres({m})": _time_to_tol(gsk, torch, s, cfg, fmt, m, sidx)}
 
 
-def _time_to_tol(gsk, torch, s, cfg, fmt, m):
+def _time_to_tol(gsk, torch, s, cfg, fmt, m, sidx="plain"):
     out = {}
     A0 = gsk.CSR.from_system(s)
     b0 = torch.tensor(s["b"], device="cuda")
@@ -702,7 +775,7 @@ def _time_to_tol(gsk, torch, s, cfg, fmt, m):
         elif p is not None:
             A, b, dp = gsk.gs_scale(A, b, p, inplace=True)
             w = None if p == 2 else d2 / dp
-        P = gsk.Plan(A, fmt=fmt, weights=w)
+        P = gsk.Plan(A, fmt=fmt, weights=w, sell_index=sidx)
         if m is None:
             _, h, r = P.bicgstab(b, tol=cfg.tol, maxit=cfg.maxit, hist=False)
         else:  # the weights only enter the reported true_relres_w

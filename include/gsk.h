@@ -93,7 +93,13 @@ typedef struct gsk_opts {
                            offsets (SELL-U): slot k of a chunk holds each row's entry at
                            delta udel[k] (ascending, <= 8 per chunk; lane masks mark
                            padding), 8 bytes of column data per 32 slots; falls back to
-                           plain columns when some chunk has more deltas */
+                           plain columns when some chunk has more deltas, 3 = row-class
+                           dictionary (RCD): a 2-byte class id per row and one 128-byte
+                           entry per class instead of any slot data, for matrices whose
+                           rows repeat (piecewise-constant coefficients: <= 4096 distinct
+                           rows of <= 8 entries); bit-identical results; falls back to
+                           plain columns when inapplicable; not used by the on-chip,
+                           cooperative and CGS2 tile engines (they read the SELL slots) */
   int32_t engine;       /* how the solvers run (all engines give bit-identical results):
                            GSK_ENGINE_AUTO (default) = one launch for the whole solve on
                            one CTA (Bi-CGSTAB n <= 2048, MGS GMRES n <= 1024) or on one
@@ -173,6 +179,17 @@ int gsk_plan_sell_dict(gsk_plan *plan, int64_t *ndict, int32_t *dict_ptr, int32_
  * entries 0), uval [nuslots] (device, nullable). */
 int gsk_plan_sell_uniform(gsk_plan *plan, int64_t *nuslots, int32_t *uptr, int32_t *udel, uint32_t *umask,
                           double *uval, void *stream);
+/* Row-class dictionary of a plan built with sell_index = 3 (RCD; the
+ * paper's piecewise-constant problems): rows with the same length,
+ * deltas col - row and bit-identical values (CSR order) share a class, numbered by
+ * first occurrence in ascending row order.  *ncls = class count, or -1 when the format
+ * is inapplicable (a row longer than 8 entries, more than 4096 classes) and the plan runs
+ * its plain SELL passes.  cls: DEVICE uint16 [n]; entries: DEVICE [ncls * 128 bytes],
+ * per class double v[8], int32 len, int32 d[8], 28 bytes of zero padding (unused places
+ * 0).  Outputs nullable.  The classes are rebuilt by gsk_plan_refresh.  A sharded plan
+ * answers the count only (cls = entries = NULL): the largest class count of this
+ * process's shards, or -1 if one of them runs its plain SELL passes. */
+int gsk_plan_row_classes(gsk_plan *plan, int64_t *ncls, uint16_t *cls, void *entries, void *stream);
 void gsk_plan_destroy(gsk_plan *plan);
 
 /* Bi-CGSTAB (van der Vorst 1992) on A x = b.
@@ -202,7 +219,8 @@ int gsk_plan_residual_norm(gsk_plan *plan, const double *b, const double *x, con
  * dominant kernel family of the last solve on this plan, sampled with CUDA events
  * around one launch per captured batch.  kind: 0 = Bi-CGSTAB fused SpMV pass
  * (v = A p), 1 = Bi-CGSTAB fused SpMV pass (t = A s), 2 = GMRES MGS projection
- * pass.  Returns samples in *count. */
+ * pass, 3 = GMRES Arnoldi SpMV pass (w = A v_j), 4 = Bi-CGSTAB x / r update pass.
+ * Returns samples in *count. */
 int gsk_plan_probe(gsk_plan *plan, int kind, double *avg_ms, int64_t *count);
 
 /* ---- Row-block sharding ------------------

@@ -24,7 +24,7 @@ ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
 SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
-           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_sell_uniform", "gsk_plan_destroy",
+           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_sell_uniform", "gsk_plan_row_classes", "gsk_plan_destroy",
            "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
            "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
            "gsk_shard_rows", "gsk_shard_halo_host", "gsk_plan_create_sharded", "gsk_nccl_unique_id",
@@ -93,6 +93,7 @@ def load(path: str = LIB_PATH):
     lib.gsk_plan_sell_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     lib.gsk_plan_sell_dict.argtypes = [vp, P(i64), vp, vp, vp, vp]
     lib.gsk_plan_sell_uniform.argtypes = [vp, P(i64), vp, vp, vp, vp, vp]
+    lib.gsk_plan_row_classes.argtypes = [vp, P(i64), vp, vp, vp]
     lib.gsk_plan_destroy.argtypes = [vp]
     lib.gsk_plan_destroy.restype = None
     lib.gsk_bicgstab_solve.argtypes = [P(CsrStruct), vp, vp, d, i32, vp, vp, P(Report), vp]
@@ -253,6 +254,9 @@ def launch_count() -> int:
     return int(load().gsk_launch_count())
 
 
+SELL_INDEX = {"plain": 0, "dict": 1, "uniform": 2, "classes": 3}
+
+
 class Plan:
     """gsk_plan: SELL build, workspace and captured graphs reused across solves."""
 
@@ -268,7 +272,7 @@ class Plan:
         self.A = A
         self.weights = _dev_f64(weights, A.n)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE[schedule], ORTH[orth], {"plain": 0, "dict": 1, "uniform": 2}[sell_index], ENGINE[engine])
+                    SCHEDULE[schedule], ORTH[orth], SELL_INDEX[sell_index], ENGINE[engine])
         self._csr = A.struct()
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))
@@ -337,6 +341,29 @@ class Plan:
         res["dict"] = res["dict"][:nd.value]
         res["sidx"] = res["sidx"][:nsl.value]
         return res
+
+    def row_classes(self):
+        """The plan's row-class dictionary (sell_index="classes"; None when inapplicable):
+        {"cls" uint16 [n], "len" [K], "delta" [K, 8], "val" [K, 8]}."""
+        lib = load()
+        k = ctypes.c_int64()
+        _check(lib.gsk_plan_row_classes(self.h, ctypes.byref(k), None, None, _stream()))
+        if k.value < 0:
+            return None
+        cls = torch.empty(self.A.n, dtype=torch.int16, device="cuda")
+        ent = torch.empty(max(k.value, 1) * 128, dtype=torch.uint8, device="cuda")
+        _check(lib.gsk_plan_row_classes(self.h, ctypes.byref(k), _ptr(cls), _ptr(ent), _stream()))
+        rec = ent.cpu().numpy()[:k.value * 128].view(
+            np.dtype([("v", "<f8", 8), ("len", "<i4"), ("d", "<i4", 8), ("pad", "<i4", 7)]))
+        assert not rec["pad"].any()
+        return {"cls": cls.cpu().numpy().view(np.uint16), "len": rec["len"].copy(),
+                "delta": rec["d"].copy(), "val": rec["v"].copy()}
+
+    def num_classes(self) -> int:
+        """Classes of the plan's row-class dictionary (-1: not built or inapplicable)."""
+        k = ctypes.c_int64()
+        _check(load().gsk_plan_row_classes(self.h, ctypes.byref(k), None, None, _stream()))
+        return k.value
 
     def sell_uniform(self):
         """The plan's SELL-U arrays (chunk-uniform column deltas; None when not built)."""
@@ -465,7 +492,7 @@ class ShardedPlan(Plan):
         self.nloc = hi - lo
         self.weights = _dev_f64(weights, self.nloc)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE["split"], ORTH["mgs"], {"plain": 0, "dict": 1, "uniform": 2}[sell_index],
+                    SCHEDULE["split"], ORTH["mgs"], SELL_INDEX[sell_index],
                     ENGINE["graph"])
         so = ShardOpts(int(shards), int(first), int(count), int(n_global is not None), ch, int(peer_reduce), 0)
         self._csr = A.struct()

@@ -52,7 +52,7 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
       OpP3 p3{vn, pn, t, rh, w, x, r, P->hist_d, P->bstate, 0, 0, 0};
       rc = run_pass(P, p1, s, ev(0, 0, k), ev(0, 1, k));
       if (rc >= 0) rc = run_pass(P, p2, s, ev(1, 0, k), ev(1, 1, k));
-      if (rc >= 0) rc = run_pass(P, p3, s);
+      if (rc >= 0) rc = run_pass(P, p3, s, ev(4, 0, k), ev(4, 1, k));
     } else if (P->bmode == 3) {  // four-pass schedule: q / p alternate between pa and vb
       double *qs = (k & 1) ? vb : pa, *pd = (k & 1) ? pa : vb;
       double *v = va, *sv = pb;
@@ -63,7 +63,7 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
       rc = run_pass(P, s1, s, ev(0, 0, k), ev(0, 1, k));
       if (rc >= 0) rc = run_pass(P, s2, s);
       if (rc >= 0) rc = run_pass(P, s3, s, ev(1, 0, k), ev(1, 1, k));
-      if (rc >= 0) rc = run_pass(P, s4, s);
+      if (rc >= 0) rc = run_pass(P, s4, s, ev(4, 0, k), ev(4, 1, k));
     } else {  // split 5-pass schedule: p = pa, v = va, s = pb
       double *p = pa, *v = va, *sv = pb;
       OpS0 s0{r, v, p, P->bstate, 0, 0};
@@ -75,7 +75,7 @@ static int capture_bicg(gsk_plan* P, double* x, int K, int copy, cudaGraphExec_t
       if (rc >= 0) rc = run_pass(P, s1, s, ev(0, 0, k), ev(0, 1, k));
       if (rc >= 0) rc = run_pass(P, s2, s);
       if (rc >= 0) rc = run_pass(P, s3, s, ev(1, 0, k), ev(1, 1, k));
-      if (rc >= 0) rc = run_pass(P, s4, s);
+      if (rc >= 0) rc = run_pass(P, s4, s, ev(4, 0, k), ev(4, 1, k));
     }
   }
   return end_capture(s, rc, out, &P->bkernels, "bicgstab");
@@ -194,8 +194,8 @@ static int bicgstab_run(gsk_plan* P, const double* b, const double* x0, double t
   // batches of K iterations; the next batch is queued before the flag of the
   // previous one is read, so the GPU never idles on the host check
   const long long maxb = (maxit + K - 1) / K + 1;
-  const int kinds[2] = {0, 1};
-  GSK_TRY(run_batches(P, P->bgraph, maxb, P->bkernels, &P->bstate->done, kinds, 2));
+  const int kinds[3] = {0, 1, 4};
+  GSK_TRY(run_batches(P, P->bgraph, maxb, P->bkernels, &P->bstate->done, kinds, 3));
   OpFinal<> fin{x, b, P->weights, P->bstate};
   if (run_pass(P, fin, s) < 0) return GSK_E_CUDA;
   GSK_CUDA(cudaEventRecord(P->t1, s));

@@ -13,6 +13,8 @@ constexpr int TB = 256;         // threads per CTA = rows per sub-tile = SELL si
 constexpr int SELL_C = 32;      // SELL chunk height (one warp)
 constexpr int SELL_SIGMA = 256; // SELL sorting window
 constexpr int SELLU_MAXL = 8;   // SELL-U: distinct column deltas per chunk (at most)
+constexpr int RCD_MAXL = 8;      // row-class dictionary: entries per row (at most)
+constexpr int RCD_MAXCLS = 4096; // ... and classes per plan (at most)
 constexpr int CSR_CAP = 1792;   // entries of a 256-row CSR window staged in smem (7 per row)
 constexpr int MAXD = 3;         // max dot products fused into one pass
 
@@ -21,6 +23,17 @@ struct CsrView {
   const int* __restrict__ rp;
   const int* __restrict__ ci;
   const double* __restrict__ v;
+};
+
+// One row class (sell.cu, DESIGN.md §5 "RCD"): the entries shared by every row of the
+// class, in CSR order — values and deltas col - row (unused places 0) — one 128-byte line.
+// The deltas are packed in 8-byte words with the length, {len, d0} {d1, d2} {d3, d4}
+// {d5, d6} {d7, 0}: a pass reads the line with warp-uniform 8-byte loads (one L1 wavefront
+// each; a 16-byte load costs four), four of them for the deltas of rows of <= 7 entries.
+struct __align__(128) RcdEntry {
+  double v[RCD_MAXL];
+  int2 ld[5];  // ld[0] = {len, d0}, ld[k] = {d(2k-1), d(2k)}, ld[4] = {d7, 0}
+  int pad_[6];
 };
 
 struct SellView {
@@ -48,6 +61,10 @@ struct SellView {
   const unsigned* __restrict__ umask;  // [nchunks * SELLU_MAXL]
   const double* __restrict__ uval;     // [nuslots]
   int l2pf;  // > 0: a pass prefetches the matrix data of the window l2pf ahead into L2
+  // optional row-class dictionary (RCD, sell.cu; null: not built or inapplicable): the
+  // class of every row and the classes' entries; the passes then read no slot data
+  const uint16_t* __restrict__ kcls;   // [n]
+  const RcdEntry* __restrict__ kdict;  // [<= RCD_MAXCLS]
 };
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the

@@ -110,12 +110,16 @@ struct SellTuning<Op, std::void_t<decltype(Op::kSellMinBlocks)>> {
 #endif
 constexpr bool SELL_DIRECT = GSK_SELL_DIRECT;
 
-// column-index encoding of a SELL pass format: FMT 2 int32, 3 SELL-D, 4 SELL-U
+// column-index encoding of a SELL pass format: FMT 2 int32, 3 SELL-D, 4 SELL-U, 5 RCD
+// (row-class dictionary: no slot data at all)
 template <int FMT>
 struct SellIdx {
-  static constexpr int value = FMT == 3 ? 1 : FMT == 4 ? 2 : 0;
+  static constexpr int value = FMT == 3 ? 1 : FMT == 4 ? 2 : FMT == 5 ? 3 : 0;
 };
 
+#ifndef GSK_RCD_MINB
+#define GSK_RCD_MINB 4
+#endif
 #ifndef GSK_SHORT_MINB
 #define GSK_SHORT_MINB 5
 #endif
@@ -126,7 +130,8 @@ struct PassOcc {
   // (Measured with dots too, leaves parked by row in shared memory and reduced once
   // per CTA: bit-exact, but S1 unchanged and S3 slower — 80 registers to not spill.)
   static constexpr bool kDirect = SELL_DIRECT && FMT >= 2 && Op::D == 0;
-  static constexpr int kMinBlocks = FMT == 1 ? 4
+  static constexpr int kMinBlocks = FMT == 5 ? GSK_RCD_MINB
+                                  : FMT == 1 ? 4
                                   : FMT == 3 ? (Op::D > 0 && SellTuning<Op>::minb == 4 ? GSK_SELLD_DOT_MINB
                                                                                        : SellTuning<Op>::minb)
                                   : (FMT == 2 || FMT == 4)
@@ -162,6 +167,39 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
   return acc;
 }
 
+// Row-class (RCD) SpMV of row `row` of class `cls` (row >= n: 0): the class line is read
+// with warp-uniform 8-byte loads (nearly every lane of a warp has the same class: one L1
+// wavefront per load), then all gathers, then the AC-3 chain in CSR order.
+// Measured at C4 and not kept (profiles/r02_experiments): two or four windows in flight
+// per thread (-10% / -35%: the pass is bound by the L1 data pipe, ncu lsu wavefronts
+// 80-86%, not by latency); the class line kept in registers across windows with a warp
+// vote (-20%) and the +-1 neighbours taken from the adjacent lanes by shuffle (wavefronts
+// -35%, but 3.4x the instructions: issue-bound, -45%).
+template <class G>
+__device__ __forceinline__ double rcd_row(const SellView& A, int row, int cls, const G& g) {
+  const RcdEntry* e = A.kdict + cls;
+  const int2 q0 = __ldg(&e->ld[0]);
+  const int L = row < A.n ? q0.x : 0;
+  int ds[RCD_MAXL];
+  double xs[RCD_MAXL];
+  ds[0] = q0.y;
+#pragma unroll
+  for (int h = 1; h < 4; ++h) {
+    const int2 q = __ldg(&e->ld[h]);
+    ds[2 * h - 1] = q.x;
+    ds[2 * h] = q.y;
+  }
+  ds[7] = L > 7 ? __ldg(&e->ld[4]).x : 0;
+#pragma unroll
+  for (int k = 0; k < RCD_MAXL; ++k)
+    if (k < L) xs[k] = g(row + ds[k]);
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < RCD_MAXL; ++k)
+    if (k < L) acc = __fma_rn(__ldg(&e->v[k]), xs[k], acc);
+  return acc;
+}
+
 // SELL window core: lane l of warp w computes slot l of chunk r0/32 + w and hands the
 // row's y with its in-window offset to sink(rl, y).  NAT: the window keeps its natural
 // row order (sell.cu), so the slot's row is r0 + t and roff is not read.
@@ -177,6 +215,12 @@ __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, cons
   if (c < A.nchunks) {
     const int rl = NAT ? (t & (TB - 1)) : A.roff[c * SELL_C + lane];
     pre(rl);
+    if constexpr (IDX == 3) {  // RCD (row r0 + t)
+      static_assert(NAT || IDX != 3, "row-class passes finish row r0 + t");
+      const int row = r0 + rl;
+      sink(rl, rcd_row(A, row, row < A.n ? (int)__ldg(A.kcls + row) : 0, g));
+      return;
+    }
     if constexpr (IDX == 2) {
       const int p0 = A.uptr[c], L = (A.uptr[c + 1] - p0) >> 5;  // <= SELLU_MAXL
       // lane k < L holds delta k and its lane mask (two 32-byte loads per chunk)
@@ -267,6 +311,10 @@ template <int IDX>
 __device__ __forceinline__ void sell_prefetch_window(const SellView& A, int r0) {
   const int c0 = r0 >> 5;
   if (c0 >= A.nchunks) return;
+  if constexpr (IDX == 3) {  // the window's class ids (512 bytes)
+    prefetch_l2(A.kcls + r0, sizeof(uint16_t) * (size_t)min(TB, A.n - r0));
+    return;
+  }
   const int c1 = min(c0 + TB / SELL_C, A.nchunks);
   const int* ptr = IDX == 2 ? A.uptr : A.cptr;
   const int s0 = ptr[c0], s1 = ptr[c1];
@@ -442,11 +490,39 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
   constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
   constexpr bool kDirect = PassOcc<FMT, Op>::kDirect;
   using Smem = std::conditional_t<
+      FMT == 5, PassSmemSell<0, true>,
+      std::conditional_t<
       kDirect, PassSmemDirect,
-      std::conditional_t<(FMT >= 2), PassSmemSell<(PassOcc<FMT, Op>::kAsync ? Op::NV : 0), NAT>, PassSmem<FMT>>>;
+      std::conditional_t<(FMT >= 2), PassSmemSell<(PassOcc<FMT, Op>::kAsync ? Op::NV : 0), NAT>, PassSmem<FMT>>>>;
   __shared__ __align__(16) Smem sm;
   const int t = threadIdx.x, warp = t >> 5;
-  if constexpr (kDirect) {
+  if constexpr (FMT == 5) {
+    // RCD: thread t finishes row r0 + t of every window; own-row operands in registers;
+    // the class id of the next window is loaded while this one computes
+    const int rb = bx * wpc * TB;
+    int kn = rb + t < n ? (int)__ldg(sell.kcls + rb + t) : 0;
+    auto g = [&](int col) { return op.gather(col); };
+    for (int w = 0; w < wpc; ++w) {
+      const int r0 = rb + w * TB;
+      double cc[DD];
+#pragma unroll
+      for (int d = 0; d < DD; ++d) cc[d] = 0.0;
+      if (r0 < n) {  // uniform over the CTA
+        const int i = r0 + t;
+        const int kc = kn;
+        double v[NVA];
+        if (i < n) load_vin(op, i, v);
+        kn = (w + 1 < wpc && i + TB < n) ? (int)__ldg(sell.kcls + i + TB) : 0;
+        const double y = rcd_row(sell, i, kc, g);
+        if (i < n) op.row(i, y, v, cc);
+      }
+      if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);
+    }
+    if constexpr (D > 0) {
+      __syncthreads();
+      if (warp == 0) cta_partial<D>(sm.wp, wpc, part, stride, bx);
+    }
+  } else if constexpr (kDirect) {
     const int rb = bx * wpc * TB;
     if (sell.l2pf && wpc >= 4 && threadIdx.x == 0)
       for (int q = 1; q <= sell.l2pf && q < wpc; ++q) sell_prefetch_window<SellIdx<FMT>::value>(sell, rb + q * TB);

@@ -113,8 +113,13 @@ struct gsk_plan {
   unsigned* umask = nullptr;
   double* uval = nullptr;
   int64_t nuslots = 0;
+  uint16_t* kcls = nullptr;        // row-class dictionary (sell_index 3): class per row,
+  gsk::RcdEntry* kdict = nullptr;  // class entries [RCD_MAXCLS]
+  void* ktab = nullptr;            // build scratch: hash table + flags (sell.cu)
+  int64_t ncls = 0;                // classes in use (0: inapplicable, plain SELL passes)
   int sell_maxlen = 0;      // longest SELL chunk (slots per lane)
-  int sell_index = 0;       // 0 plain int32 columns, 1 dictionary (SELL-D), 2 uniform (SELL-U)
+  int sell_index = 0;       // 0 plain int32 columns, 1 dictionary (SELL-D), 2 uniform (SELL-U),
+                            // 3 row-class dictionary (RCD)
   int sell_pad = -1;        // padding column value (INT_MIN in shard plans)
   // reduction scratch
   double* part = nullptr;      // [MAXD][pstride] CTA partials of the current pass
@@ -152,8 +157,9 @@ struct gsk_plan {
   int hist_cap = 0;
   // kernel probes: per kind, events recorded around one launch per batch
   // kinds: 0 Bi-CGSTAB v = A p pass, 1 Bi-CGSTAB t = A s pass, 2 GMRES MGS pass,
-  // 3 GMRES Arnoldi SpMV pass; [graph copy][start/stop]
-  static constexpr int NPROBE = 4;
+  // 3 GMRES Arnoldi SpMV pass, 4 Bi-CGSTAB x / r update pass (S4 / P3);
+  // [graph copy][start/stop]
+  static constexpr int NPROBE = 5;
   cudaEvent_t pev[NPROBE][NQ][2] = {};
   cudaEvent_t qev[NQ] = {};
   double probe_ms[NPROBE] = {};
@@ -237,7 +243,11 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     ntiles = (windows + wpc - 1) / wpc;
     // natural-order SELL plans (every window unsorted, sell.cu) run the NAT kernels
     const bool nat = P->sell.all_nat != 0;
-    if (P->fmt == GSK_FMT_SELL && P->sell.uptr) {
+    if (P->fmt == GSK_FMT_SELL && P->sell.kcls) {  // row-class dictionary (no slot data)
+      auto k = pass_kernel<5, 1, Op, true>;
+      pass_carveout(k);
+      GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
+    } else if (P->fmt == GSK_FMT_SELL && P->sell.uptr) {
       auto k = nat ? pass_kernel<4, 1, Op, true> : pass_kernel<4, 1, Op, false>;
       pass_carveout(k);
       GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
@@ -304,6 +314,7 @@ int sell_build(gsk_plan* P, cudaStream_t s);
 int sell_fill_values(gsk_plan* P, cudaStream_t s);
 int sell_dict_build(gsk_plan* P, cudaStream_t s);
 int sellu_build(gsk_plan* P, cudaStream_t s);
+int rcd_build(gsk_plan* P, cudaStream_t s);  // also the refresh (the classes depend on the values)
 int coop_bicgstab_run(gsk_plan* P, const double* b, double tol, int maxit, double* x, int* used);
 // On-chip single-CTA solvers (small.cu) for n <= GSK_SMALL_NMAX: one launch runs the
 // whole solve; the caller has set x = x0 and zeroed/initialised the state.
@@ -328,6 +339,7 @@ int shard_bicgstab_run(gsk_plan* P, const double* b, const double* x0, double to
 int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, double tol, int maxit, double* x,
                     double* hist, gsk_report* rep, cudaStream_t caller);
 int shard_refresh(gsk_plan* P, cudaStream_t s);
+int64_t shard_row_classes(gsk_plan* P);
 int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller);
 // End a stream capture begun by the caller: instantiate the graph, count its kernel
 // nodes (returned in *kernels; launches made during capture are not counted).

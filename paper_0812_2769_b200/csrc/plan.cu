@@ -497,7 +497,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
     set_error("gsk_plan_create: unknown engine %d", opts->engine);
     return GSK_E_INVALID;
   }
-  if (P->sell_index < 0 || P->sell_index > 2) {
+  if (P->sell_index < 0 || P->sell_index > 3) {
     delete P;
     set_error("gsk_plan_create: unknown sell_index %d", opts->sell_index);
     return GSK_E_INVALID;
@@ -509,6 +509,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
     if (rc == GSK_OK) rc = sell_build(P, P->st);
     if (rc == GSK_OK && P->sell_index == 1) rc = sell_dict_build(P, P->st);
     if (rc == GSK_OK && P->sell_index == 2) rc = sellu_build(P, P->st);
+    if (rc == GSK_OK && P->sell_index == 3) rc = rcd_build(P, P->st);
     if (rc == GSK_OK) rc = join_out(P, s);
     if (rc == GSK_OK && cudaStreamSynchronize(P->st) != cudaSuccess) rc = GSK_E_CUDA;
   }
@@ -546,7 +547,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->wid, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
-                  P->cpart, P->uptr, P->udel, P->umask, P->uval};
+                  P->cpart, P->uptr, P->udel, P->umask, P->uval, P->kcls, P->kdict, P->ktab};
   for (void* b : bufs) pool_release(b);  // the plan stream drained above
   if (P->h_flag) cudaFreeHost(P->h_flag);
   for (auto& k : P->pev)
@@ -702,6 +703,28 @@ int gsk_plan_sell_uniform(gsk_plan* P, int64_t* nuslots, int32_t* uptr, int32_t*
   if (udel) GSK_CUDA(cudaMemcpyAsync(udel, P->udel, sizeof(int) * nch * SELLU_MAXL, cudaMemcpyDeviceToDevice, s));
   if (umask) GSK_CUDA(cudaMemcpyAsync(umask, P->umask, sizeof(unsigned) * nch * SELLU_MAXL, cudaMemcpyDeviceToDevice, s));
   if (uval) GSK_CUDA(cudaMemcpyAsync(uval, P->uval, sizeof(double) * P->nuslots, cudaMemcpyDeviceToDevice, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  return GSK_OK;
+}
+
+int gsk_plan_row_classes(gsk_plan* P, int64_t* ncls, uint16_t* cls, void* entries, void* stream) {
+  if (P && P->shards && P->fmt == GSK_FMT_SELL && !cls && !entries) {  // count only
+    if (ncls) *ncls = shard_row_classes(P);
+    return GSK_OK;
+  }
+  if (!P || P->shards || P->fmt != GSK_FMT_SELL) {
+    set_error("gsk_plan_row_classes: plan is not an unsharded SELL plan");
+    return GSK_E_INVALID;
+  }
+  if (!P->sell.kcls) {
+    if (ncls) *ncls = -1;
+    return GSK_OK;
+  }
+  if (ncls) *ncls = P->ncls;
+  cudaStream_t s = as_stream(stream);
+  if (cls) GSK_CUDA(cudaMemcpyAsync(cls, P->kcls, sizeof(uint16_t) * (size_t)P->A.n, cudaMemcpyDeviceToDevice, s));
+  if (entries)
+    GSK_CUDA(cudaMemcpyAsync(entries, P->kdict, sizeof(RcdEntry) * (size_t)P->ncls, cudaMemcpyDeviceToDevice, s));
   GSK_CUDA(cudaStreamSynchronize(s));
   return GSK_OK;
 }

@@ -317,6 +317,7 @@ int sellu_fill_values(gsk_plan* P, cudaStream_t s);
 
 int sell_fill_values(gsk_plan* P, cudaStream_t s) {
   if (P->uval) GSK_TRY(sellu_fill_values(P, s));
+  if (P->sell_index == 3) GSK_TRY(rcd_build(P, s));  // the classes depend on the values
   const int n = P->A.n;
   const int nwin = (n + TB - 1) / TB;
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
@@ -455,6 +456,160 @@ int sellu_build(gsk_plan* P, cudaStream_t s) {
   P->sell.udel = P->udel;
   P->sell.umask = P->umask;
   P->sell.uval = P->uval;
+  return GSK_OK;
+}
+
+}  // namespace gsk
+
+namespace gsk {
+
+// ---- row-class dictionary ("RCD") ---------------------------------------
+// The paper's problems have piecewise-constant coefficients: whole
+// regions share one stencil row, before and after GS(p).  Rows with the same length,
+// deltas col - row and bit-identical values (CSR order) form a class; a pass then reads
+// a 2-byte class id per row and the class's 128-byte entry (L1-resident) instead of 12
+// bytes per nonzero — the same FMA chain on the same operands (AC-3), so bit-identical
+// results.  Classes are numbered by first occurrence (the oracle's orc_row_classes).
+//   1. hash every row (64-bit) into an open-addressing table keyed by the hash, keeping
+//      the smallest row of each key;
+//   2. host: used slots sorted by that row -> class ids (a 256 KB round trip);
+//   3. every row looks its slot up, is compared entry by entry with the class's first row
+//      (a hash collision makes the format inapplicable rather than wrong) and stores its
+//      id; a class's first row writes the dictionary entry.
+// Inapplicable (the plan keeps its plain SELL passes): a row longer than RCD_MAXL, more
+// than RCD_MAXCLS classes, a collision.
+constexpr int RCD_HT = 4 * RCD_MAXCLS;  // table slots (power of two)
+struct RcdSlot {
+  unsigned long long key;  // 0 = empty
+  int row;                 // smallest row with this key
+  int id;                  // class id (step 2)
+};
+
+__device__ __forceinline__ unsigned long long rcd_mix(unsigned long long h, unsigned long long x) {
+  h = (h ^ x) * 0xff51afd7ed558ccdull;
+  return h ^ (h >> 32);
+}
+__device__ __forceinline__ unsigned long long rcd_key(int i, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                      const double* __restrict__ v) {
+  const int a = rp[i], len = rp[i + 1] - a;
+  unsigned long long h = rcd_mix(0x9e3779b97f4a7c15ull, (unsigned long long)len);
+  for (int q = 0; q < len; ++q) {
+    h = rcd_mix(h, (unsigned long long)(long long)(ci[a + q] - i));
+    h = rcd_mix(h, (unsigned long long)__double_as_longlong(v[a + q]));
+  }
+  return h ? h : 1ull;
+}
+
+__global__ void rcd_init_kernel(RcdSlot* tab, int* flags) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < RCD_HT) tab[t] = RcdSlot{0ull, INT_MAX, -1};
+  if (t < 2) flags[t] = 0;  // [0] fail, [1] classes
+}
+
+__global__ void __launch_bounds__(TB) rcd_hash_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                      const double* __restrict__ v, RcdSlot* tab, int* flags) {
+  const int i = blockIdx.x * TB + threadIdx.x;
+  if (i >= n) return;
+  if (rp[i + 1] - rp[i] > RCD_MAXL) {
+    flags[0] = 1;
+    return;
+  }
+  const unsigned long long key = rcd_key(i, rp, ci, v);
+  int slot = (int)(key & (RCD_HT - 1));
+  for (int probe = 0; probe < RCD_HT; ++probe, slot = (slot + 1) & (RCD_HT - 1)) {
+    // a plain look first: almost every row finds its class already there
+    unsigned long long cur = *(volatile unsigned long long*)&tab[slot].key;
+    if (cur == 0ull) {
+      cur = atomicCAS(&tab[slot].key, 0ull, key);
+      if (cur == 0ull) {
+        cur = key;
+        if (atomicAdd(&flags[1], 1) >= RCD_MAXCLS) flags[0] = 1;
+      }
+    }
+    if (cur == key) {
+      if (*(volatile int*)&tab[slot].row > i) atomicMin(&tab[slot].row, i);
+      return;
+    }
+    if (*(volatile int*)&flags[0]) return;  // already inapplicable
+  }
+  flags[0] = 1;  // table full
+}
+
+__global__ void __launch_bounds__(TB) rcd_assign_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                        const double* __restrict__ v, const RcdSlot* __restrict__ tab,
+                                                        uint16_t* kcls, RcdEntry* kdict, int* flags) {
+  const int i = blockIdx.x * TB + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long key = rcd_key(i, rp, ci, v);
+  int slot = (int)(key & (RCD_HT - 1));
+  while (tab[slot].key != key) slot = (slot + 1) & (RCD_HT - 1);  // present (step 1)
+  const int rep = tab[slot].row, id = tab[slot].id;
+  const int a = rp[i], len = rp[i + 1] - a, ra = rp[rep];
+  bool same = rp[rep + 1] - ra == len;
+  for (int q = 0; q < len && same; ++q)
+    same = (ci[a + q] - i == ci[ra + q] - rep) &&
+           __double_as_longlong(v[a + q]) == __double_as_longlong(v[ra + q]);
+  if (!same) flags[0] = 2;  // two different rows with one hash
+  kcls[i] = (uint16_t)id;
+  if (i == rep) {
+    RcdEntry e;
+    int dd[RCD_MAXL + 2];
+    for (int q = 0; q < RCD_MAXL; ++q) {
+      e.v[q] = q < len ? v[a + q] : 0.0;
+      dd[q + 1] = q < len ? ci[a + q] - i : 0;
+    }
+    dd[0] = len;
+    dd[RCD_MAXL + 1] = 0;
+    for (int q = 0; q < 5; ++q) e.ld[q] = make_int2(dd[2 * q], dd[2 * q + 1]);
+    for (int q = 0; q < 6; ++q) e.pad_[q] = 0;
+    kdict[id] = e;
+  }
+}
+
+int rcd_build(gsk_plan* P, cudaStream_t s) {
+  const int n = P->A.n;
+  static_assert(sizeof(RcdEntry) == 128 && sizeof(RcdSlot) == 16, "RCD layouts");
+  const bool had = P->sell.kcls != nullptr;
+  if (!P->kcls) {
+    GSK_CUDA(pool_alloc((void**)&P->kcls, sizeof(uint16_t) * (size_t)n));
+    GSK_CUDA(pool_alloc((void**)&P->kdict, sizeof(RcdEntry) * RCD_MAXCLS));
+    GSK_CUDA(pool_alloc((void**)&P->ktab, sizeof(RcdSlot) * RCD_HT + 2 * sizeof(int)));
+  }
+  RcdSlot* tab = reinterpret_cast<RcdSlot*>(P->ktab);
+  int* flags = reinterpret_cast<int*>(tab + RCD_HT);
+  const int grid = (n + TB - 1) / TB;
+  rcd_init_kernel<<<(RCD_HT + TB - 1) / TB, TB, 0, s>>>(tab, flags);
+  rcd_hash_kernel<<<grid, TB, 0, s>>>(n, P->A.row_ptr, P->A.col_idx, P->A.values, tab, flags);
+  GSK_LAUNCHED(2);
+  std::vector<RcdSlot> h(RCD_HT);
+  int hf[2] = {0, 0};
+  GSK_CUDA(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
+  GSK_CUDA(cudaStreamSynchronize(s));
+  bool ok = hf[0] == 0 && hf[1] <= RCD_MAXCLS;
+  int ncls = 0;
+  if (ok) {
+    GSK_CUDA(cudaMemcpyAsync(h.data(), tab, sizeof(RcdSlot) * RCD_HT, cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaStreamSynchronize(s));
+    std::vector<std::pair<int, int>> used;  // (first row, slot)
+    for (int q = 0; q < RCD_HT; ++q)
+      if (h[q].key) used.emplace_back(h[q].row, q);
+    std::sort(used.begin(), used.end());
+    ncls = (int)used.size();
+    for (int k = 0; k < ncls; ++k) h[used[k].second].id = k;
+    GSK_CUDA(cudaMemcpyAsync(tab, h.data(), sizeof(RcdSlot) * RCD_HT, cudaMemcpyHostToDevice, s));
+    rcd_assign_kernel<<<grid, TB, 0, s>>>(n, P->A.row_ptr, P->A.col_idx, P->A.values, tab, P->kcls, P->kdict, flags);
+    GSK_LAUNCHED(1);
+    GSK_CUDA(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaStreamSynchronize(s));
+    ok = hf[0] == 0;
+  }
+  P->ncls = ok ? ncls : 0;
+  P->sell.kcls = ok ? P->kcls : nullptr;
+  P->sell.kdict = ok ? P->kdict : nullptr;
+  if (ok != had) {  // captured graphs hold the other kernels: capture again
+    P->bkey_b = nullptr;
+    P->gkey_b = nullptr;
+  }
   return GSK_OK;
 }
 

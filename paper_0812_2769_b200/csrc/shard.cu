@@ -590,6 +590,16 @@ int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller) {
   return GSK_OK;
 }
 
+// classes of this process's shard plans: the largest count, or -1 if one runs plain SELL
+int64_t shard_row_classes(gsk_plan* P) {
+  int64_t k = 0;
+  for (auto& d : P->shards->sh) {
+    if (!d.sub->sell.kcls) return -1;
+    k = std::max<int64_t>(k, d.sub->ncls);
+  }
+  return k;
+}
+
 int shard_refresh(gsk_plan* P, cudaStream_t caller) {
   for (auto& d : P->shards->sh) GSK_TRY(gsk_plan_refresh(d.sub, caller));
   return GSK_OK;

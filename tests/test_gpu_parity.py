@@ -780,6 +780,86 @@ def test_sell_uniform_solvers(name, N):
     assert_same_solve(SP.gmres(b, m=30, tol=1e-9, maxit=100), og)
 
 
+@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 100), ("C3", 20), ("C3", 48), ("C4", 24), ("C4", 64),
+                                    ("C5", 64), ("P4", 12), ("P1", 64)])
+def test_row_classes_parity(name, N):
+    """Row-class dictionary (RCD) built on the device == the oracle's encoding: class ids
+    (first-occurrence numbering), lengths, deltas and values bit for bit — also after a
+    value refresh (GS(2) in place) — and the plan's SpMV == the oracle's; systems whose
+    rows do not repeat (C2's node-dependent velocity at size, permuted C5) are inapplicable
+    on both sides and keep their SELL passes."""
+    s = workloads.generate(name, N=N)
+    A = gsk.CSR.from_system(s)
+    P = gsk.Plan(A, fmt="sell", sell_index="classes")
+    x = workloads.uniform(s["n"], 9, 9)
+    for val in (s["val"], oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)[0]):
+        if val is not s["val"]:
+            A.val.copy_(torch.tensor(val, device="cuda"))
+            P.refresh()
+        g = P.row_classes()
+        o = oracle.row_classes(s["row_ptr"], s["col"], val)
+        assert (g is None) == (o is None)
+        if o is not None:
+            for k in ("cls", "len", "delta"):
+                assert np.array_equal(g[k], o[k]), k
+            assert np.array_equal(g["val"].view(np.uint64), o["val"].view(np.uint64))
+        assert np.array_equal(cpu(P.spmv(x)), oracle.spmv(s["row_ptr"], s["col"], val, x))
+
+
+def test_row_classes_applicability_flips_on_refresh():
+    """A refresh that makes the rows distinct (a value per row) drops the plan back to its
+    SELL passes, and one that restores repeating rows brings the classes back; the solver
+    graphs are re-captured each time (same bits as the oracle throughout)."""
+    s, val, b, _ = system("C4", 24, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val.copy())
+    P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph")
+    assert P.row_classes() is not None
+    o = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 60)
+    assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=60), o)
+    v2 = val * (1.0 + 1e-3 * workloads.uniform(val.size, 3, 3))  # every row different
+    A.val.copy_(torch.tensor(v2, device="cuda"))
+    P.refresh()
+    assert P.row_classes() is None
+    assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=60), oracle.bicgstab(s["row_ptr"], s["col"], v2, b, 1e-9, 60))
+    A.val.copy_(torch.tensor(val, device="cuda"))
+    P.refresh()
+    assert P.row_classes() is not None
+    assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=60), o)
+
+
+@pytest.mark.parametrize("name,N,scal", [("C4", 24, 2), ("C4", 40, 2), ("C3", 20, 2), ("C3", 33, 1), ("P1", 64, 2),
+                                         ("C1", None, 2), ("P4", 12, "none")])
+def test_row_classes_solvers(name, N, scal):
+    """Solvers on row-class plans (no slot data read by the passes): the same bits as the
+    oracle — split, four-pass and fused Bi-CGSTAB, MGS and CGS2 GMRES, frame weights, x0,
+    and sharded (ragged sizes included: 33^3 and 40^3 rows are no multiple of 256)."""
+    s, val, b, _ = system(name, N, scal)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    ob = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 300)
+    og = oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 90)
+    for schedule in ("split", "split4", "fused"):
+        P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph", schedule=schedule)
+        assert P.row_classes() is not None
+        assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=300), ob)
+        assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=90), og)
+    P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph", orth="cgs2")
+    assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=90),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 90, orth="cgs2"))
+    w = workloads.uniform(s["n"], 5, 6) + 1.5
+    x0 = workloads.uniform(s["n"], 7, 8)
+    Pw = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph", weights=w)
+    assert_same_solve(Pw.bicgstab(b, x0=x0, tol=1e-9, maxit=300),
+                      oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 300, x0=x0, weights=w))
+    # the default engine choice (on-chip / cooperative engines read the SELL slots)
+    Pa = gsk.Plan(A, fmt="sell", sell_index="classes")
+    assert_same_solve(Pa.bicgstab(b, tol=1e-9, maxit=300), ob)
+    assert_same_solve(Pa.gmres(b, m=30, tol=1e-9, maxit=90), og)
+    if s["n"] >= 4096:
+        SP = gsk.ShardedPlan(A, shards=2, fmt="sell", sell_index="classes")
+        assert_same_solve(SP.bicgstab(b, tol=1e-9, maxit=300), ob)
+        assert_same_solve(SP.gmres(b, m=30, tol=1e-9, maxit=90), og)
+
+
 def test_sharded_nccl_single_rank():
     """The multi-process code path (halo send/recv groups, ncclAllGather of the shard
     values, all inside the captured graphs) on a 1-rank NCCL communicator: bit-exact."""

@@ -1,0 +1,20 @@
+# Round 2, call za: RCD windows-in-flight A/B (GSK_LIB variants), C4 and C3.
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "row_classes" > gpurun_out/r02za_tests.log 2>&1; echo "tests rc=$?"
+tail -5 gpurun_out/r02za_tests.log
+for v in default nw1 nw2m3 nw4m3 nw4m2; do
+  if [ $v = default ]; then unset GSK_LIB; else export GSK_LIB=$PWD/abvar/libgsk_$v.so; fi
+  for cfg in C4 C3; do
+    python bench.py --config $cfg --no-e2e --no-cpu --no-time-to-tol --sell-index classes > gpurun_out/r02za_${cfg}_$v.json 2> gpurun_out/r02za_${cfg}_$v.err
+  done
+done
+for f in gpurun_out/r02za_*.json; do python - "$f" <<'PY'
+import json, sys
+try:
+    d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); x = d["extra"]
+    print(sys.argv[1], round(d["value"], 1), "bicg", round(x["bicgstab"]["iters_per_s"], 1), x["bicgstab"]["iterations"], "gmres", round(x["gmres"]["iters_per_s"], 1), "spmv", round(x["spmv"]["ms"], 4), {k: round(v, 4) for k, v in x["probe_ms"].items() if v}, d["clocks"]["sm_mhz"])
+except Exception as e:
+    print(sys.argv[1], "failed", e)
+PY
+done
