@@ -15,10 +15,17 @@ value  = solver iterations per second (Bi-CGSTAB + GMRES iterations of the step,
          summed over ranks, / max-over-ranks device time); unit "iters/s".
 e2e    = the same through the public API with the system copied from pinned host
          memory every step (plan rebuilt) and x read back (summed over ranks).
-roofline: the dominant kernel (the split schedule's S1 pass v = A p, <r^,v>) —
-         algorithmic bytes 12 nnz + 4(n+1) + 3*8n per launch / its
-         CUDA-event time inside the captured graphs; traffic from the committed ncu
-         capture (profiles/r02_ncu_traffic.json).
+roofline: the probed kernel with the largest share of the step (per-launch CUDA-event
+         time inside the captured graphs x its launches per step; at C4 with the
+         row-class dictionary the GMRES MGS projection pass, 4*8n bytes per launch;
+         on plain SELL slots the Bi-CGSTAB pass v = A p, <r^,v>, 12 nnz + 4(n+1) +
+         3*8n); every probed kernel is listed in extra.roofline_all; traffic from the
+         committed ncu captures (profiles/r02_ncu_traffic*.json).
+layout:  the plan is SELL-C-32-256 built on the device; by default (--sell-index
+         classes) its passes read the row-class dictionary (a uint16
+         class id per row and one 128-byte line per distinct row instead of 12 bytes
+         per nonzero — lossless, bit-identical) where the matrix's rows repeat (C1, C3,
+         C4), else the slots; extra.sell_plain holds the same solves on the slots.
 extra  = SpMV and GS(2) rooflines, per-pass probes and time_to_tol (time to 1e-8 of
          Bi-CGSTAB and of GMRES(30) without scaling, with GS(1), GS(2) and two-sided
          scaling).
@@ -208,11 +215,16 @@ def run_reference(args, rank, world):
 def ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` (a short name or its prefix before
     the engine's variant arguments, e.g. pass_kernel<2,1,OpS1) from the committed ncu
-    --set full capture (profiles/r02_ncu_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
-            ks = json.load(f)["kernels"]
-    except (OSError, ValueError, KeyError):
+    --set full captures (profiles/r02_ncu_traffic.json: SELL slots; r02_ncu_traffic_v16.json:
+    row-class plans), or None."""
+    ks = {}
+    for name in ("r02_ncu_traffic.json", "r02_ncu_traffic_v16.json"):  # SELL slots; row classes
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                ks.update(json.load(f)["kernels"])
+        except (OSError, ValueError, KeyError):
+            pass
+    if not ks:
         return None
     for name, k in ks.items():
         if name == kernel or name.startswith(kernel.rstrip(">") + ","):
@@ -355,7 +367,12 @@ def main():
     bm = byte_model(n, nnz, rcd)
     hbm, src = peaks()
     sched = plan_schedule(args, n, nnz)
-    F = 5 if rcd else (2 if fmt == "sell" else 1)
+    try:
+        nsl = plan.num_slots() if rcd else -1
+    except Exception:
+        nsl = -1
+    # pass_kernel format argument: 1 CSR, 2 SELL slots, 5 class lines, 6 / 7 classes with a 7- / 5-delta stencil
+    F = ({7: 6, 5: 7}.get(nsl, 5)) if rcd else (2 if fmt == "sell" else 1)
     r1l, r2l = reps[-1]
     its_b, its_g = r1l["iterations"], r2l["iterations"]
     # MGS projection passes of a GMRES(m) run of its_g steps: step j of a cycle has j - 1
@@ -446,6 +463,7 @@ def main():
                      "gmres_arnoldi_spmv": probes[3], "bicg_update_pass": probes[4]},
         "roofline_all": roofs,
         "encoding": {"sell_index": args.sell_index, "row_classes": ncls if rcd else None,
+                     "stencil_slots": nsl if nsl > 0 else None,
                      "matrix_bytes_per_spmv": bm["spmv"] - 16 * n},
         "probe_gbps": {"bicg_v_pass": bm[{"split": "bicg_s1", "split4": "bicg_s1q", "fused": "bicg_p1"}[sched]]
                        / (probes[0] / 1e3) / 1e9

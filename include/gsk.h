@@ -190,6 +190,16 @@ int gsk_plan_sell_uniform(gsk_plan *plan, int64_t *nuslots, int32_t *uptr, int32
  * answers the count only (cls = entries = NULL): the largest class count of this
  * process's shards, or -1 if one of them runs its plain SELL passes. */
 int gsk_plan_row_classes(gsk_plan *plan, int64_t *ncls, uint16_t *cls, void *entries, void *stream);
+/* Stencil slots of a row-class plan: when the deltas of all classes taken
+ * together are one symmetric set {-s_k .. -1, 0, 1 .. s_k} of 5 or 7 (a 5- / 7-point
+ * stencil on a structured grid), the passes read per class a presence mask and one value
+ * per delta of that set (ascending delta = CSR order) and take the deltas from the plan.
+ * *ns = the number of deltas, or -1 when the classes do not share such a set (the passes
+ * then read the class lines of gsk_plan_row_classes); deltas: HOST int32 [8] (ascending,
+ * unused 0); slots: DEVICE [ncls * 128 bytes], per class double v[8], uint32 mask (bit k:
+ * an entry at deltas[k]), 60 bytes of zero padding.  Outputs other than ns nullable.
+ * GSK_RCD_SLOTS=0 in the environment disables the slots. */
+int gsk_plan_class_slots(gsk_plan *plan, int32_t *ns, int32_t *deltas, void *slots, void *stream);
 void gsk_plan_destroy(gsk_plan *plan);
 
 /* Bi-CGSTAB (van der Vorst 1992) on A x = b.

@@ -24,7 +24,7 @@ ORTH = {"mgs": 0, "cgs2": 1}
 
 # exported symbols (include/gsk.h); tests check the library exports all of them
 SYMBOLS = ("gsk_gs_scale", "gsk_gs_scale_sym", "gsk_gs_unscale", "gsk_spmv", "gsk_dot", "gsk_plan_create", "gsk_plan_refresh",
-           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_sell_uniform", "gsk_plan_row_classes", "gsk_plan_destroy",
+           "gsk_plan_spmv", "gsk_plan_sell_info", "gsk_plan_sell_copy", "gsk_plan_sell_dict", "gsk_plan_sell_uniform", "gsk_plan_row_classes", "gsk_plan_class_slots", "gsk_plan_destroy",
            "gsk_bicgstab_solve", "gsk_bicgstab_solve_plan", "gsk_gmres_solve",
            "gsk_gmres_solve_plan", "gsk_plan_residual_norm", "gsk_plan_probe",
            "gsk_shard_rows", "gsk_shard_halo_host", "gsk_plan_create_sharded", "gsk_nccl_unique_id",
@@ -94,6 +94,7 @@ def load(path: str = LIB_PATH):
     lib.gsk_plan_sell_dict.argtypes = [vp, P(i64), vp, vp, vp, vp]
     lib.gsk_plan_sell_uniform.argtypes = [vp, P(i64), vp, vp, vp, vp, vp]
     lib.gsk_plan_row_classes.argtypes = [vp, P(i64), vp, vp, vp]
+    lib.gsk_plan_class_slots.argtypes = [vp, P(ctypes.c_int32), vp, vp, vp]
     lib.gsk_plan_destroy.argtypes = [vp]
     lib.gsk_plan_destroy.restype = None
     lib.gsk_bicgstab_solve.argtypes = [P(CsrStruct), vp, vp, d, i32, vp, vp, P(Report), vp]
@@ -358,6 +359,28 @@ class Plan:
         assert not rec["pad"].any()
         return {"cls": cls.cpu().numpy().view(np.uint16), "len": rec["len"].copy(),
                 "delta": rec["d"].copy(), "val": rec["v"].copy()}
+
+    def class_slots(self):
+        """Stencil slots of the plan's classes (None when they do not share one symmetric
+        5- / 7-delta set): {"deltas" [ns], "mask" uint32 [K], "val" [K, 8]}."""
+        lib = load()
+        ns = ctypes.c_int32()
+        dl = (ctypes.c_int32 * 8)()
+        _check(lib.gsk_plan_class_slots(self.h, ctypes.byref(ns), dl, None, _stream()))
+        if ns.value < 0:
+            return None
+        k = self.num_classes()
+        buf = torch.empty(k * 128, dtype=torch.uint8, device="cuda")
+        _check(lib.gsk_plan_class_slots(self.h, ctypes.byref(ns), dl, _ptr(buf), _stream()))
+        rec = buf.cpu().numpy().view(np.dtype([("v", "<f8", 8), ("mask", "<u4"), ("pad", "<u4", 15)]))
+        assert not rec["pad"].any()
+        return {"deltas": np.array(dl[:ns.value]), "mask": rec["mask"].copy(), "val": rec["v"].copy()}
+
+    def num_slots(self) -> int:
+        """Deltas of the classes' shared stencil (5 or 7), or -1 (no stencil slots)."""
+        ns = ctypes.c_int32()
+        _check(load().gsk_plan_class_slots(self.h, ctypes.byref(ns), None, None, _stream()))
+        return ns.value
 
     def num_classes(self) -> int:
         """Classes of the plan's row-class dictionary (-1: not built or inapplicable)."""

@@ -36,6 +36,16 @@ struct __align__(128) RcdEntry {
   int pad_[6];
 };
 
+// Stencil slots of a row-class plan (sell.cu): when the deltas of ALL classes form one
+// symmetric set {-s_k .. -s_1, -1, 0, 1, s_1 .. s_k} (a 5- or 7-point stencil on a
+// structured grid), a class is a presence mask and one value per delta of that set, in
+// ascending delta (= CSR) order; the deltas themselves are plan constants.
+struct __align__(128) RcdSlots {
+  double v[RCD_MAXL];
+  unsigned mask;  // bit k: the class has an entry at delta sdel[k]
+  unsigned pad_[15];
+};
+
 struct SellView {
   int n;
   int nchunks;
@@ -65,6 +75,11 @@ struct SellView {
   // class of every row and the classes' entries; the passes then read no slot data
   const uint16_t* __restrict__ kcls;   // [n]
   const RcdEntry* __restrict__ kdict;  // [<= RCD_MAXCLS]
+  // optional stencil slots of the classes (null: the deltas differ between classes)
+  const RcdSlots* __restrict__ kslots; // [<= RCD_MAXCLS]
+  int sdel[RCD_MAXL];                  // the plan's ascending deltas (ns of them: 5 or 7)
+  int ns;
+  int sroll;  // 1: sdel[ns/2 + 2] == 256, the same thread's row of the next window
 };
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the

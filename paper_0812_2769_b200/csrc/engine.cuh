@@ -111,10 +111,10 @@ struct SellTuning<Op, std::void_t<decltype(Op::kSellMinBlocks)>> {
 constexpr bool SELL_DIRECT = GSK_SELL_DIRECT;
 
 // column-index encoding of a SELL pass format: FMT 2 int32, 3 SELL-D, 4 SELL-U, 5 RCD
-// (row-class dictionary: no slot data at all)
+// (row-class dictionary: no slot data at all), 6 / 7 RCD with stencil slots (7 / 5 deltas)
 template <int FMT>
 struct SellIdx {
-  static constexpr int value = FMT == 3 ? 1 : FMT == 4 ? 2 : FMT == 5 ? 3 : 0;
+  static constexpr int value = FMT == 3 ? 1 : FMT == 4 ? 2 : FMT >= 5 ? 3 : 0;
 };
 
 #ifndef GSK_RCD_MINB
@@ -130,7 +130,7 @@ struct PassOcc {
   // (Measured with dots too, leaves parked by row in shared memory and reduced once
   // per CTA: bit-exact, but S1 unchanged and S3 slower — 80 registers to not spill.)
   static constexpr bool kDirect = SELL_DIRECT && FMT >= 2 && Op::D == 0;
-  static constexpr int kMinBlocks = FMT == 5 ? GSK_RCD_MINB
+  static constexpr int kMinBlocks = FMT >= 5 ? GSK_RCD_MINB
                                   : FMT == 1 ? 4
                                   : FMT == 3 ? (Op::D > 0 && SellTuning<Op>::minb == 4 ? GSK_SELLD_DOT_MINB
                                                                                        : SellTuning<Op>::minb)
@@ -197,6 +197,46 @@ __device__ __forceinline__ double rcd_row(const SellView& A, int row, int cls, c
 #pragma unroll
   for (int k = 0; k < RCD_MAXL; ++k)
     if (k < L) acc = __fma_rn(__ldg(&e->v[k]), xs[k], acc);
+  return acc;
+}
+
+// Row-class SpMV with stencil slots (RcdSlots: every class's deltas come from the plan's
+// symmetric set sdel[0..NS), centre C = NS / 2 with sdel[C] = 0, sdel[C -+ 1] = -+1): no
+// delta loads, and the gathers that neighbouring threads already hold come from registers
+// instead of the L1 data pipe —
+//   * delta -+1: the adjacent lane's own-row value g(row -+ 1) by shuffle (lanes 0 / 31
+//     load theirs);
+//   * with roll (sdel[C + 2] == 256 = the window height: a grid line is one window): the
+//     entry at delta -+256 is this thread's own-row value of the previous / next window,
+//     kept from / loaded for the neighbouring window (xlo / xhi valid when has_lo / has_hi).
+// The values are the same loads of the same memory, the chain is ascending delta = CSR
+// order (AC-3): bit-identical to every other format.
+template <int NS, class G>
+__device__ __forceinline__ double rcd_row_slots(const SellView& A, int row, int cls, const G& g, double own,
+                                                bool has_lo, double xlo, bool has_hi, double xhi) {
+  constexpr int C = NS / 2;
+  const int lane = threadIdx.x & 31;
+  const RcdSlots* e = A.kslots + cls;
+  const unsigned mask = row < A.n ? __ldg(&e->mask) : 0u;
+  auto bit = [&](int k) { return ((mask >> k) & 1u) != 0u; };
+  double xs[NS];
+  const double up = __shfl_up_sync(0xffffffffu, own, 1);
+  const double dn = __shfl_down_sync(0xffffffffu, own, 1);
+  xs[C] = own;
+  xs[C - 1] = lane > 0 ? up : (bit(C - 1) ? g(row - 1) : 0.0);
+  xs[C + 1] = lane < 31 ? dn : (bit(C + 1) ? g(row + 1) : 0.0);
+  xs[C - 2] = has_lo ? xlo : (bit(C - 2) ? g(row + A.sdel[C - 2]) : 0.0);
+  xs[C + 2] = has_hi ? xhi : (bit(C + 2) ? g(row + A.sdel[C + 2]) : 0.0);
+  if constexpr (NS == 7) {
+    xs[0] = bit(0) ? g(row + A.sdel[0]) : 0.0;
+    xs[6] = bit(6) ? g(row + A.sdel[6]) : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    const double a = __ldg(&e->v[k]);
+    if (bit(k)) acc = __fma_rn(a, xs[k], acc);
+  }
   return acc;
 }
 
@@ -490,18 +530,22 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
   constexpr int NVA = Op::NV > 0 ? Op::NV : 1;
   constexpr bool kDirect = PassOcc<FMT, Op>::kDirect;
   using Smem = std::conditional_t<
-      FMT == 5, PassSmemSell<0, true>,
+      (FMT >= 5), PassSmemSell<0, true>,
       std::conditional_t<
       kDirect, PassSmemDirect,
       std::conditional_t<(FMT >= 2), PassSmemSell<(PassOcc<FMT, Op>::kAsync ? Op::NV : 0), NAT>, PassSmem<FMT>>>>;
   __shared__ __align__(16) Smem sm;
   const int t = threadIdx.x, warp = t >> 5;
-  if constexpr (FMT == 5) {
+  if constexpr (FMT >= 5) {
     // RCD: thread t finishes row r0 + t of every window; own-row operands in registers;
-    // the class id of the next window is loaded while this one computes
+    // the class id of the next window is loaded while this one computes.  FMT 6 / 7: the
+    // plan's classes share one 7- / 5-delta stencil (rcd_row_slots).
+    constexpr int NS = FMT == 6 ? 7 : FMT == 7 ? 5 : 0;
     const int rb = bx * wpc * TB;
     int kn = rb + t < n ? (int)__ldg(sell.kcls + rb + t) : 0;
     auto g = [&](int col) { return op.gather(col); };
+    const bool roll = NS > 0 && sell.sroll != 0;
+    double own_prev = 0.0, own_cur = 0.0, own_next = 0.0;
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
       double cc[DD];
@@ -513,7 +557,17 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
         double v[NVA];
         if (i < n) load_vin(op, i, v);
         kn = (w + 1 < wpc && i + TB < n) ? (int)__ldg(sell.kcls + i + TB) : 0;
-        const double y = rcd_row(sell, i, kc, g);
+        double y;
+        if constexpr (NS > 0) {
+          const bool more = w + 1 < wpc && i + TB < n;  // this thread's row of the next window
+          if (!roll || w == 0) own_cur = i < n ? g(i) : 0.0;
+          if (roll) own_next = more ? g(i + TB) : 0.0;
+          y = rcd_row_slots<NS>(sell, i, kc, g, own_cur, roll && w > 0, own_prev, roll && more, own_next);
+          own_prev = own_cur;
+          own_cur = own_next;
+        } else {
+          y = rcd_row(sell, i, kc, g);
+        }
         if (i < n) op.row(i, y, v, cc);
       }
       if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);

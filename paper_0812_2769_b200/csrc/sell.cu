@@ -13,6 +13,7 @@
 // in row order without the shared-memory scatter and its barrier (engine.cuh).
 #include <algorithm>
 #include <climits>
+#include <cstring>
 #include <vector>
 #include "internal.cuh"
 
@@ -606,7 +607,51 @@ int rcd_build(gsk_plan* P, cudaStream_t s) {
   P->ncls = ok ? ncls : 0;
   P->sell.kcls = ok ? P->kcls : nullptr;
   P->sell.kdict = ok ? P->kdict : nullptr;
-  if (ok != had) {  // captured graphs hold the other kernels: capture again
+  // stencil slots (engine.cuh rcd_row_slots): the classes' deltas taken together are one
+  // symmetric set {.., -1, 0, 1, ..} of 5 or 7 — then a class becomes a presence mask and
+  // one value per delta of that set (host work on <= 4096 class lines)
+  const int had_ns = P->sell.kslots ? P->sell.ns : 0;
+  P->sell.kslots = nullptr;
+  P->sell.ns = 0;
+  P->sell.sroll = 0;
+  static const bool slots_on = [] {
+    const char* e = std::getenv("GSK_RCD_SLOTS");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (ok && slots_on) {
+    std::vector<RcdEntry> ent(ncls);
+    GSK_CUDA(cudaMemcpyAsync(ent.data(), P->kdict, sizeof(RcdEntry) * ncls, cudaMemcpyDeviceToHost, s));
+    GSK_CUDA(cudaStreamSynchronize(s));
+    auto delta = [](const RcdEntry& e, int q) { return q == 0 ? e.ld[0].y : (q & 1) ? e.ld[(q + 1) / 2].x : e.ld[q / 2].y; };
+    std::vector<int> U;
+    for (const RcdEntry& e : ent)
+      for (int q = 0; q < e.ld[0].x; ++q) U.push_back(delta(e, q));
+    std::sort(U.begin(), U.end());
+    U.erase(std::unique(U.begin(), U.end()), U.end());
+    const int ns = (int)U.size(), c = ns / 2;
+    bool sym = (ns == 5 || ns == 7) && U[c] == 0 && U[c - 1] == -1 && U[c + 1] == 1;
+    for (int k = 0; sym && k < ns; ++k) sym = U[k] == -U[ns - 1 - k];
+    if (sym) {
+      std::vector<RcdSlots> sl(ncls);
+      for (int k = 0; k < ncls; ++k) {
+        RcdSlots& o = sl[k];
+        std::memset(&o, 0, sizeof o);
+        for (int q = 0; q < ent[k].ld[0].x; ++q) {
+          const int pos = (int)(std::lower_bound(U.begin(), U.end(), delta(ent[k], q)) - U.begin());
+          o.v[pos] = ent[k].v[q];
+          o.mask |= 1u << pos;
+        }
+      }
+      if (!P->kslots) GSK_CUDA(pool_alloc((void**)&P->kslots, sizeof(RcdSlots) * RCD_MAXCLS));
+      GSK_CUDA(cudaMemcpyAsync(P->kslots, sl.data(), sizeof(RcdSlots) * ncls, cudaMemcpyHostToDevice, s));
+      GSK_CUDA(cudaStreamSynchronize(s));  // sl is a local
+      P->sell.kslots = P->kslots;
+      P->sell.ns = ns;
+      for (int k = 0; k < RCD_MAXL; ++k) P->sell.sdel[k] = k < ns ? U[k] : 0;
+      P->sell.sroll = U[c + 2] == TB ? 1 : 0;
+    }
+  }
+  if (ok != had || had_ns != P->sell.ns) {  // captured graphs hold the other kernels: capture again
     P->bkey_b = nullptr;
     P->gkey_b = nullptr;
   }

@@ -12,7 +12,8 @@ the convection sweep; tests/golden/
 paper_runs_oracle.json) are compared the same way.  Runs that end in MAXIT are capped at >= 1000 iterations
 on both sides.  The comparison is bit-exact: verdict, iteration
 count, breakdown_at, every reported residual and the SHA-256 of the whole history
-and of x.
+and of x.  Where the plan's row-class dictionary applies (C1, C3, C4, the paper's
+problems) every run is made on both encodings.
 """
 import json
 import os
@@ -39,8 +40,13 @@ GOLD = {**_gold("full_runs_oracle.json"), **_gold("paper_runs_oracle.json")}
 _CACHE = {}
 
 
-@pytest.mark.parametrize("run", RUNS, ids=[r["key"] for r in RUNS])
-def test_full_size_run_to_verdict(run):
+# both plan encodings where the row-class dictionary applies (C1, C3, C4 and the paper's
+# problems); C2 and C5 have no repeating rows ("classes" falls back to the plain slots)
+CASES = [(r, e) for r in RUNS for e in (("classes", "plain") if r["config"] not in ("C2", "C5") else ("classes",))]
+
+
+@pytest.mark.parametrize("run,enc", CASES, ids=[f"{r['key']}-{e}" for r, e in CASES])
+def test_full_size_run_to_verdict(run, enc):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
@@ -48,7 +54,8 @@ def test_full_size_run_to_verdict(run):
         pytest.skip("no oracle record for this run (tools/oracle_full_runs.py)")
     import full_parity
     ref = GOLD[run["key"]]
-    got = full_parity.gpu_run(run, _CACHE)
+    got = full_parity.gpu_run(run, _CACHE, enc)
+    assert (got["row_classes"] is not None) == (enc == "classes" and run["config"] not in ("C2", "C5"))
     diff, first = full_parity.compare(ref, got)
     assert not diff, {"differs_in": diff, "first_sampled_diff": first,
                       "gpu": {k: got[k] for k in ("status", "iterations", "relres")},

@@ -806,6 +806,62 @@ def test_row_classes_parity(name, N):
         assert np.array_equal(cpu(P.spmv(x)), oracle.spmv(s["row_ptr"], s["col"], val, x))
 
 
+def _banded_system(n, deltas, seed):
+    """Rows with entries at the given deltas (inside [0, n)), values from a few repeating
+    patterns (so the rows fall into classes), diagonally dominant."""
+    pat = np.array([[-1.0, 4.5, -0.5, -1.25], [-2.0, 7.0, -1.5, -0.75], [0.5, 3.0, -0.25, 1.0]])
+    rp, cols, vals = [0], [], []
+    for r in range(n):
+        k = (r // 97) % 3
+        for d, v in zip(deltas, pat[k]):
+            if 0 <= r + d < n:
+                cols.append(r + d)
+                vals.append(v)
+        rp.append(len(cols))
+    b = workloads.uniform(n, seed, 1)
+    return np.array(rp, np.int32), np.array(cols, np.int32), np.array(vals), b
+
+
+def test_row_classes_without_stencil_slots():
+    """Classes whose deltas are no symmetric 5- / 7-point set (here {-3, 0, 1, 7}) run the
+    generic class-line kernels (no stencil slots): SpMV and both solvers == the oracle."""
+    rp, col, val, b = _banded_system(5000, (-3, 0, 1, 7), 5)
+    A = gsk.CSR(rp, col, val)
+    P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph")
+    assert P.row_classes() is not None and P.class_slots() is None
+    x = workloads.uniform(5000, 9, 9)
+    assert np.array_equal(cpu(P.spmv(x)), oracle.spmv(rp, col, val, x))
+    assert_same_solve(P.bicgstab(b, tol=1e-10, maxit=200), oracle.bicgstab(rp, col, val, b, 1e-10, 200))
+    assert_same_solve(P.gmres(b, m=20, tol=1e-10, maxit=100), oracle.gmres(rp, col, val, b, 20, 1e-10, 100))
+
+
+@pytest.mark.parametrize("name,N,ns,roll", [("C4", 24, 7, False), ("C3", 20, 7, False), ("P1", 64, 5, False),
+                                            ("C1", 256, 5, True), ("C1", None, 5, False), ("P4", 12, 7, False)])
+def test_class_slots_parity(name, N, ns, roll):
+    """Stencil slots of a row-class plan: the plan's delta set is the union of the oracle
+    classes' deltas (symmetric, 5 or 7), every class's mask and values decode back to the
+    oracle's class line (ascending delta = CSR order), and the passes on them — with the
+    +-256 entries taken from the thread's neighbouring windows when a grid line is one
+    window (P1 at 256^2) — give the oracle's bits."""
+    s, val, b, _ = system(name, N, 2)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph")
+    S = P.class_slots()
+    o = oracle.row_classes(s["row_ptr"], s["col"], val)
+    assert S is not None and len(S["deltas"]) == ns
+    U = sorted({int(d) for k, L in enumerate(o["len"]) for d in o["delta"][k, :L]})
+    assert list(S["deltas"]) == U and (U[ns // 2 + 2] == 256) == roll
+    for k, L in enumerate(o["len"]):
+        pos = [U.index(int(d)) for d in o["delta"][k, :L]]
+        assert int(S["mask"][k]) == sum(1 << q for q in pos)
+        assert np.array_equal(S["val"][k, pos].view(np.uint64), o["val"][k, :L].view(np.uint64))
+        assert not S["val"][k, [q for q in range(8) if q not in pos]].any()
+    x = workloads.uniform(s["n"], 9, 9)
+    assert np.array_equal(cpu(P.spmv(x)), oracle.spmv(s["row_ptr"], s["col"], val, x))
+    assert_same_solve(P.bicgstab(b, tol=1e-9, maxit=120), oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 120))
+    assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=60), oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 60))
+
+
 def test_row_classes_applicability_flips_on_refresh():
     """A refresh that makes the rows distinct (a value per row) drops the plan back to its
     SELL passes, and one that restores repeating rows brings the classes back; the solver

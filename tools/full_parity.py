@@ -10,6 +10,7 @@ both sides per run and an ``equal`` flag.
 
     python tools/full_parity.py [out.json] [C1 C2 ...]
     python tools/full_parity.py --paper      # the paper's workloads -> r02_paper_parity.json
+    python tools/full_parity.py --plain ...  # plain SELL slots instead of the row-class dictionary
 """
 import hashlib
 import json
@@ -40,8 +41,11 @@ def golden(which="configs"):
     return json.load(open(GOLDEN[which]))["runs"] if os.path.exists(GOLDEN[which]) else {}
 
 
-def gpu_run(run, cache):
-    """One run of the matrix on the GPU; `cache` holds the config's device system."""
+def gpu_run(run, cache, sell_index="classes"):
+    """One run of the matrix on the GPU; `cache` holds the config's device system.
+    sell_index: the plan's encoding — "classes" (the bench default: the row-class
+    dictionary where the rows repeat, C1 / C3 / C4 and the paper's problems, else the
+    plain SELL slots) or "plain"."""
     cfg = (run["config"], run["param"])
     if cache.get("name") != cfg:
         cache.clear()
@@ -57,7 +61,8 @@ def gpu_run(run, cache):
     if run["frame"] == "gs2":
         d2 = cache[2][2]
         w = d2 if dp is None else d2 / dp
-    P = gsk.Plan(A, fmt="sell", weights=w)  # GMRES: the weights only enter true_relres_w
+    P = gsk.Plan(A, fmt="sell", weights=w, sell_index=sell_index)  # GMRES: the weights only enter true_relres_w
+    ncls = P.num_classes()
     t0 = time.perf_counter()
     if run["solver"] == "bicgstab":
         x, h, rep = P.bicgstab(b, tol=run["tol"], maxit=run["maxit"])
@@ -66,7 +71,7 @@ def gpu_run(run, cache):
     secs = time.perf_counter() - t0
     P.close()
     out = {"status": gsk.STATUS[rep["status"]], "hist_sha256": sha(h), "x_sha256": sha(x.cpu().numpy()),
-           "solve_ms": rep["solve_ms"], "wall_s": round(secs, 3),
+           "solve_ms": rep["solve_ms"], "wall_s": round(secs, 3), "row_classes": ncls if ncls > 0 else None,
            "first_below": {str(t): (int(np.argmax(h < t)) if (h < t).any() else None) for t in (1e-6, 1e-8, 1e-10)}}
     for k in ("iterations", "restarts", "breakdown_at", "history_len", "relres", "true_relres", "true_relres_w",
               "best_relres"):
@@ -87,7 +92,7 @@ def compare(ref, got):
     return diff, first_diff
 
 
-def main(out_path, names, which="configs"):
+def main(out_path, names, which="configs", sell_index="classes"):
     gold = golden(which)
     cache = {}
     rows = []
@@ -97,7 +102,7 @@ def main(out_path, names, which="configs"):
         ref = gold.get(run["key"])
         if ref is None:
             continue
-        got = gpu_run(run, cache)
+        got = gpu_run(run, cache, sell_index)
         diff, first_diff = compare(ref, got)
         got.pop("hist")
         rows.append({"key": run["key"], "equal": not diff, "differs_in": diff, "first_sampled_diff": first_diff,
@@ -107,16 +112,18 @@ def main(out_path, names, which="configs"):
                          {"its": got["iterations"], "status": got["status"], "gpu_ms": round(got["solve_ms"], 1)}),
               flush=True)
     with open(out_path, "w") as f:
-        json.dump({"_doc": __doc__.split("\n\n")[0], "all_equal": all(r["equal"] for r in rows),
+        json.dump({"_doc": __doc__.split("\n\n")[0], "sell_index": sell_index,
+                   "all_equal": all(r["equal"] for r in rows),
                    "n_runs": len(rows), "gpu": torch.cuda.get_device_name(0), "runs": rows}, f, indent=1)
     return rows
 
 
 if __name__ == "__main__":
     which = "paper" if "--paper" in sys.argv else "configs"
-    args = [a for a in sys.argv[1:] if a != "--paper"]
+    sidx = "plain" if "--plain" in sys.argv else "classes"
+    args = [a for a in sys.argv[1:] if a not in ("--paper", "--plain")]
     out = args[0] if args and args[0].endswith(".json") else \
         os.path.join(ROOT, "profiles", "r02_full_parity.json" if which == "configs" else "r02_paper_parity.json")
     names = [a for a in args if not a.endswith(".json")]
-    rows = main(out, names, which)
+    rows = main(out, names, which, sidx)
     sys.exit(0 if all(r["equal"] for r in rows) else 1)

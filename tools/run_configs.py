@@ -23,6 +23,11 @@ import paper_0812_2769_b200 as gsk  # noqa: E402
 import workloads  # noqa: E402
 
 
+# plan encoding: the row-class dictionary where the rows repeat (the bench default), else
+# (and with GSK_SELL_INDEX=plain) the plain SELL slots
+SELL_INDEX = os.environ.get("GSK_SELL_INDEX", "classes")
+
+
 def first(h, tol):
     idx = np.flatnonzero(h < tol)
     return int(idx[0]) if idx.size else None
@@ -64,7 +69,8 @@ def run(name, maxit_gmres=None):
             if solver == "gmres" and m == 30 and c.m == 30 and any(r["solver"] == "gmres(30)" and
                                                                    r["scaling"] == str(scaling) for r in rows):
                 continue
-            P = gsk.Plan(A, fmt="sell", weights=w if solver == "bicgstab" else None)
+            P = gsk.Plan(A, fmt="sell", weights=w if solver == "bicgstab" else None, sell_index=SELL_INDEX)
+            ncls = P.num_classes()
             maxit = c.maxit if solver == "bicgstab" else (maxit_gmres or c.maxit)
             if solver == "bicgstab":
                 x, h, rep = P.bicgstab(b, tol=min(tols), maxit=maxit)
@@ -79,7 +85,7 @@ def run(name, maxit_gmres=None):
             its = {str(t): first(h, t) for t in tols}
             ms = rep["solve_ms"]
             n, nnz = s["n"], s["nnz"]
-            ba = 12 * nnz + 4 * (n + 1)
+            ba = 2 * n if ncls > 0 else 12 * nnz + 4 * (n + 1)  # class ids instead of slot data
             # algorithmic bytes per iteration: Bi-CGSTAB split schedule 2 B_A + 19 vectors;
             # MGS GMRES(m) averaged over a cycle: step j moves B_A + (4j + 3) vectors (S_j, h_1j, j-1 M, L),
             # the restart (X, R) B_A + (m + 5) vectors per m steps
@@ -88,6 +94,7 @@ def run(name, maxit_gmres=None):
             its_done = max(rep["iterations"], 1)
             rows.append({
                 "config": name, "scaling": str(scaling), "solver": f"{solver}" + (f"({m})" if m else ""),
+                "row_classes": ncls if ncls > 0 else None,
                 "status": gsk.STATUS[rep["status"]], "iterations": rep["iterations"], "its_to_tol": its,
                 "best_relres": rep["best_relres"], "true_relres": rep["true_relres"],
                 "true_relres_gs2_frame": tr2 if tr2 is not None else rep["true_relres_w"],
@@ -102,11 +109,12 @@ def run(name, maxit_gmres=None):
 
 
 def markdown(rows):
-    out = ["| config | scaling | solver | verdict | its to tol | best rel-res | solve ms | ms/it | GB/s (model) | GS ms |",
-           "|---|---|---|---|---|---|---|---|---|---|"]
+    out = ["| config | scaling | solver | classes | verdict | its to tol | best rel-res | solve ms | ms/it | GB/s (model) | GS ms |",
+           "|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         its = ", ".join(f"{k}: {v if v is not None else '—'}" for k, v in r["its_to_tol"].items())
-        out.append(f"| {r['config']} | {r['scaling']} | {r['solver']} | {r['status']} ({r['iterations']}) | {its} | "
+        out.append(f"| {r['config']} | {r['scaling']} | {r['solver']} | {r.get('row_classes') or '—'} | "
+                   f"{r['status']} ({r['iterations']}) | {its} | "
                    f"{r['best_relres']:.2e} | {r['solve_ms']:.1f} | {r['ms_per_iter']:.3f} | {r['gbps_model']:.0f} | "
                    f"{r['gs_ms']:.2f} |")
     return "\n".join(out) + "\n"
