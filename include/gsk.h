@@ -23,7 +23,11 @@
  *    GSK_PDL=0 (no programmatic dependent launch), GSK_WPC=1|2|4|8|16 (256-row
  *    windows per CTA of SpMV passes, default 8), GSK_ALT=0 (no alternating CTA
  *    order of consecutive passes), GSK_CARVEOUT=<percent>|-1 (shared-memory
- *    carveout of SELL passes, default 25; -1 = the driver's choice).
+ *    carveout of SELL passes, default 25; -1 = the driver's choice), GSK_L2PF=<n>
+ *    (windows of L2 prefetch lead of the SELL slot passes), GSK_RCD_SLOTS=0 (row-
+ *    class plans read the class lines, never the stencil slots), GSK_POOL_MB=<MB>
+ *    (plan workspace cache, default 32768; 0 = off), GSK_TRACE_PLAN=1 (host time
+ *    of the plan-build phases on stderr).
  */
 #ifndef GSK_H
 #define GSK_H

@@ -11,6 +11,7 @@
 #include <unordered_map>
 #include <string>
 #include <vector>
+#include <chrono>
 #include "internal.cuh"
 
 namespace gsk {
@@ -502,17 +503,29 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
     set_error("gsk_plan_create: unknown sell_index %d", opts->sell_index);
     return GSK_E_INVALID;
   }
+  // GSK_TRACE_PLAN=1: host time of the phases of a plan build on stderr
+  static const bool trace = std::getenv("GSK_TRACE_PLAN") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   int rc = plan_alloc_common(P);
+  const auto t1 = now();
+  auto t2 = t1, t3 = t1;
   if (rc == GSK_OK && fmt == GSK_FMT_SELL) {
     cudaStream_t s = stream;
     rc = join_in(P, s);
     if (rc == GSK_OK) rc = sell_build(P, P->st);
+    t2 = now();
     if (rc == GSK_OK && P->sell_index == 1) rc = sell_dict_build(P, P->st);
     if (rc == GSK_OK && P->sell_index == 2) rc = sellu_build(P, P->st);
     if (rc == GSK_OK && P->sell_index == 3) rc = rcd_build(P, P->st);
     if (rc == GSK_OK) rc = join_out(P, s);
     if (rc == GSK_OK && cudaStreamSynchronize(P->st) != cudaSuccess) rc = GSK_E_CUDA;
+    t3 = now();
   }
+  if (trace)
+    std::fprintf(stderr, "[gsk] plan n=%d: alloc %.2f ms, SELL build %.2f ms, encodings %.2f ms\n", A->n, ms(t0, t1),
+                 ms(t1, t2), ms(t2, t3));
   if (rc != GSK_OK) {
     gsk_plan_destroy(P);
     return rc;

@@ -12,8 +12,8 @@ the convection sweep; tests/golden/
 paper_runs_oracle.json) are compared the same way.  Runs that end in MAXIT are capped at >= 1000 iterations
 on both sides.  The comparison is bit-exact: verdict, iteration
 count, breakdown_at, every reported residual and the SHA-256 of the whole history
-and of x.  Where the plan's row-class dictionary applies (C1, C3, C4, the paper's
-problems) every run is made on both encodings.
+and of x.  Where the plan's row-class dictionary applies (C1, C3, C4, Problem 4)
+every run is made on both encodings.
 """
 import json
 import os
@@ -40,9 +40,12 @@ GOLD = {**_gold("full_runs_oracle.json"), **_gold("paper_runs_oracle.json")}
 _CACHE = {}
 
 
-# both plan encodings where the row-class dictionary applies (C1, C3, C4 and the paper's
-# problems); C2 and C5 have no repeating rows ("classes" falls back to the plain slots)
-CASES = [(r, e) for r in RUNS for e in (("classes", "plain") if r["config"] not in ("C2", "C5") else ("classes",))]
+# both plan encodings where the row-class dictionary applies (C1, C3, C4 and Problem 4:
+# piecewise-constant coefficients, constant velocity); the rows of C2 (node-dependent
+# velocity), C5 (random field) and Problem 1 (the conservative d(du)/dx term at 128^2:
+# 16384 distinct rows) do not repeat, and "classes" falls back to the plain slots
+RCD = ("C1", "C3", "C4", "P4", "P4conv")
+CASES = [(r, e) for r in RUNS for e in (("classes", "plain") if r["config"] in RCD else ("classes",))]
 
 
 @pytest.mark.parametrize("run,enc", CASES, ids=[f"{r['key']}-{e}" for r, e in CASES])
@@ -55,7 +58,7 @@ def test_full_size_run_to_verdict(run, enc):
     import full_parity
     ref = GOLD[run["key"]]
     got = full_parity.gpu_run(run, _CACHE, enc)
-    assert (got["row_classes"] is not None) == (enc == "classes" and run["config"] not in ("C2", "C5"))
+    assert (got["row_classes"] is not None) == (enc == "classes" and run["config"] in RCD)
     diff, first = full_parity.compare(ref, got)
     assert not diff, {"differs_in": diff, "first_sampled_diff": first,
                       "gpu": {k: got[k] for k in ("status", "iterations", "relres")},
