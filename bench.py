@@ -215,10 +215,10 @@ def run_reference(args, rank, world):
 def ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` (a short name or its prefix before
     the engine's variant arguments, e.g. pass_kernel<2,1,OpS1) from the committed ncu
-    --set full captures (profiles/r02_ncu_traffic.json: SELL slots; r02_ncu_traffic_v16.json:
+    --set full captures (profiles/r02_ncu_traffic.json: SELL slots; r02_ncu_traffic_rcd.json:
     row-class plans), or None."""
     ks = {}
-    for name in ("r02_ncu_traffic.json", "r02_ncu_traffic_v16.json"):  # SELL slots; row classes
+    for name in ("r02_ncu_traffic.json", "r02_ncu_traffic_rcd.json"):  # SELL slots; row classes
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 ks.update(json.load(f)["kernels"])

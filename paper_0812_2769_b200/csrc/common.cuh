@@ -46,11 +46,30 @@ struct __align__(128) RcdSlots {
   unsigned pad_[15];
 };
 
+// Row-class data of a plan (device-resident; SellView::rcd points at it when the plan's
+// passes read the classes): the class of every row, the class lines and, when all
+// classes share one stencil, the slots and the plan's deltas.
+struct RcdView {
+  const uint16_t* __restrict__ kcls;   // [n]
+  const RcdEntry* __restrict__ kdict;  // [<= RCD_MAXCLS]
+  const RcdSlots* __restrict__ kslots; // [<= RCD_MAXCLS] (null: the deltas differ between classes)
+  int sdel[RCD_MAXL];                  // the plan's ascending deltas (ns of them: 5 or 7)
+  int ns;
+  int sroll;  // 1: sdel[ns/2 + 2] == 256, the same thread's row of the next window
+};
+
+// NOTE: exactly 128 bytes.  With a larger SellView nvcc 12.9 generates different (less
+// unrolled) code for every SELL pass kernel — the plain SpMV went from 0.264 to 0.312 ms
+// at C4 when two pointers were added here — so optional encodings hang off one pointer.
 struct SellView {
   int n;
   int nchunks;
+  int pad;  // column value of padding slots: -1, or INT_MIN in a shard plan, whose
+            // remapped columns may be negative (left halo, DESIGN.md §8)
+  int all_nat;  // every window keeps its natural row order (sell.cu; 0: use roff)
+  int l2pf;  // > 0: a pass prefetches the matrix data of the window l2pf ahead into L2
   const int* __restrict__ cptr;     // [nchunks+1] slot offsets
-  const int* __restrict__ scol;     // [nslots], -1 = padding
+  const int* __restrict__ scol;     // [nslots], pad = padding
   const double* __restrict__ sval;  // [nslots]
   const uint8_t* __restrict__ roff; // [nchunks*32] in-window row offset
   // optional column-index dictionary (null: scol is used): per slot a uint8 index into
@@ -58,29 +77,20 @@ struct SellView {
   const uint8_t* __restrict__ sidx;  // [nslots]
   const int* __restrict__ dptr;      // [nchunks+1]
   const int* __restrict__ dict;      // [ndict]
-  int pad;  // column value of padding slots: -1, or INT_MIN in a shard plan, whose
-            // remapped columns may be negative (left halo, DESIGN.md §8)
   // windows kept in natural row order (sell.cu): wid[w] = 1 when lane l of warp k of
-  // window w holds row 32 k + l; all_nat = every window is (null / 0: use roff)
+  // window w holds row 32 k + l
   const uint8_t* __restrict__ wid;  // [nwindows]
-  int all_nat;
   // optional chunk-uniform column offsets (SELL-U, sell.cu; null: not built): per chunk
   // SELLU_MAXL deltas col - row and lane masks, slot offsets and values of that layout
   const int* __restrict__ uptr;        // [nchunks+1]
   const int* __restrict__ udel;        // [nchunks * SELLU_MAXL]
   const unsigned* __restrict__ umask;  // [nchunks * SELLU_MAXL]
   const double* __restrict__ uval;     // [nuslots]
-  int l2pf;  // > 0: a pass prefetches the matrix data of the window l2pf ahead into L2
   // optional row-class dictionary (RCD, sell.cu; null: not built or inapplicable): the
-  // class of every row and the classes' entries; the passes then read no slot data
-  const uint16_t* __restrict__ kcls;   // [n]
-  const RcdEntry* __restrict__ kdict;  // [<= RCD_MAXCLS]
-  // optional stencil slots of the classes (null: the deltas differ between classes)
-  const RcdSlots* __restrict__ kslots; // [<= RCD_MAXCLS]
-  int sdel[RCD_MAXL];                  // the plan's ascending deltas (ns of them: 5 or 7)
-  int ns;
-  int sroll;  // 1: sdel[ns/2 + 2] == 256, the same thread's row of the next window
+  // passes then read no slot data
+  const RcdView* __restrict__ rcd;
 };
+static_assert(sizeof(SellView) == 128, "SellView must stay 128 bytes (see the note above)");
 
 // Programmatic dependent launch (PDL): every pass / finish kernel waits for the
 // previous kernel's completion (and memory) at entry, then lets the next kernel of the

@@ -176,10 +176,10 @@ __device__ __forceinline__ double csr_window(const CsrView& A, int r0, const G& 
 // vote (-20%) and the +-1 neighbours taken from the adjacent lanes by shuffle (wavefronts
 // -35%, but 3.4x the instructions: issue-bound, -45%).
 template <class G>
-__device__ __forceinline__ double rcd_row(const SellView& A, int row, int cls, const G& g) {
+__device__ __forceinline__ double rcd_row(const RcdView& A, int n, int row, int cls, const G& g) {
   const RcdEntry* e = A.kdict + cls;
   const int2 q0 = __ldg(&e->ld[0]);
-  const int L = row < A.n ? q0.x : 0;
+  const int L = row < n ? q0.x : 0;
   int ds[RCD_MAXL];
   double xs[RCD_MAXL];
   ds[0] = q0.y;
@@ -212,12 +212,12 @@ __device__ __forceinline__ double rcd_row(const SellView& A, int row, int cls, c
 // The values are the same loads of the same memory, the chain is ascending delta = CSR
 // order (AC-3): bit-identical to every other format.
 template <int NS, class G>
-__device__ __forceinline__ double rcd_row_slots(const SellView& A, int row, int cls, const G& g, double own,
+__device__ __forceinline__ double rcd_row_slots(const RcdView& A, int n, int row, int cls, const G& g, double own,
                                                 bool has_lo, double xlo, bool has_hi, double xhi) {
   constexpr int C = NS / 2;
   const int lane = threadIdx.x & 31;
   const RcdSlots* e = A.kslots + cls;
-  const unsigned mask = row < A.n ? __ldg(&e->mask) : 0u;
+  const unsigned mask = row < n ? __ldg(&e->mask) : 0u;
   auto bit = [&](int k) { return ((mask >> k) & 1u) != 0u; };
   double xs[NS];
   const double up = __shfl_up_sync(0xffffffffu, own, 1);
@@ -258,7 +258,8 @@ __device__ __forceinline__ void sell_window_sink(const SellView& A, int r0, cons
     if constexpr (IDX == 3) {  // RCD (row r0 + t)
       static_assert(NAT || IDX != 3, "row-class passes finish row r0 + t");
       const int row = r0 + rl;
-      sink(rl, rcd_row(A, row, row < A.n ? (int)__ldg(A.kcls + row) : 0, g));
+      const RcdView R = *A.rcd;
+      sink(rl, rcd_row(R, A.n, row, row < A.n ? (int)__ldg(R.kcls + row) : 0, g));
       return;
     }
     if constexpr (IDX == 2) {
@@ -352,7 +353,7 @@ __device__ __forceinline__ void sell_prefetch_window(const SellView& A, int r0) 
   const int c0 = r0 >> 5;
   if (c0 >= A.nchunks) return;
   if constexpr (IDX == 3) {  // the window's class ids (512 bytes)
-    prefetch_l2(A.kcls + r0, sizeof(uint16_t) * (size_t)min(TB, A.n - r0));
+    prefetch_l2(A.rcd->kcls + r0, sizeof(uint16_t) * (size_t)min(TB, A.n - r0));
     return;
   }
   const int c1 = min(c0 + TB / SELL_C, A.nchunks);
@@ -542,9 +543,10 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
     // plan's classes share one 7- / 5-delta stencil (rcd_row_slots).
     constexpr int NS = FMT == 6 ? 7 : FMT == 7 ? 5 : 0;
     const int rb = bx * wpc * TB;
-    int kn = rb + t < n ? (int)__ldg(sell.kcls + rb + t) : 0;
+    const RcdView R = *sell.rcd;  // (device-resident: SellView itself must stay 128 bytes)
+    int kn = rb + t < n ? (int)__ldg(R.kcls + rb + t) : 0;
     auto g = [&](int col) { return op.gather(col); };
-    const bool roll = NS > 0 && sell.sroll != 0;
+    const bool roll = NS > 0 && R.sroll != 0;
     double own_prev = 0.0, own_cur = 0.0, own_next = 0.0;
     for (int w = 0; w < wpc; ++w) {
       const int r0 = rb + w * TB;
@@ -556,17 +558,17 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
         const int kc = kn;
         double v[NVA];
         if (i < n) load_vin(op, i, v);
-        kn = (w + 1 < wpc && i + TB < n) ? (int)__ldg(sell.kcls + i + TB) : 0;
+        kn = (w + 1 < wpc && i + TB < n) ? (int)__ldg(R.kcls + i + TB) : 0;
         double y;
         if constexpr (NS > 0) {
           const bool more = w + 1 < wpc && i + TB < n;  // this thread's row of the next window
           if (!roll || w == 0) own_cur = i < n ? g(i) : 0.0;
           if (roll) own_next = more ? g(i + TB) : 0.0;
-          y = rcd_row_slots<NS>(sell, i, kc, g, own_cur, roll && w > 0, own_prev, roll && more, own_next);
+          y = rcd_row_slots<NS>(R, n, i, kc, g, own_cur, roll && w > 0, own_prev, roll && more, own_next);
           own_prev = own_cur;
           own_cur = own_next;
         } else {
-          y = rcd_row(sell, i, kc, g);
+          y = rcd_row(R, n, i, kc, g);
         }
         if (i < n) op.row(i, y, v, cc);
       }

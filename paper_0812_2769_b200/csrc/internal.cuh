@@ -117,6 +117,8 @@ struct gsk_plan {
   gsk::RcdEntry* kdict = nullptr;  // class entries [RCD_MAXCLS]
   void* ktab = nullptr;            // build scratch: hash table + flags (sell.cu)
   gsk::RcdSlots* kslots = nullptr; // stencil slots of the classes [RCD_MAXCLS] (when they share one stencil)
+  gsk::RcdView hrcd{};             // host copy of the row-class view in use (kcls null: not in use)
+  gsk::RcdView* drcd = nullptr;    // its device copy (SellView::rcd)
   int64_t ncls = 0;                // classes in use (0: inapplicable, plain SELL passes)
   int sell_maxlen = 0;      // longest SELL chunk (slots per lane)
   int sell_index = 0;       // 0 plain int32 columns, 1 dictionary (SELL-D), 2 uniform (SELL-U),
@@ -244,9 +246,9 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     ntiles = (windows + wpc - 1) / wpc;
     // natural-order SELL plans (every window unsorted, sell.cu) run the NAT kernels
     const bool nat = P->sell.all_nat != 0;
-    if (P->fmt == GSK_FMT_SELL && P->sell.kcls) {  // row-class dictionary (no slot data)
-      auto k = !P->sell.kslots ? pass_kernel<5, 1, Op, true>
-                               : P->sell.ns == 7 ? pass_kernel<6, 1, Op, true> : pass_kernel<7, 1, Op, true>;
+    if (P->fmt == GSK_FMT_SELL && P->sell.rcd) {  // row-class dictionary (no slot data)
+      auto k = !P->hrcd.kslots ? pass_kernel<5, 1, Op, true>
+                               : P->hrcd.ns == 7 ? pass_kernel<6, 1, Op, true> : pass_kernel<7, 1, Op, true>;
       pass_carveout(k);
       GSK_CUDA(launch_k(k, ntiles, TB, 0, s, P->csr, P->sell, n, wpc, op, P->part, P->pstride, rev));
     } else if (P->fmt == GSK_FMT_SELL && P->sell.uptr) {

@@ -560,7 +560,7 @@ void gsk_plan_destroy(gsk_plan* P) {
     if (g) cudaGraphExecDestroy(g);
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->wid, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
-                  P->cpart, P->uptr, P->udel, P->umask, P->uval, P->kcls, P->kdict, P->ktab, P->kslots};
+                  P->cpart, P->uptr, P->udel, P->umask, P->uval, P->kcls, P->kdict, P->ktab, P->kslots, P->drcd};
   for (void* b : bufs) pool_release(b);  // the plan stream drained above
   if (P->h_flag) cudaFreeHost(P->h_flag);
   for (auto& k : P->pev)
@@ -729,7 +729,7 @@ int gsk_plan_row_classes(gsk_plan* P, int64_t* ncls, uint16_t* cls, void* entrie
     set_error("gsk_plan_row_classes: plan is not an unsharded SELL plan");
     return GSK_E_INVALID;
   }
-  if (!P->sell.kcls) {
+  if (!P->sell.rcd) {
     if (ncls) *ncls = -1;
     return GSK_OK;
   }
@@ -747,10 +747,11 @@ int gsk_plan_class_slots(gsk_plan* P, int32_t* ns, int32_t* deltas, void* slots,
     set_error("gsk_plan_class_slots: plan is not an unsharded SELL plan (or ns is NULL)");
     return GSK_E_INVALID;
   }
-  *ns = P->sell.kslots ? P->sell.ns : -1;
-  if (!P->sell.kslots) return GSK_OK;
+  const bool on = P->sell.rcd && P->hrcd.kslots;
+  *ns = on ? P->hrcd.ns : -1;
+  if (!on) return GSK_OK;
   if (deltas)
-    for (int k = 0; k < RCD_MAXL; ++k) deltas[k] = P->sell.sdel[k];
+    for (int k = 0; k < RCD_MAXL; ++k) deltas[k] = P->hrcd.sdel[k];
   if (slots) {
     cudaStream_t s = as_stream(stream);
     GSK_CUDA(cudaMemcpyAsync(slots, P->kslots, sizeof(RcdSlots) * (size_t)P->ncls, cudaMemcpyDeviceToDevice, s));

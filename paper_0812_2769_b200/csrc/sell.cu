@@ -206,8 +206,16 @@ int sell_build(gsk_plan* P, cudaStream_t s) {
   sell_fill_kernel<<<nwin, TB, 0, s>>>(n, (int)P->nchunks, P->A.row_ptr, P->A.col_idx, P->A.values,
                                        P->cptr, P->roff, P->scol, P->sval, false, P->sell_pad);
   GSK_LAUNCHED(1);
-  P->sell = SellView{n, (int)P->nchunks, P->cptr, P->scol, P->sval, P->roff, nullptr, nullptr, nullptr,
-                     P->sell_pad, P->wid, all_nat};
+  P->sell = SellView{};
+  P->sell.n = n;
+  P->sell.nchunks = (int)P->nchunks;
+  P->sell.pad = P->sell_pad;
+  P->sell.all_nat = all_nat;
+  P->sell.cptr = P->cptr;
+  P->sell.scol = P->scol;
+  P->sell.sval = P->sval;
+  P->sell.roff = P->roff;
+  P->sell.wid = P->wid;
   // L2 prefetch lead in windows (engine.cuh): 1 when the slot data is far larger than
   // L2 (C4: SpMV 0.274 -> 0.266 ms, S3 0.283 -> 0.275 ms), else 0 — with a matrix of
   // 1.5-2x L2 (C3, C5) it cost 3-6% (profiles/r02_experiments); passes with fewer than
@@ -570,8 +578,9 @@ __global__ void __launch_bounds__(TB) rcd_assign_kernel(int n, const int* __rest
 int rcd_build(gsk_plan* P, cudaStream_t s) {
   const int n = P->A.n;
   static_assert(sizeof(RcdEntry) == 128 && sizeof(RcdSlot) == 16, "RCD layouts");
-  const bool had = P->sell.kcls != nullptr;
+  const bool had = P->sell.rcd != nullptr;
   if (!P->kcls) {
+    GSK_CUDA(pool_alloc((void**)&P->drcd, sizeof(RcdView)));
     GSK_CUDA(pool_alloc((void**)&P->kcls, sizeof(uint16_t) * (size_t)n));
     GSK_CUDA(pool_alloc((void**)&P->kdict, sizeof(RcdEntry) * RCD_MAXCLS));
     GSK_CUDA(pool_alloc((void**)&P->ktab, sizeof(RcdSlot) * RCD_HT + 2 * sizeof(int)));
@@ -605,15 +614,13 @@ int rcd_build(gsk_plan* P, cudaStream_t s) {
     ok = hf[0] == 0;
   }
   P->ncls = ok ? ncls : 0;
-  P->sell.kcls = ok ? P->kcls : nullptr;
-  P->sell.kdict = ok ? P->kdict : nullptr;
+  const int had_ns = (had && P->hrcd.kslots) ? P->hrcd.ns : 0;
+  P->hrcd = RcdView{};
+  P->hrcd.kcls = ok ? P->kcls : nullptr;
+  P->hrcd.kdict = ok ? P->kdict : nullptr;
   // stencil slots (engine.cuh rcd_row_slots): the classes' deltas taken together are one
   // symmetric set {.., -1, 0, 1, ..} of 5 or 7 — then a class becomes a presence mask and
   // one value per delta of that set (host work on <= 4096 class lines)
-  const int had_ns = P->sell.kslots ? P->sell.ns : 0;
-  P->sell.kslots = nullptr;
-  P->sell.ns = 0;
-  P->sell.sroll = 0;
   static const bool slots_on = [] {
     const char* e = std::getenv("GSK_RCD_SLOTS");
     return !e || std::atoi(e) != 0;
@@ -645,13 +652,18 @@ int rcd_build(gsk_plan* P, cudaStream_t s) {
       if (!P->kslots) GSK_CUDA(pool_alloc((void**)&P->kslots, sizeof(RcdSlots) * RCD_MAXCLS));
       GSK_CUDA(cudaMemcpyAsync(P->kslots, sl.data(), sizeof(RcdSlots) * ncls, cudaMemcpyHostToDevice, s));
       GSK_CUDA(cudaStreamSynchronize(s));  // sl is a local
-      P->sell.kslots = P->kslots;
-      P->sell.ns = ns;
-      for (int k = 0; k < RCD_MAXL; ++k) P->sell.sdel[k] = k < ns ? U[k] : 0;
-      P->sell.sroll = U[c + 2] == TB ? 1 : 0;
+      P->hrcd.kslots = P->kslots;
+      P->hrcd.ns = ns;
+      for (int k = 0; k < RCD_MAXL; ++k) P->hrcd.sdel[k] = k < ns ? U[k] : 0;
+      P->hrcd.sroll = U[c + 2] == TB ? 1 : 0;
     }
   }
-  if (ok != had || had_ns != P->sell.ns) {  // captured graphs hold the other kernels: capture again
+  if (ok) {
+    GSK_CUDA(cudaMemcpyAsync(P->drcd, &P->hrcd, sizeof(RcdView), cudaMemcpyHostToDevice, s));
+    GSK_CUDA(cudaStreamSynchronize(s));
+  }
+  P->sell.rcd = ok ? P->drcd : nullptr;
+  if (ok != had || had_ns != P->hrcd.ns) {  // captured graphs hold the other kernels: capture again
     P->bkey_b = nullptr;
     P->gkey_b = nullptr;
   }

@@ -594,7 +594,7 @@ int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller) {
 int64_t shard_row_classes(gsk_plan* P) {
   int64_t k = 0;
   for (auto& d : P->shards->sh) {
-    if (!d.sub->sell.kcls) return -1;
+    if (!d.sub->sell.rcd) return -1;
     k = std::max<int64_t>(k, d.sub->ncls);
   }
   return k;
