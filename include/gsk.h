@@ -21,7 +21,7 @@
  *    deterministic and bit-identical run to run.
  *  - Tuning environment (read once per process; none changes any result bit):
  *    GSK_PDL=0 (no programmatic dependent launch), GSK_WPC=1|2|4|8|16 (256-row
- *    windows per CTA of SpMV passes, default 8), GSK_ALT=0 (no alternating CTA
+ *    windows per CTA of SpMV passes, default 8; 16 on row-class plans), GSK_ALT=0 (no alternating CTA
  *    order of consecutive passes), GSK_CARVEOUT=<percent>|-1 (shared-memory
  *    carveout of SELL passes, default 25; -1 = the driver's choice), GSK_L2PF=<n>
  *    (windows of L2 prefetch lead of the SELL slot passes), GSK_RCD_SLOTS=0 (row-

@@ -200,6 +200,16 @@ __device__ __forceinline__ double rcd_row(const RcdView& A, int n, int row, int 
   return acc;
 }
 
+// Ops that gather one vector expose it (gathered()): the row-class passes prefetch it.
+template <class Op, class = void>
+struct OpGathers : std::false_type {};
+template <class Op>
+struct OpGathers<Op, std::void_t<decltype(std::declval<const Op&>().gathered())>> : std::true_type {};
+
+#ifndef GSK_RCD_PF
+#define GSK_RCD_PF 1
+#endif
+
 // Row-class SpMV with stencil slots (RcdSlots: every class's deltas come from the plan's
 // symmetric set sdel[0..NS), centre C = NS / 2 with sdel[C] = 0, sdel[C -+ 1] = -+1): no
 // delta loads, and the gathers that neighbouring threads already hold come from registers
@@ -544,6 +554,27 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
     constexpr int NS = FMT == 6 ? 7 : FMT == 7 ? 5 : 0;
     const int rb = bx * wpc * TB;
     const RcdView R = *sell.rcd;  // (device-resident: SellView itself must stay 128 bytes)
+    // A thread has one row in flight, so its loads that miss L2 (its own rows of the
+    // streamed vectors, the class ids, the far plane first touched by this CTA) would each
+    // cost a DRAM latency per window: thread 0 asks for all of them at once — TMA bulk L2
+    // prefetches of the CTA's whole row block (no registers, nothing to wait for)
+    if (GSK_RCD_PF && t == 0 && rb < n) {
+      const int rows = min(wpc * TB, n - rb);
+      prefetch_l2(R.kcls + rb, sizeof(uint16_t) * (size_t)rows);
+#pragma unroll
+      for (int k = 0; k < Op::NV; ++k)
+        if (op.vin(k)) prefetch_l2(op.vin(k) + rb, sizeof(double) * (size_t)rows);
+      if constexpr (OpGathers<Op>::value) {
+        const double* gx = op.gathered();
+        prefetch_l2(gx + rb, sizeof(double) * (size_t)rows);
+        if constexpr (NS > 0) {
+          const int far = R.sdel[NS - 1];  // the outermost deltas -+far: one of the two
+          // planes is first touched by this CTA (which one depends on the pass direction)
+          if (rb + far < n) prefetch_l2(gx + rb + far, sizeof(double) * (size_t)min(rows, n - rb - far));
+          if (rb - far >= 0) prefetch_l2(gx + rb - far, sizeof(double) * (size_t)rows);
+        }
+      }
+    }
     int kn = rb + t < n ? (int)__ldg(R.kcls + rb + t) : 0;
     auto g = [&](int col) { return op.gather(col); };
     const bool roll = NS > 0 && R.sroll != 0;

@@ -177,7 +177,7 @@ namespace gsk {
 // plan's format (CSR or SELL) or a pure vector pass.
 int num_sms();
 bool pdl_enabled();  // GSK_PDL=0 in the environment disables programmatic launches
-int spmv_wpc_max();
+int spmv_wpc_max(bool rcd = false);
 bool pass_alternate();  // alternate the CTA order of consecutive passes (GSK_ALT=0: off)  // windows per CTA of SpMV passes (8; GSK_WPC overrides, pow2 <= 16)
 
 // Kernel launch with the programmatic-stream-serialization attribute (PDL).
@@ -241,7 +241,8 @@ int launch_pass(gsk_plan* P, const Op& op, cudaStream_t s, int* ntiles_out, cuda
     }
   } else {
     const int windows = (n + TB - 1) / TB;
-    int wpc = spmv_wpc_max();  // windows per CTA: as many as keep >= 3 CTAs per SM busy
+    // windows per CTA: as many as keep >= 3 CTAs per SM busy
+    int wpc = spmv_wpc_max(P->fmt == GSK_FMT_SELL && P->sell.rcd != nullptr);
     while (wpc > 1 && (long long)windows < (long long)wpc * 3 * sms) wpc >>= 1;
     ntiles = (windows + wpc - 1) / wpc;
     // natural-order SELL plans (every window unsorted, sell.cu) run the NAT kernels

@@ -74,14 +74,17 @@ bool pdl_enabled() {
   return on == 1;
 }
 
-int spmv_wpc_max() {
+// rcd: a row-class plan (16 windows per CTA: its passes prefetch the CTA's whole row
+// block at once; measured at C4 / C3 +1.5% over 8, 4 is -5%; the slot kernels are 1.4%
+// slower at 16)
+int spmv_wpc_max(bool rcd) {
   static int w = 0;
   if (!w) {
     const char* e = std::getenv("GSK_WPC");
-    w = e ? std::atoi(e) : 8;
-    if (w != 1 && w != 2 && w != 4 && w != 8 && w != 16) w = 8;
+    w = e ? std::atoi(e) : -1;
+    if (w != 1 && w != 2 && w != 4 && w != 8 && w != 16) w = -1;
   }
-  return w;
+  return w > 0 ? w : (rcd ? 16 : 8);
 }
 
 bool pass_alternate() {
@@ -262,6 +265,7 @@ struct OpSpmv {
   double* y;
   __device__ bool begin() { return true; }
   __device__ const double* vin(int) const { return nullptr; }
+  __device__ const double* gathered() const { return x; }  // the one vector gather() reads
   __device__ double gather(int c) const { return __ldg(x + c); }
   __device__ void row(int i, double v, const double (&)[1], double (&)[1]) const { y[i] = v; }
 };
