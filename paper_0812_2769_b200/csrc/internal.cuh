@@ -208,6 +208,8 @@ bool short_slots_enabled();  // GSK_SHORT=0 disables the <= 5-slot kernels
 void read_fault(int* kind, int* it);  // GSK_FAULT test hook (BicgState)
 // plan workspace cache (plan.cu): pool_alloc / pool_release instead of cudaMalloc /
 // cudaFree for plan-owned buffers; release only what no queued work still uses
+cudaError_t pinned_flags_alloc(int** p);  // a plan's pinned host flags (never freed: plan.cu)
+void pinned_flags_release(int* p);
 cudaError_t pool_alloc(void** p, size_t bytes);
 void pool_release(void* p);
 // per-device "function attributes already set" registry (keyed by any pointer)

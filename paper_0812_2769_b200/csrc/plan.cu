@@ -223,6 +223,35 @@ void pool_release(void* p) {
   g_pool_bytes[key.first] += key.second;
 }
 
+// A plan's pinned host flags (16 ints) come from a process-wide free list and are never
+// returned to the driver: cudaFreeHost was measured at 8-500 ms per plan now and then (it
+// synchronises and unmaps; profiles/r02_e2e_breakdown.txt), the dominant cost of a plan's
+// life cycle in a build / solve / destroy loop.
+static std::mutex g_pin_mu;
+static std::vector<int*> g_pin_free;
+cudaError_t pinned_flags_alloc(int** p) {
+  {
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      *p = g_pin_free.back();
+      g_pin_free.pop_back();
+    } else {
+      *p = nullptr;
+    }
+  }
+  if (!*p) {
+    const cudaError_t e = cudaMallocHost(p, sizeof(int) * 16);
+    if (e != cudaSuccess) return e;
+  }
+  for (int q = 0; q < 16; ++q) (*p)[q] = 0;
+  return cudaSuccess;
+}
+void pinned_flags_release(int* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 void set_pass_carveout(const void* kern) {
   const int pct = smem_carveout();
   if (pct < 0 || device_attr_done(kern)) return;
@@ -249,10 +278,13 @@ int num_sms() {
 int alloc_reduction(gsk_plan* P, cudaStream_t s, bool async) {
   P->pstride = ((P->geo.n + TB - 1) / TB + 7) & ~7;  // multiple of 8: 16-byte aligned rows
   const size_t bytes = sizeof(double) * MAXD * (size_t)P->pstride;
-  if (async)
-    GSK_CUDA(cudaMallocAsync(&P->part, bytes, s));
-  else
-    GSK_CUDA(pool_alloc((void**)&P->part, bytes));
+  // (no stream-ordered allocation anywhere in the library: the default memory pool
+  // returns its memory to the OS at the next synchronisation and maps it again at the next
+  // cudaMallocAsync — measured as random 50-700 ms stalls in a plan build / destroy loop,
+  // profiles/r02_e2e_breakdown.txt; everything comes from the workspace cache instead)
+  (void)s;
+  (void)async;
+  GSK_CUDA(pool_alloc((void**)&P->part, bytes));
   return GSK_OK;
 }
 
@@ -313,8 +345,7 @@ static int plan_alloc_common(gsk_plan* P) {
   GSK_TRY(alloc_reduction(P, nullptr, false));
   GSK_CUDA(pool_alloc((void**)&P->scratch, sizeof(double) * 8));
   GSK_CUDA(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
-  GSK_CUDA(cudaMallocHost(&P->h_flag, sizeof(int) * 16));
-  for (int q = 0; q < 16; ++q) P->h_flag[q] = 0;
+  GSK_CUDA(pinned_flags_alloc(&P->h_flag));
   GSK_CUDA(cudaEventCreate(&P->t0));
   GSK_CUDA(cudaEventCreate(&P->t1));
   for (auto& k : P->pev)
@@ -556,17 +587,25 @@ int gsk_plan_refresh(gsk_plan* P, void* stream) {
 
 void gsk_plan_destroy(gsk_plan* P) {
   if (!P) return;
+  static const bool trace = std::getenv("GSK_TRACE_PLAN") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   if (P->st) cudaStreamSynchronize(P->st);
   if (P->shards) shard_destroy(P->shards);
+  const auto t1 = now();
   for (auto g : P->bgraph)
     if (g) cudaGraphExecDestroy(g);
   for (auto g : P->ggraph)
     if (g) cudaGraphExecDestroy(g);
+  const auto t2 = now();
   void* bufs[] = {P->cptr, P->clen, P->scol, P->sval, P->roff, P->wid, P->part, P->scratch,
                   P->bvec, P->bstate, P->W, P->gstate, P->garr, P->hist_d, P->mpart, P->sidx, P->dptr, P->dict,
                   P->cpart, P->uptr, P->udel, P->umask, P->uval, P->kcls, P->kdict, P->ktab, P->kslots, P->drcd};
   for (void* b : bufs) pool_release(b);  // the plan stream drained above
-  if (P->h_flag) cudaFreeHost(P->h_flag);
+  const auto t3 = now();
+  pinned_flags_release(P->h_flag);
+  const auto t4 = now();
   for (auto& k : P->pev)
     for (auto& e : k) {
       if (e[0]) cudaEventDestroy(e[0]);
@@ -577,6 +616,10 @@ void gsk_plan_destroy(gsk_plan* P) {
   if (P->t0) cudaEventDestroy(P->t0);
   if (P->t1) cudaEventDestroy(P->t1);
   if (P->st) cudaStreamDestroy(P->st);
+  const auto t5 = now();
+  if (trace)
+    std::fprintf(stderr, "[gsk] destroy: sync %.2f ms, graphs %.2f ms, buffers %.2f ms, pinned %.2f ms, events+stream %.2f ms\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
   delete P;
 }
 
@@ -632,15 +675,15 @@ int gsk_dot(int64_t n, const double* a, const double* b, double* result, void* s
   cudaStream_t s = as_stream(stream);
   GSK_TRY(alloc_reduction(&tmp, s, true));
   double* out = nullptr;
-  GSK_CUDA(cudaMallocAsync(&out, sizeof(double), s));
+  GSK_CUDA(pool_alloc((void**)&out, sizeof(double)));
   OpDot op{a, b, out};
   int rc = run_pass(&tmp, op, s) < 0 ? GSK_E_CUDA : GSK_OK;
   double v = 0;
   if (rc == GSK_OK && cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     rc = GSK_E_CUDA;
-  cudaFreeAsync(tmp.part, s);
-  cudaFreeAsync(out, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) rc = GSK_E_CUDA;
+  pool_release(tmp.part);  // the stream drained above
+  pool_release(out);
   *result = v;
   return rc;
 }

@@ -135,15 +135,15 @@ __global__ void __launch_bounds__(SCAN_T) sell_scan_final(int nchunks, const int
 static int sell_scan(int nchunks, const int* clen, int* cptr, int mult, cudaStream_t s, long long* total) {
   const int nb = (nchunks + SCAN_B - 1) / SCAN_B;
   long long* bsum = nullptr;
-  GSK_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (nb + 1), s));
+  GSK_CUDA(pool_alloc((void**)&bsum, sizeof(long long) * (nb + 1)));  // (not cudaMallocAsync: plan.cu)
   sell_scan_sums<<<nb, SCAN_T, 0, s>>>(nchunks, clen, bsum, mult);
   sell_scan_offsets<<<1, SCAN_T, 0, s>>>(nb, bsum);
   sell_scan_final<<<nb, SCAN_T, 0, s>>>(nchunks, clen, bsum, cptr, mult);
   GSK_LAUNCHED(3);
   long long tot = 0;
   GSK_CUDA(cudaMemcpyAsync(&tot, bsum + nb, sizeof tot, cudaMemcpyDeviceToHost, s));
-  GSK_CUDA(cudaFreeAsync(bsum, s));
   GSK_CUDA(cudaStreamSynchronize(s));
+  pool_release(bsum);
   if (total) *total = tot;
   if (tot > INT_MAX) {
     set_error("SELL layout: %lld slots do not fit int32 offsets (limit 2^31 - 1)", tot);

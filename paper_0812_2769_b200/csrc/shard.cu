@@ -207,8 +207,9 @@ void shard_destroy(ShardSet* S) {
   if (!S) return;
   for (auto& s : S->sh) {
     if (s.sub) gsk_plan_destroy(s.sub);
-    for (void* b : {(void*)s.rp, (void*)s.ci, (void*)s.bvec, (void*)s.W, (void*)s.gx})
-      if (b) cudaFree(b);
+    // (the workspace cache, as a plan's buffers: the parent plan's stream was drained by
+    // gsk_plan_destroy before this is called)
+    for (void* b : {(void*)s.rp, (void*)s.ci, (void*)s.bvec, (void*)s.W, (void*)s.gx}) pool_release(b);
   }
   if (S->gath) cudaFree(S->gath);
   if (S->mm) cudaFree(S->mm);
@@ -410,8 +411,8 @@ int shard_bicgstab_run(gsk_plan* P, const double* b, const double* x0, double to
                        double* hist, gsk_report* rep, cudaStream_t caller) {
   ShardSet* S = P->shards;
   for (auto& d : S->sh)
-    if (!d.bvec) GSK_CUDA(cudaMalloc(&d.bvec, sizeof(double) * 7 * d.pitch));
-  if (!P->bstate) GSK_CUDA(cudaMalloc(&P->bstate, sizeof(BicgState)));
+    if (!d.bvec) GSK_CUDA(pool_alloc((void**)&d.bvec, sizeof(double) * 7 * d.pitch));
+  if (!P->bstate) GSK_CUDA(pool_alloc((void**)&P->bstate, sizeof(BicgState)));
   GSK_TRY(ensure_hist(P, maxit));
   int K = P->poll;
   if (K <= 0) K = (int)std::min<long long>(64, std::max<long long>(4, (1LL << 26) / P->A.n));
@@ -499,9 +500,12 @@ int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doubl
   }
   for (auto& d : S->sh) {
     if (d.Wm < m) {
-      if (d.W) GSK_CUDA(cudaFree(d.W));
+      if (d.W) {
+        GSK_CUDA(cudaStreamSynchronize(P->st));  // no queued pass still uses it
+        pool_release(d.W);
+      }
       d.W = nullptr;
-      cudaError_t e = cudaMalloc(&d.W, sizeof(double) * (size_t)(m + 1) * d.pitch);
+      cudaError_t e = pool_alloc((void**)&d.W, sizeof(double) * (size_t)(m + 1) * d.pitch);
       if (e != cudaSuccess) {
         set_error("gmres: cannot allocate a shard's (m+1) x n basis: %s", cudaGetErrorString(e));
         d.Wm = 0;
@@ -514,11 +518,11 @@ int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doubl
           g = nullptr;
         }
     }
-    if (!d.gx) GSK_CUDA(cudaMalloc(&d.gx, sizeof(double) * d.pitch));
+    if (!d.gx) GSK_CUDA(pool_alloc((void**)&d.gx, sizeof(double) * d.pitch));
   }
   const size_t garr = (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8);
-  if (!P->gstate) GSK_CUDA(cudaMalloc(&P->gstate, sizeof(GmresState)));
-  if (!P->garr) GSK_CUDA(cudaMalloc(&P->garr, sizeof(double) * garr));
+  if (!P->gstate) GSK_CUDA(pool_alloc((void**)&P->gstate, sizeof(GmresState)));
+  if (!P->garr) GSK_CUDA(pool_alloc((void**)&P->garr, sizeof(double) * garr));
   GSK_TRY(ensure_hist(P, maxit));
   if (!P->ggraph[0] || P->gkey_b != b || P->gkey_m != m || P->gkey_h != P->hist_d) {
     for (auto& g : P->ggraph)
@@ -579,7 +583,7 @@ struct OpShardSpmv {
 int shard_spmv(gsk_plan* P, const double* x, double* y, cudaStream_t caller) {
   ShardSet* S = P->shards;
   for (auto& d : S->sh)
-    if (!d.bvec) GSK_CUDA(cudaMalloc(&d.bvec, sizeof(double) * 7 * d.pitch));
+    if (!d.bvec) GSK_CUDA(pool_alloc((void**)&d.bvec, sizeof(double) * 7 * d.pitch));
   cudaStream_t s = P->st;
   GSK_TRY(join_in(P, caller));
   GSK_TRY(shard_x_in(P, x, bicg_x, s));
@@ -873,8 +877,8 @@ int gsk_plan_create_sharded(const gsk_csr* A, const gsk_opts* opts, const gsk_sh
     int k01[2];
     if (entry_range(r, k01) != GSK_OK) return fail(GSK_E_CUDA);
     const int64_t nnz = k01[1] - k01[0];
-    if (cudaMalloc(&d.rp, sizeof(int) * (d.n + 1)) != cudaSuccess ||
-        cudaMalloc(&d.ci, sizeof(int) * (nnz > 0 ? nnz : 1)) != cudaSuccess) {
+    if (pool_alloc((void**)&d.rp, sizeof(int) * (d.n + 1)) != cudaSuccess ||
+        pool_alloc((void**)&d.ci, sizeof(int) * (nnz > 0 ? nnz : 1)) != cudaSuccess) {
       set_error("gsk_plan_create_sharded: allocation failed");
       return fail(GSK_E_NOMEM);
     }

@@ -29,7 +29,7 @@ def step(out):
     A = gsk.CSR(dev["row_ptr"], dev["col"], dev["val"])
     As, bs, _ = gsk.gs_scale(A, dev["b"], 2, inplace=True)
     mark("gs")
-    P = gsk.Plan(As, fmt="sell")
+    P = gsk.Plan(As, fmt="sell", sell_index=os.environ.get("GSK_SELL_INDEX", "classes"))
     mark("plan")
     x1, _, r1 = P.bicgstab(bs, tol=1e-8, maxit=10000, hist=False)
     mark("bicgstab")
@@ -44,7 +44,7 @@ def step(out):
 
 
 res = {}
-for _ in range(3):
+for _ in range(int(os.environ.get("E2E_STEPS", "3"))):
     step(res)
 for k, v in res.items():
     print(f"{k:10s} " + " ".join(f"{x:8.1f}" for x in v))
