@@ -27,7 +27,8 @@
  *    (windows of L2 prefetch lead of the SELL slot passes), GSK_RCD_SLOTS=0 (row-
  *    class plans read the class lines, never the stencil slots), GSK_POOL_MB=<MB>
  *    (plan workspace cache, default 32768; 0 = off), GSK_TRACE_PLAN=1 (host time
- *    of the plan-build phases on stderr).
+ *    of the plan-build phases on stderr).  Test hook: GSK_RCD_HASH_BITS=<bits>
+ *    truncates the row-class hash (collisions must end in the plain passes).
  */
 #ifndef GSK_H
 #define GSK_H

@@ -498,14 +498,17 @@ __device__ __forceinline__ unsigned long long rcd_mix(unsigned long long h, unsi
   h = (h ^ x) * 0xff51afd7ed558ccdull;
   return h ^ (h >> 32);
 }
+// kmask: all ones, or fewer bits under the test hook GSK_RCD_HASH_BITS (forces different
+// rows onto one key, which the entry-by-entry comparison of step 3 must catch)
 __device__ __forceinline__ unsigned long long rcd_key(int i, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                      const double* __restrict__ v) {
+                                                      const double* __restrict__ v, unsigned long long kmask) {
   const int a = rp[i], len = rp[i + 1] - a;
   unsigned long long h = rcd_mix(0x9e3779b97f4a7c15ull, (unsigned long long)len);
   for (int q = 0; q < len; ++q) {
     h = rcd_mix(h, (unsigned long long)(long long)(ci[a + q] - i));
     h = rcd_mix(h, (unsigned long long)__double_as_longlong(v[a + q]));
   }
+  h &= kmask;
   return h ? h : 1ull;
 }
 
@@ -516,14 +519,15 @@ __global__ void rcd_init_kernel(RcdSlot* tab, int* flags) {
 }
 
 __global__ void __launch_bounds__(TB) rcd_hash_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                      const double* __restrict__ v, RcdSlot* tab, int* flags) {
+                                                      const double* __restrict__ v, RcdSlot* tab, int* flags,
+                                                      unsigned long long kmask) {
   const int i = blockIdx.x * TB + threadIdx.x;
   if (i >= n) return;
   if (rp[i + 1] - rp[i] > RCD_MAXL) {
     flags[0] = 1;
     return;
   }
-  const unsigned long long key = rcd_key(i, rp, ci, v);
+  const unsigned long long key = rcd_key(i, rp, ci, v, kmask);
   int slot = (int)(key & (RCD_HT - 1));
   for (int probe = 0; probe < RCD_HT; ++probe, slot = (slot + 1) & (RCD_HT - 1)) {
     // a plain look first: almost every row finds its class already there
@@ -546,10 +550,11 @@ __global__ void __launch_bounds__(TB) rcd_hash_kernel(int n, const int* __restri
 
 __global__ void __launch_bounds__(TB) rcd_assign_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                                                         const double* __restrict__ v, const RcdSlot* __restrict__ tab,
-                                                        uint16_t* kcls, RcdEntry* kdict, int* flags) {
+                                                        uint16_t* kcls, RcdEntry* kdict, int* flags,
+                                                        unsigned long long kmask) {
   const int i = blockIdx.x * TB + threadIdx.x;
   if (i >= n) return;
-  const unsigned long long key = rcd_key(i, rp, ci, v);
+  const unsigned long long key = rcd_key(i, rp, ci, v, kmask);
   int slot = (int)(key & (RCD_HT - 1));
   while (tab[slot].key != key) slot = (slot + 1) & (RCD_HT - 1);  // present (step 1)
   const int rep = tab[slot].row, id = tab[slot].id;
@@ -588,8 +593,13 @@ int rcd_build(gsk_plan* P, cudaStream_t s) {
   RcdSlot* tab = reinterpret_cast<RcdSlot*>(P->ktab);
   int* flags = reinterpret_cast<int*>(tab + RCD_HT);
   const int grid = (n + TB - 1) / TB;
+  static const unsigned long long kmask = [] {  // test hook: hash keys of GSK_RCD_HASH_BITS bits
+    const char* e = std::getenv("GSK_RCD_HASH_BITS");
+    const int bits = e ? std::atoi(e) : 64;
+    return bits > 0 && bits < 64 ? (1ull << bits) - 1 : ~0ull;
+  }();
   rcd_init_kernel<<<(RCD_HT + TB - 1) / TB, TB, 0, s>>>(tab, flags);
-  rcd_hash_kernel<<<grid, TB, 0, s>>>(n, P->A.row_ptr, P->A.col_idx, P->A.values, tab, flags);
+  rcd_hash_kernel<<<grid, TB, 0, s>>>(n, P->A.row_ptr, P->A.col_idx, P->A.values, tab, flags, kmask);
   GSK_LAUNCHED(2);
   std::vector<RcdSlot> h(RCD_HT);
   int hf[2] = {0, 0};
@@ -607,7 +617,8 @@ int rcd_build(gsk_plan* P, cudaStream_t s) {
     ncls = (int)used.size();
     for (int k = 0; k < ncls; ++k) h[used[k].second].id = k;
     GSK_CUDA(cudaMemcpyAsync(tab, h.data(), sizeof(RcdSlot) * RCD_HT, cudaMemcpyHostToDevice, s));
-    rcd_assign_kernel<<<grid, TB, 0, s>>>(n, P->A.row_ptr, P->A.col_idx, P->A.values, tab, P->kcls, P->kdict, flags);
+    rcd_assign_kernel<<<grid, TB, 0, s>>>(n, P->A.row_ptr, P->A.col_idx, P->A.values, tab, P->kcls, P->kdict, flags,
+                                          kmask);
     GSK_LAUNCHED(1);
     GSK_CUDA(cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, s));
     GSK_CUDA(cudaStreamSynchronize(s));

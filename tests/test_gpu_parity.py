@@ -862,6 +862,35 @@ def test_class_slots_parity(name, N, ns, roll):
     assert_same_solve(P.gmres(b, m=30, tol=1e-9, maxit=60), oracle.gmres(s["row_ptr"], s["col"], val, b, 30, 1e-9, 60))
 
 
+def test_row_classes_hash_collision_falls_back():
+    """Lossless by construction: with the hash truncated to 3 bits (test hook
+    GSK_RCD_HASH_BITS, read at the first build: a fresh process) different rows share a
+    key, the entry-by-entry comparison with the class's first row catches it, and the plan
+    keeps its SELL slot passes — the SpMV and Bi-CGSTAB still give the oracle's bits."""
+    import subprocess
+    import sys
+    code = """
+import numpy as np, oracle, workloads, paper_0812_2769_b200 as gsk
+s = workloads.generate("C4", N=24)
+val, b, _ = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+A = gsk.CSR(s["row_ptr"], s["col"], val)
+P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph")
+assert oracle.row_classes(s["row_ptr"], s["col"], val) is not None
+assert P.row_classes() is None and P.num_classes() == -1, "collisions must make the format inapplicable"
+x = workloads.uniform(s["n"], 9, 9)
+assert np.array_equal(P.spmv(x).cpu().numpy(), oracle.spmv(s["row_ptr"], s["col"], val, x))
+xg, hg, rg = P.bicgstab(b, tol=1e-9, maxit=60)
+xo, ho, ro = oracle.bicgstab(s["row_ptr"], s["col"], val, b, 1e-9, 60)
+assert np.array_equal(hg, ho) and np.array_equal(xg.cpu().numpy(), xo)
+print("fallback ok")
+"""
+    env = dict(os.environ, GSK_RCD_HASH_BITS="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env["PYTHONPATH"] = root + os.pathsep + env.get("PYTHONPATH", "")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "fallback ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_row_classes_applicability_flips_on_refresh():
     """A refresh that makes the rows distinct (a value per row) drops the plan back to its
     SELL passes, and one that restores repeating rows brings the classes back; the solver
