@@ -410,6 +410,11 @@ def main():
                       "ms_per_launch": p_ms, "launches_per_step": count,
                       "share_of_step": p_ms * count / step_ms_last, "peak_source": src,
                       "frac_of_8TBps": ach / 8000.0})
+    for r in roofs:
+        if r["frac"] > 1.0:  # algorithmic bytes / time above the copy peak: part of them never reach DRAM
+            r["note"] = ("achieved > peak: consecutive passes alternate their row order, so a pass starts on the "
+                         "rows the previous one left in the 126 MB L2 (DESIGN.md §5); compare `traffic` (ncu DRAM "
+                         "bytes per launch) with bytes_per_launch")
     roofs.sort(key=lambda r: -r["share_of_step"])
     roof = roofs[0] if roofs else None
     p1_ms = probes[0]

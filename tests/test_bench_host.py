@@ -62,3 +62,18 @@ def test_roofline_traffic_from_committed_ncu():
     t = bench.ncu_traffic("pass_kernel<2,1,OpS1>")
     alg = bench.byte_model(16777216, 117047296)["bicg_s1"]
     assert t is not None and 0.9 * alg < t < 1.1 * alg
+
+
+def test_byte_model_row_classes_and_traffic():
+    """Row-class plans: the matrix stream of an SpMV pass is the 2-byte class ids (the
+    class lines stay in L1), and the committed ncu capture of the row-class kernels
+    (profiles/r02_ncu_traffic_rcd.json) shows DRAM bytes within 10% of that model for the
+    Bi-CGSTAB passes and the MGS pass — nothing re-read."""
+    n, nnz = 16777216, 117047296
+    bm = bench.byte_model(n, nnz, rcd=True)
+    assert bm["spmv"] == 2 * n + 16 * n and bm["bicg_s1"] == 2 * n + 24 * n
+    assert bm["bicg_iter_split"] == 2 * 2 * n + 19 * 8 * n
+    for name, key in (("pass_kernel<6,1,OpS1>", "bicg_s1"), ("pass_kernel<6,1,OpS3>", "bicg_s3"),
+                      ("pass_kernel<0,8,OpMgs>", "gmres_mgs"), ("pass_kernel<0,4,OpS4>", "bicg_s4")):
+        t = bench.ncu_traffic(name)
+        assert t is not None and 0.9 * bm[key] < t < 1.1 * bm[key], (name, t, bm[key])
