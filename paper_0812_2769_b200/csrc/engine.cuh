@@ -209,6 +209,10 @@ struct OpGathers<Op, std::void_t<decltype(std::declval<const Op&>().gathered())>
 #ifndef GSK_RCD_PF
 #define GSK_RCD_PF 1
 #endif
+#ifndef GSK_RCD_LB
+#define GSK_RCD_LB 1
+#endif
+constexpr int RCD_LB = GSK_RCD_LB;  // windows whose dot-product leaves are reduced together (1, 2, 4)
 
 // Row-class SpMV with stencil slots (RcdSlots: every class's deltas come from the plan's
 // symmetric set sdel[0..NS), centre C = NS / 2 with sdel[C] = 0, sdel[C -+ 1] = -+1): no
@@ -579,9 +583,9 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
     auto g = [&](int col) { return op.gather(col); };
     const bool roll = NS > 0 && R.sroll != 0;
     double own_prev = 0.0, own_cur = 0.0, own_next = 0.0;
-    for (int w = 0; w < wpc; ++w) {
+    // one window: y of row r0 + t, the Op's row epilogue, the dot-product leaves in cc
+    auto window = [&](int w, double (&cc)[DD]) {
       const int r0 = rb + w * TB;
-      double cc[DD];
 #pragma unroll
       for (int d = 0; d < DD; ++d) cc[d] = 0.0;
       if (r0 < n) {  // uniform over the CTA
@@ -603,7 +607,22 @@ __global__ void __launch_bounds__(TB, PassOcc<FMT, Op, MAXL>::kMinBlocks)
         }
         if (i < n) op.row(i, y, v, cc);
       }
-      if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);
+    };
+    if (D > 0 && RCD_LB > 1 && wpc >= RCD_LB) {
+      // the leaves of RCD_LB windows are reduced together: one reduce-scatter (K/2 + K/4 +
+      // ... shuffles instead of 5 per value) and one dependent chain per RCD_LB windows
+      for (int w0 = 0; w0 < wpc; w0 += RCD_LB) {
+        double cb[RCD_LB][DD];
+#pragma unroll
+        for (int j = 0; j < RCD_LB; ++j) window(w0 + j, cb[j]);
+        if constexpr (D > 0) warp_leaves_multi<RCD_LB, DD>(cb, sm.wp + (size_t)w0 * MAXD * 8);
+      }
+    } else {
+      for (int w = 0; w < wpc; ++w) {
+        double cc[DD];
+        window(w, cc);
+        if constexpr (D > 0) warp_leaves<D>(cc, sm.wp, w);
+      }
     }
     if constexpr (D > 0) {
       __syncthreads();
