@@ -212,6 +212,9 @@ struct OpGathers<Op, std::void_t<decltype(std::declval<const Op&>().gathered())>
 #ifndef GSK_RCD_LB
 #define GSK_RCD_LB 1
 #endif
+#ifndef GSK_RCD_EXP
+#define GSK_RCD_EXP 0  // timing probes of the stencil-slot row code (1, 2: wrong results; never in a build)
+#endif
 constexpr int RCD_LB = GSK_RCD_LB;  // windows whose dot-product leaves are reduced together (1, 2, 4)
 
 // Row-class SpMV with stencil slots (RcdSlots: every class's deltas come from the plan's
@@ -242,13 +245,22 @@ __device__ __forceinline__ double rcd_row_slots(const RcdView& A, int n, int row
   xs[C - 2] = has_lo ? xlo : (bit(C - 2) ? g(row + A.sdel[C - 2]) : 0.0);
   xs[C + 2] = has_hi ? xhi : (bit(C + 2) ? g(row + A.sdel[C + 2]) : 0.0);
   if constexpr (NS == 7) {
+#if GSK_RCD_EXP == 1  // timing probe only (wrong results): no far-plane gathers
+    xs[0] = own;
+    xs[6] = own;
+#else
     xs[0] = bit(0) ? g(row + A.sdel[0]) : 0.0;
     xs[6] = bit(6) ? g(row + A.sdel[6]) : 0.0;
+#endif
   }
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
+#if GSK_RCD_EXP == 2  // timing probe only (wrong results): no class-value loads
+    const double a = 1.0 + k;
+#else
     const double a = __ldg(&e->v[k]);
+#endif
     if (bit(k)) acc = __fma_rn(a, xs[k], acc);
   }
   return acc;
