@@ -822,6 +822,29 @@ def _banded_system(n, deltas, seed):
     return np.array(rp, np.int32), np.array(cols, np.int32), np.array(vals), b
 
 
+def test_row_classes_with_empty_rows():
+    """Empty rows form a class of length 0 (y = +0.0 there, as in CSR); the other rows of
+    these 5- / 7-point Laplacians keep the plan's stencil slots."""
+    for name, N in (("lap2d", 40), ("lap3d", 12)):
+        s = workloads.generate(name, N=N)
+        rp, col, val = s["row_ptr"], s["col"], s["val"]
+        keep = np.ones(len(col), bool)
+        for r in range(3, s["n"], 37):
+            keep[rp[r]:rp[r + 1]] = False
+        ln = np.add.reduceat(keep.astype(np.int64), rp[:-1])
+        rp2 = np.concatenate([[0], np.cumsum(ln)]).astype(np.int32)
+        col2, val2 = col[keep], val[keep]
+        A = gsk.CSR(rp2, col2, val2)
+        P = gsk.Plan(A, fmt="sell", sell_index="classes", engine="graph")
+        o = oracle.row_classes(rp2, col2, val2)
+        g = P.row_classes()
+        assert g is not None and np.array_equal(g["cls"], o["cls"]) and 0 in list(o["len"])
+        x = workloads.uniform(s["n"], 9, 9)
+        y = cpu(P.spmv(x))
+        assert np.array_equal(y, oracle.spmv(rp2, col2, val2, x))
+        assert not np.signbit(y[3]) and y[3] == 0.0
+
+
 def test_row_classes_without_stencil_slots():
     """Classes whose deltas are no symmetric 5- / 7-point set (here {-3, 0, 1, 7}) run the
     generic class-line kernels (no stencil slots): SpMV and both solvers == the oracle."""
