@@ -75,6 +75,9 @@ def _lib():
         lib.orc_gmres_orth.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, d, i32, i32, vp, vp,
                                        ctypes.POINTER(Report)]
         lib.orc_gmres_orth.restype = i32
+        lib.orc_gmres_wstop.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, d, i32, i32, i32, vp, vp,
+                                        ctypes.POINTER(Report)]
+        lib.orc_gmres_wstop.restype = i32
         _LIB = lib
     return _LIB
 
@@ -258,18 +261,19 @@ def bicgstab(row_ptr, col, val, b, tol, maxit, x0=None, weights=None):
     return x, hist[:rep.history_len].copy(), rep.as_dict()
 
 
-def gmres(row_ptr, col, val, b, m, tol, maxit, x0=None, weights=None, orth="mgs"):
+def gmres(row_ptr, col, val, b, m, tol, maxit, x0=None, weights=None, orth="mgs", wstop=False):
     """Returns (x, hist, report-dict).  orth: "mgs" (north star) or "cgs2" (AZTEC's
-    double classical Gram-Schmidt)."""
+    double classical Gram-Schmidt).  wstop: stop on the weighted true
+    residual at cycle ends instead of the least-squares estimate (reading B2w)."""
     row_ptr, col, val, b = _i32(row_ptr), _i32(col), _f64(val), _f64(b)
     x0, w = _f64(x0), _f64(weights)
     n = row_ptr.size - 1
     x = np.empty(n, np.float64)
     hist = np.empty(maxit + 1, np.float64)
     rep = Report()
-    rc = _lib().orc_gmres_orth(n, _p(row_ptr), _p(col), _p(val), _p(b), _p(x0), _p(w), int(m),
-                               float(tol), int(maxit), {"mgs": 0, "cgs2": 1}[orth], _p(x), _p(hist),
-                               ctypes.byref(rep))
+    rc = _lib().orc_gmres_wstop(n, _p(row_ptr), _p(col), _p(val), _p(b), _p(x0), _p(w), int(m),
+                                float(tol), int(maxit), {"mgs": 0, "cgs2": 1}[orth], int(bool(wstop)),
+                                _p(x), _p(hist), ctypes.byref(rep))
     if rc != 0:
         raise ValueError("bad arguments")
     return x, hist[:rep.history_len].copy(), rep.as_dict()

@@ -500,6 +500,9 @@ int orc_bicgstab(int64_t n, const int32_t* rp, const int32_t* ci, const double* 
 int orc_gmres_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
                    const double* b, const double* x0, const double* w, int m, double tol, int maxit,
                    int orth, double* x, double* hist, orc_report* rep);
+int orc_gmres_wstop(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+                    const double* b, const double* x0, const double* w, int m, double tol, int maxit,
+                    int orth, int wstop, double* x, double* hist, orc_report* rep);
 
 int orc_gmres(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
               const double* b, const double* x0, const double* w, int m, double tol, int maxit,
@@ -510,6 +513,19 @@ int orc_gmres(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
 int orc_gmres_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
                    const double* b, const double* x0, const double* w, int m, double tol, int maxit,
                    int orth, double* x, double* hist, orc_report* rep) {
+  return orc_gmres_wstop(n, rp, ci, v, b, x0, w, m, tol, maxit, orth, 0, x, hist, rep);
+}
+
+// wstop = 1 (reading B2w): the paper measured the relative residual "always"
+// on the GS(2)-scaled system.  GMRES's per-step residual is the
+// least-squares estimate, which exists only in the frame of the system solved, so with
+// frame weights w the stopping test moves to where a residual vector exists: the estimate
+// no longer stops the run, and at the end of every cycle (after x += V y and r = b - A x,
+// which the restart computes anyway) the run is CONVERGED when ||w o r|| / ||w o r_0|| <
+// tol.  The history keeps the per-step estimates.  wstop = 0: the estimate stops (B1/B2).
+int orc_gmres_wstop(int64_t n, const int32_t* rp, const int32_t* ci, const double* v,
+                    const double* b, const double* x0, const double* w, int m, double tol, int maxit,
+                    int orth, int wstop, double* x, double* hist, orc_report* rep) {
   if (orth != 0 && orth != 1) return -1;
   if (n < 1 || maxit < 1 || m < 1 || !(tol > 0)) return -1;
   std::vector<double> r(n), ax(n), wv(n);
@@ -572,7 +588,7 @@ int orc_gmres_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double
       H.push_back(rel);
       k = j + 1;
       if (!std::isfinite(rel)) { stop_div = true; break; }
-      if (rel < tol) { stop_conv = true; break; }
+      if (rel < tol && !wstop) { stop_conv = true; break; }
       if (hn == 0.0 || it == maxit) break;
       double invh = 1.0 / hn;
       for (int64_t q = 0; q < n; ++q) V[j + 1][q] = wv[q] * invh;
@@ -591,6 +607,12 @@ int orc_gmres_orth(int64_t n, const int32_t* rp, const int32_t* ci, const double
     bool fin = true;
     for (int kk = 0; kk < k; ++kk) fin = fin && std::isfinite(y[kk]);
     if (!fin) { status = 3; break; }
+    if (wstop) {  // the weighted true residual of the cycle's end
+      const double twc = std::sqrt(orc_wnorm2(n, r.data(), w));
+      const double relw = n0w == 0.0 ? 0.0 : twc / n0w;
+      if (!std::isfinite(relw)) { status = 3; break; }
+      if (relw < tol) stop_conv = true;
+    }
     if (stop_conv) { status = 0; break; }
     if (it >= maxit) { status = 1; break; }
     ++restarts;

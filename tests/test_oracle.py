@@ -683,3 +683,55 @@ def test_row_classes_constructed_and_inapplicable():
     assert oracle.row_classes(np.array(rp), np.array(cols), np.array(vals), maxlen=4, maxcls=3) is None
     s = workloads.generate("C2", N=96)
     assert oracle.row_classes(s["row_ptr"], s["col"], s["val"]) is None
+
+
+def test_gmres_weighted_stop_at_cycle_ends():
+    """Reading B2w (the relative residual "always" measured on the
+    GS(2)-scaled system): with wstop the least-squares estimate no longer stops GMRES; the
+    run ends CONVERGED at the first cycle end whose weighted TRUE residual is below tol.
+    Pinned independently of the oracle's own stopping code: cycle ends are found by running
+    the plain solver with maxit = k m (iterates do not depend on tol or maxit, B11) and
+    the weighted residual of each is recomputed with numpy."""
+    s = workloads.generate("C1")
+    rp, col, val, b = s["row_ptr"], s["col"], s["val"], s["b"]
+    v1, b1, d1 = oracle.gs_scale(rp, val, b, 1)
+    _, _, d2 = oracle.gs_scale(rp, val, b, 2)
+    w = d2 / d1  # GS(2) frame of the GS(1)-scaled system
+    m, tol = 20, 1e-4
+    A = np.zeros((s["n"], s["n"]))
+    for i in range(s["n"]):
+        A[i, col[rp[i]:rp[i + 1]]] = v1[rp[i]:rp[i + 1]]
+    n0w = np.linalg.norm(w * b1)
+    first = None
+    for k in range(1, 8):
+        xk, hk, rk = oracle.gmres(rp, col, v1, b1, m, 1e-300, k * m)
+        if np.linalg.norm(w * (b1 - A @ xk)) / n0w < tol:
+            first = k
+            break
+    assert first is not None and first > 1
+    x, h, r = oracle.gmres(rp, col, v1, b1, m, tol, 2000, weights=w, wstop=True)
+    assert r["status"] == 0 and r["iterations"] == first * m and r["restarts"] == first - 1
+    assert np.array_equal(x, xk) and np.array_equal(h, hk)  # the same iterates and estimates
+    assert r["true_relres_w"] < tol
+    assert abs(r["true_relres_w"] - np.linalg.norm(w * (b1 - A @ x)) / n0w) <= 1e-12 * r["true_relres_w"] + 1e-18
+    # the estimate alone stops earlier, mid-cycle (B1), and its history is a prefix
+    x0, h0, r0 = oracle.gmres(rp, col, v1, b1, m, tol, 2000, weights=w)
+    assert r0["status"] == 0 and r0["iterations"] < r["iterations"] and r0["iterations"] % m != 0
+    assert np.array_equal(h0, h[:len(h0)])
+    # without weights wstop tests the plain true residual at cycle ends
+    xu, hu, ru = oracle.gmres(rp, col, v1, b1, m, tol, 2000, wstop=True)
+    assert ru["status"] == 0 and ru["iterations"] % m == 0 and ru["true_relres"] < tol
+
+
+def test_gmres_weighted_stop_refuses_the_unscaled_estimate():
+    """The advisor's case: unscaled C1, tol 1e-3.  The least-squares estimate (unscaled
+    frame) crosses tol at step 19 while the GS(2)-frame residual is still 0.84; with wstop
+    the run is not CONVERGED (MAXIT, GS(2)-frame residual >= tol)."""
+    s = workloads.generate("C1")
+    rp, col, val, b = s["row_ptr"], s["col"], s["val"], s["b"]
+    _, _, d2 = oracle.gs_scale(rp, val, b, 2)
+    _, _, r0 = oracle.gmres(rp, col, val, b, 20, 1e-3, 600, weights=d2)
+    assert r0["status"] == 0 and r0["iterations"] == 19 and r0["true_relres_w"] > 0.5
+    _, h, r = oracle.gmres(rp, col, val, b, 20, 1e-3, 600, weights=d2, wstop=True)
+    assert r["status"] == 1 and r["iterations"] == 600 and r["true_relres_w"] >= 1e-3
+    assert h.min() < 1e-3  # the estimate did cross
