@@ -79,11 +79,12 @@ typedef struct gsk_report {
  * weights: NULL, or DEVICE [n] w_i > 0.  When set, Bi-CGSTAB's stopping test and
  * history use ||w o r|| / ||w o r0|| — the paper measures the relative residual on
  * the GS(2)-scaled system, i.e. w = d_GS(2) / d_applied.
- * GMRES does NOT stop in the weighted frame: its per-step residual is the
- * least-squares estimate |g_{j+1}|, which exists only in the solved frame (the
- * weighted norm of r_j = V_{j+1} Q^T e_{j+1} g_{j+1} would cost a pass over the basis
- * per step), so GMRES stops and records history in the solved frame and the weights
- * enter only the reported true_relres_w (reading B2).
+ * GMRES's per-step residual is the least-squares estimate |g_{j+1}|, which exists only
+ * in the solved frame (the weighted norm of r_j = V_{j+1} Q^T e_{j+1} g_{j+1} would
+ * cost a pass over the basis per step), so by default GMRES stops and records history
+ * in the solved frame and the weights enter only the reported true_relres_w (DESIGN.md
+ * reading B2); gmres_wstop = 1 moves its stopping test to the weighted true residual
+ * at cycle ends (reading B2w).
  * poll: iterations per device-resident batch between host checks (0 = auto). */
 typedef struct gsk_opts {
   int32_t format;
@@ -117,6 +118,16 @@ typedef struct gsk_opts {
                            plain-column SELL or CSR; else the passes); GSK_ENGINE_SMALL = the one-CTA solver
                            whenever n <= GSK_SMALL_NMAX; GSK_ENGINE_CLUSTER = the cluster
                            solver whenever it fits. */
+  int32_t gmres_wstop;  /* 0 (default): GMRES stops when its least-squares estimate, which
+                           exists only in the frame of the system solved, is below tol
+                           (the weights then enter only true_relres_w).  1: the paper's
+                           protocol for GMRES too (reading B2w) — the
+                           estimate no longer stops the run; at the end of every restart
+                           cycle (and at maxit) the run is CONVERGED when the TRUE residual
+                           ||w o (b - A x)|| / ||w o (b - A x0)|| is below tol (w = the
+                           plan's weights, or 1), so iteration counts are multiples of m;
+                           the history keeps the per-step estimates. */
+  int32_t pad_;
 } gsk_opts;
 
 enum { GSK_ENGINE_AUTO = 0, GSK_ENGINE_GRAPH = 1, GSK_ENGINE_COOP = 2, GSK_ENGINE_SMALL = 3,

@@ -52,7 +52,8 @@ class Report(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("poll", ctypes.c_int32), ("weights", ctypes.c_void_p),
                 ("bicg_schedule", ctypes.c_int32), ("gmres_orth", ctypes.c_int32),
-                ("sell_index", ctypes.c_int32), ("engine", ctypes.c_int32)]
+                ("sell_index", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("gmres_wstop", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class ShardOpts(ctypes.Structure):
@@ -262,7 +263,7 @@ class Plan:
     """gsk_plan: SELL build, workspace and captured graphs reused across solves."""
 
     def __init__(self, A: CSR, fmt: str = "csr", weights=None, poll: int = 0, schedule: str = "auto",
-                 orth: str = "mgs", sell_index: str = "plain", engine: str = "auto"):
+                 orth: str = "mgs", sell_index: str = "plain", engine: str = "auto", gmres_wstop: bool = False):
         """engine: "auto" (one launch per solve on one CTA up to 2048 / 1024 rows or on
         one thread-block cluster up to 32768 / 65536 rows for Bi-CGSTAB / GMRES, or a
         persistent cooperative grid up to 81920 rows for Bi-CGSTAB, where measured
@@ -273,7 +274,8 @@ class Plan:
         self.A = A
         self.weights = _dev_f64(weights, A.n)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
-                    SCHEDULE[schedule], ORTH[orth], SELL_INDEX[sell_index], ENGINE[engine])
+                    SCHEDULE[schedule], ORTH[orth], SELL_INDEX[sell_index], ENGINE[engine],
+                    int(bool(gmres_wstop)), 0)
         self._csr = A.struct()
         h = ctypes.c_void_p()
         _check(lib.gsk_plan_create(ctypes.byref(self._csr), ctypes.byref(opts), ctypes.byref(h), _stream()))
@@ -497,7 +499,7 @@ class ShardedPlan(Plan):
 
     def __init__(self, A: CSR, shards: int = 2, fmt: str = "csr", weights=None, poll: int = 0,
                  comm: "NcclComm" = None, n_global: int = None, sell_index: str = "plain",
-                 peer_reduce: bool = False):
+                 peer_reduce: bool = False, gmres_wstop: bool = False):
         lib = load()
         self.A = A
         if comm is None:
@@ -516,7 +518,7 @@ class ShardedPlan(Plan):
         self.weights = _dev_f64(weights, self.nloc)
         opts = Opts(FMT[fmt], int(poll), None if self.weights is None else self.weights.data_ptr(),
                     SCHEDULE["split"], ORTH["mgs"], SELL_INDEX[sell_index],
-                    ENGINE["graph"])
+                    ENGINE["graph"], int(bool(gmres_wstop)), 0)
         so = ShardOpts(int(shards), int(first), int(count), int(n_global is not None), ch, int(peer_reduce), 0)
         self._csr = A.struct()
         self._csr.n = ng

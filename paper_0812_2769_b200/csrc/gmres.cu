@@ -190,6 +190,7 @@ static int gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doub
   h.tol = tol;
   h.maxit = maxit;
   h.m = m;
+  h.wstop = P->wstop;
   GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * (size_t)((MAX_M + 1) * MAX_M + 7 * MAX_M + 8), s));
   GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   int cused = 0;

@@ -48,12 +48,28 @@ struct OpGResid {
         return;
       }
     } else if (st->final_) {
-      st->status = st->diverged ? GSK_DIVERGED : (st->conv ? GSK_CONVERGED : GSK_MAXIT);
+      const double relw = st->n0w == 0.0 ? 0.0 : sqrt(s[1]) / st->n0w;
+      int conv = st->conv, div = st->diverged;
+      if (st->wstop && !div) {  // reading B2w: the weighted true residual decides
+        div = !isfinite(relw);
+        conv = relw < st->tol;
+      }
+      st->status = div ? GSK_DIVERGED : (conv ? GSK_CONVERGED : GSK_MAXIT);
       st->true_rel = beta / st->beta0;
-      st->true_rel_w = st->n0w == 0.0 ? 0.0 : sqrt(s[1]) / st->n0w;
+      st->true_rel_w = relw;
       st->done = 1;
       return;
     } else {
+      if (st->wstop) {  // a cycle's end: CONVERGED when ||w o r|| / ||w o r_0|| < tol (B2w)
+        const double relw = st->n0w == 0.0 ? 0.0 : sqrt(s[1]) / st->n0w;
+        if (!isfinite(relw) || relw < st->tol) {
+          st->status = isfinite(relw) ? GSK_CONVERGED : GSK_DIVERGED;
+          st->true_rel = beta / st->beta0;
+          st->true_rel_w = relw;
+          st->done = 1;
+          return;
+        }
+      }
       st->restarts += 1;
     }
     st->inv[1] = 1.0 / beta;
@@ -188,7 +204,7 @@ static __device__ void arnoldi_finish(GmresState* S, double* hist, int j, double
       S->skip_x = 1;
       S->final_ = 1;
       stop = 1;
-    } else if (rel < S->tol) {
+    } else if (rel < S->tol && !S->wstop) {  // (wstop: the estimate does not stop the run)
       S->conv = 1;
       S->final_ = 1;
       stop = 1;

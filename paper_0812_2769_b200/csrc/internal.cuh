@@ -77,7 +77,8 @@ struct GmresState {
   double *H, *cs, *sn, *g, *y, *inv;
   double *c1, *c2;  // CGS2: the two classical projections of the current step
   int it, maxit, m, k, cycle_stop, final_, conv, diverged, skip_x, done, status, restarts,
-      hist_len, pad;
+      hist_len;
+  int wstop;  // gsk_opts.gmres_wstop: stop on the weighted true residual at cycle ends
 };
 
 cudaStream_t as_stream(void* s);
@@ -92,6 +93,7 @@ struct gsk_plan {
   int poll = 0;
   int bmode = 2;  // Bi-CGSTAB schedule: 1 fused, 2 split
   int orth = 0;   // GMRES orthogonalisation: 0 MGS, 1 double classical Gram-Schmidt
+  int wstop = 0;  // GMRES stops on the weighted true residual at cycle ends (gsk_opts.gmres_wstop)
   const double* weights = nullptr;
   gsk::Geometry geo;
   gsk::CsrView csr{};

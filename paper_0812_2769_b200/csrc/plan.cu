@@ -527,6 +527,7 @@ int plan_create_impl(const gsk_csr* A, const gsk_opts* opts, int sell_pad, gsk_p
   }
   P->orth = orth;
   P->sell_index = opts ? opts->sell_index : 0;
+  P->wstop = (opts && opts->gmres_wstop) ? 1 : 0;
   P->engine = opts ? opts->engine : GSK_ENGINE_AUTO;
   if (P->engine < GSK_ENGINE_AUTO || P->engine > GSK_ENGINE_CLUSTER) {
     delete P;

@@ -552,6 +552,7 @@ int shard_gmres_run(gsk_plan* P, const double* b, const double* x0, int m, doubl
   h.tol = tol;
   h.maxit = maxit;
   h.m = m;
+  h.wstop = P->wstop;
   GSK_CUDA(cudaMemsetAsync(P->garr, 0, sizeof(double) * garr, s));
   GSK_CUDA(cudaMemcpyAsync(P->gstate, &h, sizeof h, cudaMemcpyHostToDevice, s));
   auto Bv = [&](int i) { return b + (S->sh[i].lo - S->rows0); };

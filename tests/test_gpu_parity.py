@@ -968,6 +968,39 @@ def test_row_classes_solvers(name, N, scal):
         assert_same_solve(SP.gmres(b, m=30, tol=1e-9, maxit=90), og)
 
 
+@pytest.mark.parametrize("name,N,scal,m,tol", [("C1", None, 1, 20, 1e-4), ("C1", None, "none", 20, 1e-3),
+                                               ("C3", 20, 1, 30, 1e-6), ("C4", 24, "none", 30, 1e-5),
+                                               ("C2", 100, 1, 30, 1e-6), ("C4", 40, 2, 10, 1e-7)])
+def test_gmres_weighted_stop_parity(name, N, scal, m, tol):
+    """gsk_opts.gmres_wstop (reading B2w): GMRES stopping on the GS(2)-frame
+    true residual at cycle ends == the oracle's orc_gmres_wstop bit for bit (verdict,
+    iteration count, history, x, both true residuals) — on every engine that runs the size
+    (graph passes on CSR / SELL slots / row classes, the one-CTA and cluster solvers via
+    engine auto, CGS2, sharded), with and without weights."""
+    s, val, b, dp = system(name, N, scal)
+    _, _, d2 = oracle.gs_scale(s["row_ptr"], s["val"], s["b"], 2)
+    w = None if scal == 2 else (d2 if dp is None else d2 / dp)
+    A = gsk.CSR(s["row_ptr"], s["col"], val)
+    maxit = 12 * m
+    o = oracle.gmres(s["row_ptr"], s["col"], val, b, m, tol, maxit, weights=w, wstop=True)
+    assert o[2]["iterations"] % m == 0 or o[2]["status"] != 0
+    for kw in (dict(fmt="csr", engine="graph"), dict(fmt="sell", engine="graph"),
+               dict(fmt="sell", engine="graph", sell_index="classes"), dict(fmt="csr"), dict(fmt="sell")):
+        P = gsk.Plan(A, weights=w, gmres_wstop=True, **kw)
+        assert_same_solve(P.gmres(b, m=m, tol=tol, maxit=maxit), o)
+        P.close()
+    P = gsk.Plan(A, fmt="sell", engine="graph", orth="cgs2", weights=w, gmres_wstop=True)
+    assert_same_solve(P.gmres(b, m=m, tol=tol, maxit=maxit),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, m, tol, maxit, weights=w, orth="cgs2", wstop=True))
+    if s["n"] >= 4096:
+        SP = gsk.ShardedPlan(A, shards=2, fmt="sell", weights=w, gmres_wstop=True)
+        assert_same_solve(SP.gmres(b, m=m, tol=tol, maxit=maxit), o)
+    # the default (estimate-stopped) runs are untouched by the option's existence
+    P = gsk.Plan(A, fmt="sell", engine="graph", weights=w)
+    assert_same_solve(P.gmres(b, m=m, tol=tol, maxit=maxit),
+                      oracle.gmres(s["row_ptr"], s["col"], val, b, m, tol, maxit, weights=w))
+
+
 def test_sharded_nccl_single_rank():
     """The multi-process code path (halo send/recv groups, ncclAllGather of the shard
     values, all inside the captured graphs) on a 1-rank NCCL communicator: bit-exact."""
