@@ -16,7 +16,12 @@
 //                 of 8 warps and the tree over the CTA's windows, and writes ONE
 //                 partial per CTA.  No fences, no atomics: the CTA ends as soon as its
 //                 stores are issued.  SpMV passes prefetch the next window's own-row
-//                 operands into shared memory with cp.async.
+//                 operands into shared memory with cp.async.  Row-class plans (FMT 5:
+//                 class lines; 6 / 7: stencil slots of 7 / 5 deltas; sell.cu) read a
+//                 uint16 class id per row instead of the slot data: thread t finishes
+//                 row r0 + t of every window, +-1 entries come from the adjacent lanes,
+//                 +-256 ones from the thread's own rows of the neighbouring windows, and
+//                 thread 0 bulk-prefetches the CTA's whole row block into L2.
 //   finish_kernel one CTA of 1024 threads reduces the CTA partials with the same
 //                 canonical tree (AC-5) and runs the Op's scalar
 //                 epilogue (alpha, omega, Givens, stopping tests, ...) on the device.
@@ -536,7 +541,8 @@ __device__ __forceinline__ void cta_partial(const double* wp, int nw, double* pa
 }
 
 // FMT 0: vector pass, RPT windows (rows r0 + 256 w + t) per CTA, all loads in flight.
-// FMT 1/2/3: SpMV pass over wpc windows (CSR, SELL, SELL with column dictionary).
+// FMT 1/2/3/4: SpMV pass over wpc windows (CSR, SELL, SELL-D, SELL-U); FMT 5/6/7: over the
+// plan's row classes (class lines / stencil slots of 7 / 5 deltas).
 // NAT (SELL only): every window of the plan keeps its natural row order (sell.cu), so
 // thread t computes row r0 + t itself — no roff, no scatter, no per-window barrier.
 // A compile-time choice: one code path per kernel keeps the 64-register budget.
