@@ -254,6 +254,8 @@ def reduce_over_ranks(ms, its, dist, device):
 
 
 def config_desc(args, cfg, s, ncls=None):
+    """The `config` object — the same in both arms (it depends on the arguments and the
+    workload only; what the plan detected is in extra.encoding)."""
     N = cfg.N if args.N is None else args.N
     if cfg.name == "C4w":
         G = int(s["n"]) // N ** 3
@@ -261,19 +263,19 @@ def config_desc(args, cfg, s, ncls=None):
                     f"medium per GPU; weak scaling, DESIGN.md §8)", f"{N}x{N}x{N * G}")
     else:
         wl, grid = f"{cfg.name}: BASELINE.json configs[{int(cfg.name[1]) - 1}]", f"{N}^{3 if cfg.cfg in (3, 4) else 2}"
-    return {"workload": wl, "n": int(s["n"]), "nnz": int(s["nnz"]), "grid": grid,
-            "format": ("SELL-C-32-256" if getattr(args, "fmt", "sell") == "sell" else "CSR")
-            + " (built on the device from the CSR input)"
-            + (f"; passes read the plan's row-class dictionary ({ncls} classes: a uint16 class id per row + "
-               "128-byte class lines instead of the slot data; lossless, bit-identical results; DESIGN.md §5)"
-               if ncls else ""), "scaling": "GS(2)",
+    sell = getattr(args, "fmt", "sell") == "sell"
+    fmt = ("SELL-C-32-256" if sell else "CSR") + " (built on the device from the CSR input)"
+    if sell and getattr(args, "sell_index", "classes") == "classes":
+        fmt += ("; where the matrix's rows repeat the passes read the plan's row-class dictionary (a uint16 class "
+                "id per row + 128-byte class lines instead of the slot data; lossless, bit-identical results; "
+                "DESIGN.md §5; extra.encoding says whether it applied)")
+    return {"workload": wl, "n": int(s["n"]), "nnz": int(s["nnz"]), "grid": grid, "format": fmt, "scaling": "GS(2)",
             "solvers": ["Bi-CGSTAB to tol (maxit %d)" % cfg.maxit,
                         "GMRES(30) for %d iterations (or to tol)" % args.gmres_maxit],
             "tol": cfg.tol, "seed": cfg.seed,
-            "l2": ("inputs larger than L2 (8 solver vectors of %.0f MB + %.0f MB of class ids per Bi-CGSTAB "
-                   "iteration, a %.2f GB GMRES basis > 126 MB)" % (8 * s["n"] / 1e6, 2 * s["n"] / 1e6,
-                                                                   31 * 8 * s["n"] / 1e9)) if ncls else
-                  "inputs larger than L2 (matrix %.2f GB > 126 MB)" % ((12 * s["nnz"] + 4 * s["n"]) / 1e9)}
+            "l2": ("inputs larger than L2 (126 MB): matrix %.2f GB, 8 solver vectors of %.0f MB per Bi-CGSTAB "
+                   "iteration, a %.2f GB GMRES basis" % ((12 * s["nnz"] + 4 * s["n"]) / 1e9, 8 * s["n"] / 1e6,
+                                                        31 * 8 * s["n"] / 1e9))}
 
 
 def main():
